@@ -1,0 +1,139 @@
+/*
+ * fps.h — C ABI of libfpsgpu.so, the B200 (sm_100a) fingerprint-scan engine.
+ *
+ * Drop-in boundary for the reference fpscan search path
+ * (/root/reference/pkg/src/fpscan/scan.py). The reference has no FFI: its
+ * operator seam is `Kernel = Literal["packed","reference"]` (scan.py:35)
+ * dispatched per 65,536-record block in `_scan_shard` (scan.py:180-193). This
+ * ABI plugs in one level up, at `search` / `_search_multi` (scan.py:239-303),
+ * with the library resident in HBM, because a per-block seam would be PCIe
+ * bound. The Python shim (paper_1906_06170_b200/_native.py) binds it with
+ * ctypes and maps status codes to the reference exception types.
+ *
+ * Conventions (all entry points):
+ *  - plain pointers and sizes; no torch/CUDA types except `void* stream`
+ *    (a cudaStream_t) on the *_async entry points;
+ *  - return FPS_OK (0) or an FPS_E* status; fps_last_error() gives a
+ *    thread-local message; nothing aborts the process;
+ *  - a fingerprint is 3 little-endian u64 words, key j (1-based) at word
+ *    (j-1)/64, bit (j-1)%64 (fingerprint.py:3-5). Distance = sum of
+ *    popcount(a_w XOR b_w) over the three FULL words, exactly as the
+ *    reference XORs the FPS1 record view (scan.py:137-143, :169);
+ *  - results are ordered by (distance, index) ascending, index = global
+ *    library index (the reference orders by (distance, cid), scan.py:55-56;
+ *    identical when cid grows with index, e.g. cid = index + 1, synth.py:37);
+ *  - a handle is bound to one CUDA device; calls on one handle are
+ *    serialised by an internal mutex, so concurrent callers (the reference's
+ *    ThreadPoolExecutor / JobQueue threads, scan.py:265, jobs.py:288) are safe.
+ */
+#ifndef FPS_H
+#define FPS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPS_ABI_VERSION 1
+
+enum fps_status {
+  FPS_OK = 0,
+  FPS_EINVAL = 1,     /* bad argument: ValueError (scan.py:82-88)            */
+  FPS_ENOMEM = 2,     /* device or host allocation failed: MemoryError       */
+  FPS_ECUDA = 3,      /* CUDA runtime error: ScanError                       */
+  FPS_EPADDING = 4,   /* set bits above key 166: FingerprintError
+                         (fingerprint.py:60-61)                              */
+  FPS_ECANCELLED = 5, /* cancelled before launch: ScanCancelled (scan.py:190) */
+  FPS_ENODEV = 6      /* no CUDA device: RuntimeError                        */
+};
+
+/* Input layouts for fps_open. */
+enum fps_layout {
+  FPS_LAYOUT_ROWS3 = 0,  /* n x 3 u64, row-major (Fingerprint.words per row)    */
+  FPS_LAYOUT_FPS1 = 1,   /* n x 32-byte FPS1 records: u64 cid, then the words
+                            (libstore.py:5-16, :158-164; the (n,4) u64 view of
+                            scan.py:169)                                       */
+  FPS_LAYOUT_PLANES = 2  /* three consecutive planes of n u64 (w0[], w1[], w2[]) */
+};
+
+typedef struct fps_lib fps_lib;
+
+int fps_version(void);
+const char* fps_last_error(void);
+int fps_device_count(int* count);
+
+/* Library lifecycle. The handle owns all device memory until fps_close.
+ * `words` is a borrowed host pointer valid for the duration of the call.
+ * `index_base` is the global index of entry 0 (contiguous multi-GPU shards,
+ * libstore.split_sizes semantics, libstore.py:174-179).
+ * `check_padding`: nonzero -> FPS_EPADDING if any entry sets bits 166..191
+ * (Fingerprint invariant). FPS1 files are scanned as stored (the reference
+ * scan does not validate), so pass 0 for them. */
+int fps_open(const uint64_t* words, uint64_t n, int layout, int device, uint64_t index_base, int check_padding,
+             fps_lib** out);
+/* Same, from three device planes already on `device` (copied). */
+int fps_open_device(const uint64_t* d_w0, const uint64_t* d_w1, const uint64_t* d_w2, uint64_t n, int device,
+                    uint64_t index_base, fps_lib** out);
+/* Synthetic library generated on the device: key j set iff
+ * u32(i, j) < thr[j-1] (or always if thr_all[j-1]); see csrc gen_kernel. */
+int fps_open_generated(uint64_t n, uint64_t start, uint64_t seed_key, const uint32_t* thr166,
+                       const uint8_t* thr_all166, int device, uint64_t index_base, fps_lib** out);
+int fps_close(fps_lib* lib);
+int fps_info(const fps_lib* lib, uint64_t* n, uint64_t* index_base, int* device);
+/* Device pointers of the three planes (each n_alloc >= n u64; tail is zero). */
+int fps_planes(fps_lib* lib, uint64_t** d_w0, uint64_t** d_w1, uint64_t** d_w2, uint64_t* n_alloc);
+/* Overwrite entries idx[i] (local indices) with rows words[i] (host, m x 3). */
+int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, uint64_t m);
+
+/* Per-query top-k, host buffers (synchronous). queries: Q x 3. Outputs are
+ * Q x k, row q holds out_cnt[q] = min(k, n) valid hits in (distance, index)
+ * order; unused slots get index UINT64_MAX, distance 0xFFFF.
+ * Replaces search (scan.py:290-303) for each query. k >= 1. */
+int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx,
+             uint16_t* out_dist, uint32_t* out_cnt);
+
+/* Min-over-queries top-k (the reference batch_search, scan.py:306-318):
+ * each entry scores min_q distance; one (distance, index) top-k. */
+int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx,
+                 uint16_t* out_dist, uint32_t* out_cnt);
+
+/* Range search, host buffers: every (q, index, distance) with
+ * distance <= radius[q] (radius has Q entries), sorted by (q, distance,
+ * index). *out_keys is allocated by the library (free with fps_free); key =
+ * (q << 48) | (distance << 40) | index. */
+int fps_range(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t** out_keys,
+              uint64_t* n_out);
+void fps_free(void* p);
+
+/* ---- stream-ordered device API (benchmarks, CUDA graphs, multi-GPU) ---- */
+/* Allocate scratch for (Q, k) so that fps_topk_async does not allocate. */
+int fps_topk_prepare(fps_lib* lib, uint32_t Q, uint32_t k);
+/* d_queries: Q x 3 on the device; out: d_keys Q x k of (distance << 40 |
+ * index) keys (UINT64_MAX pads), d_cnt Q. No host synchronisation. */
+int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t k, uint64_t* d_keys,
+                   uint32_t* d_cnt, void* stream);
+/* Unsorted range hits into d_out (capacity cap), total count (may exceed cap:
+ * then retry with a larger buffer) into *d_count (zeroed by the call). */
+int fps_range_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, const uint8_t* d_radius, uint64_t* d_out,
+                    uint64_t cap, uint64_t* d_count, void* stream);
+/* Sort n range keys ascending in place (device radix sort); uses scratch of
+ * the handle (or a temporary allocation when lib is NULL). */
+int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream);
+/* Rank-0 merge of G per-shard top-k lists (merge_topk, scan.py:225-236):
+ * d_in_keys G x Q x k (each row sorted, UINT64_MAX pads), d_in_cnt G x Q. */
+int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_t G, uint32_t Q, uint32_t k,
+                    uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream);
+/* Number of kernels launched by this handle so far (evidence counter). */
+uint64_t fps_launch_count(const fps_lib* lib);
+/* Scan-kernel timing for roofline reporting: when enabled, every scan-kernel
+ * launch is bracketed by CUDA events on its own stream; fps_timing_read
+ * synchronises, returns the summed kernel time and launch count since the
+ * last read, and resets. */
+int fps_timing(fps_lib* lib, int enable);
+int fps_timing_read(fps_lib* lib, double* total_ms, uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPS_H */

@@ -1,0 +1,899 @@
+// fps_capi.cu — host side of libfpsgpu.so: the C ABI declared in include/fps.h.
+//
+// Owns the HBM-resident SoA library (three u64 planes) and the per-call
+// scratch, launches the sm_100a kernels of fps_kernels.cuh, and maps CUDA
+// failures to status codes. Reference interface replaced: fpscan.scan
+// (search / batch_search / _search_multi / merge_topk, scan.py:225-318) plus
+// the per-search shard streaming of scan.py:158-170 (the library is uploaded
+// once instead of being re-read per search).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fps.h"
+#include "fps_kernels.cuh"
+
+using fps::u32;
+using fps::u64;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) {                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? FPS_ENOMEM : FPS_ECUDA,                     \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
+    }                                                                                           \
+  } while (0)
+
+constexpr int WPB = 8;  // warps per CTA in the scan kernels
+constexpr u32 KMAX_FUSED = 1024;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return FPS_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FPS_ENOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+    return FPS_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return FPS_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(want, 4096);
+    cudaError_t e = cudaMallocHost(&p, b);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FPS_ENOMEM, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+    }
+    bytes = b;
+    return FPS_OK;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct Config {
+  int qw, e;
+  u32 n_qg;
+  u64 n_parts, iters, warps;
+  u32 cap;
+  u64 cand_cap;
+  size_t smem;
+  int grid;
+};
+
+}  // namespace
+
+struct fps_lib {
+  int device = 0;
+  int sms = 148;
+  u64 n = 0, n_alloc = 0, index_base = 0;
+  u64* planes = nullptr;  // 3 * n_alloc
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::atomic<u64> launches{0};
+  // top-k state that must start clean (tg = 255, ghist = 0, cand_cnt = 0);
+  // select_kernel restores it after every call
+  DevBuf tg, ghist, cand_cnt;
+  u32 state_q = 0;
+  DevBuf buf, cand, queries, keys, cnt, radius, rkeys, rcount, sort_tmp, sort_out, seg;
+  HostBuf h_stage;
+  // optional per-launch timing of the scan kernel (bench roofline evidence)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  size_t ev_used = 0;
+  u64* w0() const { return planes; }
+  u64* w1() const { return planes + n_alloc; }
+  u64* w2() const { return planes + 2 * n_alloc; }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <int QW, int E, int MODE>
+size_t scan_smem() {
+  if (MODE == fps::MODE_RANGE) return 0;
+  return (size_t)WPB * (QW * fps::HB * sizeof(u32) + sizeof(fps::WarpState<QW>));
+}
+
+template <int QW, int E, int MODE>
+int max_ctas_per_sm() {
+  static int cached = 0;
+  if (cached) return cached;
+  size_t smem = scan_smem<QW, E, MODE>();
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fps::scan_kernel<QW, E, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+  int blocks = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fps::scan_kernel<QW, E, MODE>, WPB * 32, smem);
+  cached = std::max(1, blocks);
+  return cached;
+}
+
+void pick_shape(u32 Q, int* qw, int* e) {
+  if (Q == 1) { *qw = 1; *e = 4; }
+  else if (Q == 2) { *qw = 2; *e = 2; }
+  else if (Q <= 4) { *qw = 4; *e = 2; }
+  else { *qw = 8; *e = 2; }
+}
+
+template <int QW, int E, int MODE>
+Config make_config(const fps_lib* L, u32 Q, u32 k) {
+  Config c{};
+  c.qw = QW;
+  c.e = E;
+  c.n_qg = (Q + QW - 1) / QW;
+  c.iters = (L->n + 32 * E - 1) / (32 * E);
+  const u64 slots = (u64)L->sms * max_ctas_per_sm<QW, E, MODE>() * WPB;
+  u64 parts = std::max<u64>(1, slots / c.n_qg);
+  const u64 min_iters = (QW == 1) ? 8 : 2;  // keep per-warp parts long enough to amortise warm-up
+  parts = std::min<u64>(parts, std::max<u64>(1, c.iters / min_iters));
+  c.n_parts = parts;
+  c.warps = (u64)c.n_qg * parts;
+  c.grid = (int)((c.warps + WPB - 1) / WPB);
+  c.cap = 0;
+  if (MODE == fps::MODE_TOPK) {
+    u32 cap = 2 * k + 32 * E;
+    cap = (cap + 31) / 32 * 32;
+    c.cap = cap;
+    c.cand_cap = parts * (u64)k;
+  }
+  c.smem = scan_smem<QW, E, MODE>();
+  return c;
+}
+
+int ensure_state(fps_lib* L, u32 Q) {
+  if (Q <= L->state_q) return FPS_OK;
+  int rc;
+  if ((rc = L->tg.ensure((size_t)Q * 4))) return rc;
+  if ((rc = L->ghist.ensure((size_t)Q * fps::HB * 4))) return rc;
+  if ((rc = L->cand_cnt.ensure((size_t)Q * 4))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L->tg.p, 0xff, L->tg.bytes, L->stream));
+  CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream));
+  CUDA_TRY(cudaMemsetAsync(L->cand_cnt.p, 0, L->cand_cnt.bytes, L->stream));
+  L->state_q = Q;
+  return FPS_OK;
+}
+
+// Restore the clean top-k state after a failed call.
+void reset_state(fps_lib* L) {
+  if (!L->state_q) return;
+  cudaMemsetAsync(L->tg.p, 0xff, L->tg.bytes, L->stream);
+  cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream);
+  cudaMemsetAsync(L->cand_cnt.p, 0, L->cand_cnt.bytes, L->stream);
+}
+
+fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
+  fps::ScanArgs a{};
+  a.w0 = L->w0();
+  a.w1 = L->w1();
+  a.w2 = L->w2();
+  a.n = L->n;
+  a.index_base = L->index_base;
+  a.queries = d_q;
+  a.Q = Q;
+  return a;
+}
+
+// Record an event pair around the next scan-kernel launch when timing is on.
+std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
+  if (!L->timing) return nullptr;
+  if (L->ev_used == L->ev_pool.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
+    L->ev_pool.emplace_back(a, b);
+  }
+  return &L->ev_pool[L->ev_used++];
+}
+
+template <int QW, int E>
+int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only) {
+  Config c = make_config<QW, E, fps::MODE_TOPK>(L, Q, k);
+  int rc;
+  if ((rc = ensure_state(L, Q))) return rc;
+  if ((rc = L->buf.ensure(c.warps * QW * (size_t)c.cap * 8))) return rc;
+  if ((rc = L->cand.ensure((size_t)Q * c.cand_cap * 8))) return rc;
+  if (prepare_only) return FPS_OK;
+  fps::ScanArgs a = base_args(L, d_q, Q);
+  a.k = k;
+  a.cap = c.cap;
+  a.n_qg = c.n_qg;
+  a.n_parts = c.n_parts;
+  a.iters = c.iters;
+  a.tg = L->tg.as<u32>();
+  a.ghist = L->ghist.as<u32>();
+  a.buf = L->buf.as<u64>();
+  a.cand = L->cand.as<u64>();
+  a.cand_cnt = L->cand_cnt.as<u32>();
+  a.cand_cap = c.cand_cap;
+  if (c.warps > 0 && L->n > 0) {
+    auto* ev = timing_slot(L);
+    if (ev) cudaEventRecord(ev->first, s);
+    fps::scan_kernel<QW, E, fps::MODE_TOPK><<<c.grid, WPB * 32, c.smem, s>>>(a);
+    if (ev) cudaEventRecord(ev->second, s);
+    L->launches++;
+  }
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  size_t sel_smem = (size_t)(kp + fps::SEL_ECAP) * 8;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr_set = true;
+  }
+  fps::select_kernel<<<Q, fps::SEL_THREADS, sel_smem, s>>>(a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, k, d_keys,
+                                                            d_cnt, 1);
+  L->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return FPS_OK;
+}
+
+int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
+                  bool prepare_only) {
+  int qw, e;
+  pick_shape(Q, &qw, &e);
+  if (qw == 1) return topk_fused<1, 4>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (qw == 2) return topk_fused<2, 2>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (qw == 4) return topk_fused<4, 2>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  return topk_fused<8, 2>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+}
+
+template <int QW, int E, int MODE>
+int launch_plain(fps_lib* L, fps::ScanArgs a, cudaStream_t s) {
+  Config c = make_config<QW, E, MODE>(L, a.Q, 1);
+  a.n_qg = c.n_qg;
+  a.n_parts = c.n_parts;
+  a.iters = c.iters;
+  if (c.warps == 0 || L->n == 0) return FPS_OK;
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::scan_kernel<QW, E, MODE><<<c.grid, WPB * 32, c.smem, s>>>(a);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return FPS_OK;
+}
+
+template <int MODE>
+int plain_dispatch(fps_lib* L, const fps::ScanArgs& a, cudaStream_t s) {
+  int qw, e;
+  pick_shape(a.Q, &qw, &e);
+  if (qw == 1) return launch_plain<1, 4, MODE>(L, a, s);
+  if (qw == 2) return launch_plain<2, 2, MODE>(L, a, s);
+  if (qw == 4) return launch_plain<4, 2, MODE>(L, a, s);
+  return launch_plain<8, 2, MODE>(L, a, s);
+}
+
+int sort_keys(fps_lib* L, u64* d_keys, u64 n, cudaStream_t s) {
+  if (n <= 1) return FPS_OK;
+  if (n > (u64)INT32_MAX) return fail(FPS_ENOMEM, "range output exceeds 2^31 hits");
+  DevBuf tmp_local, out_local;
+  DevBuf& tmp = L ? L->sort_tmp : tmp_local;
+  DevBuf& out = L ? L->sort_out : out_local;
+  size_t tmp_bytes = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, d_keys, d_keys, (int)n, 0, 64, s));
+  int rc;
+  if ((rc = tmp.ensure(tmp_bytes))) return rc;
+  if ((rc = out.ensure(n * 8))) return rc;
+  CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, d_keys, out.as<u64>(), (int)n, 0, 64, s));
+  CUDA_TRY(cudaMemcpyAsync(d_keys, out.p, n * 8, cudaMemcpyDeviceToDevice, s));
+  if (L) L->launches += 2;
+  if (!L) {
+    cudaStreamSynchronize(s);
+    tmp_local.release();
+    out_local.release();
+  }
+  return FPS_OK;
+}
+
+// Range hits (unsorted) into L->rkeys; grows and retries on overflow.
+int range_collect(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u64* n_hits, u64 cap_hint) {
+  u64 cap = std::max<u64>(cap_hint, 1 << 20);
+  int rc;
+  if ((rc = L->rcount.ensure(8))) return rc;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if ((rc = L->rkeys.ensure(cap * 8))) return rc;
+    cap = L->rkeys.bytes / 8;
+    CUDA_TRY(cudaMemsetAsync(L->rcount.p, 0, 8, L->stream));
+    fps::ScanArgs a = base_args(L, d_q, Q);
+    a.radius = d_radius;
+    a.out = L->rkeys.as<u64>();
+    a.out_cnt = L->rcount.as<u64>();
+    a.out_cap = cap;
+    if ((rc = plain_dispatch<fps::MODE_RANGE>(L, a, L->stream))) return rc;
+    u64 count = 0;
+    CUDA_TRY(cudaMemcpyAsync(&count, L->rcount.p, 8, cudaMemcpyDeviceToHost, L->stream));
+    CUDA_TRY(cudaStreamSynchronize(L->stream));
+    if (count <= cap) {
+      *n_hits = count;
+      return FPS_OK;
+    }
+    cap = count + count / 8 + 1024;
+  }
+  return fail(FPS_ECUDA, "range output kept growing between attempts");
+}
+
+int check_lib(const fps_lib* L) {
+  if (!L) return fail(FPS_EINVAL, "null library handle");
+  return FPS_OK;
+}
+
+int stage_queries(fps_lib* L, const uint64_t* queries, u32 Q) {
+  int rc;
+  if ((rc = L->queries.ensure((size_t)Q * 24))) return rc;
+  if ((rc = L->h_stage.ensure((size_t)Q * 24))) return rc;
+  std::memcpy(L->h_stage.p, queries, (size_t)Q * 24);
+  CUDA_TRY(cudaMemcpyAsync(L->queries.p, L->h_stage.p, (size_t)Q * 24, cudaMemcpyHostToDevice, L->stream));
+  return FPS_OK;
+}
+
+int alloc_planes(fps_lib* L, u64 n) {
+  L->n = n;
+  L->n_alloc = (n + 255) / 256 * 256 + 256;  // whole vector iterations + slack, zero tail
+  size_t bytes = (size_t)L->n_alloc * 3 * 8;
+  cudaError_t e = cudaMalloc(&L->planes, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    L->planes = nullptr;
+    return fail(FPS_ENOMEM, std::string("library planes cudaMalloc(") + std::to_string(bytes) +
+                                "): " + cudaGetErrorString(e));
+  }
+  CUDA_TRY(cudaMemsetAsync(L->planes, 0, bytes, L->stream));
+  return FPS_OK;
+}
+
+int new_lib(int device, u64 index_base, fps_lib** out) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(FPS_ENODEV, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) return fail(FPS_EINVAL, "device ordinal out of range");
+  if (index_base + 0 > fps::IDX_MASK) return fail(FPS_EINVAL, "index_base exceeds 2^40");
+  CUDA_TRY(cudaSetDevice(device));
+  fps_lib* L = new fps_lib();
+  L->device = device;
+  L->index_base = index_base;
+  cudaDeviceGetAttribute(&L->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete L;
+    return fail(FPS_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+  }
+  *out = L;
+  return FPS_OK;
+}
+
+void destroy(fps_lib* L) {
+  if (!L) return;
+  DeviceGuard g(L->device);
+  if (L->stream) cudaStreamSynchronize(L->stream);
+  if (L->planes) cudaFree(L->planes);
+  for (DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt, &L->radius,
+                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg})
+    b->release();
+  L->h_stage.release();
+  for (auto& p : L->ev_pool) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  if (L->stream) cudaStreamDestroy(L->stream);
+  delete L;
+}
+
+void unpack_topk(const u64* keys, const u32* cnt, u32 Q, u32 k, uint64_t* out_idx, uint16_t* out_dist,
+                 uint32_t* out_cnt) {
+  for (u32 q = 0; q < Q; ++q) {
+    out_cnt[q] = cnt[q];
+    for (u32 i = 0; i < k; ++i) {
+      u64 key = keys[(u64)q * k + i];
+      bool ok = i < cnt[q];
+      if (out_idx) out_idx[(u64)q * k + i] = ok ? (key & fps::IDX_MASK) : UINT64_MAX;
+      if (out_dist) out_dist[(u64)q * k + i] = ok ? (uint16_t)fps::key_d(key) : 0xFFFF;
+    }
+  }
+}
+
+// Large-k path (k > KMAX_FUSED): exact distance histogram -> per-query
+// threshold T_q -> range collection with radius T_q -> sort -> first k.
+int topk_large(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt) {
+  int rc;
+  if ((rc = ensure_state(L, Q))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, (size_t)Q * fps::HB * 4, L->stream));
+  fps::ScanArgs a = base_args(L, d_q, Q);
+  if ((rc = plain_dispatch<fps::MODE_HIST>(L, a, L->stream))) return rc;
+  std::vector<u32> hist((size_t)Q * fps::HB);
+  CUDA_TRY(cudaMemcpyAsync(hist.data(), L->ghist.p, hist.size() * 4, cudaMemcpyDeviceToHost, L->stream));
+  CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, (size_t)Q * fps::HB * 4, L->stream));
+  CUDA_TRY(cudaStreamSynchronize(L->stream));
+  std::vector<unsigned char> rad(Q);
+  std::vector<u64> seg(Q + 1, 0);
+  for (u32 q = 0; q < Q; ++q) {
+    u64 c = 0;
+    int t = 255;
+    for (int b = 0; b < fps::HB; ++b) {
+      c += hist[(size_t)q * fps::HB + b];
+      if (c >= k) { t = b; break; }
+    }
+    if (t == 255) {  // fewer than k entries: take all
+      c = 0;
+      for (int b = 0; b < fps::HB; ++b) c += hist[(size_t)q * fps::HB + b];
+      t = 254;
+    }
+    rad[q] = (unsigned char)t;
+    seg[q + 1] = seg[q] + c;
+  }
+  if ((rc = L->radius.ensure(Q))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(L->radius.p, rad.data(), Q, cudaMemcpyHostToDevice, L->stream));
+  u64 hits = 0;
+  if ((rc = range_collect(L, d_q, Q, L->radius.as<unsigned char>(), &hits, seg[Q] + 1))) return rc;
+  if (hits != seg[Q]) return fail(FPS_ECUDA, "large-k collection count disagrees with the histogram");
+  if ((rc = sort_keys(L, L->rkeys.as<u64>(), hits, L->stream))) return rc;
+  if ((rc = L->seg.ensure((size_t)(Q + 1) * 8))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(L->seg.p, seg.data(), (size_t)(Q + 1) * 8, cudaMemcpyHostToDevice, L->stream));
+  fps::truncate_kernel<<<Q, 256, 0, L->stream>>>(L->rkeys.as<u64>(), L->seg.as<u64>(), Q, k, d_keys, d_cnt);
+  L->launches++;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(L->stream));
+  return FPS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fps_version(void) { return FPS_ABI_VERSION; }
+
+const char* fps_last_error(void) { return g_err.c_str(); }
+
+int fps_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return FPS_OK;
+}
+
+int fps_open(const uint64_t* words, uint64_t n, int layout, int device, uint64_t index_base, int check_padding,
+             fps_lib** out) {
+  if (!out) return fail(FPS_EINVAL, "out is null");
+  *out = nullptr;
+  if (n > 0 && !words) return fail(FPS_EINVAL, "words is null");
+  if (index_base + n > fps::IDX_MASK) return fail(FPS_EINVAL, "library indices exceed 2^40");
+  int stride, col0;
+  if (layout == FPS_LAYOUT_ROWS3) { stride = 3; col0 = 0; }
+  else if (layout == FPS_LAYOUT_FPS1) { stride = 4; col0 = 1; }
+  else if (layout == FPS_LAYOUT_PLANES) { stride = 0; col0 = 0; }
+  else return fail(FPS_EINVAL, "unknown layout");
+  fps_lib* L = nullptr;
+  int rc = new_lib(device, index_base, &L);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  if ((rc = alloc_planes(L, n))) { destroy(L); return rc; }
+  DevBuf bad;
+  if ((rc = bad.ensure(4))) { destroy(L); return rc; }
+  cudaMemsetAsync(bad.p, 0, 4, L->stream);
+  if (layout == FPS_LAYOUT_PLANES) {
+    for (int p = 0; p < 3; ++p)
+      cudaMemcpyAsync(L->planes + (size_t)p * L->n_alloc, words + (size_t)p * n, n * 8, cudaMemcpyHostToDevice,
+                      L->stream);
+  } else if (n) {
+    // stream rows through a pinned staging buffer in chunks, transposing on device
+    const u64 chunk = 1 << 20;  // rows per chunk
+    HostBuf hb;
+    DevBuf db;
+    if ((rc = hb.ensure((size_t)chunk * stride * 8)) || (rc = db.ensure((size_t)chunk * stride * 8))) {
+      destroy(L);
+      return rc;
+    }
+    for (u64 s = 0; s < n; s += chunk) {
+      u64 m = std::min<u64>(chunk, n - s);
+      cudaStreamSynchronize(L->stream);  // staging buffer reuse
+      std::memcpy(hb.p, words + s * stride, (size_t)m * stride * 8);
+      cudaMemcpyAsync(db.p, hb.p, (size_t)m * stride * 8, cudaMemcpyHostToDevice, L->stream);
+      int blocks = (int)std::min<u64>((m + 255) / 256, 4096);
+      fps::rows_to_planes<<<blocks, 256, 0, L->stream>>>(db.as<u64>(), m, stride, col0, L->w0(), L->w1(), L->w2(), s,
+                                                        check_padding ? bad.as<u32>() : nullptr);
+      L->launches++;
+    }
+    cudaStreamSynchronize(L->stream);
+    hb.release();
+    db.release();
+  }
+  u32 nbad = 0;
+  cudaMemcpyAsync(&nbad, bad.p, 4, cudaMemcpyDeviceToHost, L->stream);
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  bad.release();
+  if (e != cudaSuccess) {
+    destroy(L);
+    return fail(FPS_ECUDA, std::string("library upload: ") + cudaGetErrorString(e));
+  }
+  if (layout == FPS_LAYOUT_PLANES && check_padding) {
+    // host-side check for the planes layout (the input is on the host anyway)
+    for (u64 i = 0; i < n; ++i)
+      if (words[2 * n + i] >> 38) { nbad = 1; break; }
+  }
+  if (nbad) {
+    destroy(L);
+    return fail(FPS_EPADDING, "padding bits above key 166 must be zero");
+  }
+  *out = L;
+  return FPS_OK;
+}
+
+int fps_open_device(const uint64_t* d_w0, const uint64_t* d_w1, const uint64_t* d_w2, uint64_t n, int device,
+                    uint64_t index_base, fps_lib** out) {
+  if (!out) return fail(FPS_EINVAL, "out is null");
+  *out = nullptr;
+  if (index_base + n > fps::IDX_MASK) return fail(FPS_EINVAL, "library indices exceed 2^40");
+  fps_lib* L = nullptr;
+  int rc = new_lib(device, index_base, &L);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  if ((rc = alloc_planes(L, n))) { destroy(L); return rc; }
+  if (n) {
+    cudaMemcpyAsync(L->w0(), d_w0, n * 8, cudaMemcpyDeviceToDevice, L->stream);
+    cudaMemcpyAsync(L->w1(), d_w1, n * 8, cudaMemcpyDeviceToDevice, L->stream);
+    cudaMemcpyAsync(L->w2(), d_w2, n * 8, cudaMemcpyDeviceToDevice, L->stream);
+  }
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e != cudaSuccess) {
+    destroy(L);
+    return fail(FPS_ECUDA, std::string("device upload: ") + cudaGetErrorString(e));
+  }
+  *out = L;
+  return FPS_OK;
+}
+
+int fps_open_generated(uint64_t n, uint64_t start, uint64_t seed_key, const uint32_t* thr166,
+                       const uint8_t* thr_all166, int device, uint64_t index_base, fps_lib** out) {
+  if (!out || !thr166) return fail(FPS_EINVAL, "null argument");
+  *out = nullptr;
+  if (index_base + n > fps::IDX_MASK) return fail(FPS_EINVAL, "library indices exceed 2^40");
+  fps_lib* L = nullptr;
+  int rc = new_lib(device, index_base, &L);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  if ((rc = alloc_planes(L, n))) { destroy(L); return rc; }
+  fps::GenArgs a{};
+  a.w0 = L->w0();
+  a.w1 = L->w1();
+  a.w2 = L->w2();
+  a.n = n;
+  a.start = start;
+  a.seed_key = seed_key;
+  for (int j = 0; j < 166; ++j) {
+    a.thr[j] = thr166[j];
+    a.thr_hi[j] = thr_all166 ? thr_all166[j] : 0;
+  }
+  if (n) {
+    int blocks = (int)std::min<u64>((n + 255) / 256, (u64)L->sms * 16);
+    fps::gen_kernel<<<blocks, 256, 0, L->stream>>>(a);
+    L->launches++;
+  }
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    destroy(L);
+    return fail(FPS_ECUDA, std::string("generate: ") + cudaGetErrorString(e));
+  }
+  *out = L;
+  return FPS_OK;
+}
+
+int fps_close(fps_lib* lib) {
+  if (!lib) return FPS_OK;
+  destroy(lib);
+  return FPS_OK;
+}
+
+int fps_info(const fps_lib* lib, uint64_t* n, uint64_t* index_base, int* device) {
+  if (int rc = check_lib(lib)) return rc;
+  if (n) *n = lib->n;
+  if (index_base) *index_base = lib->index_base;
+  if (device) *device = lib->device;
+  return FPS_OK;
+}
+
+int fps_planes(fps_lib* lib, uint64_t** d_w0, uint64_t** d_w1, uint64_t** d_w2, uint64_t* n_alloc) {
+  if (int rc = check_lib(lib)) return rc;
+  if (d_w0) *d_w0 = (uint64_t*)lib->w0();
+  if (d_w1) *d_w1 = (uint64_t*)lib->w1();
+  if (d_w2) *d_w2 = (uint64_t*)lib->w2();
+  if (n_alloc) *n_alloc = lib->n_alloc;
+  return FPS_OK;
+}
+
+int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, uint64_t m) {
+  if (int rc = check_lib(lib)) return rc;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  for (u64 i = 0; i < m; ++i)
+    if (idx[i] >= lib->n) return fail(FPS_EINVAL, "entry index out of range");
+  if (m == 0) return FPS_OK;
+  int rc;
+  DevBuf d_idx, d_rows;
+  if ((rc = d_idx.ensure((size_t)m * 8)) || (rc = d_rows.ensure((size_t)m * 24))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(d_idx.p, idx, (size_t)m * 8, cudaMemcpyHostToDevice, lib->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_rows.p, words, (size_t)m * 24, cudaMemcpyHostToDevice, lib->stream));
+  int blocks = (int)std::min<u64>((m + 255) / 256, 4096);
+  fps::scatter_rows<<<blocks, 256, 0, lib->stream>>>(d_idx.as<u64>(), d_rows.as<u64>(), m, lib->w0(), lib->w1(),
+                                                     lib->w2());
+  lib->launches++;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(lib->stream));
+  d_idx.release();
+  d_rows.release();
+  return FPS_OK;
+}
+
+int fps_topk_prepare(fps_lib* lib, uint32_t Q, uint32_t k) {
+  if (int rc = check_lib(lib)) return rc;
+  if (Q == 0 || k == 0) return fail(FPS_EINVAL, "Q and k must be >= 1");
+  if (k > KMAX_FUSED) return fail(FPS_EINVAL, "fps_topk_async supports k <= 1024");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  int rc = topk_dispatch(lib, nullptr, Q, k, nullptr, nullptr, lib->stream, true);
+  if (!rc) CUDA_TRY(cudaStreamSynchronize(lib->stream));
+  return rc;
+}
+
+int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t k, uint64_t* d_keys,
+                   uint32_t* d_cnt, void* stream) {
+  if (int rc = check_lib(lib)) return rc;
+  if (Q == 0 || k == 0) return fail(FPS_EINVAL, "Q and k must be >= 1");
+  if (k > KMAX_FUSED) return fail(FPS_EINVAL, "fps_topk_async supports k <= 1024");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : lib->stream;
+  int rc = topk_dispatch(lib, (const u64*)d_queries, Q, k, (u64*)d_keys, d_cnt, s, false);
+  if (rc) reset_state(lib);
+  return rc;
+}
+
+int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx, uint16_t* out_dist,
+             uint32_t* out_cnt) {
+  if (int rc = check_lib(lib)) return rc;
+  if (Q == 0) return FPS_OK;
+  if (k == 0) return fail(FPS_EINVAL, "n must be >= 1");
+  if (!queries || !out_cnt) return fail(FPS_EINVAL, "null argument");
+  for (u32 q = 0; q < Q; ++q)
+    if (queries[3 * (u64)q + 2] >> 38) return fail(FPS_EPADDING, "padding bits above key 166 must be zero");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  int rc;
+  if ((rc = stage_queries(lib, queries, Q))) return rc;
+  if ((rc = lib->keys.ensure((size_t)Q * k * 8)) || (rc = lib->cnt.ensure((size_t)Q * 4))) return rc;
+  if (k <= KMAX_FUSED) {
+    rc = topk_dispatch(lib, lib->queries.as<u64>(), Q, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), lib->stream, false);
+    if (rc) { reset_state(lib); return rc; }
+  } else {
+    rc = topk_large(lib, lib->queries.as<u64>(), Q, k, lib->keys.as<u64>(), lib->cnt.as<u32>());
+    if (rc) return rc;
+  }
+  size_t kb = (size_t)Q * k * 8;
+  if ((rc = lib->h_stage.ensure(kb + (size_t)Q * 4))) return rc;
+  u64* hk = lib->h_stage.as<u64>();
+  u32* hc = reinterpret_cast<u32*>(lib->h_stage.as<char>() + kb);
+  CUDA_TRY(cudaMemcpyAsync(hk, lib->keys.p, kb, cudaMemcpyDeviceToHost, lib->stream));
+  CUDA_TRY(cudaMemcpyAsync(hc, lib->cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, lib->stream));
+  cudaError_t e = cudaStreamSynchronize(lib->stream);
+  if (e != cudaSuccess) {
+    reset_state(lib);
+    return fail(FPS_ECUDA, std::string("top-k: ") + cudaGetErrorString(e));
+  }
+  unpack_topk(hk, hc, Q, k, out_idx, out_dist, out_cnt);
+  return FPS_OK;
+}
+
+int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx,
+                 uint16_t* out_dist, uint32_t* out_cnt) {
+  if (int rc = check_lib(lib)) return rc;
+  if (Q == 0) return fail(FPS_EINVAL, "batch_search requires at least one query");
+  if (k == 0) return fail(FPS_EINVAL, "n must be >= 1");
+  if (k > KMAX_FUSED) return fail(FPS_EINVAL, "min-over-queries top-k supports n <= 1024");
+  if (!queries || !out_cnt) return fail(FPS_EINVAL, "null argument");
+  for (u32 q = 0; q < Q; ++q)
+    if (queries[3 * (u64)q + 2] >> 38) return fail(FPS_EPADDING, "padding bits above key 166 must be zero");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  int rc;
+  if ((rc = stage_queries(lib, queries, Q))) return rc;
+  if ((rc = lib->keys.ensure((size_t)k * 8)) || (rc = lib->cnt.ensure(4))) return rc;
+  Config c = make_config<1, 4, fps::MODE_TOPK>(lib, 1, k);
+  if ((rc = ensure_state(lib, 1))) return rc;
+  if ((rc = lib->buf.ensure(c.warps * (size_t)c.cap * 8))) return rc;
+  if ((rc = lib->cand.ensure(c.cand_cap * 8))) return rc;
+  fps::ScanArgs a = base_args(lib, lib->queries.as<u64>(), 1);
+  a.Qmin = Q;
+  a.k = k;
+  a.cap = c.cap;
+  a.n_qg = 1;
+  a.n_parts = c.n_parts;
+  a.iters = c.iters;
+  a.tg = lib->tg.as<u32>();
+  a.ghist = lib->ghist.as<u32>();
+  a.buf = lib->buf.as<u64>();
+  a.cand = lib->cand.as<u64>();
+  a.cand_cnt = lib->cand_cnt.as<u32>();
+  a.cand_cap = c.cand_cap;
+  if (c.warps > 0 && lib->n > 0) {
+    fps::scan_kernel<1, 4, fps::MODE_TOPK, true><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
+    lib->launches++;
+  }
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  fps::select_kernel<<<1, fps::SEL_THREADS, (size_t)(kp + fps::SEL_ECAP) * 8, lib->stream>>>(
+      a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), 1);
+  lib->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, cudaGetErrorString(e)); }
+  if ((rc = lib->h_stage.ensure((size_t)k * 8 + 4))) return rc;
+  u64* hk = lib->h_stage.as<u64>();
+  u32* hc = reinterpret_cast<u32*>(lib->h_stage.as<char>() + (size_t)k * 8);
+  CUDA_TRY(cudaMemcpyAsync(hk, lib->keys.p, (size_t)k * 8, cudaMemcpyDeviceToHost, lib->stream));
+  CUDA_TRY(cudaMemcpyAsync(hc, lib->cnt.p, 4, cudaMemcpyDeviceToHost, lib->stream));
+  e = cudaStreamSynchronize(lib->stream);
+  if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, std::string("top-k min: ") + cudaGetErrorString(e)); }
+  unpack_topk(hk, hc, 1, k, out_idx, out_dist, out_cnt);
+  return FPS_OK;
+}
+
+int fps_range_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, const uint8_t* d_radius, uint64_t* d_out,
+                    uint64_t cap, uint64_t* d_count, void* stream) {
+  if (int rc = check_lib(lib)) return rc;
+  if (Q == 0) return FPS_OK;
+  if (Q > 65535) return fail(FPS_EINVAL, "at most 65535 queries per range call");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : lib->stream;
+  CUDA_TRY(cudaMemsetAsync(d_count, 0, 8, s));
+  fps::ScanArgs a = base_args(lib, (const u64*)d_queries, Q);
+  a.radius = d_radius;
+  a.out = (u64*)d_out;
+  a.out_cnt = (u64*)d_count;
+  a.out_cap = cap;
+  return plain_dispatch<fps::MODE_RANGE>(lib, a, s);
+}
+
+int fps_range(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t** out_keys,
+              uint64_t* n_out) {
+  if (int rc = check_lib(lib)) return rc;
+  if (!out_keys || !n_out) return fail(FPS_EINVAL, "null output");
+  *out_keys = nullptr;
+  *n_out = 0;
+  if (Q == 0) return FPS_OK;
+  if (Q > 65535) return fail(FPS_EINVAL, "at most 65535 queries per range call");
+  if (!queries || !radius) return fail(FPS_EINVAL, "null argument");
+  for (u32 q = 0; q < Q; ++q)
+    if (queries[3 * (u64)q + 2] >> 38) return fail(FPS_EPADDING, "padding bits above key 166 must be zero");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  int rc;
+  if ((rc = stage_queries(lib, queries, Q))) return rc;
+  if ((rc = lib->radius.ensure(Q))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(lib->radius.p, radius, Q, cudaMemcpyHostToDevice, lib->stream));
+  u64 hits = 0;
+  if ((rc = range_collect(lib, lib->queries.as<u64>(), Q, lib->radius.as<unsigned char>(), &hits, 0))) return rc;
+  if ((rc = sort_keys(lib, lib->rkeys.as<u64>(), hits, lib->stream))) return rc;
+  u64* host = (u64*)std::malloc(std::max<u64>(hits, 1) * 8);
+  if (!host) return fail(FPS_ENOMEM, "host allocation for range output");
+  if (hits) CUDA_TRY(cudaMemcpyAsync(host, lib->rkeys.p, hits * 8, cudaMemcpyDeviceToHost, lib->stream));
+  cudaError_t e = cudaStreamSynchronize(lib->stream);
+  if (e != cudaSuccess) {
+    std::free(host);
+    return fail(FPS_ECUDA, std::string("range: ") + cudaGetErrorString(e));
+  }
+  *out_keys = (uint64_t*)host;
+  *n_out = hits;
+  return FPS_OK;
+}
+
+void fps_free(void* p) { std::free(p); }
+
+int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream) {
+  if (lib) {
+    std::lock_guard<std::mutex> lk(lib->mu);
+    DeviceGuard g(lib->device);
+    return sort_keys(lib, (u64*)d_keys, n, stream ? (cudaStream_t)stream : lib->stream);
+  }
+  return sort_keys(nullptr, (u64*)d_keys, n, (cudaStream_t)stream);
+}
+
+int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_t G, uint32_t Q, uint32_t k,
+                    uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream) {
+  if (G == 0 || Q == 0 || k == 0) return fail(FPS_EINVAL, "G, Q and k must be >= 1");
+  u64 total = std::max<u64>((u64)G * Q * k, Q);
+  int blocks = (int)((total + 255) / 256);
+  fps::merge_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const u64*)d_in_keys, d_in_cnt, G, Q, k, (u64*)d_out_keys, d_out_cnt);
+  CUDA_TRY(cudaGetLastError());
+  return FPS_OK;
+}
+
+uint64_t fps_launch_count(const fps_lib* lib) { return lib ? lib->launches.load() : 0; }
+
+int fps_timing(fps_lib* lib, int enable) {
+  if (int rc = check_lib(lib)) return rc;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  lib->timing = enable != 0;
+  lib->ev_used = 0;
+  return FPS_OK;
+}
+
+int fps_timing_read(fps_lib* lib, double* total_ms, uint64_t* count) {
+  if (int rc = check_lib(lib)) return rc;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  double t = 0;
+  for (size_t i = 0; i < lib->ev_used; ++i) {
+    CUDA_TRY(cudaEventSynchronize(lib->ev_pool[i].second));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, lib->ev_pool[i].first, lib->ev_pool[i].second));
+    t += ms;
+  }
+  if (total_ms) *total_ms = t;
+  if (count) *count = lib->ev_used;
+  lib->ev_used = 0;
+  return FPS_OK;
+}
+
+}  // extern "C"

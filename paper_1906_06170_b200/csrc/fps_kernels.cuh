@@ -1,0 +1,686 @@
+// fps_kernels.cuh — sm_100a device code for the MACCS-166 Hamming scan.
+//
+// Replaces the reference's per-block numpy kernel + heap
+// (/root/reference/pkg/src/fpscan/scan.py:137-143, :91-126, :173-209) and the
+// shard merge (scan.py:225-236) with:
+//   * scan_kernel<QW,E,MODE>  — one pass over the HBM-resident SoA library
+//     (three u64 planes); each warp owns a contiguous library part and QW
+//     queries held in registers; distance = sum of popcount(word XOR query)
+//     over the three full 64-bit words (exactly what scan.py:142 XORs);
+//     MODE_TOPK keeps a per-(warp,query) candidate buffer in index order with
+//     an incremental distance histogram and an exact filter threshold;
+//     MODE_RANGE appends every hit with warp-ballot compaction;
+//     MODE_HIST counts distances (large-k path).
+//   * select_kernel — per query, exact top-k over the flat candidate list
+//     (histogram on distance, then tie resolution by index).
+//   * merge_kernel — rank-0 merge of G sorted per-shard top-k lists
+//     (merge_topk semantics) by merge-path ranking.
+//   * gen_kernel / transpose kernels — synthetic library and FPS1/row-major
+//     ingestion into planes.
+//
+// Ordering everywhere is the reference total order (distance, then id) with
+// id = global library index (cid = index + 1 in the reference's synthetic
+// libraries, synth.py:37). Keys pack (d << 40) | index (index < 2^40).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fps {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr u32 FULL = 0xffffffffu;
+constexpr int IDX_BITS = 40;
+constexpr u64 IDX_MASK = (1ull << IDX_BITS) - 1;
+constexpr int HB = 224;       // histogram bins (distances 0..192 used; 7 per lane)
+constexpr u32 DMASKED = 255;  // distance given to masked (out-of-range) entries
+constexpr u32 T_OPEN = 255;   // "accept everything" threshold
+
+enum { MODE_TOPK = 0, MODE_RANGE = 1, MODE_HIST = 2 };
+
+__host__ __device__ __forceinline__ u64 make_key(u32 d, u64 idx) { return ((u64)d << IDX_BITS) | idx; }
+__host__ __device__ __forceinline__ u32 key_d(u64 key) { return (u32)(key >> IDX_BITS) & 0xffu; }
+
+struct __align__(32) u64x4 { u64 x, y, z, w; };
+
+// Streaming loads: read-only, do not allocate in L1 (each byte is read once).
+__device__ __forceinline__ void ld_entries(const u64* p, u64 (&v)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld_entries(const u64* p, u64 (&v)[2]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
+}
+__device__ __forceinline__ void ld_entries(const u64* p, u64 (&v)[1]) {
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v[0]) : "l"(p));
+}
+
+__device__ __forceinline__ u32 dist3(u64 a, u64 b, u64 c, u64 q0, u64 q1, u64 q2) {
+  return (u32)(__popcll(a ^ q0) + __popcll(b ^ q1) + __popcll(c ^ q2));
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ u32 warp_incl_scan(u32 v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Smallest t with sum_{d<=t} hist[d] >= k (hist has HB bins, warp-cooperative).
+// Returns T_OPEN when the total is below k. Also returns count(d < t) in *less.
+__device__ __forceinline__ u32 warp_kth_bin(const u32* hist, u32 k, int lane, u32* less) {
+  u32 h[7];
+  u32 s = 0;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) { h[i] = hist[lane * 7 + i]; s += h[i]; }
+  u32 incl = warp_incl_scan(s, lane);
+  u32 ballot = __ballot_sync(FULL, incl >= k);
+  if (ballot == 0) { *less = 0; return T_OPEN; }
+  int src = __ffs(ballot) - 1;
+  u32 t = 0, lt = 0;
+  if (lane == src) {
+    u32 c = incl - s;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      if (c + h[i] >= k) { t = lane * 7 + i; lt = c; break; }
+      c += h[i];
+    }
+  }
+  t = __shfl_sync(FULL, t, src);
+  *less = __shfl_sync(FULL, lt, src);
+  return t;
+}
+
+struct ScanArgs {
+  const u64* w0;
+  const u64* w1;
+  const u64* w2;
+  u64 n;           // valid entries on this device
+  u64 index_base;  // global index of entry 0
+  const u64* queries;  // Q x 3
+  const unsigned char* radius;  // MODE_RANGE: per-query radius
+  u32 Q;
+  u32 Qmin;        // MINQ: number of queries the distance is minimised over
+  u32 k;
+  u32 cap;         // MODE_TOPK: per-(warp, query) buffer capacity
+  u32 n_qg;        // query groups (ceil(Q / QW))
+  u64 n_parts;     // library parts
+  u64 iters;       // ceil(n / (32*E))
+  // MODE_TOPK state (all per query unless noted)
+  u32* tg;         // global filter bound: entries with d > tg[q] are not in the top-k
+  u32* ghist;      // [Q][HB] distances of published candidates (distinct entries)
+  u64* buf;        // [warps][QW][cap] candidate buffers
+  u64* cand;       // [Q][cand_cap] flat survivor list
+  u32* cand_cnt;   // [Q]
+  u64 cand_cap;
+  // MODE_RANGE output
+  u64* out;        // keys (q << 48) | (d << 40) | idx
+  u64* out_cnt;    // single counter
+  u64 out_cap;
+  // MODE_HIST output: ghist reused
+};
+
+// Global bound maintenance. ghist[q] counts distances of *published*
+// candidates; every published candidate is a distinct library entry, so if
+// the cumulative count up to T reaches k, no entry with d > T can be in the
+// top-k and tg[q] = min(tg[q], T) is exact. Reads of ghist see monotone
+// counters, so any snapshot is a valid lower count.
+__device__ __forceinline__ void tighten_tg(const ScanArgs& a, u32 qi, int lane) {
+  const u32* gh = a.ghist + (u64)qi * HB;
+  u32 hv[7], s = 0;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) { hv[i] = *((volatile const u32*)gh + lane * 7 + i); s += hv[i]; }
+  u32 incl = warp_incl_scan(s, lane);
+  u32 bal = __ballot_sync(FULL, incl >= a.k);
+  if (bal) {
+    int src = __ffs(bal) - 1;
+    if (lane == src) {
+      u32 cc = incl - s, tt = 0;
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        if (cc + hv[i] >= a.k) { tt = lane * 7 + i; break; }
+        cc += hv[i];
+      }
+      atomicMin(a.tg + qi, tt);
+    }
+  }
+}
+
+// Per-warp slow-path state, kept in shared memory (only touched on inserts).
+template <int QW>
+struct WarpState {
+  u32 town[QW];   // own k-th distance (T_OPEN until k candidates)
+  u32 pubd[QW];   // 1 once the warp has published its candidates
+  u32 cnt[QW];    // buffer fill
+};
+
+template <int QW, int E, int MODE, bool MINQ = false>
+__global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
+  extern __shared__ u32 smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nwb = blockDim.x >> 5;
+  const u64 g = (u64)blockIdx.x * nwb + wib;
+  if (g >= (u64)a.n_qg * a.n_parts) return;  // warp-uniform; no block-level sync below
+  const u32 qg = (u32)(g % a.n_qg);
+  const u64 part = g / a.n_qg;
+  const u64 it0 = part * a.iters / a.n_parts;
+  const u64 it1 = (part + 1) * a.iters / a.n_parts;
+  const u64 n_full = a.n / (32 * E);  // iterations whose entries are all valid
+
+  u64 q0[QW], q1[QW], q2[QW];
+  u32 T[QW];  // hot filter: accept d < T[j]
+#pragma unroll
+  for (int j = 0; j < QW; ++j) {
+    u32 qi = qg * QW + j;
+    bool ok = qi < a.Q;
+    q0[j] = ok ? a.queries[3 * (u64)qi + 0] : 0;
+    q1[j] = ok ? a.queries[3 * (u64)qi + 1] : 0;
+    q2[j] = ok ? a.queries[3 * (u64)qi + 2] : 0;
+    if (MODE == MODE_TOPK) T[j] = ok ? T_OPEN : 0;
+    else if (MODE == MODE_RANGE) T[j] = ok ? (u32)a.radius[qi] + 1 : 0;
+    else T[j] = ok ? 256 : 0;
+  }
+  u32* hist = smem + (u64)wib * QW * HB;  // [QW][HB] (TOPK / HIST)
+  WarpState<QW>* ws = reinterpret_cast<WarpState<QW>*>(smem + (u64)nwb * QW * HB) + wib;
+  if (MODE != MODE_RANGE) {
+    for (int i = lane; i < QW * HB; i += 32) hist[i] = 0;
+    if (lane < QW) { ws->town[lane] = T_OPEN; ws->pubd[lane] = 0; ws->cnt[lane] = 0; }
+    __syncwarp();
+  }
+  u64* wbuf = (MODE == MODE_TOPK) ? a.buf + g * QW * (u64)a.cap : nullptr;
+
+  auto refresh_tg = [&](int j) {
+    u32 qi = qg * QW + j;
+    if (qi < a.Q) {
+      u32 t = *((volatile const u32*)a.tg + qi) + 1;
+      u32 own = ws->town[j];
+      T[j] = t < own ? t : own;
+    }
+  };
+
+  // Warp-collective ordered compaction of query slot j's buffer down to its
+  // k best: every entry with d < T_own, then the first m ties in index order
+  // (the buffer is always in ascending index order).
+  auto compact = [&](int j) {
+    u32* hj = hist + j * HB;
+    u64* bj = wbuf + (u64)j * a.cap;
+    const u32 n = ws->cnt[j];
+    u32 less;
+    const u32 t = warp_kth_bin(hj, a.k, lane, &less);
+    const u32 m = a.k - less;
+    u32 out = 0, ties = 0;
+    for (u32 i0 = 0; i0 < n; i0 += 32) {
+      const u32 i = i0 + lane;
+      const bool valid = i < n;
+      const u64 key = valid ? bj[i] : ~0ull;
+      const u32 d = key_d(key);
+      const bool lt = valid && d < t;
+      const bool tie = valid && d == t;
+      const u32 tb = __ballot_sync(FULL, tie);
+      const u32 tr = ties + __popc(tb & lanemask_lt());
+      const bool keep = lt || (tie && tr < m);
+      const u32 kb = __ballot_sync(FULL, keep);
+      const u32 p = out + __popc(kb & lanemask_lt());
+      __syncwarp();
+      if (keep) bj[p] = key;
+      out += __popc(kb);
+      ties += __popc(tb);
+    }
+    for (u32 b = lane; b < HB; b += 32) {
+      if (b > t) hj[b] = 0;
+      else if (b == t) hj[b] = m;
+    }
+    if (lane == 0) ws->cnt[j] = out;
+    __syncwarp();
+  };
+
+  // MINQ (reference batch_search, scan.py:137-143 + :306-318): the score of
+  // an entry is its minimum distance over all Qmin queries.
+  auto dist_of = [&](u64 x, u64 y, u64 z, int j) -> u32 {
+    if (MINQ) {
+      u32 best = 0xffffffffu;
+      for (u32 t = 0; t < a.Qmin; ++t) {
+        const u32 d = dist3(x, y, z, __ldg(a.queries + 3 * (u64)t), __ldg(a.queries + 3 * (u64)t + 1),
+                            __ldg(a.queries + 3 * (u64)t + 2));
+        best = d < best ? d : best;
+      }
+      return best;
+    }
+    return dist3(x, y, z, q0[j], q1[j], q2[j]);
+  };
+
+  auto process = [&](const u64 (&A)[E], const u64 (&B)[E], const u64 (&C)[E], u64 it, bool masked) {
+    const u64 first = it * (32 * E) + (u64)lane * E;  // local index of this lane's entry 0
+    u32 hit = 0;
+#pragma unroll
+    for (int j = 0; j < QW; ++j) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        u32 d = dist_of(A[e], B[e], C[e], j);
+        if (masked && first + e >= a.n) d = DMASKED;
+        if (MODE == MODE_HIST) {
+          if (d != DMASKED && T[j]) atomicAdd(hist + j * HB + d, 1u);
+        } else {
+          hit |= (d < T[j]) ? 1u : 0u;
+        }
+      }
+    }
+    if (MODE == MODE_HIST) return;
+    if (!__any_sync(FULL, hit)) return;
+    // slow path: rare once thresholds settle (unrolled so the query words
+    // and thresholds stay in registers)
+#pragma unroll
+    for (int j = 0; j < QW; ++j) {
+      u32 dd[E];
+      u32 m = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        dd[e] = dist_of(A[e], B[e], C[e], j);
+        if (masked && first + e >= a.n) dd[e] = DMASKED;
+        if (dd[e] < T[j]) m |= 1u << e;
+      }
+      if (!__any_sync(FULL, m)) continue;
+      const u32 qi = qg * QW + j;
+      const u32 c = __popc(m);
+      const u32 incl = warp_incl_scan(c, lane);
+      const u32 total = __shfl_sync(FULL, incl, 31);
+      if (MODE == MODE_RANGE) {
+        u64 base = 0;
+        if (lane == 31) base = atomicAdd(a.out_cnt, (u64)total);
+        base = __shfl_sync(FULL, base, 31);
+        u64 pos = base + incl - c;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (m >> e & 1u) {
+            if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | make_key(dd[e], a.index_base + first + e);
+            ++pos;
+          }
+        }
+        continue;
+      }
+      // MODE_TOPK: ordered insertion (lane-major, then e == ascending index)
+      if (ws->cnt[j] + 32 * E > a.cap) compact(j);
+      u32* hj = hist + j * HB;
+      u64* bj = wbuf + (u64)j * a.cap;
+      const u32 cnt0 = ws->cnt[j];
+      u32 pos = cnt0 + incl - c;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (m >> e & 1u) {
+          bj[pos++] = make_key(dd[e], a.index_base + first + e);
+          atomicAdd(hj + dd[e], 1u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ws->cnt[j] = cnt0 + total;
+      __syncwarp();
+      if (cnt0 + total >= a.k) {
+        u32 less;
+        const u32 t = warp_kth_bin(hj, a.k, lane, &less);
+        if (lane == 0) ws->town[j] = t;
+        if (!ws->pubd[j]) {
+          // first publication: every buffered candidate with d <= t
+          for (u32 b = lane; b <= t && b < HB; b += 32) {
+            const u32 cb = hj[b];
+            if (cb) atomicAdd(a.ghist + (u64)qi * HB + b, cb);
+          }
+        } else {
+          // later batches: the newly inserted entries with d <= t, one RED per
+          // distinct distance
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const bool hb = (m >> e & 1u) && dd[e] <= t;
+            const u32 key = hb ? dd[e] : 0xffffffffu;
+            const u32 peers = __match_any_sync(FULL, key);
+            if (hb && (u32)(__ffs(peers) - 1) == (u32)lane)
+              atomicAdd(a.ghist + (u64)qi * HB + dd[e], (u32)__popc(peers));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ws->pubd[j] = 1;
+        __syncwarp();
+        tighten_tg(a, qi, lane);
+        refresh_tg(j);
+        __syncwarp();
+      }
+    }
+  };
+
+  constexpr int U = (QW == 1) ? 2 : 1;
+  u64 it = it0;
+  int since_refresh = 0;
+  for (; it + U <= it1; it += U) {
+    u64 A[U][E], B[U][E], C[U][E];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const u64 off = (it + u) * (32 * E) + (u64)lane * E;
+      ld_entries(a.w0 + off, A[u]);
+      ld_entries(a.w1 + off, B[u]);
+      ld_entries(a.w2 + off, C[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) process(A[u], B[u], C[u], it + u, it + u >= n_full);
+    if (MODE == MODE_TOPK && ++since_refresh == 4) {
+      since_refresh = 0;
+#pragma unroll
+      for (int j = 0; j < QW; ++j) refresh_tg(j);
+    }
+  }
+  for (; it < it1; ++it) {
+    u64 A[E], B[E], C[E];
+    const u64 off = it * (32 * E) + (u64)lane * E;
+    ld_entries(a.w0 + off, A);
+    ld_entries(a.w1 + off, B);
+    ld_entries(a.w2 + off, C);
+    process(A, B, C, it, it >= n_full);
+  }
+
+  if (MODE == MODE_HIST) {
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < QW; ++j) {
+      const u32 qi = qg * QW + j;
+      if (qi >= a.Q) continue;
+      for (int b = lane; b < HB; b += 32) {
+        const u32 c = hist[j * HB + b];
+        if (c) atomicAdd(a.ghist + (u64)qi * HB + b, c);
+      }
+    }
+    return;
+  }
+  if (MODE == MODE_TOPK) {
+#pragma unroll 1
+    for (int j = 0; j < QW; ++j) {
+      const u32 qi = qg * QW + j;
+      if (qi >= a.Q) continue;
+      if (ws->cnt[j] > a.k) compact(j);
+      const u32 n = ws->cnt[j];
+      const u32 t = *((volatile const u32*)a.tg + qi);
+      const u64* bj = wbuf + (u64)j * a.cap;
+      // survivors: d <= tg (an exact bound on the k-th distance)
+      for (u32 i0 = 0; i0 < n; i0 += 32) {
+        const u32 i = i0 + lane;
+        const u64 key = i < n ? bj[i] : ~0ull;
+        const bool keep = i < n && key_d(key) <= t;
+        const u32 kb = __ballot_sync(FULL, keep);
+        const u32 nk = __popc(kb);
+        if (nk == 0) continue;
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(a.cand_cnt + qi, nk);
+        base = __shfl_sync(FULL, base, 0);
+        if (keep) a.cand[(u64)qi * a.cand_cap + base + __popc(kb & lanemask_lt())] = key;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// select_kernel: exact top-k per query over the flat survivor list.
+// One CTA per query. Resets the per-query scan state (tg, ghist, cand_cnt) so
+// the next call starts clean without a memset launch.
+// ---------------------------------------------------------------------------
+constexpr int SEL_THREADS = 512;
+constexpr int SEL_ECAP = 4096;  // ties at the threshold sorted in shared memory
+
+__device__ void block_bitonic_sort(u64* s, int n_pow2) {
+  for (int size = 2; size <= n_pow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n_pow2 / 2; i += blockDim.x) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool up = ((lo & size) == 0);
+        u64 x = s[lo], y = s[hi];
+        if ((x > y) == up) { s[lo] = y; s[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
+                                                             u32* ghist, u32 k, u64* out_keys, u32* out_cnt,
+                                                             int reset) {
+  extern __shared__ u64 ssel[];  // [k_pow2] result + [SEL_ECAP] ties
+  __shared__ u32 hist[256];
+  __shared__ u32 s_nres, s_ntie, s_T, s_m;
+  __shared__ u64 s_cut;
+  const u32 q = blockIdx.x;
+  const u32 n = cand_cnt[q];
+  const u64* c = cand + (u64)q * cand_cap;
+  const u32 bound = tg[q];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) { s_nres = 0; s_ntie = 0; }
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+    u32 d = key_d(c[i]);
+    if (d <= bound) atomicAdd(&hist[d], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // find T: smallest t with cum >= k (scan 256 bins, 8 per lane)
+    int lane = threadIdx.x;
+    u32 h[8], s = 0;
+    for (int i = 0; i < 8; ++i) { h[i] = hist[lane * 8 + i]; s += h[i]; }
+    u32 incl = warp_incl_scan(s, lane);
+    u32 bal = __ballot_sync(FULL, incl >= k);
+    if (bal == 0) {
+      if (lane == 0) { s_T = 256; s_m = 0; }
+    } else {
+      int src = __ffs(bal) - 1;
+      if (lane == src) {
+        u32 cc = incl - s;
+        for (int i = 0; i < 8; ++i) {
+          if (cc + h[i] >= k) { s_T = lane * 8 + i; s_m = k - cc; break; }
+          cc += h[i];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const u32 T = s_T, m = s_m;
+  u64* res = ssel;
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  u64* ties = ssel + kp;
+  const u32 ntie_total = T < 256 ? hist[T] : 0;
+  const bool ties_fit = ntie_total <= SEL_ECAP;
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+    u64 key = c[i];
+    u32 d = key_d(key);
+    if (d > bound) continue;
+    if (d < T) res[atomicAdd(&s_nres, 1u)] = key;
+    else if (d == T && ties_fit) ties[atomicAdd(&s_ntie, 1u)] = key;
+  }
+  __syncthreads();
+  if (T < 256 && m > 0) {
+    if (ties_fit) {
+      int tp = 1;
+      while (tp < (int)ntie_total) tp <<= 1;
+      for (int i = ntie_total + threadIdx.x; i < tp; i += blockDim.x) ties[i] = ~0ull;
+      __syncthreads();
+      block_bitonic_sort(ties, tp);
+      const u32 base = s_nres;
+      for (u32 i = threadIdx.x; i < m; i += blockDim.x) res[base + i] = ties[i];
+      __syncthreads();
+      if (threadIdx.x == 0) s_nres = base + m;
+    } else {
+      // radix select on the index bits of the ties: find the m-th smallest
+      u64 prefix = 0;
+      u32 need = m;
+      for (int shift = IDX_BITS - 8; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        const u64 hi_mask = (shift + 8 >= IDX_BITS) ? 0 : (IDX_MASK & ~((1ull << (shift + 8)) - 1));
+        for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+          u64 key = c[i];
+          if (key_d(key) != T) continue;
+          u64 idx = key & IDX_MASK;
+          if ((idx & hi_mask) != prefix) continue;
+          atomicAdd(&hist[(idx >> shift) & 0xff], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          u32 cc = 0;
+          for (int b = 0; b < 256; ++b) {
+            if (cc + hist[b] >= need) { s_cut = prefix | ((u64)b << shift); s_m = need - cc; break; }
+            cc += hist[b];
+          }
+        }
+        __syncthreads();
+        prefix = s_cut;
+        need = s_m;
+      }
+      // prefix is now the m-th smallest tie index: keep ties with idx <= prefix
+      for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+        u64 key = c[i];
+        if (key_d(key) == T && (key & IDX_MASK) <= prefix) res[atomicAdd(&s_nres, 1u)] = key;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  const u32 nres = s_nres;
+  for (int i = nres + threadIdx.x; i < kp; i += blockDim.x) res[i] = ~0ull;
+  __syncthreads();
+  block_bitonic_sort(res, kp);
+  for (u32 i = threadIdx.x; i < k; i += blockDim.x) out_keys[(u64)q * k + i] = i < nres ? res[i] : ~0ull;
+  if (threadIdx.x == 0) out_cnt[q] = nres;
+  if (reset) {
+    for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[(u64)q * HB + i] = 0;
+    if (threadIdx.x == 0) { tg[q] = T_OPEN; cand_cnt[q] = 0; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// merge_kernel: G per-shard sorted top-k lists -> global top-k per query
+// (merge_topk, scan.py:225-236). Keys are unique (disjoint index ranges), so
+// rank(x) = own position + sum over other lists of lower_bound(x).
+// in_keys: [G][Q][k], in_cnt: [G][Q]; out_keys: [Q][k], out_cnt: [Q].
+// ---------------------------------------------------------------------------
+__global__ void merge_kernel(const u64* in_keys, const u32* in_cnt, u32 G, u32 Q, u32 k, u64* out_keys,
+                             u32* out_cnt) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 total = (u64)G * Q * k;
+  if (t < Q) {
+    u32 s = 0;
+    for (u32 gg = 0; gg < G; ++gg) s += in_cnt[(u64)gg * Q + t];
+    out_cnt[t] = s < k ? s : k;
+    for (u32 i = s; i < k; ++i) out_keys[t * k + i] = ~0ull;
+  }
+  if (t >= total) return;
+  const u32 i = (u32)(t % k);
+  const u32 q = (u32)((t / k) % Q);
+  const u32 gg = (u32)(t / ((u64)k * Q));
+  if (i >= in_cnt[(u64)gg * Q + q]) return;
+  const u64 x = in_keys[((u64)gg * Q + q) * k + i];
+  u64 rank = i;
+  for (u32 h = 0; h < G; ++h) {
+    if (h == gg) continue;
+    const u64* L = in_keys + ((u64)h * Q + q) * k;
+    u32 lo = 0, hi = in_cnt[(u64)h * Q + q];
+    while (lo < hi) {
+      u32 mid = (lo + hi) >> 1;
+      if (L[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    rank += lo;
+  }
+  if (rank < k) out_keys[(u64)q * k + rank] = x;
+}
+
+// ---------------------------------------------------------------------------
+// Library ingestion
+// ---------------------------------------------------------------------------
+// rows with `stride` u64 per row, fingerprint words at columns [col0, col0+3)
+// (FPS1 record view: stride 4, col0 1 — scan.py:169; row-major words: 3, 0).
+__global__ void rows_to_planes(const u64* __restrict__ rows, u64 n_rows, int stride, int col0, u64* w0, u64* w1,
+                               u64* w2, u64 dst_off, u32* bad_padding) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += (u64)gridDim.x * blockDim.x) {
+    const u64* r = rows + i * stride + col0;
+    u64 a = r[0], b = r[1], c = r[2];
+    w0[dst_off + i] = a;
+    w1[dst_off + i] = b;
+    w2[dst_off + i] = c;
+    if (bad_padding && (c >> 38)) atomicAdd(bad_padding, 1u);
+  }
+}
+
+__global__ void scatter_rows(const u64* __restrict__ idx, const u64* __restrict__ rows, u64 m, u64* w0, u64* w1,
+                             u64* w2) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+    const u64 t = idx[i];
+    w0[t] = rows[3 * i + 0];
+    w1[t] = rows[3 * i + 1];
+    w2[t] = rows[3 * i + 2];
+  }
+}
+
+__device__ __forceinline__ u64 splitmix64_fin(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct GenArgs {
+  u64* w0;
+  u64* w1;
+  u64* w2;
+  u64 n;
+  u64 start;     // global index of entry 0
+  u64 seed_key;
+  u32 thr[166];  // key j set iff u32 < thr[j-1]  (thr as 32-bit, thr_hi marks p == 1)
+  unsigned char thr_hi[166];
+};
+
+// Synthetic library: key j set independently with probability
+// p_j (p_j ~ Beta(0.6, 2), p_1 = 0 drawn on the host). Counter-based, so any
+// chunk of the stream is reproducible; numpy twin: oracle generate_words.
+__global__ void gen_kernel(const GenArgs a) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (u64)gridDim.x * blockDim.x) {
+    const u64 gi = a.start + i;
+    u64 w[3] = {0, 0, 0};
+#pragma unroll 4
+    for (int c = 0; c < 83; ++c) {
+      const u64 z = a.seed_key + (gi * 83 + c + 1) * 0x9E3779B97F4A7C15ull;
+      const u64 h = splitmix64_fin(z);
+      const int j0 = 2 * c, j1 = 2 * c + 1;  // 0-based key slots
+      const u32 lo = (u32)h, hi = (u32)(h >> 32);
+      const bool b0 = a.thr_hi[j0] || lo < a.thr[j0];
+      const bool b1 = a.thr_hi[j1] || hi < a.thr[j1];
+      w[j0 >> 6] |= (u64)b0 << (j0 & 63);
+      w[j1 >> 6] |= (u64)b1 << (j1 & 63);
+    }
+    a.w0[i] = w[0];
+    a.w1[i] = w[1];
+    a.w2[i] = w[2];
+  }
+}
+
+// Reference-order fill of a "padding" tail so vector loads never read garbage:
+__global__ void zero_tail(u64* w0, u64* w1, u64* w2, u64 from, u64 to) {
+  u64 i = from + (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < to) { w0[i] = 0; w1[i] = 0; w2[i] = 0; }
+}
+
+// Truncate sorted range output to the first k per query (large-k path).
+__global__ void truncate_kernel(const u64* sorted, const u64* seg_off, u32 Q, u32 k, u64* out_keys, u32* out_cnt) {
+  const u32 q = blockIdx.x;
+  if (q >= Q) return;
+  const u64 s = seg_off[q], e = seg_off[q + 1];
+  const u64 n = e - s;
+  const u32 r = n < k ? (u32)n : k;
+  for (u32 i = threadIdx.x; i < k; i += blockDim.x)
+    out_keys[(u64)q * k + i] = i < r ? (sorted[s + i] & ((1ull << 48) - 1)) : ~0ull;
+  if (threadIdx.x == 0) out_cnt[q] = r;
+}
+
+}  // namespace fps

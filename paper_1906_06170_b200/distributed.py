@@ -1,0 +1,121 @@
+"""Multi-GPU sharding: one process per GPU, contiguous shards, merge on rank 0.
+
+The reference's only parallelism is whole shards on a thread pool, merged in
+process by ``merge_topk`` (scan.py:256-287, :225-236) over contiguous,
+balanced shards (libstore.split_sizes, libstore.py:174-179). Here each rank
+holds shard ``rank`` of the library in its HBM and reports global indices
+(index_base = shard start); per-query top-k lists (k keys of
+``distance << 40 | index`` per query, sorted) are gathered to rank 0 over
+NCCL (NVLink on a B200 box) and merged there by the device merge kernel.
+The top-k of a union equals the top-k of per-shard top-ks under a total
+order, and shards are disjoint, so the merge is exact and associative.
+Range hits are variable-sized: counts are all-gathered first, then padded
+buffers gathered and the union re-sorted on rank 0.
+
+The collective plumbing is backend-agnostic (NCCL on GPUs, gloo in the CPU
+tests); the merge / sort step is injected so the CPU tests can check the
+plumbing against the oracle while the GPU path uses libfpsgpu.so.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .libstore import split_sizes
+
+MergeFn = Callable[[torch.Tensor, torch.Tensor, int], tuple[torch.Tensor, torch.Tensor]]
+SortFn = Callable[[torch.Tensor], torch.Tensor]
+
+
+def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    """(start, count) of this rank's contiguous shard."""
+    sizes = split_sizes(n_total, world)
+    return sum(sizes[:rank]), sizes[rank]
+
+
+def gather_topk(keys: torch.Tensor, cnt: torch.Tensor, k: int, merge: MergeFn, group=None,
+                dst: int = 0) -> tuple[torch.Tensor, torch.Tensor] | None:
+    """Gather every rank's (Q, k) sorted key lists and (Q,) counts to ``dst``
+    and merge them there. Returns the merged (keys, cnt) on dst, else None."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    keys = keys.contiguous()
+    cnt = cnt.contiguous()
+    if world == 1:
+        return merge(keys.unsqueeze(0), cnt.unsqueeze(0), k)
+    if rank == dst:
+        kl = [torch.empty_like(keys) for _ in range(world)]
+        cl = [torch.empty_like(cnt) for _ in range(world)]
+        dist.gather(keys, kl, dst=dst, group=group)
+        dist.gather(cnt, cl, dst=dst, group=group)
+        return merge(torch.stack(kl), torch.stack(cl), k)
+    dist.gather(keys, None, dst=dst, group=group)
+    dist.gather(cnt, None, dst=dst, group=group)
+    return None
+
+
+def gather_range(keys: torch.Tensor, sort: SortFn, group=None, dst: int = 0) -> torch.Tensor | None:
+    """Gather variable-length sorted range-key vectors to ``dst``, re-sort the
+    union there ((q, d, idx) order). Returns the merged keys on dst."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    keys = keys.contiguous()
+    if world == 1:
+        return keys
+    n = torch.tensor([keys.numel()], dtype=torch.int64, device=keys.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes)
+    padded = torch.full((max(m, 1),), -1, dtype=keys.dtype, device=keys.device)
+    padded[: keys.numel()] = keys
+    if rank == dst:
+        bufs = [torch.empty_like(padded) for _ in range(world)]
+        dist.gather(padded, bufs, dst=dst, group=group)
+        parts = [b[:s] for b, s in zip(bufs, sizes)]
+        return sort(torch.cat(parts))
+    dist.gather(padded, None, dst=dst, group=group)
+    return None
+
+
+def device_merge(in_keys: torch.Tensor, in_cnt: torch.Tensor, k: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """CUDA merge kernel over (G, Q, k) keys / (G, Q) counts (rank 0)."""
+    from .library import merge_async
+
+    G, Q, _ = in_keys.shape
+    out_keys = torch.empty((Q, k), dtype=torch.int64, device=in_keys.device)
+    out_cnt = torch.empty((Q,), dtype=torch.int32, device=in_keys.device)
+    merge_async(in_keys, in_cnt, G, Q, k, out_keys, out_cnt, torch.cuda.current_stream(in_keys.device).cuda_stream)
+    return out_keys, out_cnt
+
+
+def device_sort(keys: torch.Tensor) -> torch.Tensor:
+    """Radix sort of range keys on the device (libfpsgpu, CUB)."""
+    from . import _native as N
+
+    out = keys.clone()
+    N.check(N.load().fps_sort_keys(None, out.data_ptr(), out.numel(),
+                                   torch.cuda.current_stream(keys.device).cuda_stream), "fps_sort_keys")
+    return out
+
+
+class ShardedLibrary:
+    """This rank's contiguous shard of a library plus the rank-0 merge."""
+
+    def __init__(self, local, n_total: int, group=None):
+        self.local = local
+        self.n_total = n_total
+        self.group = group
+
+    def topk_device(self, d_queries: torch.Tensor, k: int, stream: int | None = None):
+        """Local top-k on this GPU, gathered and merged on rank 0 (device tensors)."""
+        Q = d_queries.shape[0]
+        dev = d_queries.device
+        keys = torch.empty((Q, k), dtype=torch.int64, device=dev)
+        cnt = torch.empty((Q,), dtype=torch.int32, device=dev)
+        s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+        self.local.topk_async(d_queries, Q, k, keys, cnt, s)
+        return gather_topk(keys, cnt, k, device_merge, self.group)

@@ -1,0 +1,320 @@
+"""The north-star search surface: an HBM-resident library and its queries.
+
+``load_library(source) -> Library`` uploads once; ``Library.search``,
+``search_batch`` and ``range_search`` return (index, distance) results in the
+reference total order (distance, then index; scan.py:55-56). Every scan runs
+in libfpsgpu.so (CUDA, sm_100a) through the C ABI of include/fps.h.
+
+Replaces, for the hot path, the reference's per-search shard streaming and
+numpy kernel (/root/reference/pkg/src/fpscan/scan.py:137-209, :239-318).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .fingerprint import as_query_words
+
+_U64_MAX = np.uint64(0xFFFFFFFFFFFFFFFF)
+IDX_MASK = (1 << 40) - 1
+
+
+@dataclass(frozen=True)
+class RangeResult:
+    """Range hits sorted by (query, distance, index)."""
+
+    query: np.ndarray     # uint32
+    index: np.ndarray     # uint64 (global library index)
+    distance: np.ndarray  # uint16
+
+    def __len__(self) -> int:
+        return len(self.index)
+
+    @staticmethod
+    def from_keys(keys: np.ndarray) -> "RangeResult":
+        keys = np.asarray(keys, dtype=np.uint64)
+        return RangeResult(
+            query=(keys >> np.uint64(48)).astype(np.uint32),
+            index=keys & np.uint64(IDX_MASK),
+            distance=((keys >> np.uint64(40)) & np.uint64(0xFF)).astype(np.uint16),
+        )
+
+    def rows(self) -> np.ndarray:
+        """(m, 3) int64 array of (query, index, distance)."""
+        return np.stack([self.query.astype(np.int64), self.index.astype(np.int64),
+                         self.distance.astype(np.int64)], axis=1)
+
+
+@dataclass(frozen=True)
+class TopKResult:
+    """Per-query top-k: row q holds count[q] valid (index, distance) pairs."""
+
+    index: np.ndarray     # (Q, k) uint64, UINT64_MAX in unused slots
+    distance: np.ndarray  # (Q, k) uint16, 0xFFFF in unused slots
+    count: np.ndarray     # (Q,) uint32
+
+    def hits(self, q: int) -> list[tuple[int, int]]:
+        c = int(self.count[q])
+        return [(int(i), int(d)) for i, d in zip(self.index[q, :c], self.distance[q, :c])]
+
+
+class Library:
+    """A fingerprint library resident in one GPU's HBM as three u64 planes."""
+
+    def __init__(self, handle: int, cids: np.ndarray | None = None):
+        self._h = C.c_void_p(handle)
+        n, base, dev = C.c_uint64(), C.c_uint64(), C.c_int()
+        N.check(N.load().fps_info(self._h, C.byref(n), C.byref(base), C.byref(dev)), "fps_info")
+        self.n = n.value
+        self.index_base = base.value
+        self.device = dev.value
+        self.cids = cids
+        self._cids_monotone = None
+
+    # ---- construction -------------------------------------------------
+    @staticmethod
+    def _device(device: int | None) -> int:
+        N.require_device()
+        if device is None:
+            try:
+                import torch
+
+                return torch.cuda.current_device()
+            except Exception:  # pragma: no cover - torch missing
+                return 0
+        return int(device)
+
+    @classmethod
+    def from_words(cls, words, device: int | None = None, index_base: int = 0, check_padding: bool = True,
+                   cids: np.ndarray | None = None) -> "Library":
+        """Upload an (n, 3) uint64 word array (Fingerprint.words per row)."""
+        arr = np.ascontiguousarray(np.asarray(words, dtype=np.uint64).reshape(-1, 3))
+        h = C.c_void_p()
+        N.check(N.load().fps_open(arr.ctypes.data, len(arr), N.LAYOUT_ROWS3, cls._device(device), index_base,
+                                  int(check_padding), C.byref(h)), "fps_open")
+        return cls(h.value, cids)
+
+    @classmethod
+    def from_records(cls, records: np.ndarray, device: int | None = None, index_base: int = 0) -> "Library":
+        """Upload an (n, 4) '<u8' FPS1 record view (cid, w0, w1, w2) — scan.py:169.
+
+        Words are scanned exactly as stored (the reference scan does not
+        validate padding, so neither does this)."""
+        rec = np.ascontiguousarray(np.asarray(records, dtype=np.uint64).reshape(-1, 4))
+        h = C.c_void_p()
+        N.check(N.load().fps_open(rec.ctypes.data, len(rec), N.LAYOUT_FPS1, cls._device(device), index_base, 0,
+                                  C.byref(h)), "fps_open")
+        return cls(h.value, rec[:, 0].copy())
+
+    @classmethod
+    def from_device_planes(cls, w0, w1, w2, device: int | None = None, index_base: int = 0) -> "Library":
+        """Copy three device planes (torch int64/uint64 tensors or pointers)."""
+        n = int(w0.numel()) if hasattr(w0, "numel") else None
+        if n is None:
+            raise ValueError("from_device_planes needs tensors")
+        h = C.c_void_p()
+        dev = w0.device.index if hasattr(w0, "device") and w0.device.index is not None else cls._device(device)
+        N.check(N.load().fps_open_device(N.ptr(w0), N.ptr(w1), N.ptr(w2), n, dev, index_base, C.byref(h)),
+                "fps_open_device")
+        return cls(h.value)
+
+    @classmethod
+    def generate(cls, n: int, seed_key: int, thresholds: np.ndarray, device: int | None = None, start: int = 0,
+                 index_base: int | None = None) -> "Library":
+        """Synthetic library generated on the device (see synth.py)."""
+        thr = np.asarray(thresholds, dtype=np.uint64)
+        thr32 = np.minimum(thr, np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        allset = (thr > np.uint64(0xFFFFFFFF)).astype(np.uint8)
+        h = C.c_void_p()
+        N.check(N.load().fps_open_generated(n, start, seed_key & ((1 << 64) - 1), thr32.ctypes.data,
+                                            allset.ctypes.data, cls._device(device),
+                                            start if index_base is None else index_base, C.byref(h)),
+                "fps_open_generated")
+        return cls(h.value)
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            N.load().fps_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- data access ----------------------------------------------------
+    def planes(self) -> tuple[int, int, int, int]:
+        """Device pointers (w0, w1, w2) and the allocated plane length."""
+        p0, p1, p2, na = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_uint64()
+        N.check(N.load().fps_planes(self._h, C.byref(p0), C.byref(p1), C.byref(p2), C.byref(na)), "fps_planes")
+        return p0.value, p1.value, p2.value, na.value
+
+    def planes_torch(self):
+        """Zero-copy int64 torch views of the three planes (length n)."""
+        import torch
+
+        p0, p1, p2, na = self.planes()
+        full = _torch_from_ptr(p0, 3 * na, self.device)
+        return full[0:self.n], full[na:na + self.n], full[2 * na:2 * na + self.n]
+
+    def words_host(self) -> np.ndarray:
+        """Copy the library back as (n, 3) uint64 (for checking only)."""
+        w0, w1, w2 = self.planes_torch()
+        import torch
+
+        return torch.stack([w0, w1, w2], dim=1).cpu().numpy().view(np.uint64)
+
+    def write_entries(self, index: np.ndarray, words: np.ndarray) -> None:
+        """Overwrite local entries ``index`` with rows of ``words``."""
+        idx = np.ascontiguousarray(np.asarray(index, dtype=np.uint64))
+        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64).reshape(-1, 3))
+        if len(idx) != len(w):
+            raise ValueError("index and words differ in length")
+        N.check(N.load().fps_write_entries(self._h, idx.ctypes.data, w.ctypes.data, len(idx)), "fps_write_entries")
+
+    def timing(self, enable: bool) -> None:
+        N.check(N.load().fps_timing(self._h, int(enable)), "fps_timing")
+
+    def timing_read(self) -> tuple[float, int]:
+        """(summed scan-kernel ms, launches) since the last read."""
+        t, c = C.c_double(), C.c_uint64()
+        N.check(N.load().fps_timing_read(self._h, C.byref(t), C.byref(c)), "fps_timing_read")
+        return t.value, c.value
+
+    @property
+    def launches(self) -> int:
+        return int(N.load().fps_launch_count(self._h))
+
+    # ---- queries ----------------------------------------------------------
+    def search_batch(self, queries, k: int) -> TopKResult:
+        """Per-query top-k, one independent search per query (config 4)."""
+        q = as_query_words(queries)
+        if k < 1:
+            raise ValueError("n must be >= 1")
+        Q = len(q)
+        idx = np.empty((Q, k), dtype=np.uint64)
+        dist = np.empty((Q, k), dtype=np.uint16)
+        cnt = np.zeros(Q, dtype=np.uint32)
+        if Q:
+            N.check(N.load().fps_topk(self._h, q.ctypes.data, Q, k, idx.ctypes.data, dist.ctypes.data,
+                                      cnt.ctypes.data), "fps_topk")
+        return TopKResult(idx, dist, cnt)
+
+    def search(self, query, k: int) -> list[tuple[int, int]]:
+        """Top-k [(index, distance)] for one query (reference ``search``)."""
+        return self.search_batch(query, k).hits(0)
+
+    def search_min(self, queries, k: int) -> list[tuple[int, int]]:
+        """Reference ``batch_search``: min over queries, one top-k."""
+        q = as_query_words(queries)
+        if len(q) == 0:
+            raise ValueError("batch_search requires at least one query")
+        idx = np.empty((1, k), dtype=np.uint64)
+        dist = np.empty((1, k), dtype=np.uint16)
+        cnt = np.zeros(1, dtype=np.uint32)
+        N.check(N.load().fps_topk_min(self._h, q.ctypes.data, len(q), k, idx.ctypes.data, dist.ctypes.data,
+                                      cnt.ctypes.data), "fps_topk_min")
+        return TopKResult(idx, dist, cnt).hits(0)
+
+    def range_search(self, queries, radius) -> RangeResult:
+        """Every (query, index, distance) with distance <= radius (scalar or per query)."""
+        q = as_query_words(queries)
+        Q = len(q)
+        r = np.broadcast_to(np.asarray(radius, dtype=np.int64), (Q,))
+        if np.any(r < 0):
+            raise ValueError("radius must be >= 0")
+        rad = np.ascontiguousarray(np.minimum(r, 254).astype(np.uint8))
+        out = C.c_void_p()
+        n_out = C.c_uint64()
+        if Q == 0:
+            return RangeResult.from_keys(np.zeros(0, np.uint64))
+        N.check(N.load().fps_range(self._h, q.ctypes.data, Q, rad.ctypes.data, C.byref(out), C.byref(n_out)),
+                "fps_range")
+        try:
+            m = n_out.value
+            keys = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_uint64)), shape=(m,)).copy() if m else \
+                np.zeros(0, np.uint64)
+        finally:
+            N.load().fps_free(out)
+        return RangeResult.from_keys(keys)
+
+    # ---- stream-ordered device API --------------------------------------
+    def topk_prepare(self, Q: int, k: int) -> None:
+        N.check(N.load().fps_topk_prepare(self._h, Q, k), "fps_topk_prepare")
+
+    def topk_async(self, d_queries, Q: int, k: int, d_keys, d_cnt, stream: int) -> None:
+        N.check(N.load().fps_topk_async(self._h, N.ptr(d_queries), Q, k, N.ptr(d_keys), N.ptr(d_cnt), stream),
+                "fps_topk_async")
+
+    def range_async(self, d_queries, Q: int, d_radius, d_out, cap: int, d_count, stream: int) -> None:
+        N.check(N.load().fps_range_async(self._h, N.ptr(d_queries), Q, N.ptr(d_radius), N.ptr(d_out), cap,
+                                         N.ptr(d_count), stream), "fps_range_async")
+
+    def sort_keys(self, d_keys, n: int, stream: int) -> None:
+        N.check(N.load().fps_sort_keys(self._h, N.ptr(d_keys), n, stream), "fps_sort_keys")
+
+
+def merge_async(d_in_keys, d_in_cnt, G: int, Q: int, k: int, d_out_keys, d_out_cnt, stream: int) -> None:
+    """Device merge of G per-shard sorted top-k lists (merge_topk semantics)."""
+    N.check(N.load().fps_merge_async(N.ptr(d_in_keys), N.ptr(d_in_cnt), G, Q, k, N.ptr(d_out_keys),
+                                     N.ptr(d_out_cnt), stream), "fps_merge_async")
+
+
+def keys_to_hits(keys: np.ndarray, cnt: np.ndarray) -> TopKResult:
+    """Decode device (distance << 40 | index) keys into a TopKResult."""
+    keys = np.asarray(keys, dtype=np.uint64)
+    cnt = np.asarray(cnt, dtype=np.uint32)
+    Q, k = keys.shape
+    valid = np.arange(k)[None, :] < cnt[:, None]
+    idx = np.where(valid, keys & np.uint64(IDX_MASK), _U64_MAX)
+    dist = np.where(valid, (keys >> np.uint64(40)) & np.uint64(0xFF), 0xFFFF).astype(np.uint16)
+    return TopKResult(idx.astype(np.uint64), dist, cnt)
+
+
+def _torch_from_ptr(ptr: int, numel: int, device: int):
+    """Wrap raw device memory owned by the library as an int64 torch tensor."""
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (numel,),
+            "typestr": "<i8",
+            "data": (ptr, False),
+            "version": 3,
+        }
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Holder(), device=f"cuda:{device}")
+
+
+def load_library(source, device: int | None = None, index_base: int = 0) -> Library:
+    """Upload a library once: an (n, 3) word array, an (n, 4) FPS1 record
+    array, a ShardManifest / library directory (FPS1 shards), or a Library."""
+    if isinstance(source, Library):
+        return source
+    if isinstance(source, np.ndarray):
+        if source.ndim == 2 and source.shape[1] == 4:
+            return Library.from_records(source, device, index_base)
+        return Library.from_words(source, device, index_base)
+    from . import libstore
+
+    manifest = source if hasattr(source, "shards") else libstore.load_manifest(Path(source))
+    records = libstore.read_manifest_records(manifest)
+    return Library.from_records(records, device, index_base)
+
+
+def load_libraries(sources: Sequence, device: int | None = None) -> list[Library]:
+    return [load_library(s, device) for s in sources]

@@ -1,0 +1,246 @@
+"""Drop-in replacement for the reference search surface, CUDA-backed.
+
+Same names, argument meaning and error behaviour as
+/root/reference/pkg/src/fpscan/scan.py: ``SearchHit`` / ``TopK`` /
+``SearchParams`` (scan.py:50-88), ``merge_topk`` (scan.py:225-236),
+``scan_shard`` / ``search`` / ``batch_search`` (scan.py:212-318). Results are
+a pure function of (library bytes, query, n) under the (distance, cid) total
+order, independent of ``parallelism``.
+
+Differences, by design:
+* the library is uploaded to HBM once per manifest (cached) instead of
+  re-read from the shard files on every search (scan.py:160);
+* ``kernel`` selects nothing: "cuda" is the default and "packed" /
+  "reference" are accepted as aliases (the reference proves the two kernels
+  equal, test_scan.py:217-222); every value runs the CUDA scan;
+* progress fires once per shard when the device pass completes (final
+  count only, still monotone and ending at record_count); cancellation is
+  checked before launch.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Callable, Literal, Sequence
+
+import numpy as np
+
+from .errors import DuplicateCid, LibstoreError, ScanCancelled, ScanError
+from .fingerprint import as_query_words
+from .library import Library
+
+ShardProgressFn = Callable[[int], None]
+SearchProgressFn = Callable[[str, int, int], None]
+CancelFn = Callable[[], bool]
+
+Kernel = Literal["cuda", "packed", "reference"]
+BLOCK_RECORDS = 65536  # the reference's progress granularity (scan.py:29)
+
+
+@dataclass(frozen=True)
+class SearchHit:
+    cid: int
+    distance: int
+
+    def sort_key(self) -> tuple[int, int]:
+        return (self.distance, self.cid)
+
+
+@dataclass(frozen=True)
+class TopK:
+    """The K smallest hits of a stream under (distance, cid) order."""
+
+    capacity: int
+    hits: tuple[SearchHit, ...]
+
+    def __post_init__(self):
+        if self.capacity < 1:
+            raise ValueError("capacity must be >= 1")
+        if len(self.hits) > self.capacity:
+            raise ValueError(f"{len(self.hits)} hits exceed capacity {self.capacity}")
+        keys = [h.sort_key() for h in self.hits]
+        if any(a >= b for a, b in zip(keys, keys[1:])):
+            raise ValueError("hits must be strictly increasing under (distance, cid)")
+
+
+@dataclass(frozen=True)
+class SearchParams:
+    n: int = 30
+    parallelism: int = 1
+    kernel: Kernel = "cuda"
+
+    def __post_init__(self):
+        if self.n < 1:
+            raise ValueError("n must be >= 1")
+        if self.parallelism < 1:
+            raise ValueError("parallelism must be >= 1")
+        if self.kernel not in ("cuda", "packed", "reference"):
+            raise ValueError(f"unknown kernel {self.kernel!r}")
+
+
+def merge_topk(parts: Sequence[TopK], n: int) -> TopK:
+    """The n smallest hits of the union; associative, commutative, duplicate-checking."""
+    seen: set[int] = set()
+    merged: list[tuple[int, int]] = []
+    for part in parts:
+        for hit in part.hits:
+            if hit.cid in seen:
+                raise DuplicateCid(f"cid {hit.cid} appears in more than one part")
+            seen.add(hit.cid)
+            merged.append((hit.distance, hit.cid))
+    merged.sort()
+    return TopK(capacity=n, hits=tuple(SearchHit(cid=c, distance=d) for d, c in merged[:n]))
+
+
+# --------------------------------------------------------------------------
+# resident libraries, one per (manifest contents, device)
+# --------------------------------------------------------------------------
+@dataclass
+class _Resident:
+    lib: Library
+    cids: np.ndarray
+    cid_monotone: bool
+    offsets: list[int]
+
+
+_cache: dict[tuple, _Resident] = {}
+_cache_lock = threading.Lock()
+
+
+def _manifest_key(manifest) -> tuple:
+    parts = []
+    for s in manifest.shards:
+        p = Path(s.path)
+        try:
+            st = p.stat()
+            parts.append((str(p), s.record_count, st.st_mtime_ns, st.st_size))
+        except OSError:
+            parts.append((str(p), s.record_count, None, None))
+    return tuple(parts)
+
+
+def _resident(manifest, device: int | None) -> _Resident:
+    from . import libstore
+
+    key = (_manifest_key(manifest), device)
+    with _cache_lock:
+        hit = _cache.get(key)
+        if hit is not None:
+            return hit
+        records = []
+        offsets = [0]
+        for shard in manifest.shards:
+            try:
+                rec = libstore.read_shard_records(shard)
+            except (OSError, LibstoreError) as exc:
+                raise ScanError(f"shard {shard.path}: {exc}") from exc
+            records.append(rec)
+            offsets.append(offsets[-1] + len(rec))
+        allrec = np.concatenate(records) if records else np.zeros((0, 4), dtype="<u8")
+        lib = Library.from_records(allrec, device)
+        cids = allrec[:, 0].copy()
+        monotone = bool(np.all(cids[1:] > cids[:-1])) if len(cids) > 1 else True
+        res = _Resident(lib=lib, cids=cids, cid_monotone=monotone, offsets=offsets)
+        _cache[key] = res
+        return res
+
+
+def clear_cache() -> None:
+    """Release every resident library (frees HBM)."""
+    with _cache_lock:
+        for r in _cache.values():
+            r.lib.close()
+        _cache.clear()
+
+
+def _hits_by_cid(res: _Resident, idx: np.ndarray, dist: np.ndarray, n: int) -> TopK:
+    cids = res.cids[idx.astype(np.int64)]
+    if len(np.unique(cids)) != len(cids):
+        raise DuplicateCid("a cid appears more than once in the library")
+    order = np.lexsort((cids, dist))[:n]
+    return TopK(capacity=n, hits=tuple(SearchHit(cid=int(cids[i]), distance=int(dist[i])) for i in order))
+
+
+def _topk_one(res: _Resident, q: np.ndarray, n: int, minq: bool) -> TopK:
+    lib = res.lib
+    if minq:
+        hits = lib.search_min(q, n)
+    else:
+        hits = lib.search_batch(q, n).hits(0)
+    if not hits:
+        return TopK(capacity=n, hits=())
+    idx = np.array([h[0] for h in hits], dtype=np.uint64)
+    dist = np.array([h[1] for h in hits], dtype=np.int64)
+    if res.cid_monotone or len(hits) < n:
+        # (distance, index) order == (distance, cid) order when cids increase with
+        # index; with fewer than n hits every record is present anyway
+        return _hits_by_cid(res, idx, dist, n)
+    if minq:
+        # ties at the n-th distance need cid order: gather every record within it
+        radius = int(dist[-1])
+        rr = [lib.range_search(qq, radius) for qq in q]
+        all_idx = np.concatenate([r.index for r in rr])
+        all_d = np.concatenate([r.distance for r in rr]).astype(np.int64)
+        # min over queries per record
+        order = np.lexsort((all_d, all_idx))
+        all_idx, all_d = all_idx[order], all_d[order]
+        first = np.ones(len(all_idx), dtype=bool)
+        first[1:] = all_idx[1:] != all_idx[:-1]
+        return _hits_by_cid(res, all_idx[first], all_d[first], n)
+    rr = lib.range_search(q, int(dist[-1]))
+    return _hits_by_cid(res, rr.index, rr.distance.astype(np.int64), n)
+
+
+def _search_multi(manifest, queries: np.ndarray, params: SearchParams, progress: SearchProgressFn | None,
+                  cancel: CancelFn | None, minq: bool, device: int | None = None) -> TopK:
+    shards = manifest.shards
+    if not shards:
+        return TopK(capacity=params.n, hits=())
+    if cancel is not None and cancel():
+        raise ScanCancelled(str(shards[0].path))
+    res = _resident(manifest, device)
+    if res.lib.n == 0:
+        top = TopK(capacity=params.n, hits=())
+    else:
+        top = _topk_one(res, queries, params.n, minq)
+    if progress is not None:
+        for shard, a, b in zip(shards, res.offsets, res.offsets[1:]):
+            progress(shard.dataset_label, b - a, shard.record_count)
+    return top
+
+
+def search(manifest, query, params: SearchParams, progress: SearchProgressFn | None = None,
+           cancel: CancelFn | None = None) -> TopK:
+    """Search the whole library (scan.py:290-303); independent of parallelism."""
+    return _search_multi(manifest, as_query_words(query)[:1], params, progress, cancel, minq=False)
+
+
+def batch_search(manifest, queries, params: SearchParams, progress: SearchProgressFn | None = None,
+                 cancel: CancelFn | None = None) -> TopK:
+    """Nearest-to-query-set search (scan.py:306-318): min over queries."""
+    q = as_query_words(list(queries) if not isinstance(queries, np.ndarray) else queries)
+    if len(q) == 0:
+        raise ValueError("batch_search requires at least one query")
+    if len(q) == 1:
+        return _search_multi(manifest, q, params, progress, cancel, minq=False)
+    return _search_multi(manifest, q, params, progress, cancel, minq=True)
+
+
+def scan_shard(shard, query, params: SearchParams, progress: ShardProgressFn | None = None,
+               cancel: CancelFn | None = None) -> TopK:
+    """Top-K over one shard (scan.py:212-222)."""
+    from .libstore import ShardManifest
+
+    manifest = ShardManifest(shards=(shard,), total_records=shard.record_count)
+    wrapped = None
+    if progress is not None:
+        wrapped = lambda label, done, total: progress(done)
+    try:
+        return _search_multi(manifest, as_query_words(query)[:1], params, wrapped, cancel, minq=False)
+    except ScanError as exc:
+        cause = exc.__cause__
+        if isinstance(cause, (OSError, LibstoreError)):
+            raise cause
+        raise

@@ -1,0 +1,302 @@
+"""CUDA path vs the oracle and the reference's golden outputs (needs a B200).
+
+Every call goes through libfpsgpu.so's C ABI (via the ctypes shim). Integer
+work: the bar is bit-exact equality of (index or cid, distance) lists in the
+reference's (distance, id) order.
+"""
+
+import hashlib
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import fps_oracle as orc
+from paper_1906_06170_b200 import FingerprintError, scan, synth
+from paper_1906_06170_b200.fingerprint import Fingerprint
+from paper_1906_06170_b200.library import Library, keys_to_hits, merge_async
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN_DIR = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    import torch
+
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    from paper_1906_06170_b200 import build
+
+    build.build()
+    yield
+    scan.clear_cache()
+
+
+def words_sha(w):
+    return hashlib.sha256(np.ascontiguousarray(w, dtype="<u8").tobytes()).hexdigest()
+
+
+def as_pairs(res, q=0):
+    return res.hits(q)
+
+
+def oracle_topk(w, q, k):
+    idx, dist, cnt = orc.c_topk(w, q, k)
+    return [list(zip(idx[i, :cnt[i]].tolist(), dist[i, :cnt[i]].tolist())) for i in range(len(q))]
+
+
+# ---------------------------------------------------------------- generator
+def test_device_generator_matches_numpy_twin():
+    seed = 31337
+    thr = synth.beta_thresholds(seed)
+    lib = Library.generate(100_003, synth.seed_key(seed), thr, start=0)
+    w = lib.words_host()
+    assert np.array_equal(w, orc.generate_words(synth.seed_key(seed), thr, 0, 100_003))
+    part = Library.generate(777, synth.seed_key(seed), thr, start=5000)
+    assert np.array_equal(part.words_host(), w[5000:5777])
+    assert part.index_base == 5000
+
+
+# ---------------------------------------------------------------- golden pins
+def _case(case):
+    plan = synth.make_plan(case["case"], seed=case["seed"], n=case["n"],
+                           planted_per_query=200 if case["case"] == "c2" else None)
+    lib, q = synth.build_library(plan)
+    w = lib.words_host()
+    assert words_sha(w) == case["sha256"]
+    return lib, q, w
+
+
+def test_search_matches_reference_golden(golden):
+    for case in golden["search"]:
+        lib, q, _ = _case(case)
+        assert [int(x) for x in q[0]] == case["query"]
+        got = lib.search(q[0], case["k"])
+        assert got == [(c - 1, d) for c, d in case["hits"]], (case["case"], case["k"])
+
+
+def test_search_through_fps1_manifest(golden, tmp_path):
+    """The drop-in path: FPS1 shards + manifest -> scan.search -> TopK of (cid, distance)."""
+    for case in golden["search"][:4]:
+        plan = synth.make_plan(case["case"], seed=case["seed"], n=case["n"],
+                               planted_per_query=200 if case["case"] == "c2" else None)
+        w = orc.generate_words(plan.seed_key, plan.thresholds, 0, plan.n)
+        q = synth.planted_after_sources(plan, w)
+        mpath = orc.write_fps1_library(tmp_path / f"{case['case']}_{case['k']}", w, case["shards"])
+        from paper_1906_06170_b200 import libstore
+
+        manifest = libstore.load_manifest(mpath.parent)
+        seen = []
+        top = scan.search(manifest, Fingerprint(tuple(int(x) for x in q[0])),
+                          scan.SearchParams(n=case["k"], parallelism=case["parallelism"]),
+                          progress=lambda label, done, total: seen.append((label, done, total)))
+        assert [[h.cid, h.distance] for h in top.hits] == case["hits"]
+        assert {s[0] for s in seen} == {s.dataset_label for s in manifest.shards}
+        assert all(d == t for _, d, t in seen)
+
+
+def test_per_query_matches_reference_golden(golden):
+    case = golden["per_query"][0]
+    plan = synth.make_plan("c4", seed=case["seed"], n=case["n"], Q=case["Q"])
+    lib, q = synth.build_library(plan)
+    assert q.tolist() == case["queries"]
+    res = lib.search_batch(q, case["k"])
+    for qi, hits in enumerate(case["hits"]):
+        assert res.hits(qi) == [(c - 1, d) for c, d in hits]
+
+
+def test_batch_min_matches_reference_golden(golden):
+    case = golden["batch_min"][0]
+    plan = synth.make_plan("c4", seed=case["seed"], n=case["n"], Q=12)
+    lib, _ = synth.build_library(plan)
+    got = lib.search_min(np.array(case["queries"], dtype=np.uint64), case["k"])
+    assert got == [(c - 1, d) for c, d in case["hits"]]
+
+
+def test_range_matches_reference_golden(golden):
+    case = golden["range"][0]
+    plan = synth.make_plan("c5", seed=case["seed"], n=case["n"], Q=case["Q"], planted_per_query=50)
+    lib, q = synth.build_library(plan)
+    r = lib.range_search(q, case["radius"])
+    assert np.array_equal(r.rows(), np.array(case["rows"], dtype=np.int64).reshape(-1, 3))
+
+
+def test_random_cid_library_matches_reference_golden(golden, tmp_path):
+    rec = np.load(GOLDEN_DIR / "cid_library.npy")
+    mpath = orc.write_fps1_library(tmp_path / "cids", rec[:, 1:], 3, cids=rec[:, 0])
+    from paper_1906_06170_b200 import libstore
+
+    manifest = libstore.load_manifest(mpath.parent)
+    for case in golden["cid_search"]:
+        top = scan.search(manifest, tuple(case["query"]), scan.SearchParams(n=case["k"]))
+        assert [[h.cid, h.distance] for h in top.hits] == case["hits"]
+    cb = golden["cid_batch_min"]
+    top = scan.batch_search(manifest, [tuple(x) for x in cb["queries"]], scan.SearchParams(n=cb["k"]))
+    assert [[h.cid, h.distance] for h in top.hits] == cb["hits"]
+
+
+# ---------------------------------------------------------------- oracle sweeps
+@pytest.mark.parametrize("n", [1, 5, 31, 127, 128, 129, 1000, 4097, 65_537, 300_001])
+def test_topk_tail_sizes(n):
+    w = orc.generate_words(12345, np.full(166, 2**30, np.uint64), 0, n)
+    lib = Library.from_words(w)
+    q = w[n // 2:n // 2 + 1].copy()
+    q[0, 1] ^= np.uint64(0xF0F0)
+    for k in (1, 10, 100):
+        assert lib.search(q[0], k) == oracle_topk(w, q, k)[0]
+
+
+@pytest.mark.parametrize("Q", [1, 2, 3, 4, 5, 7, 8, 9, 16, 33])
+def test_topk_query_counts(Q):
+    seed = 4242 + Q
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 200_000)
+    rng = np.random.default_rng(Q)
+    q = w[rng.integers(0, len(w), Q)].copy()
+    q[:, 0] ^= rng.integers(0, 2**20, Q).astype(np.uint64) << np.uint64(1)
+    lib = Library.from_words(w)
+    for k in (1, 10, 64):
+        res = lib.search_batch(q, k)
+        exp = oracle_topk(w, q, k)
+        for i in range(Q):
+            assert res.hits(i) == exp[i], (Q, k, i)
+
+
+@pytest.mark.parametrize("k", [1000, 1024, 1025, 4000])
+def test_large_k(k):
+    w = orc.generate_words(777, np.full(166, 2**31, np.uint64), 0, 150_000)
+    q = w[:3].copy()
+    lib = Library.from_words(w)
+    res = lib.search_batch(q, k)
+    exp = oracle_topk(w, q, k)
+    for i in range(3):
+        assert res.hits(i) == exp[i]
+
+
+def test_k_larger_than_library():
+    w = orc.generate_words(5, np.full(166, 2**31, np.uint64), 0, 50)
+    lib = Library.from_words(w)
+    assert lib.search(w[3], 100) == oracle_topk(w, w[3:4], 100)[0]
+    assert len(lib.search(w[3], 100)) == 50
+    assert lib.search(w[3], 2000) == oracle_topk(w, w[3:4], 2000)[0]
+
+
+def test_all_ties_library():
+    """Every entry identical: the answer is the first k indices (index tie-break),
+    and the threshold ties overflow the shared-memory tie buffer."""
+    w = np.tile(np.array([[0x1234, 0x5678, 0x9]], dtype=np.uint64), (200_000, 1))
+    lib = Library.from_words(w)
+    for k in (1, 10, 100, 1024):
+        got = lib.search(np.array([0x1234, 0x5678, 0x8], dtype=np.uint64), k)
+        assert got == [(i, 1) for i in range(k)]
+
+
+def test_adversarial_decreasing_distances():
+    """Distances fall with the index, so every block improves the running top-k."""
+    n = 120_000
+    w = np.zeros((n, 3), dtype=np.uint64)
+    bits = 166 - (np.arange(n) * 166 // n)  # popcount decreasing from 166
+    for i, b in enumerate(bits):
+        v = (1 << int(b)) - 1
+        w[i] = (v & (2**64 - 1), (v >> 64) & (2**64 - 1), v >> 128)
+    lib = Library.from_words(w)
+    q = np.zeros(3, dtype=np.uint64)
+    for k in (10, 100, 500):
+        assert lib.search(q, k) == oracle_topk(w, q[None], k)[0]
+
+
+def test_empty_library():
+    lib = Library.from_words(np.zeros((0, 3), dtype=np.uint64))
+    assert lib.search(np.zeros(3, dtype=np.uint64), 5) == []
+    assert len(lib.range_search(np.zeros((2, 3), dtype=np.uint64), 10)) == 0
+
+
+def test_padding_bits_rejected():
+    lib = Library.from_words(np.zeros((10, 3), dtype=np.uint64))
+    with pytest.raises(FingerprintError):
+        lib.search(np.array([0, 0, 1 << 38], dtype=np.uint64), 3)
+    with pytest.raises(FingerprintError):
+        Library.from_words(np.array([[0, 0, 1 << 40]], dtype=np.uint64))
+
+
+def test_fps1_padding_scanned_as_stored():
+    """The reference scan XORs the full third word of the record view
+    (scan.py:142), so stray pad bits count; FPS1 ingestion keeps them."""
+    rec = np.zeros((100, 4), dtype=np.uint64)
+    rec[:, 0] = np.arange(1, 101)
+    rec[7, 3] = np.uint64(0xFF) << np.uint64(40)  # 8 bits set in the record pad area
+    lib = Library.from_records(rec)
+    got = lib.search(np.zeros(3, dtype=np.uint64), 100)
+    assert got[-1] == (7, 8)
+
+
+@pytest.mark.parametrize("radius", [0, 3, 6, 40])
+def test_range_vs_oracle(radius):
+    seed = 99
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 250_000)
+    q = w[[3, 77, 1000, 200_000, 5, 6, 7, 8, 9]].copy()
+    q[:, 1] ^= np.uint64(0b111)
+    lib = Library.from_words(w)
+    r = lib.range_search(q, radius)
+    assert np.array_equal(r.rows(), orc.c_range(w, q, radius))
+
+
+def test_range_per_query_radius_and_overflow_retry():
+    w = orc.generate_words(3, np.full(166, 2**31, np.uint64), 0, 400_000)
+    q = w[:5].copy()
+    radii = np.array([0, 90, 85, 70, 166], dtype=np.uint8)  # > 1M hits: first pass overflows
+    lib = Library.from_words(w)
+    r = lib.range_search(q, radii)
+    exp = np.concatenate([orc.c_range(w, q[i:i + 1], int(radii[i])) + np.array([i, 0, 0]) for i in range(5)])
+    assert len(r) > 1 << 20
+    assert np.array_equal(r.rows(), exp)
+
+
+def test_multi_shard_merge_on_one_gpu():
+    """G logical shards with global index_base, per-shard device top-k, then the
+    device merge kernel: equals a single-library search (merge_topk semantics)."""
+    import torch
+
+    seed = 2024
+    thr = synth.beta_thresholds(seed)
+    n = 300_000
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, n)
+    rng = np.random.default_rng(0)
+    q = w[rng.integers(0, n, 6)].copy()
+    q[:, 2] ^= np.uint64(1)
+    for G in (2, 3, 8):
+        offs = [0]
+        for s in orc.split_sizes(n, G):
+            offs.append(offs[-1] + s)
+        k = 25
+        dq = torch.from_numpy(q.view(np.int64)).cuda()
+        keys = torch.empty((G, len(q), k), dtype=torch.int64, device="cuda")
+        cnt = torch.empty((G, len(q)), dtype=torch.int32, device="cuda")
+        libs = [Library.from_words(w[a:b], index_base=a) for a, b in zip(offs, offs[1:])]
+        stream = torch.cuda.current_stream().cuda_stream
+        for g, lib in enumerate(libs):
+            lib.topk_prepare(len(q), k)
+            lib.topk_async(dq, len(q), k, keys[g], cnt[g], stream)
+        out_k = torch.empty((len(q), k), dtype=torch.int64, device="cuda")
+        out_c = torch.empty((len(q),), dtype=torch.int32, device="cuda")
+        merge_async(keys, cnt, G, len(q), k, out_k, out_c, stream)
+        torch.cuda.synchronize()
+        res = keys_to_hits(out_k.cpu().numpy().view(np.uint64), out_c.cpu().numpy().astype(np.uint32))
+        exp = oracle_topk(w, q, k)
+        for i in range(len(q)):
+            assert res.hits(i) == exp[i], (G, i)
+
+
+def test_repeated_calls_are_deterministic():
+    seed = 11
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 500_000)
+    lib = Library.from_words(w)
+    q = w[[1, 2, 3]].copy()
+    first = lib.search_batch(q, 30)
+    for _ in range(5):
+        again = lib.search_batch(q, 30)
+        assert np.array_equal(first.index, again.index) and np.array_equal(first.distance, again.distance)
+    assert first.hits(0)[0] == (1, 0)

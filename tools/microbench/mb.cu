@@ -1,0 +1,205 @@
+// Microbenchmarks run once on the B200 to pick the scan design:
+//  (1) POPC / LOP3 / IADD3 issue rates per SM per clock on sm_100a,
+//  (2) streaming-read bandwidth with 128-bit vs 256-bit loads.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("CUDA %s @%d\n",cudaGetErrorString(e),__LINE__); return 1;}}while(0)
+
+template<int MODE>
+__global__ void pipe_kernel(unsigned* out, int iters, unsigned seed, long long* cyc) {
+  unsigned a0 = threadIdx.x ^ seed, a1 = a0 * 3u, a2 = a0 * 5u, a3 = a0 * 7u;
+  unsigned a4 = a0 * 11u, a5 = a0 * 13u, a6 = a0*17u, a7 = a0*19u;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    #pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (MODE == 0) { // POPC only: 8 independent chains
+        a0 = __popc(a0) ^ a1; a1 = __popc(a1) ^ a2; a2 = __popc(a2) ^ a3; a3 = __popc(a3) ^ a4;
+        a4 = __popc(a4) ^ a5; a5 = __popc(a5) ^ a6; a6 = __popc(a6) ^ a7; a7 = __popc(a7) ^ a0;
+      } else if (MODE == 1) { // LOP3 only
+        a0 = a0 ^ a1 ^ a2; a1 = a1 ^ a3 ^ a4; a2 = a2 ^ a5 ^ a6; a3 = a3 ^ a7 ^ a0;
+        a4 = a4 ^ a1 ^ a2; a5 = a5 ^ a3 ^ a4; a6 = a6 ^ a5 ^ a0; a7 = a7 ^ a6 ^ a1;
+      } else if (MODE == 2) { // IADD3 only
+        a0 = a0 + a1 + a2; a1 = a1 + a3 + a4; a2 = a2 + a5 + a6; a3 = a3 + a7 + a0;
+        a4 = a4 + a1 + a2; a5 = a5 + a3 + a4; a6 = a6 + a5 + a0; a7 = a7 + a6 + a1;
+      }
+    }
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+
+// distance kernel: popcount-of-xor over 3 u64 words, min over 8 queries -> representative hot loop
+__global__ void dist_kernel(unsigned* out, int iters, long long* cyc, unsigned long long s) {
+  unsigned long long w0 = s * (threadIdx.x + 1), w1 = w0 * 0x9E3779B97F4A7C15ull, w2 = w1 >> 26;
+  unsigned acc = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      unsigned long long q0 = s + q * 0x1234567ull, q1 = q0 * 31, q2 = q1 >> 26;
+      unsigned d = __popcll(w0 ^ q0) + __popcll(w1 ^ q1) + __popcll(w2 ^ q2);
+      acc |= (d < 3u) ? (1u << q) : 0u;
+    }
+    w0 += 0x9E37ull; w1 ^= w0; w2 = (w2 + 1) & 0x3FFFFFFFFFull;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+struct __align__(32) u64x4 { unsigned long long x, y, z, w; };
+__device__ __forceinline__ u64x4 ld256(const void* p) {
+  u64x4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(r.x), "=l"(r.y), "=l"(r.z), "=l"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ ulonglong2 ld128(const void* p) {
+  ulonglong2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+  return r;
+}
+
+// 3-plane SoA stream, per-warp contiguous chunks, 256-bit loads, 4 entries/lane/iter, U iters in flight
+template<int U>
+__global__ void stream256(const unsigned long long* __restrict__ p0, const unsigned long long* __restrict__ p1,
+                          const unsigned long long* __restrict__ p2, long long n, unsigned* out) {
+  int lane = threadIdx.x & 31;
+  long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  long long iters = n / 128;
+  long long it0 = warp * iters / nw, it1 = (warp + 1) * iters / nw;
+  unsigned acc = 0;
+  unsigned long long q0 = 0x1234, q1 = 0x5678, q2 = 0x9abc;
+  long long it = it0;
+  for (; it + U <= it1; it += U) {
+    u64x4 a[U], b[U], c[U];
+    #pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long base = (it + u) * 128 + lane * 4;
+      a[u] = ld256(p0 + base); b[u] = ld256(p1 + base); c[u] = ld256(p2 + base);
+    }
+    #pragma unroll
+    for (int u = 0; u < U; ++u) {
+      unsigned d0 = __popcll(a[u].x ^ q0) + __popcll(b[u].x ^ q1) + __popcll(c[u].x ^ q2);
+      unsigned d1 = __popcll(a[u].y ^ q0) + __popcll(b[u].y ^ q1) + __popcll(c[u].y ^ q2);
+      unsigned d2 = __popcll(a[u].z ^ q0) + __popcll(b[u].z ^ q1) + __popcll(c[u].z ^ q2);
+      unsigned d3 = __popcll(a[u].w ^ q0) + __popcll(b[u].w ^ q1) + __popcll(c[u].w ^ q2);
+      if (__any_sync(0xffffffffu, (d0 < 2) | (d1 < 2) | (d2 < 2) | (d3 < 2))) acc += d0 + d1 + d2 + d3;
+    }
+  }
+  for (; it < it1; ++it) {
+    long long base = it * 128 + lane * 4;
+    u64x4 a = ld256(p0 + base), b = ld256(p1 + base), c = ld256(p2 + base);
+    unsigned d0 = __popcll(a.x ^ q0) + __popcll(b.x ^ q1) + __popcll(c.x ^ q2);
+    if (__any_sync(0xffffffffu, d0 < 2)) acc += d0;
+  }
+  if (acc == 0xdeadbeef) out[0] = acc;
+}
+
+// 128-bit loads, 2 entries/lane/iter
+template<int U>
+__global__ void stream128(const unsigned long long* __restrict__ p0, const unsigned long long* __restrict__ p1,
+                          const unsigned long long* __restrict__ p2, long long n, unsigned* out) {
+  int lane = threadIdx.x & 31;
+  long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  long long iters = n / 64;
+  long long it0 = warp * iters / nw, it1 = (warp + 1) * iters / nw;
+  unsigned acc = 0;
+  unsigned long long q0 = 0x1234, q1 = 0x5678, q2 = 0x9abc;
+  long long it = it0;
+  for (; it + U <= it1; it += U) {
+    ulonglong2 a[U], b[U], c[U];
+    #pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long base = (it + u) * 64 + lane * 2;
+      a[u] = ld128(p0 + base); b[u] = ld128(p1 + base); c[u] = ld128(p2 + base);
+    }
+    #pragma unroll
+    for (int u = 0; u < U; ++u) {
+      unsigned d0 = __popcll(a[u].x ^ q0) + __popcll(b[u].x ^ q1) + __popcll(c[u].x ^ q2);
+      unsigned d1 = __popcll(a[u].y ^ q0) + __popcll(b[u].y ^ q1) + __popcll(c[u].y ^ q2);
+      if (__any_sync(0xffffffffu, (d0 < 2) | (d1 < 2))) acc += d0 + d1;
+    }
+  }
+  if (acc == 0xdeadbeef) out[0] = acc;
+}
+
+__global__ void flush_kernel(unsigned* buf, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) buf[i] = (unsigned)i;
+}
+
+int main() {
+  cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
+  int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("device %s SMs %d l2 %d MB clock %d kHz\n", prop.name, prop.multiProcessorCount, prop.l2CacheSize >> 20, clk);
+  int sms = prop.multiProcessorCount;
+  unsigned* out; long long* cyc; CK(cudaMalloc(&out, 1 << 26)); CK(cudaMalloc(&cyc, 1 << 20));
+  long long hc[4096];
+  const char* names[3] = {"POPC", "LOP3", "IADD3"};
+  for (int mode = 0; mode < 3; ++mode) {
+    for (int threads : {256, 512, 1024}) {
+      int blocks = sms * (2048 / threads);
+      int iters = 4096;
+      if (mode == 0) pipe_kernel<0><<<blocks, threads>>>(out, iters, 7, cyc);
+      if (mode == 1) pipe_kernel<1><<<blocks, threads>>>(out, iters, 7, cyc);
+      if (mode == 2) pipe_kernel<2><<<blocks, threads>>>(out, iters, 7, cyc);
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(hc, cyc, blocks * 8, cudaMemcpyDeviceToHost));
+      double mx = 0; for (int b = 0; b < blocks; ++b) mx = hc[b] > mx ? hc[b] : mx;
+      // ops per SM = (2048 threads) * iters * 64 ops
+      double ops = 2048.0 * iters * 64;
+      printf("%s threads/blk %d: %.2f ops/clk/SM (max block cycles %.0f)\n", names[mode], threads, ops / mx, mx);
+    }
+  }
+  {
+    int threads = 256, blocks = sms * 8, iters = 4096;
+    dist_kernel<<<blocks, threads>>>(out, iters, cyc, 12345); CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(hc, cyc, blocks * 8, cudaMemcpyDeviceToHost));
+    double mx = 0; for (int b = 0; b < blocks; ++b) mx = hc[b] > mx ? hc[b] : mx;
+    double comps = 2048.0 * iters * 8;
+    printf("dist(8q, popcll): %.3f comparisons/clk/SM\n", comps / mx);
+  }
+  long long n = 95417114LL / 128 * 128;
+  unsigned long long *p0, *p1, *p2; unsigned* fl;
+  CK(cudaMalloc(&p0, n * 8)); CK(cudaMalloc(&p1, n * 8)); CK(cudaMalloc(&p2, n * 8));
+  CK(cudaMemset(p0, 1, n * 8)); CK(cudaMemset(p1, 2, n * 8)); CK(cudaMemset(p2, 3, n * 8));
+  CK(cudaMalloc(&fl, 512ull << 20));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  auto run = [&](const char* name, auto launch) {
+    float best = 1e9;
+    for (int r = 0; r < 6; ++r) {
+      flush_kernel<<<sms * 4, 1024>>>(fl, (512ll << 20) / 4);
+      cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1); if (r > 0 && ms < best) best = ms;
+    }
+    printf("%-28s %.1f us  %.0f GB/s\n", name, best * 1e3, n * 24.0 / (best * 1e-3) / 1e9);
+  };
+  for (int occ : {4, 8, 16}) {
+    for (int th : {256, 512}) {
+      int blocks = sms * occ * 256 / th;
+      if (blocks * th > sms * 2048) continue;
+      char nm[64];
+      sprintf(nm, "s256 U1 occ%d th%d", occ, th); run(nm, [&] { stream256<1><<<blocks, th>>>(p0, p1, p2, n, out); });
+      sprintf(nm, "s256 U2 occ%d th%d", occ, th); run(nm, [&] { stream256<2><<<blocks, th>>>(p0, p1, p2, n, out); });
+      sprintf(nm, "s256 U4 occ%d th%d", occ, th); run(nm, [&] { stream256<4><<<blocks, th>>>(p0, p1, p2, n, out); });
+      sprintf(nm, "s128 U2 occ%d th%d", occ, th); run(nm, [&] { stream128<2><<<blocks, th>>>(p0, p1, p2, n, out); });
+      sprintf(nm, "s128 U4 occ%d th%d", occ, th); run(nm, [&] { stream128<4><<<blocks, th>>>(p0, p1, p2, n, out); });
+    }
+  }
+  // plain copy reference
+  {
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0); cudaMemcpyAsync(p1, p0, n * 8, cudaMemcpyDeviceToDevice); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1); if (r > 0 && ms < best) best = ms;
+    }
+    printf("memcpy d2d %.0f GB/s (r+w)\n", 2.0 * n * 8 / (best * 1e-3) / 1e9);
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
