@@ -136,7 +136,7 @@ def scan_shard(words: np.ndarray, qwords: np.ndarray, k: int, ids: np.ndarray | 
     """
     if k < 1:
         raise ValueError("n must be >= 1")
-    if ids is None:
+    if ids is None and blocks is None:
         ids = np.arange(len(words), dtype=np.uint64)
     qwords = np.atleast_2d(np.asarray(qwords, dtype=np.uint64))
     acc = TopKAccumulator(k)
@@ -451,3 +451,59 @@ def write_fps1_library(out_dir, words: np.ndarray, shard_count: int, cids: np.nd
     path = out_dir / "manifest.json"
     path.write_text(_json.dumps(doc, indent=2) + "\n", encoding="utf-8")
     return path
+
+
+# --------------------------------------------------------------------------
+# file-streaming restatement: the reference reads FPS1 shards per search
+# (scan.py:158-170) with one worker thread per shard (scan.py:256-287)
+# --------------------------------------------------------------------------
+def iter_fps1_blocks(path):
+    """(ids, words) blocks of 65,536 records read with f.read, as scan.py:158-170."""
+    with open(path, "rb") as f:
+        head = f.read(HEADER_SIZE)
+        if len(head) < HEADER_SIZE or head[:4] != b"FPS1":
+            raise ValueError(f"{path}: bad FPS1 header")
+        count = int.from_bytes(head[8:16], "little")
+        remaining = count
+        while remaining > 0:
+            n = min(remaining, BLOCK_RECORDS)
+            buf = f.read(n * RECORD_SIZE)
+            if len(buf) < n * RECORD_SIZE:
+                raise ValueError(f"{path}: truncated")
+            block = np.frombuffer(buf, dtype="<u8").reshape(n, 4)
+            yield block[:, 0], block[:, 1:4]
+            remaining -= n
+
+
+def search_fps1(manifest_path, qwords, k: int, parallelism: int = 1) -> list[tuple[int, int]]:
+    """The reference ``search`` restated over FPS1 files: per-shard block scan
+    (ids are the stored CIDs) on a thread pool, then merge_topk."""
+    doc = _json.loads(_Path(manifest_path).read_text())
+    base = _Path(manifest_path).parent
+    paths = [base / s["path"] for s in doc["shards"]]
+
+    def run(p):
+        return scan_shard(None, qwords, k, blocks=iter_fps1_blocks(p))
+
+    if not paths:
+        return []
+    if parallelism == 1 or len(paths) == 1:
+        parts = [run(p) for p in paths]
+    else:
+        with ThreadPoolExecutor(max_workers=min(parallelism, len(paths))) as pool:
+            parts = list(pool.map(run, paths))
+    return merge_topk(parts, k)
+
+
+def generate_words_parallel(seed_key: int, thresholds: np.ndarray, start: int, count: int,
+                            threads: int | None = None, chunk: int = 1 << 18) -> np.ndarray:
+    """generate_words over chunks on a thread pool (numpy releases the GIL)."""
+    out = np.empty((count, 3), dtype=np.uint64)
+
+    def one(s):
+        m = min(chunk, count - s)
+        out[s:s + m] = generate_words(seed_key, thresholds, start + s, m)
+
+    with ThreadPoolExecutor(max_workers=threads or cpu_threads()) as pool:
+        list(pool.map(one, range(0, count, chunk)))
+    return out

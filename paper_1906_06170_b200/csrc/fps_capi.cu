@@ -197,29 +197,53 @@ Config make_config(const fps_lib* L, u32 Q, u32 k) {
   return c;
 }
 
+// Spread the per-query global histogram bins over distinct L2 lines/slices
+// when many warps share a query (small Q); dense layout otherwise.
+u32 ghist_stride(u32 Q) { return Q <= 64 ? 64u : 1u; }
+
+// tg[q] = T_OPEN (255) for every query slot the buffer holds.
+cudaError_t fill_tg(fps_lib* L) {
+  std::vector<u32> open(L->tg.bytes / 4, fps::T_OPEN);
+  cudaError_t e = cudaMemcpyAsync(L->tg.p, open.data(), open.size() * 4, cudaMemcpyHostToDevice, L->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
+  return e;
+}
+
 int ensure_state(fps_lib* L, u32 Q) {
-  if (Q <= L->state_q) return FPS_OK;
+  const size_t gh = (size_t)Q * fps::HB * 4 * ghist_stride(Q);
+  if (Q <= L->state_q && gh <= L->ghist.bytes) return FPS_OK;
+  const u32 Qa = std::max(Q, L->state_q);
   int rc;
-  if ((rc = L->tg.ensure((size_t)Q * 4))) return rc;
-  if ((rc = L->ghist.ensure((size_t)Q * fps::HB * 4))) return rc;
-  if ((rc = L->cand_cnt.ensure((size_t)Q * 4))) return rc;
-  CUDA_TRY(cudaMemsetAsync(L->tg.p, 0xff, L->tg.bytes, L->stream));
+  if ((rc = L->tg.ensure((size_t)Qa * 4))) return rc;
+  if ((rc = L->ghist.ensure(std::max(gh, (size_t)Qa * fps::HB * 4)))) return rc;
+  if ((rc = L->cand_cnt.ensure((size_t)Qa * 4))) return rc;
+  CUDA_TRY(fill_tg(L));
   CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream));
   CUDA_TRY(cudaMemsetAsync(L->cand_cnt.p, 0, L->cand_cnt.bytes, L->stream));
-  L->state_q = Q;
+  CUDA_TRY(cudaStreamSynchronize(L->stream));
+  L->state_q = Qa;
   return FPS_OK;
 }
 
 // Restore the clean top-k state after a failed call.
 void reset_state(fps_lib* L) {
   if (!L->state_q) return;
-  cudaMemsetAsync(L->tg.p, 0xff, L->tg.bytes, L->stream);
+  fill_tg(L);
   cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream);
   cudaMemsetAsync(L->cand_cnt.p, 0, L->cand_cnt.bytes, L->stream);
 }
 
+u32 scan_flags() {
+  static u32 f = [] {
+    const char* e = std::getenv("FPS_SCAN_FLAGS");
+    return e ? (u32)std::strtoul(e, nullptr, 0) : 0u;
+  }();
+  return f;
+}
+
 fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
   fps::ScanArgs a{};
+  a.flags = scan_flags();
   a.w0 = L->w0();
   a.w1 = L->w1();
   a.w2 = L->w2();
@@ -257,6 +281,8 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   a.iters = c.iters;
   a.tg = L->tg.as<u32>();
   a.ghist = L->ghist.as<u32>();
+  a.gstride = ghist_stride(Q);
+  a.pub_every = (u32)std::max<u64>(1, c.n_parts / 512);
   a.buf = L->buf.as<u64>();
   a.cand = L->cand.as<u64>();
   a.cand_cnt = L->cand_cnt.as<u32>();
@@ -276,7 +302,7 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
     cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr_set = true;
   }
-  fps::select_kernel<<<Q, fps::SEL_THREADS, sel_smem, s>>>(a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, k, d_keys,
+  fps::select_kernel<<<Q, fps::SEL_THREADS, sel_smem, s>>>(a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, k, d_keys,
                                                             d_cnt, 1);
   L->launches++;
   CUDA_TRY(cudaGetLastError());
@@ -456,6 +482,8 @@ int topk_large(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   if ((rc = ensure_state(L, Q))) return rc;
   CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, (size_t)Q * fps::HB * 4, L->stream));
   fps::ScanArgs a = base_args(L, d_q, Q);
+  a.ghist = L->ghist.as<u32>();
+  a.gstride = 1;  // dense: read back by the host
   if ((rc = plain_dispatch<fps::MODE_HIST>(L, a, L->stream))) return rc;
   std::vector<u32> hist((size_t)Q * fps::HB);
   CUDA_TRY(cudaMemcpyAsync(hist.data(), L->ghist.p, hist.size() * 4, cudaMemcpyDeviceToHost, L->stream));
@@ -703,7 +731,7 @@ int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t
   if (k > KMAX_FUSED) return fail(FPS_EINVAL, "fps_topk_async supports k <= 1024");
   std::lock_guard<std::mutex> lk(lib->mu);
   DeviceGuard g(lib->device);
-  cudaStream_t s = stream ? (cudaStream_t)stream : lib->stream;
+  cudaStream_t s = (cudaStream_t)stream;  // used as given (0 = legacy default stream)
   int rc = topk_dispatch(lib, (const u64*)d_queries, Q, k, (u64*)d_keys, d_cnt, s, false);
   if (rc) reset_state(lib);
   return rc;
@@ -771,6 +799,8 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   a.iters = c.iters;
   a.tg = lib->tg.as<u32>();
   a.ghist = lib->ghist.as<u32>();
+  a.gstride = ghist_stride(1);
+  a.pub_every = (u32)std::max<u64>(1, c.n_parts / 512);
   a.buf = lib->buf.as<u64>();
   a.cand = lib->cand.as<u64>();
   a.cand_cnt = lib->cand_cnt.as<u32>();
@@ -783,7 +813,7 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   while (kp < (int)k) kp <<= 1;
   cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   fps::select_kernel<<<1, fps::SEL_THREADS, (size_t)(kp + fps::SEL_ECAP) * 8, lib->stream>>>(
-      a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), 1);
+      a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), 1);
   lib->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, cudaGetErrorString(e)); }
@@ -805,7 +835,7 @@ int fps_range_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, const u
   if (Q > 65535) return fail(FPS_EINVAL, "at most 65535 queries per range call");
   std::lock_guard<std::mutex> lk(lib->mu);
   DeviceGuard g(lib->device);
-  cudaStream_t s = stream ? (cudaStream_t)stream : lib->stream;
+  cudaStream_t s = (cudaStream_t)stream;  // used as given (0 = legacy default stream)
   CUDA_TRY(cudaMemsetAsync(d_count, 0, 8, s));
   fps::ScanArgs a = base_args(lib, (const u64*)d_queries, Q);
   a.radius = d_radius;
@@ -854,7 +884,7 @@ int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream) {
   if (lib) {
     std::lock_guard<std::mutex> lk(lib->mu);
     DeviceGuard g(lib->device);
-    return sort_keys(lib, (u64*)d_keys, n, stream ? (cudaStream_t)stream : lib->stream);
+    return sort_keys(lib, (u64*)d_keys, n, (cudaStream_t)stream);
   }
   return sort_keys(nullptr, (u64*)d_keys, n, (cudaStream_t)stream);
 }

@@ -113,6 +113,9 @@ struct ScanArgs {
   u32 k;
   u32 cap;         // MODE_TOPK: per-(warp, query) buffer capacity
   u32 n_qg;        // query groups (ceil(Q / QW))
+  u32 flags;       // experiment knobs (FPS_SCAN_FLAGS): 1 = no global publish, 2 = no tg refresh
+  u32 gstride;     // words between consecutive ghist bins (spreads hot atomics over L2 slices)
+  u32 pub_every;   // only library parts with part % pub_every == 0 publish to ghist
   u64 n_parts;     // library parts
   u64 iters;       // ceil(n / (32*E))
   // MODE_TOPK state (all per query unless noted)
@@ -134,11 +137,14 @@ struct ScanArgs {
 // the cumulative count up to T reaches k, no entry with d > T can be in the
 // top-k and tg[q] = min(tg[q], T) is exact. Reads of ghist see monotone
 // counters, so any snapshot is a valid lower count.
+__device__ __forceinline__ u32* gbin(const ScanArgs& a, u32 qi, u32 b) {
+  return a.ghist + ((u64)qi * HB + b) * a.gstride;
+}
+
 __device__ __forceinline__ void tighten_tg(const ScanArgs& a, u32 qi, int lane) {
-  const u32* gh = a.ghist + (u64)qi * HB;
   u32 hv[7], s = 0;
 #pragma unroll
-  for (int i = 0; i < 7; ++i) { hv[i] = *((volatile const u32*)gh + lane * 7 + i); s += hv[i]; }
+  for (int i = 0; i < 7; ++i) { hv[i] = *(volatile const u32*)gbin(a, qi, lane * 7 + i); s += hv[i]; }
   u32 incl = warp_incl_scan(s, lane);
   u32 bal = __ballot_sync(FULL, incl >= a.k);
   if (bal) {
@@ -164,7 +170,7 @@ struct WarpState {
 };
 
 template <int QW, int E, int MODE, bool MINQ = false>
-__global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const ScanArgs a) {
   extern __shared__ u32 smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -199,12 +205,20 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
   }
   u64* wbuf = (MODE == MODE_TOPK) ? a.buf + g * QW * (u64)a.cap : nullptr;
 
+  // Register arrays indexed by a runtime slot j would be demoted to local
+  // memory; the slow path selects / updates slot j with unrolled compares.
+  auto setT = [&](int j, u32 v) {
+#pragma unroll
+    for (int jj = 0; jj < QW; ++jj)
+      if (jj == j) T[jj] = v;
+  };
   auto refresh_tg = [&](int j) {
     u32 qi = qg * QW + j;
-    if (qi < a.Q) {
-      u32 t = *((volatile const u32*)a.tg + qi) + 1;
+    if (qi < a.Q && !(a.flags & 2)) {
+      u32 t = *((volatile const u32*)a.tg + qi);
+      t = (t < T_OPEN ? t : T_OPEN - 1) + 1;
       u32 own = ws->town[j];
-      T[j] = t < own ? t : own;
+      setT(j, t < own ? t : own);
     }
   };
 
@@ -277,17 +291,21 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
     }
     if (MODE == MODE_HIST) return;
     if (!__any_sync(FULL, hit)) return;
-    // slow path: rare once thresholds settle (unrolled so the query words
-    // and thresholds stay in registers)
-#pragma unroll
+    // slow path: rare once thresholds settle
+#pragma unroll 1
     for (int j = 0; j < QW; ++j) {
+      u64 x0 = 0, x1 = 0, x2 = 0;
+      u32 Tj = 0;
+#pragma unroll
+      for (int jj = 0; jj < QW; ++jj)
+        if (jj == j) { x0 = q0[jj]; x1 = q1[jj]; x2 = q2[jj]; Tj = T[jj]; }
       u32 dd[E];
       u32 m = 0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        dd[e] = dist_of(A[e], B[e], C[e], j);
+        dd[e] = MINQ ? dist_of(A[e], B[e], C[e], 0) : dist3(A[e], B[e], C[e], x0, x1, x2);
         if (masked && first + e >= a.n) dd[e] = DMASKED;
-        if (dd[e] < T[j]) m |= 1u << e;
+        if (dd[e] < Tj) m |= 1u << e;
       }
       if (!__any_sync(FULL, m)) continue;
       const u32 qi = qg * QW + j;
@@ -328,11 +346,18 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
         u32 less;
         const u32 t = warp_kth_bin(hj, a.k, lane, &less);
         if (lane == 0) ws->town[j] = t;
+        if ((a.flags & 1) || (part % a.pub_every) != 0) {
+          // not a publisher: only follow the global bound
+          __syncwarp();
+          if (!(a.flags & 2)) refresh_tg(j);
+          else setT(j, t < Tj ? t : Tj);
+          continue;
+        }
         if (!ws->pubd[j]) {
           // first publication: every buffered candidate with d <= t
           for (u32 b = lane; b <= t && b < HB; b += 32) {
             const u32 cb = hj[b];
-            if (cb) atomicAdd(a.ghist + (u64)qi * HB + b, cb);
+            if (cb) atomicAdd(gbin(a, qi, b), cb);
           }
         } else {
           // later batches: the newly inserted entries with d <= t, one RED per
@@ -342,8 +367,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
             const bool hb = (m >> e & 1u) && dd[e] <= t;
             const u32 key = hb ? dd[e] : 0xffffffffu;
             const u32 peers = __match_any_sync(FULL, key);
-            if (hb && (u32)(__ffs(peers) - 1) == (u32)lane)
-              atomicAdd(a.ghist + (u64)qi * HB + dd[e], (u32)__popc(peers));
+            if (hb && (u32)(__ffs(peers) - 1) == (u32)lane) atomicAdd(gbin(a, qi, dd[e]), (u32)__popc(peers));
           }
         }
         __syncwarp();
@@ -357,8 +381,28 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
   };
 
   constexpr int U = (QW == 1) ? 2 : 1;
+  constexpr int REFRESH = 8;  // loop trips between global-bound refreshes (one hot L2 line)
   u64 it = it0;
   int since_refresh = 0;
+  // The global bound is loaded one refresh period before it is applied, so the
+  // load latency hides behind the scan instead of stalling it. Applying it is
+  // monotone (T only decreases), and T <= T_own holds since every insertion.
+  // (single-query kernel only: the multi-query kernels are compute bound and
+  // refresh directly, keeping registers for the query words.)
+  u32 tgp = T_OPEN;
+  auto prefetch_tg = [&]() {
+    if (QW == 1 && qg < a.Q) tgp = *((volatile const u32*)a.tg + qg);
+  };
+  auto apply_tg = [&]() {
+    if (QW == 1) {
+      const u32 t = (tgp < T_OPEN ? tgp : T_OPEN - 1) + 1;
+      T[0] = t < T[0] ? t : T[0];
+    } else {
+#pragma unroll
+      for (int j = 0; j < QW; ++j) refresh_tg(j);
+    }
+  };
+  if (MODE == MODE_TOPK && !(a.flags & 2)) prefetch_tg();
   for (; it + U <= it1; it += U) {
     u64 A[U][E], B[U][E], C[U][E];
 #pragma unroll
@@ -370,10 +414,10 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) process(A[u], B[u], C[u], it + u, it + u >= n_full);
-    if (MODE == MODE_TOPK && ++since_refresh == 4) {
+    if (MODE == MODE_TOPK && !(a.flags & 2) && ++since_refresh == REFRESH) {
       since_refresh = 0;
-#pragma unroll
-      for (int j = 0; j < QW; ++j) refresh_tg(j);
+      apply_tg();
+      prefetch_tg();
     }
   }
   for (; it < it1; ++it) {
@@ -393,7 +437,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanArgs a) {
       if (qi >= a.Q) continue;
       for (int b = lane; b < HB; b += 32) {
         const u32 c = hist[j * HB + b];
-        if (c) atomicAdd(a.ghist + (u64)qi * HB + b, c);
+        if (c) atomicAdd(gbin(a, qi, b), c);
       }
     }
     return;
@@ -448,8 +492,8 @@ __device__ void block_bitonic_sort(u64* s, int n_pow2) {
 }
 
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
-                                                             u32* ghist, u32 k, u64* out_keys, u32* out_cnt,
-                                                             int reset) {
+                                                             u32* ghist, u32 gstride, u32 k, u64* out_keys,
+                                                             u32* out_cnt, int reset) {
   extern __shared__ u64 ssel[];  // [k_pow2] result + [SEL_ECAP] ties
   __shared__ u32 hist[256];
   __shared__ u32 s_nres, s_ntie, s_T, s_m;
@@ -556,7 +600,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   for (u32 i = threadIdx.x; i < k; i += blockDim.x) out_keys[(u64)q * k + i] = i < nres ? res[i] : ~0ull;
   if (threadIdx.x == 0) out_cnt[q] = nres;
   if (reset) {
-    for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[(u64)q * HB + i] = 0;
+    for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
     if (threadIdx.x == 0) { tg[q] = T_OPEN; cand_cnt[q] = 0; }
   }
 }

@@ -246,7 +246,7 @@ def test_range_vs_oracle(radius):
 def test_range_per_query_radius_and_overflow_retry():
     w = orc.generate_words(3, np.full(166, 2**31, np.uint64), 0, 400_000)
     q = w[:5].copy()
-    radii = np.array([0, 90, 85, 70, 166], dtype=np.uint8)  # > 1M hits: first pass overflows
+    radii = np.array([0, 95, 90, 80, 166], dtype=np.uint8)  # > 1M hits: first pass overflows
     lib = Library.from_words(w)
     r = lib.range_search(q, radii)
     exp = np.concatenate([orc.c_range(w, q[i:i + 1], int(radii[i])) + np.array([i, 0, 0]) for i in range(5)])
