@@ -121,6 +121,7 @@ struct fps_lib {
   DevBuf tg, ghist, cand_cnt;
   u32 state_q = 0;
   DevBuf buf, cand, queries, keys, cnt, radius, rkeys, rcount, sort_tmp, sort_out, seg;
+  DevBuf sched;  // 2 x u32 chunk scheduler of the single-query kernels (self-resetting)
   HostBuf h_stage;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
   bool timing = false;
@@ -188,7 +189,7 @@ Config make_config(const fps_lib* L, u32 Q, u32 k) {
   c.grid = (int)((c.warps + WPB - 1) / WPB);
   c.cap = 0;
   if (MODE == fps::MODE_TOPK) {
-    u32 cap = 2 * k + 32 * E;
+    u32 cap = std::max<u32>(2 * k + 32 * E, k + 256);
     cap = (cap + 31) / 32 * 32;
     c.cap = cap;
     c.cand_cap = parts * (u64)k;
@@ -200,6 +201,7 @@ Config make_config(const fps_lib* L, u32 Q, u32 k) {
 // Spread the per-query global histogram bins over distinct L2 lines/slices
 // when many warps share a query (small Q); dense layout otherwise.
 u32 ghist_stride(u32 Q) { return Q <= 64 ? 64u : 1u; }
+u32 tg_replicas(u32 Q) { return Q <= 64 ? 16u : 1u; }
 
 // tg[q] = T_OPEN (255) for every query slot the buffer holds.
 cudaError_t fill_tg(fps_lib* L) {
@@ -211,10 +213,11 @@ cudaError_t fill_tg(fps_lib* L) {
 
 int ensure_state(fps_lib* L, u32 Q) {
   const size_t gh = (size_t)Q * fps::HB * 4 * ghist_stride(Q);
-  if (Q <= L->state_q && gh <= L->ghist.bytes) return FPS_OK;
+  const size_t tgb = (size_t)Q * tg_replicas(Q) * ghist_stride(Q) * 4;
+  if (Q <= L->state_q && gh <= L->ghist.bytes && tgb <= L->tg.bytes) return FPS_OK;
   const u32 Qa = std::max(Q, L->state_q);
   int rc;
-  if ((rc = L->tg.ensure((size_t)Qa * 4))) return rc;
+  if ((rc = L->tg.ensure(std::max((size_t)Qa * 4, (size_t)Q * tg_replicas(Q) * ghist_stride(Q) * 4)))) return rc;
   if ((rc = L->ghist.ensure(std::max(gh, (size_t)Qa * fps::HB * 4)))) return rc;
   if ((rc = L->cand_cnt.ensure((size_t)Qa * 4))) return rc;
   CUDA_TRY(fill_tg(L));
@@ -227,6 +230,7 @@ int ensure_state(fps_lib* L, u32 Q) {
 
 // Restore the clean top-k state after a failed call.
 void reset_state(fps_lib* L) {
+  cudaMemsetAsync(L->sched.p, 0, 16, L->stream);
   if (!L->state_q) return;
   fill_tg(L);
   cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream);
@@ -244,6 +248,14 @@ u32 scan_flags() {
 fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
   fps::ScanArgs a{};
   a.flags = scan_flags();
+  // dynamic chunk claiming measured slower than static contiguous parts on B200
+  // (profiles/r01_experiments.md); kept behind FPS_SCAN_FLAGS bit 4
+  a.sched = (a.flags & 4) ? L->sched.as<u32>() : nullptr;
+  static const u32 chunk = [] {
+    const char* e = std::getenv("FPS_CHUNK");
+    return e ? (u32)std::strtoul(e, nullptr, 0) : 8u;
+  }();
+  a.chunk_iters = chunk;
   a.w0 = L->w0();
   a.w1 = L->w1();
   a.w2 = L->w2();
@@ -252,6 +264,25 @@ fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
   a.queries = d_q;
   a.Q = Q;
   return a;
+}
+
+// select_kernel launched as a programmatic dependent of the scan kernel: its
+// launch and block scheduling overlap the scan's tail, and griddepcontrol.wait
+// inside it orders it after the scan's completion (and memory flush).
+cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
+                          u32* ghist, u32 gstride, u32 tg_rep, u32 k, u64* out_keys, u32* out_cnt, bool pdl) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(Q);
+  cfg.blockDim = dim3(fps::SEL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fps::select_kernel, cand, cand_cnt, cand_cap, tg, ghist, gstride, tg_rep, k, out_keys,
+                            out_cnt, 1);
 }
 
 // Record an event pair around the next scan-kernel launch when timing is on.
@@ -282,6 +313,7 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   a.tg = L->tg.as<u32>();
   a.ghist = L->ghist.as<u32>();
   a.gstride = ghist_stride(Q);
+  a.tg_rep = tg_replicas(Q);
   a.pub_every = (u32)std::max<u64>(1, c.n_parts / 512);
   a.buf = L->buf.as<u64>();
   a.cand = L->cand.as<u64>();
@@ -294,6 +326,15 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
     if (ev) cudaEventRecord(ev->second, s);
     L->launches++;
   }
+  if (std::getenv("FPS_DEBUG")) {
+    std::vector<u32> cc(std::min<u32>(Q, 8));
+    cudaStreamSynchronize(s);
+    cudaMemcpy(cc.data(), a.cand_cnt, cc.size() * 4, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "[fps] Q=%u k=%u warps=%llu parts=%llu candidates:", Q, k, (unsigned long long)c.warps,
+                 (unsigned long long)c.n_parts);
+    for (u32 v : cc) std::fprintf(stderr, " %u", v);
+    std::fprintf(stderr, "\n");
+  }
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
   size_t sel_smem = (size_t)(kp + fps::SEL_ECAP) * 8;
@@ -302,8 +343,8 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
     cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr_set = true;
   }
-  fps::select_kernel<<<Q, fps::SEL_THREADS, sel_smem, s>>>(a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, k, d_keys,
-                                                            d_cnt, 1);
+  CUDA_TRY(launch_select(Q, sel_smem, s, a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, a.tg_rep, k,
+                         d_keys, d_cnt, !(a.flags & 32)));
   L->launches++;
   CUDA_TRY(cudaGetLastError());
   return FPS_OK;
@@ -441,6 +482,11 @@ int new_lib(int device, u64 index_base, fps_lib** out) {
     delete L;
     return fail(FPS_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
   }
+  if (L->sched.ensure(256) || cudaMemsetAsync(L->sched.p, 0, 256, L->stream) != cudaSuccess) {
+    cudaStreamDestroy(L->stream);
+    delete L;
+    return fail(FPS_ENOMEM, "scheduler allocation");
+  }
   *out = L;
   return FPS_OK;
 }
@@ -451,7 +497,7 @@ void destroy(fps_lib* L) {
   if (L->stream) cudaStreamSynchronize(L->stream);
   if (L->planes) cudaFree(L->planes);
   for (DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt, &L->radius,
-                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg})
+                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->sched})
     b->release();
   L->h_stage.release();
   for (auto& p : L->ev_pool) {
@@ -800,6 +846,7 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   a.tg = lib->tg.as<u32>();
   a.ghist = lib->ghist.as<u32>();
   a.gstride = ghist_stride(1);
+  a.tg_rep = tg_replicas(1);
   a.pub_every = (u32)std::max<u64>(1, c.n_parts / 512);
   a.buf = lib->buf.as<u64>();
   a.cand = lib->cand.as<u64>();
@@ -812,8 +859,8 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
   cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  fps::select_kernel<<<1, fps::SEL_THREADS, (size_t)(kp + fps::SEL_ECAP) * 8, lib->stream>>>(
-      a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), 1);
+  CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, lib->stream, a.cand, a.cand_cnt, c.cand_cap, a.tg,
+                         a.ghist, a.gstride, a.tg_rep, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), true));
   lib->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, cudaGetErrorString(e)); }

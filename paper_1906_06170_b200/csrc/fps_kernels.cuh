@@ -60,6 +60,9 @@ __device__ __forceinline__ u32 dist3(u64 a, u64 b, u64 c, u64 q0, u64 q1, u64 q2
   return (u32)(__popcll(a ^ q0) + __popcll(b ^ q1) + __popcll(c ^ q2));
 }
 
+// Release/acquire fence at GPU scope (cheaper than __threadfence()'s fence.sc).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ u32 lanemask_lt() {
   u32 m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -113,8 +116,12 @@ struct ScanArgs {
   u32 k;
   u32 cap;         // MODE_TOPK: per-(warp, query) buffer capacity
   u32 n_qg;        // query groups (ceil(Q / QW))
-  u32 flags;       // experiment knobs (FPS_SCAN_FLAGS): 1 = no global publish, 2 = no tg refresh
-  u32 gstride;     // words between consecutive ghist bins (spreads hot atomics over L2 slices)
+  u32 flags;       // experiment knobs (FPS_SCAN_FLAGS): 1 = no global publish, 2 = no tg refresh,
+                   // 4 = dynamic chunk claiming
+  u32 gstride;     // words between consecutive ghist bins / tg replicas (spreads hot lines over L2 slices)
+  u32 tg_rep;      // replicas of tg[q] (all receive every atomicMin; warp g reads replica g % tg_rep)
+  u32* sched;      // QW == 1: {next chunk, warps done}; zero between launches (the last warp resets it)
+  u32 chunk_iters; // iterations per dynamically claimed chunk
   u32 pub_every;   // only library parts with part % pub_every == 0 publish to ghist
   u64 n_parts;     // library parts
   u64 iters;       // ceil(n / (32*E))
@@ -140,25 +147,30 @@ struct ScanArgs {
 __device__ __forceinline__ u32* gbin(const ScanArgs& a, u32 qi, u32 b) {
   return a.ghist + ((u64)qi * HB + b) * a.gstride;
 }
+__device__ __forceinline__ u32* tgrep(const ScanArgs& a, u32 qi, u32 r) {
+  return a.tg + ((u64)qi * a.tg_rep + r) * a.gstride;
+}
 
-__device__ __forceinline__ void tighten_tg(const ScanArgs& a, u32 qi, int lane) {
+__device__ __forceinline__ u32 tighten_tg(const ScanArgs& a, u32 qi, int lane) {
   u32 hv[7], s = 0;
 #pragma unroll
   for (int i = 0; i < 7; ++i) { hv[i] = *(volatile const u32*)gbin(a, qi, lane * 7 + i); s += hv[i]; }
   u32 incl = warp_incl_scan(s, lane);
   u32 bal = __ballot_sync(FULL, incl >= a.k);
-  if (bal) {
-    int src = __ffs(bal) - 1;
-    if (lane == src) {
-      u32 cc = incl - s, tt = 0;
+  if (!bal) return T_OPEN;
+  const int src = __ffs(bal) - 1;
+  u32 tt = 0;
+  if (lane == src) {
+    u32 cc = incl - s;
 #pragma unroll
-      for (int i = 0; i < 7; ++i) {
-        if (cc + hv[i] >= a.k) { tt = lane * 7 + i; break; }
-        cc += hv[i];
-      }
-      atomicMin(a.tg + qi, tt);
+    for (int i = 0; i < 7; ++i) {
+      if (cc + hv[i] >= a.k) { tt = lane * 7 + i; break; }
+      cc += hv[i];
     }
   }
+  tt = __shfl_sync(FULL, tt, src);
+  for (u32 r = lane; r < a.tg_rep; r += 32) atomicMin(tgrep(a, qi, r), tt);
+  return tt;
 }
 
 // Per-warp slow-path state, kept in shared memory (only touched on inserts).
@@ -170,12 +182,15 @@ struct WarpState {
 };
 
 template <int QW, int E, int MODE, bool MINQ = false>
-__global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel(const ScanArgs a) {
   extern __shared__ u32 smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nwb = blockDim.x >> 5;
   const u64 g = (u64)blockIdx.x * nwb + wib;
+  // let a programmatic dependent (select_kernel) launch early; it still waits
+  // for this grid to complete before reading its results
+  asm volatile("griddepcontrol.launch_dependents;");
   if (g >= (u64)a.n_qg * a.n_parts) return;  // warp-uniform; no block-level sync below
   const u32 qg = (u32)(g % a.n_qg);
   const u64 part = g / a.n_qg;
@@ -215,7 +230,7 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
   auto refresh_tg = [&](int j) {
     u32 qi = qg * QW + j;
     if (qi < a.Q && !(a.flags & 2)) {
-      u32 t = *((volatile const u32*)a.tg + qi);
+      u32 t = *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));
       t = (t < T_OPEN ? t : T_OPEN - 1) + 1;
       u32 own = ws->town[j];
       setT(j, t < own ? t : own);
@@ -347,10 +362,9 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
         const u32 t = warp_kth_bin(hj, a.k, lane, &less);
         if (lane == 0) ws->town[j] = t;
         if ((a.flags & 1) || (part % a.pub_every) != 0) {
-          // not a publisher: only follow the global bound
+          // not a publisher: the global bound arrives with the periodic refresh
           __syncwarp();
-          if (!(a.flags & 2)) refresh_tg(j);
-          else setT(j, t < Tj ? t : Tj);
+          setT(j, t < Tj ? t : Tj);
           continue;
         }
         if (!ws->pubd[j]) {
@@ -373,15 +387,19 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
         __syncwarp();
         if (lane == 0) ws->pubd[j] = 1;
         __syncwarp();
-        tighten_tg(a, qi, lane);
-        refresh_tg(j);
+        const u32 tt = tighten_tg(a, qi, lane);
+        const u32 lim = (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
+        const u32 nt = t < lim ? t : lim;
+        setT(j, nt < Tj ? nt : Tj);
         __syncwarp();
       }
     }
   };
 
-  constexpr int U = (QW == 1) ? 2 : 1;
-  constexpr int REFRESH = 8;  // loop trips between global-bound refreshes (one hot L2 line)
+  constexpr int U = 1;  // iterations per trip (QW == 1 keeps two trips in flight)
+  // loop trips between global-bound refreshes (tg is replicated over L2 slices
+  // for small Q, so the single-query kernel can afford one load per trip)
+  constexpr int REFRESH = (QW == 1) ? 2 : 8;
   u64 it = it0;
   int since_refresh = 0;
   // The global bound is loaded one refresh period before it is applied, so the
@@ -391,7 +409,7 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
   // refresh directly, keeping registers for the query words.)
   u32 tgp = T_OPEN;
   auto prefetch_tg = [&]() {
-    if (QW == 1 && qg < a.Q) tgp = *((volatile const u32*)a.tg + qg);
+    if (QW == 1 && qg < a.Q) tgp = *(volatile const u32*)tgrep(a, qg, (u32)(g % a.tg_rep));
   };
   auto apply_tg = [&]() {
     if (QW == 1) {
@@ -403,21 +421,114 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
     }
   };
   if (MODE == MODE_TOPK && !(a.flags & 2)) prefetch_tg();
-  for (; it + U <= it1; it += U) {
+  // Only the globally last iteration can hold entries >= n; the main range is
+  // scanned without per-entry masking.
+  const u64 it_main = it1 < n_full ? it1 : n_full;
+  struct Trip {
     u64 A[U][E], B[U][E], C[U][E];
+  };
+  auto load_trip = [&](Trip& t, u64 i0) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const u64 off = (it + u) * (32 * E) + (u64)lane * E;
-      ld_entries(a.w0 + off, A[u]);
-      ld_entries(a.w1 + off, B[u]);
-      ld_entries(a.w2 + off, C[u]);
+      const u64 off = (i0 + u) * (32 * E) + (u64)lane * E;
+      ld_entries(a.w0 + off, t.A[u]);
+      ld_entries(a.w1 + off, t.B[u]);
+      ld_entries(a.w2 + off, t.C[u]);
     }
+  };
+  auto run_trip = [&](const Trip& t, u64 i0) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) process(A[u], B[u], C[u], it + u, it + u >= n_full);
+    for (int u = 0; u < U; ++u) process(t.A[u], t.B[u], t.C[u], i0 + u, false);
     if (MODE == MODE_TOPK && !(a.flags & 2) && ++since_refresh == REFRESH) {
       since_refresh = 0;
       apply_tg();
       prefetch_tg();
+    }
+  };
+  if (QW == 1 && a.sched != nullptr) {
+    // HBM-bound single-query scan. Warps claim chunks of chunk_iters
+    // iterations from a global counter (dynamic balance: no straggler parts);
+    // claims only grow, so every warp still walks the library in ascending
+    // index order and the exact tie rule of the filter holds. The next claim
+    // is issued a whole chunk before it is needed, and the next iteration's
+    // loads are in flight while the current one is processed.
+    const u64 CH = a.chunk_iters;
+    const u64 n_chunks = (a.iters + CH - 1) / CH;
+    auto claim = [&]() -> u32 { return lane == 0 ? atomicAdd(a.sched, 1u) : 0u; };
+    u32 pend = claim();
+    u64 cur = __shfl_sync(FULL, pend, 0);
+    pend = claim();
+    u64 nxt = n_chunks;  // resolved from `pend` at the first chunk switch
+    bool have_pend = true;
+    auto advance = [&](u64& i, u64& e) -> bool {
+      if (++i < e) return true;
+      if (have_pend) { nxt = __shfl_sync(FULL, pend, 0); have_pend = false; }
+      if (nxt >= n_chunks) return false;
+      i = nxt * CH;
+      e = i + CH < a.iters ? i + CH : a.iters;
+      pend = claim();
+      have_pend = true;
+      return true;
+    };
+    auto step = [&](const Trip& t, u64 i) {
+      if (i < n_full) run_trip(t, i);
+      else process(t.A[0], t.B[0], t.C[0], i, true);
+    };
+    if (cur < n_chunks) {
+      u64 i = cur * CH;
+      u64 e = i + CH < a.iters ? i + CH : a.iters;
+      Trip P, R;
+      load_trip(P, i);
+      while (true) {
+        u64 ni = i, ne = e;
+        bool more = advance(ni, ne);
+        if (more) load_trip(R, ni);
+        step(P, i);
+        if (!more) break;
+        i = ni;
+        e = ne;
+        ni = i;
+        ne = e;
+        more = advance(ni, ne);
+        if (more) load_trip(P, ni);
+        step(R, i);
+        if (!more) break;
+        i = ni;
+        e = ne;
+      }
+    } else if (have_pend) {
+      (void)__shfl_sync(FULL, pend, 0);
+    }
+    it = it1;  // the static tail loop below has nothing left to do
+    fence_acq_rel_gpu();
+    if (lane == 0) {
+      const u32 done = atomicAdd(a.sched + 1, 1u);
+      if (done == (u32)(a.n_qg * a.n_parts) - 1) {
+        a.sched[0] = 0;
+        a.sched[1] = 0;
+      }
+    }
+  } else if (QW == 1) {
+    // static parts, software-pipelined (used when no scheduler is supplied)
+    Trip P, R;
+    if (it + U <= it_main) load_trip(P, it);
+    while (it + U <= it_main) {
+      const bool more = it + 2 * U <= it_main;
+      if (more) load_trip(R, it + U);
+      run_trip(P, it);
+      it += U;
+      if (!more) break;
+      const bool more2 = it + 2 * U <= it_main;
+      if (more2) load_trip(P, it + U);
+      run_trip(R, it);
+      it += U;
+      if (!more2) break;
+    }
+  } else {
+    for (; it + U <= it_main; it += U) {
+      Trip t;
+      load_trip(t, it);
+      run_trip(t, it);
     }
   }
   for (; it < it1; ++it) {
@@ -447,9 +558,10 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
     for (int j = 0; j < QW; ++j) {
       const u32 qi = qg * QW + j;
       if (qi >= a.Q) continue;
+      if (a.flags & 16) continue;  // experiment: skip the survivor flush (wrong results)
       if (ws->cnt[j] > a.k) compact(j);
       const u32 n = ws->cnt[j];
-      const u32 t = *((volatile const u32*)a.tg + qi);
+      const u32 t = *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));
       const u64* bj = wbuf + (u64)j * a.cap;
       // survivors: d <= tg (an exact bound on the k-th distance)
       for (u32 i0 = 0; i0 < n; i0 += 32) {
@@ -474,7 +586,8 @@ __global__ void __launch_bounds__(256, (QW >= 4 ? 2 : 3)) scan_kernel(const Scan
 // the next call starts clean without a memset launch.
 // ---------------------------------------------------------------------------
 constexpr int SEL_THREADS = 512;
-constexpr int SEL_ECAP = 4096;  // ties at the threshold sorted in shared memory
+constexpr int SEL_ECAP = 4096;      // ties at the threshold held in shared memory
+constexpr u32 SEL_RANK_MAX = 2048;  // rank-select / rank-sort (one pass) up to this many keys
 
 __device__ void block_bitonic_sort(u64* s, int n_pow2) {
   for (int size = 2; size <= n_pow2; size <<= 1) {
@@ -492,22 +605,31 @@ __device__ void block_bitonic_sort(u64* s, int n_pow2) {
 }
 
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
-                                                             u32* ghist, u32 gstride, u32 k, u64* out_keys,
-                                                             u32* out_cnt, int reset) {
+                                                             u32* ghist, u32 gstride, u32 tg_rep, u32 k,
+                                                             u64* out_keys, u32* out_cnt, int reset) {
   extern __shared__ u64 ssel[];  // [k_pow2] result + [SEL_ECAP] ties
   __shared__ u32 hist[256];
   __shared__ u32 s_nres, s_ntie, s_T, s_m;
   __shared__ u64 s_cut;
+  // launched as a programmatic dependent of the scan: wait for its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const u32 q = blockIdx.x;
   const u32 n = cand_cnt[q];
   const u64* c = cand + (u64)q * cand_cap;
-  const u32 bound = tg[q];
+  const u32 bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
   for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
   if (threadIdx.x == 0) { s_nres = 0; s_ntie = 0; }
   __syncthreads();
-  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
-    u32 d = key_d(c[i]);
-    if (d <= bound) atomicAdd(&hist[d], 1u);
+  const int lane = threadIdx.x & 31;
+  // uniform trip counts so every warp-collective below sees the full warp
+  for (u32 base = 0; base < n; base += blockDim.x) {
+    const u32 i = base + threadIdx.x;
+    const u32 d = i < n ? key_d(c[i]) : 0xffffu;
+    const bool valid = i < n && d <= bound;
+    // hot bins (many candidates share a distance): one shared atomic per
+    // distinct distance per warp instead of one per candidate
+    const u32 peers = __match_any_sync(FULL, valid ? d : 0xffffu);
+    if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&hist[d], (u32)__popc(peers));
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -538,16 +660,44 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   u64* ties = ssel + kp;
   const u32 ntie_total = T < 256 ? hist[T] : 0;
   const bool ties_fit = ntie_total <= SEL_ECAP;
-  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
-    u64 key = c[i];
-    u32 d = key_d(key);
-    if (d > bound) continue;
-    if (d < T) res[atomicAdd(&s_nres, 1u)] = key;
-    else if (d == T && ties_fit) ties[atomicAdd(&s_ntie, 1u)] = key;
+  for (u32 base = 0; base < n; base += blockDim.x) {
+    const u32 i = base + threadIdx.x;
+    const u64 key = i < n ? c[i] : ~0ull;
+    const u32 d = key_d(key);
+    const bool ok = i < n && d <= bound;
+    const bool take = ok && d < T;
+    const bool tie = ok && d == T && ties_fit;
+    // warp-aggregated appends (one shared atomic per warp per list)
+    const u32 tb = __ballot_sync(FULL, take), eb = __ballot_sync(FULL, tie);
+    u32 rb = 0, ebase = 0;
+    if (lane == 0) {
+      if (tb) rb = atomicAdd(&s_nres, (u32)__popc(tb));
+      if (eb) ebase = atomicAdd(&s_ntie, (u32)__popc(eb));
+    }
+    rb = __shfl_sync(FULL, rb, 0);
+    ebase = __shfl_sync(FULL, ebase, 0);
+    if (take) res[rb + __popc(tb & lanemask_lt())] = key;
+    if (tie) ties[ebase + __popc(eb & lanemask_lt())] = key;
   }
   __syncthreads();
   if (T < 256 && m > 0) {
-    if (ties_fit) {
+    if (ntie_total <= m) {
+      // every tie is in the answer
+      for (u32 i = threadIdx.x; i < ntie_total; i += blockDim.x) res[s_nres + i] = ties[i];
+      __syncthreads();
+      if (threadIdx.x == 0) s_nres += ntie_total;
+    } else if (ties_fit && ntie_total <= SEL_RANK_MAX) {
+      // rank selection: keys are unique, so the m smallest have ranks 0..m-1
+      const u32 base = s_nres;
+      for (u32 i = threadIdx.x; i < ntie_total; i += blockDim.x) {
+        const u64 x = ties[i];
+        u32 r = 0;
+        for (u32 j = 0; j < ntie_total; ++j) r += ties[j] < x;
+        if (r < m) res[base + r] = x;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_nres = base + m;
+    } else if (ties_fit) {
       int tp = 1;
       while (tp < (int)ntie_total) tp <<= 1;
       for (int i = ntie_total + threadIdx.x; i < tp; i += blockDim.x) ties[i] = ~0ull;
@@ -575,9 +725,9 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
         __syncthreads();
         if (threadIdx.x == 0) {
           u32 cc = 0;
-          for (int b = 0; b < 256; ++b) {
-            if (cc + hist[b] >= need) { s_cut = prefix | ((u64)b << shift); s_m = need - cc; break; }
-            cc += hist[b];
+          for (int bb = 0; bb < 256; ++bb) {
+            if (cc + hist[bb] >= need) { s_cut = prefix | ((u64)bb << shift); s_m = need - cc; break; }
+            cc += hist[bb];
           }
         }
         __syncthreads();
@@ -589,19 +739,31 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
         u64 key = c[i];
         if (key_d(key) == T && (key & IDX_MASK) <= prefix) res[atomicAdd(&s_nres, 1u)] = key;
       }
-      __syncthreads();
     }
   }
   __syncthreads();
   const u32 nres = s_nres;
-  for (int i = nres + threadIdx.x; i < kp; i += blockDim.x) res[i] = ~0ull;
-  __syncthreads();
-  block_bitonic_sort(res, kp);
-  for (u32 i = threadIdx.x; i < k; i += blockDim.x) out_keys[(u64)q * k + i] = i < nres ? res[i] : ~0ull;
+  u64* out = out_keys + (u64)q * k;
+  if (nres <= SEL_RANK_MAX) {
+    // final order by rank (unique keys): one pass, no shared-memory sort
+    for (u32 i = threadIdx.x; i < nres; i += blockDim.x) {
+      const u64 x = res[i];
+      u32 r = 0;
+      for (u32 j = 0; j < nres; ++j) r += res[j] < x;
+      out[r] = x;
+    }
+    for (u32 i = nres + threadIdx.x; i < k; i += blockDim.x) out[i] = ~0ull;
+  } else {
+    for (int i = nres + threadIdx.x; i < kp; i += blockDim.x) res[i] = ~0ull;
+    __syncthreads();
+    block_bitonic_sort(res, kp);
+    for (u32 i = threadIdx.x; i < k; i += blockDim.x) out[i] = i < nres ? res[i] : ~0ull;
+  }
   if (threadIdx.x == 0) out_cnt[q] = nres;
   if (reset) {
     for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
-    if (threadIdx.x == 0) { tg[q] = T_OPEN; cand_cnt[q] = 0; }
+    for (u32 r = threadIdx.x; r < tg_rep; r += blockDim.x) tg[((u64)q * tg_rep + r) * gstride] = T_OPEN;
+    if (threadIdx.x == 0) cand_cnt[q] = 0;
   }
 }
 

@@ -133,7 +133,8 @@ __global__ void flush_kernel(unsigned* buf, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) buf[i] = (unsigned)i;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  bool only_stream = argc > 2;
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("device %s SMs %d l2 %d MB clock %d kHz\n", prop.name, prop.multiProcessorCount, prop.l2CacheSize >> 20, clk);
@@ -141,7 +142,7 @@ int main() {
   unsigned* out; long long* cyc; CK(cudaMalloc(&out, 1 << 26)); CK(cudaMalloc(&cyc, 1 << 20));
   long long hc[4096];
   const char* names[3] = {"POPC", "LOP3", "IADD3"};
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < (only_stream ? 0 : 3); ++mode) {
     for (int threads : {256, 512, 1024}) {
       int blocks = sms * (2048 / threads);
       int iters = 4096;
@@ -156,7 +157,7 @@ int main() {
       printf("%s threads/blk %d: %.2f ops/clk/SM (max block cycles %.0f)\n", names[mode], threads, ops / mx, mx);
     }
   }
-  {
+  if (!only_stream) {
     int threads = 256, blocks = sms * 8, iters = 4096;
     dist_kernel<<<blocks, threads>>>(out, iters, cyc, 12345); CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(hc, cyc, blocks * 8, cudaMemcpyDeviceToHost));
@@ -164,7 +165,7 @@ int main() {
     double comps = 2048.0 * iters * 8;
     printf("dist(8q, popcll): %.3f comparisons/clk/SM\n", comps / mx);
   }
-  long long n = 95417114LL / 128 * 128;
+  long long n = (argc > 1 ? atoll(argv[1]) : 95417114LL) / 128 * 128;
   unsigned long long *p0, *p1, *p2; unsigned* fl;
   CK(cudaMalloc(&p0, n * 8)); CK(cudaMalloc(&p1, n * 8)); CK(cudaMalloc(&p2, n * 8));
   CK(cudaMemset(p0, 1, n * 8)); CK(cudaMemset(p1, 2, n * 8)); CK(cudaMemset(p2, 3, n * 8));
