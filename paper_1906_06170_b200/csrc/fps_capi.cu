@@ -346,6 +346,14 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   CUDA_TRY(launch_select(Q, sel_smem, s, a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, a.tg_rep, k,
                          d_keys, d_cnt, !(a.flags & 32)));
   L->launches++;
+  if (std::getenv("FPS_DEBUG")) {
+    unsigned long long t[12] = {0};
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(t, fps::g_sel_clock, sizeof(t));
+    std::fprintf(stderr, "[fps] select phases (cycles from start):");
+    for (int i = 1; i < 12; ++i) std::fprintf(stderr, " %lld", t[i] ? (long long)(t[i] - t[0]) : -1ll);
+    std::fprintf(stderr, "\n");
+  }
   CUDA_TRY(cudaGetLastError());
   return FPS_OK;
 }

@@ -60,6 +60,20 @@ __device__ __forceinline__ u32 dist3(u64 a, u64 b, u64 c, u64 q0, u64 q1, u64 q2
   return (u32)(__popcll(a ^ q0) + __popcll(b ^ q1) + __popcll(c ^ q2));
 }
 
+// Same distance with 4 POPC instead of 6: two full adders (carry-save) fold
+// the six 32-bit XOR words into sums s1, s2 and carries c1, c2 with
+// popc(x0)+popc(x1)+popc(x2) = popc(s1) + 2 popc(c1). POPC issues at 16/clk/SM
+// on B200 vs 64/clk for LOP3, so the compute-bound multi-query scan trades
+// two POPC for four LOP3 per comparison.
+__device__ __forceinline__ u32 dist3_csa(u64 a, u64 b, u64 c, u64 q0, u64 q1, u64 q2) {
+  const u64 ya = a ^ q0, yb = b ^ q1, yc = c ^ q2;
+  const u32 x0 = (u32)ya, x1 = (u32)(ya >> 32), x2 = (u32)yb;
+  const u32 x3 = (u32)(yb >> 32), x4 = (u32)yc, x5 = (u32)(yc >> 32);
+  const u32 s1 = x0 ^ x1 ^ x2, c1 = (x0 & x1) | (x2 & (x0 ^ x1));
+  const u32 s2 = x3 ^ x4 ^ x5, c2 = (x3 & x4) | (x5 & (x3 ^ x4));
+  return (u32)(__popc(s1) + __popc(s2)) + 2u * (u32)(__popc(c1) + __popc(c2));
+}
+
 // Release/acquire fence at GPU scope (cheaper than __threadfence()'s fence.sc).
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
@@ -285,7 +299,7 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
       }
       return best;
     }
-    return dist3(x, y, z, q0[j], q1[j], q2[j]);
+    return QW >= 2 ? dist3_csa(x, y, z, q0[j], q1[j], q2[j]) : dist3(x, y, z, q0[j], q1[j], q2[j]);
   };
 
   auto process = [&](const u64 (&A)[E], const u64 (&B)[E], const u64 (&C)[E], u64 it, bool masked) {
@@ -318,7 +332,8 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
       u32 m = 0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        dd[e] = MINQ ? dist_of(A[e], B[e], C[e], 0) : dist3(A[e], B[e], C[e], x0, x1, x2);
+        dd[e] = MINQ ? dist_of(A[e], B[e], C[e], 0)
+                     : (QW >= 2 ? dist3_csa(A[e], B[e], C[e], x0, x1, x2) : dist3(A[e], B[e], C[e], x0, x1, x2));
         if (masked && first + e >= a.n) dd[e] = DMASKED;
         if (dd[e] < Tj) m |= 1u << e;
       }
@@ -586,6 +601,23 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
 // the next call starts clean without a memset launch.
 // ---------------------------------------------------------------------------
 constexpr int SEL_THREADS = 512;
+
+// Number of keys in s[0, n) smaller than x; four independent counters keep
+// the dependent add chain short (shared-memory broadcast reads).
+__device__ __forceinline__ u32 rank_in(const u64* s, u32 n, u64 x) {
+  u32 r0 = 0, r1 = 0, r2 = 0, r3 = 0, j = 0;
+  for (; j + 4 <= n; j += 4) {
+    r0 += s[j] < x;
+    r1 += s[j + 1] < x;
+    r2 += s[j + 2] < x;
+    r3 += s[j + 3] < x;
+  }
+  for (; j < n; ++j) r0 += s[j] < x;
+  return r0 + r1 + r2 + r3;
+}
+// phase timestamps of the last select CTA (debug: FPS_DEBUG prints them)
+__device__ unsigned long long g_sel_clock[12];
+#define SEL_MARK(i) do { if (threadIdx.x == 0) g_sel_clock[i] = clock64(); } while (0)
 constexpr int SEL_ECAP = 4096;      // ties at the threshold held in shared memory
 constexpr u32 SEL_RANK_MAX = 2048;  // rank-select / rank-sort (one pass) up to this many keys
 
@@ -613,13 +645,14 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   __shared__ u64 s_cut;
   // launched as a programmatic dependent of the scan: wait for its results
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  SEL_MARK(0);
   const u32 q = blockIdx.x;
   const u32 n = cand_cnt[q];
   const u64* c = cand + (u64)q * cand_cap;
   const u32 bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
   for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
   if (threadIdx.x == 0) { s_nres = 0; s_ntie = 0; }
-  __syncthreads();
+  __syncthreads(); SEL_MARK(1);
   const int lane = threadIdx.x & 31;
   // uniform trip counts so every warp-collective below sees the full warp
   for (u32 base = 0; base < n; base += blockDim.x) {
@@ -631,7 +664,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
     const u32 peers = __match_any_sync(FULL, valid ? d : 0xffffu);
     if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&hist[d], (u32)__popc(peers));
   }
-  __syncthreads();
+  __syncthreads(); SEL_MARK(2);
   if (threadIdx.x < 32) {
     // find T: smallest t with cum >= k (scan 256 bins, 8 per lane)
     int lane = threadIdx.x;
@@ -652,7 +685,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
       }
     }
   }
-  __syncthreads();
+  __syncthreads(); SEL_MARK(3);
   const u32 T = s_T, m = s_m;
   u64* res = ssel;
   int kp = 1;
@@ -679,7 +712,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
     if (take) res[rb + __popc(tb & lanemask_lt())] = key;
     if (tie) ties[ebase + __popc(eb & lanemask_lt())] = key;
   }
-  __syncthreads();
+  __syncthreads(); SEL_MARK(4);
   if (T < 256 && m > 0) {
     if (ntie_total <= m) {
       // every tie is in the answer
@@ -690,10 +723,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
       // rank selection: keys are unique, so the m smallest have ranks 0..m-1
       const u32 base = s_nres;
       for (u32 i = threadIdx.x; i < ntie_total; i += blockDim.x) {
-        const u64 x = ties[i];
-        u32 r = 0;
-        for (u32 j = 0; j < ntie_total; ++j) r += ties[j] < x;
-        if (r < m) res[base + r] = x;
+        const u32 r = rank_in(ties, ntie_total, ties[i]);
+        if (r < m) res[base + r] = ties[i];
       }
       __syncthreads();
       if (threadIdx.x == 0) s_nres = base + m;
@@ -741,17 +772,12 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
       }
     }
   }
-  __syncthreads();
+  __syncthreads(); SEL_MARK(5);
   const u32 nres = s_nres;
   u64* out = out_keys + (u64)q * k;
   if (nres <= SEL_RANK_MAX) {
     // final order by rank (unique keys): one pass, no shared-memory sort
-    for (u32 i = threadIdx.x; i < nres; i += blockDim.x) {
-      const u64 x = res[i];
-      u32 r = 0;
-      for (u32 j = 0; j < nres; ++j) r += res[j] < x;
-      out[r] = x;
-    }
+    for (u32 i = threadIdx.x; i < nres; i += blockDim.x) out[rank_in(res, nres, res[i])] = res[i];
     for (u32 i = nres + threadIdx.x; i < k; i += blockDim.x) out[i] = ~0ull;
   } else {
     for (int i = nres + threadIdx.x; i < kp; i += blockDim.x) res[i] = ~0ull;
@@ -760,6 +786,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
     for (u32 i = threadIdx.x; i < k; i += blockDim.x) out[i] = i < nres ? res[i] : ~0ull;
   }
   if (threadIdx.x == 0) out_cnt[q] = nres;
+  SEL_MARK(11);
   if (reset) {
     for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
     for (u32 r = threadIdx.x; r < tg_rep; r += blockDim.x) tg[((u64)q * tg_rep + r) * gstride] = T_OPEN;
