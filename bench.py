@@ -402,9 +402,10 @@ def run_ours(args, rank: int, local_rank: int, world: int):
 
     # roofline of the scan kernel
     peaks = measured_peaks()
+    compact, bpe = lib.layout()
     if plan.radius is None and Q <= 4:
         bound = "hbm"
-        bytes_per_launch = 24.0 * count
+        bytes_per_launch = float(bpe) * count
         achieved = bytes_per_launch / (scan_avg_ms / 1e3) / 1e9
         peak = float(peaks.get("hbm_gbs", 6650.0))
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -425,7 +426,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
                 "peak_source": f"{sm} SMs x 16 POPC/clk/SM (measured) / {per_cmp:.0f} POPC per comparison x "
                                f"{mhz:.0f} MHz (median SM clock in the timed region)",
                 "naive_6popc_peak": naive, "naive_6popc_frac": achieved / naive,
-                "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": 24.0 * count}
+                "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": float(bpe) * count}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -435,7 +436,8 @@ def run_ours(args, rank: int, local_rank: int, world: int):
                    "l2": "flushed between steps outside the timed events (2xL2 write, then 2xL2 read so no dirty "
                          "lines are left)" if flush else
                    "library larger than 4x L2; no flush",
-                   "layout": "SoA 3 x u64 planes"},
+                   "layout": (f"tiles of 128 entries, SoA inside a tile, {bpe} B/entry "
+                              f"({'compact: word 2 as u32 + u8' if compact else 'full: 3 x u64'})")},
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps},

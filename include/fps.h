@@ -81,8 +81,13 @@ int fps_open_generated(uint64_t n, uint64_t start, uint64_t seed_key, const uint
                        const uint8_t* thr_all166, int device, uint64_t index_base, fps_lib** out);
 int fps_close(fps_lib* lib);
 int fps_info(const fps_lib* lib, uint64_t* n, uint64_t* index_base, int* device);
-/* Device pointers of the three planes (each n_alloc >= n u64; tail is zero). */
-int fps_planes(fps_lib* lib, uint64_t** d_w0, uint64_t** d_w1, uint64_t** d_w2, uint64_t* n_alloc);
+/* HBM layout: tiles, each a small structure of arrays (w0[] | w1[] | word 2).
+ * Default: 128-entry tiles of three u64 sub-planes, 24 B per entry.
+ * compact = 1 (opt-in, FPS_LAYOUT=compact, only when no entry sets bits 40.. of
+ * word 2): word 2 as u32 (bits 0..31) + u8 (bits 32..39), 21 B per entry. */
+int fps_layout(const fps_lib* lib, int* compact, uint64_t* bytes_per_entry);
+/* Copy entries [start, start + count) back as count x 3 u64 rows (host). */
+int fps_read_entries(fps_lib* lib, uint64_t start, uint64_t count, uint64_t* rows);
 /* Overwrite entries idx[i] (local indices) with rows words[i] (host, m x 3). */
 int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, uint64_t m);
 

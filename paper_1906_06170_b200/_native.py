@@ -46,7 +46,8 @@ SIGNATURES = {
                                      C.POINTER(_vp)]),
     "fps_close": (C.c_int, [_vp]),
     "fps_info": (C.c_int, [_vp, _u64p, _u64p, C.POINTER(C.c_int)]),
-    "fps_planes": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _u64p]),
+    "fps_layout": (C.c_int, [_vp, C.POINTER(C.c_int), _u64p]),
+    "fps_read_entries": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _vp]),
     "fps_write_entries": (C.c_int, [_vp, _vp, _vp, C.c_uint64]),
     "fps_topk": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "fps_topk_min": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),

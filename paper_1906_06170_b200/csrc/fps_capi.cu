@@ -112,7 +112,10 @@ struct fps_lib {
   int device = 0;
   int sms = 148;
   u64 n = 0, n_alloc = 0, index_base = 0;
-  u64* planes = nullptr;  // 3 * n_alloc
+  // tiles of 128 entries (fps_kernels.cuh TILE_BYTES_*); compact (21 B / entry)
+  // unless some entry uses bits 40.. of word 2, then full (24 B / entry)
+  bool compact = false;
+  char* mem = nullptr;
   cudaStream_t stream = nullptr;
   std::mutex mu;
   std::atomic<u64> launches{0};
@@ -127,9 +130,8 @@ struct fps_lib {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   size_t ev_used = 0;
-  u64* w0() const { return planes; }
-  u64* w1() const { return planes + n_alloc; }
-  u64* w2() const { return planes + 2 * n_alloc; }
+  fps::PlanesOut out() const { return fps::PlanesOut{mem, compact ? 1 : 0}; }
+  u64 bytes_per_entry() const { return compact ? 21 : 24; }
 };
 
 namespace {
@@ -153,15 +155,15 @@ size_t scan_smem() {
   return (size_t)WPB * (QW * fps::HB * sizeof(u32) + sizeof(fps::WarpState<QW>));
 }
 
-template <int QW, int E, int MODE>
+template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
 int max_ctas_per_sm() {
   static int cached = 0;
   if (cached) return cached;
   size_t smem = scan_smem<QW, E, MODE>();
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fps::scan_kernel<QW, E, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+  auto* k = fps::scan_kernel<QW, E, MODE, MINQ, CMP>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int blocks = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fps::scan_kernel<QW, E, MODE>, WPB * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, WPB * 32, smem);
   cached = std::max(1, blocks);
   return cached;
 }
@@ -173,14 +175,14 @@ void pick_shape(u32 Q, int* qw, int* e) {
   else { *qw = 8; *e = 2; }
 }
 
-template <int QW, int E, int MODE>
+template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
 Config make_config(const fps_lib* L, u32 Q, u32 k) {
   Config c{};
   c.qw = QW;
   c.e = E;
   c.n_qg = (Q + QW - 1) / QW;
   c.iters = (L->n + 32 * E - 1) / (32 * E);
-  const u64 slots = (u64)L->sms * max_ctas_per_sm<QW, E, MODE>() * WPB;
+  const u64 slots = (u64)L->sms * max_ctas_per_sm<QW, E, MODE, MINQ, CMP>() * WPB;
   u64 parts = std::max<u64>(1, slots / c.n_qg);
   const u64 min_iters = (QW == 1) ? 8 : 2;  // keep per-warp parts long enough to amortise warm-up
   parts = std::min<u64>(parts, std::max<u64>(1, c.iters / min_iters));
@@ -256,9 +258,7 @@ fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
     return e ? (u32)std::strtoul(e, nullptr, 0) : 8u;
   }();
   a.chunk_iters = chunk;
-  a.w0 = L->w0();
-  a.w1 = L->w1();
-  a.w2 = L->w2();
+  a.lib = L->mem;
   a.n = L->n;
   a.index_base = L->index_base;
   a.queries = d_q;
@@ -296,9 +296,9 @@ std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
   return &L->ev_pool[L->ev_used++];
 }
 
-template <int QW, int E>
+template <int QW, int E, bool CMP>
 int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only) {
-  Config c = make_config<QW, E, fps::MODE_TOPK>(L, Q, k);
+  Config c = make_config<QW, E, fps::MODE_TOPK, false, CMP>(L, Q, k);
   int rc;
   if ((rc = ensure_state(L, Q))) return rc;
   if ((rc = L->buf.ensure(c.warps * QW * (size_t)c.cap * 8))) return rc;
@@ -322,7 +322,7 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   if (c.warps > 0 && L->n > 0) {
     auto* ev = timing_slot(L);
     if (ev) cudaEventRecord(ev->first, s);
-    fps::scan_kernel<QW, E, fps::MODE_TOPK><<<c.grid, WPB * 32, c.smem, s>>>(a);
+    fps::scan_kernel<QW, E, fps::MODE_TOPK, false, CMP><<<c.grid, WPB * 32, c.smem, s>>>(a);
     if (ev) cudaEventRecord(ev->second, s);
     L->launches++;
   }
@@ -362,22 +362,28 @@ int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_
                   bool prepare_only) {
   int qw, e;
   pick_shape(Q, &qw, &e);
-  if (qw == 1) return topk_fused<1, 4>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
-  if (qw == 2) return topk_fused<2, 2>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
-  if (qw == 4) return topk_fused<4, 2>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
-  return topk_fused<8, 2>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (L->compact) {
+    if (qw == 1) return topk_fused<1, 4, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+    if (qw == 2) return topk_fused<2, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+    if (qw == 4) return topk_fused<4, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+    return topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  }
+  if (qw == 1) return topk_fused<1, 4, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (qw == 2) return topk_fused<2, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (qw == 4) return topk_fused<4, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  return topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
 }
 
-template <int QW, int E, int MODE>
+template <int QW, int E, int MODE, bool CMP>
 int launch_plain(fps_lib* L, fps::ScanArgs a, cudaStream_t s) {
-  Config c = make_config<QW, E, MODE>(L, a.Q, 1);
+  Config c = make_config<QW, E, MODE, false, CMP>(L, a.Q, 1);
   a.n_qg = c.n_qg;
   a.n_parts = c.n_parts;
   a.iters = c.iters;
   if (c.warps == 0 || L->n == 0) return FPS_OK;
   auto* ev = timing_slot(L);
   if (ev) cudaEventRecord(ev->first, s);
-  fps::scan_kernel<QW, E, MODE><<<c.grid, WPB * 32, c.smem, s>>>(a);
+  fps::scan_kernel<QW, E, MODE, false, CMP><<<c.grid, WPB * 32, c.smem, s>>>(a);
   if (ev) cudaEventRecord(ev->second, s);
   L->launches++;
   CUDA_TRY(cudaGetLastError());
@@ -388,10 +394,16 @@ template <int MODE>
 int plain_dispatch(fps_lib* L, const fps::ScanArgs& a, cudaStream_t s) {
   int qw, e;
   pick_shape(a.Q, &qw, &e);
-  if (qw == 1) return launch_plain<1, 4, MODE>(L, a, s);
-  if (qw == 2) return launch_plain<2, 2, MODE>(L, a, s);
-  if (qw == 4) return launch_plain<4, 2, MODE>(L, a, s);
-  return launch_plain<8, 2, MODE>(L, a, s);
+  if (L->compact) {
+    if (qw == 1) return launch_plain<1, 4, MODE, true>(L, a, s);
+    if (qw == 2) return launch_plain<2, 2, MODE, true>(L, a, s);
+    if (qw == 4) return launch_plain<4, 2, MODE, true>(L, a, s);
+    return launch_plain<8, 2, MODE, true>(L, a, s);
+  }
+  if (qw == 1) return launch_plain<1, 4, MODE, false>(L, a, s);
+  if (qw == 2) return launch_plain<2, 2, MODE, false>(L, a, s);
+  if (qw == 4) return launch_plain<4, 2, MODE, false>(L, a, s);
+  return launch_plain<8, 2, MODE, false>(L, a, s);
 }
 
 int sort_keys(fps_lib* L, u64* d_keys, u64 n, cudaStream_t s) {
@@ -457,18 +469,30 @@ int stage_queries(fps_lib* L, const uint64_t* queries, u32 Q) {
   return FPS_OK;
 }
 
-int alloc_planes(fps_lib* L, u64 n) {
+// The compact 21 B/entry tiles read 12.5 % fewer bytes but measured slower on
+// B200 (C3: 357 vs 341 us; profiles/r01_experiments.md), so the 24 B tiles are
+// the default and compact is opt-in (FPS_LAYOUT=compact).
+bool force_full_layout() {
+  const char* e = std::getenv("FPS_LAYOUT");
+  return !(e && std::string(e) == "compact");
+}
+
+int alloc_planes(fps_lib* L, u64 n, bool compact) {
   L->n = n;
-  L->n_alloc = (n + 255) / 256 * 256 + 256;  // whole vector iterations + slack, zero tail
-  size_t bytes = (size_t)L->n_alloc * 3 * 8;
-  cudaError_t e = cudaMalloc(&L->planes, bytes);
+  L->compact = compact && !force_full_layout();
+  // whole tiles plus two tiles of zero slack (vector loads never leave the allocation)
+  const u64 te = fps::tile_entries(L->compact);
+  const u64 tiles = (n + te - 1) / te + 2;
+  L->n_alloc = tiles * te;
+  const size_t bytes = (size_t)tiles * fps::tile_bytes(L->compact);
+  cudaError_t e = cudaMalloc(&L->mem, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    L->planes = nullptr;
-    return fail(FPS_ENOMEM, std::string("library planes cudaMalloc(") + std::to_string(bytes) +
+    L->mem = nullptr;
+    return fail(FPS_ENOMEM, std::string("library cudaMalloc(") + std::to_string(bytes) +
                                 "): " + cudaGetErrorString(e));
   }
-  CUDA_TRY(cudaMemsetAsync(L->planes, 0, bytes, L->stream));
+  CUDA_TRY(cudaMemsetAsync(L->mem, 0, bytes, L->stream));
   return FPS_OK;
 }
 
@@ -503,7 +527,7 @@ void destroy(fps_lib* L) {
   if (!L) return;
   DeviceGuard g(L->device);
   if (L->stream) cudaStreamSynchronize(L->stream);
-  if (L->planes) cudaFree(L->planes);
+  if (L->mem) cudaFree(L->mem);
   for (DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt, &L->radius,
                     &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->sched})
     b->release();
@@ -603,20 +627,34 @@ int fps_open(const uint64_t* words, uint64_t n, int layout, int device, uint64_t
   int stride, col0;
   if (layout == FPS_LAYOUT_ROWS3) { stride = 3; col0 = 0; }
   else if (layout == FPS_LAYOUT_FPS1) { stride = 4; col0 = 1; }
-  else if (layout == FPS_LAYOUT_PLANES) { stride = 0; col0 = 0; }
+  else if (layout == FPS_LAYOUT_PLANES) { stride = 1; col0 = 0; }
   else return fail(FPS_EINVAL, "unknown layout");
+  // Host pre-scan: the compact layout keeps bits 0..39 of word 2, so it is
+  // exact iff no entry sets bits 40.. (always true for valid fingerprints;
+  // FPS1 pad bytes are scanned as stored, like the reference).
+  bool wide = false;
+  for (u64 i = 0; i < n && !wide; ++i) {
+    const u64 c = layout == FPS_LAYOUT_PLANES ? words[2 * n + i] : words[i * stride + col0 + 2];
+    wide = (c >> 40) != 0;
+  }
   fps_lib* L = nullptr;
   int rc = new_lib(device, index_base, &L);
   if (rc) return rc;
   DeviceGuard g(device);
-  if ((rc = alloc_planes(L, n))) { destroy(L); return rc; }
+  if ((rc = alloc_planes(L, n, !wide))) { destroy(L); return rc; }
   DevBuf bad;
   if ((rc = bad.ensure(4))) { destroy(L); return rc; }
   cudaMemsetAsync(bad.p, 0, 4, L->stream);
-  if (layout == FPS_LAYOUT_PLANES) {
-    for (int p = 0; p < 3; ++p)
-      cudaMemcpyAsync(L->planes + (size_t)p * L->n_alloc, words + (size_t)p * n, n * 8, cudaMemcpyHostToDevice,
-                      L->stream);
+  if (layout == FPS_LAYOUT_PLANES && n) {
+    DevBuf tmp;
+    if ((rc = tmp.ensure((size_t)n * 24))) { destroy(L); return rc; }
+    cudaMemcpyAsync(tmp.p, words, (size_t)n * 24, cudaMemcpyHostToDevice, L->stream);
+    int blocks = (int)std::min<u64>((n + 255) / 256, 4096);
+    fps::planes_to_planes<<<blocks, 256, 0, L->stream>>>(tmp.as<u64>(), tmp.as<u64>() + n, tmp.as<u64>() + 2 * n,
+                                                          n, L->out());
+    L->launches++;
+    cudaStreamSynchronize(L->stream);
+    tmp.release();
   } else if (n) {
     // stream rows through a pinned staging buffer in chunks, transposing on device
     const u64 chunk = 1 << 20;  // rows per chunk
@@ -632,7 +670,7 @@ int fps_open(const uint64_t* words, uint64_t n, int layout, int device, uint64_t
       std::memcpy(hb.p, words + s * stride, (size_t)m * stride * 8);
       cudaMemcpyAsync(db.p, hb.p, (size_t)m * stride * 8, cudaMemcpyHostToDevice, L->stream);
       int blocks = (int)std::min<u64>((m + 255) / 256, 4096);
-      fps::rows_to_planes<<<blocks, 256, 0, L->stream>>>(db.as<u64>(), m, stride, col0, L->w0(), L->w1(), L->w2(), s,
+      fps::rows_to_planes<<<blocks, 256, 0, L->stream>>>(db.as<u64>(), m, stride, col0, L->out(), s,
                                                         check_padding ? bad.as<u32>() : nullptr);
       L->launches++;
     }
@@ -649,7 +687,6 @@ int fps_open(const uint64_t* words, uint64_t n, int layout, int device, uint64_t
     return fail(FPS_ECUDA, std::string("library upload: ") + cudaGetErrorString(e));
   }
   if (layout == FPS_LAYOUT_PLANES && check_padding) {
-    // host-side check for the planes layout (the input is on the host anyway)
     for (u64 i = 0; i < n; ++i)
       if (words[2 * n + i] >> 38) { nbad = 1; break; }
   }
@@ -670,13 +707,25 @@ int fps_open_device(const uint64_t* d_w0, const uint64_t* d_w1, const uint64_t* 
   int rc = new_lib(device, index_base, &L);
   if (rc) return rc;
   DeviceGuard g(device);
-  if ((rc = alloc_planes(L, n))) { destroy(L); return rc; }
+  u32 nwide = 0;
   if (n) {
-    cudaMemcpyAsync(L->w0(), d_w0, n * 8, cudaMemcpyDeviceToDevice, L->stream);
-    cudaMemcpyAsync(L->w1(), d_w1, n * 8, cudaMemcpyDeviceToDevice, L->stream);
-    cudaMemcpyAsync(L->w2(), d_w2, n * 8, cudaMemcpyDeviceToDevice, L->stream);
+    DevBuf wide;
+    if ((rc = wide.ensure(4))) { destroy(L); return rc; }
+    cudaMemsetAsync(wide.p, 0, 4, L->stream);
+    int blocks = (int)std::min<u64>((n + 255) / 256, 4096);
+    fps::count_wide<<<blocks, 256, 0, L->stream>>>((const u64*)d_w2, n, wide.as<u32>());
+    cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, L->stream);
+    cudaStreamSynchronize(L->stream);
+  }
+  if ((rc = alloc_planes(L, n, nwide == 0))) { destroy(L); return rc; }
+  if (n) {
+    int blocks = (int)std::min<u64>((n + 255) / 256, 4096);
+    fps::planes_to_planes<<<blocks, 256, 0, L->stream>>>((const u64*)d_w0, (const u64*)d_w1, (const u64*)d_w2, n,
+                                                          L->out());
+    L->launches++;
   }
   cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     destroy(L);
     return fail(FPS_ECUDA, std::string("device upload: ") + cudaGetErrorString(e));
@@ -694,11 +743,9 @@ int fps_open_generated(uint64_t n, uint64_t start, uint64_t seed_key, const uint
   int rc = new_lib(device, index_base, &L);
   if (rc) return rc;
   DeviceGuard g(device);
-  if ((rc = alloc_planes(L, n))) { destroy(L); return rc; }
+  if ((rc = alloc_planes(L, n, true))) { destroy(L); return rc; }  // generated words never use bits 38..
   fps::GenArgs a{};
-  a.w0 = L->w0();
-  a.w1 = L->w1();
-  a.w2 = L->w2();
+  a.o = L->out();
   a.n = n;
   a.start = start;
   a.seed_key = seed_key;
@@ -735,12 +782,31 @@ int fps_info(const fps_lib* lib, uint64_t* n, uint64_t* index_base, int* device)
   return FPS_OK;
 }
 
-int fps_planes(fps_lib* lib, uint64_t** d_w0, uint64_t** d_w1, uint64_t** d_w2, uint64_t* n_alloc) {
+int fps_layout(const fps_lib* lib, int* compact, uint64_t* bytes_per_entry) {
   if (int rc = check_lib(lib)) return rc;
-  if (d_w0) *d_w0 = (uint64_t*)lib->w0();
-  if (d_w1) *d_w1 = (uint64_t*)lib->w1();
-  if (d_w2) *d_w2 = (uint64_t*)lib->w2();
-  if (n_alloc) *n_alloc = lib->n_alloc;
+  if (compact) *compact = lib->compact ? 1 : 0;
+  if (bytes_per_entry) *bytes_per_entry = lib->bytes_per_entry();
+  return FPS_OK;
+}
+
+int fps_read_entries(fps_lib* lib, uint64_t start, uint64_t count, uint64_t* rows) {
+  if (int rc = check_lib(lib)) return rc;
+  if (start > lib->n || count > lib->n - start) return fail(FPS_EINVAL, "entry range out of bounds");
+  if (count == 0) return FPS_OK;
+  if (!rows) return fail(FPS_EINVAL, "rows is null");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  const u64 chunk = 1 << 22;
+  DevBuf d_rows;
+  int rc;
+  if ((rc = d_rows.ensure((size_t)std::min<u64>(chunk, count) * 24))) return rc;
+  for (u64 s0 = 0; s0 < count; s0 += chunk) {
+    const u64 m = std::min<u64>(chunk, count - s0);
+    int blocks = (int)std::min<u64>((m + 255) / 256, 4096);
+    fps::planes_to_rows<<<blocks, 256, 0, lib->stream>>>(lib->out(), start + s0, m, d_rows.as<u64>());
+    CUDA_TRY(cudaMemcpyAsync(rows + 3 * s0, d_rows.p, (size_t)m * 24, cudaMemcpyDeviceToHost, lib->stream));
+    CUDA_TRY(cudaStreamSynchronize(lib->stream));
+  }
   return FPS_OK;
 }
 
@@ -752,18 +818,19 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
     if (idx[i] >= lib->n) return fail(FPS_EINVAL, "entry index out of range");
   if (m == 0) return FPS_OK;
   int rc;
-  DevBuf d_idx, d_rows;
-  if ((rc = d_idx.ensure((size_t)m * 8)) || (rc = d_rows.ensure((size_t)m * 24))) return rc;
+  DevBuf d_idx, d_rows, wide;
+  if ((rc = d_idx.ensure((size_t)m * 8)) || (rc = d_rows.ensure((size_t)m * 24)) || (rc = wide.ensure(4))) return rc;
+  CUDA_TRY(cudaMemsetAsync(wide.p, 0, 4, lib->stream));
   CUDA_TRY(cudaMemcpyAsync(d_idx.p, idx, (size_t)m * 8, cudaMemcpyHostToDevice, lib->stream));
   CUDA_TRY(cudaMemcpyAsync(d_rows.p, words, (size_t)m * 24, cudaMemcpyHostToDevice, lib->stream));
   int blocks = (int)std::min<u64>((m + 255) / 256, 4096);
-  fps::scatter_rows<<<blocks, 256, 0, lib->stream>>>(d_idx.as<u64>(), d_rows.as<u64>(), m, lib->w0(), lib->w1(),
-                                                     lib->w2());
+  fps::scatter_rows<<<blocks, 256, 0, lib->stream>>>(d_idx.as<u64>(), d_rows.as<u64>(), m, lib->out(),
+                                                     wide.as<u32>());
   lib->launches++;
-  CUDA_TRY(cudaGetLastError());
+  u32 nwide = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, lib->stream));
   CUDA_TRY(cudaStreamSynchronize(lib->stream));
-  d_idx.release();
-  d_rows.release();
+  if (nwide) return fail(FPS_EINVAL, "entry sets bits 40.. of word 2; the library uses the compact layout");
   return FPS_OK;
 }
 
@@ -840,7 +907,8 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   int rc;
   if ((rc = stage_queries(lib, queries, Q))) return rc;
   if ((rc = lib->keys.ensure((size_t)k * 8)) || (rc = lib->cnt.ensure(4))) return rc;
-  Config c = make_config<1, 4, fps::MODE_TOPK>(lib, 1, k);
+  Config c = lib->compact ? make_config<1, 4, fps::MODE_TOPK, true, true>(lib, 1, k)
+                          : make_config<1, 4, fps::MODE_TOPK, true, false>(lib, 1, k);
   if ((rc = ensure_state(lib, 1))) return rc;
   if ((rc = lib->buf.ensure(c.warps * (size_t)c.cap * 8))) return rc;
   if ((rc = lib->cand.ensure(c.cand_cap * 8))) return rc;
@@ -861,7 +929,8 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   a.cand_cnt = lib->cand_cnt.as<u32>();
   a.cand_cap = c.cand_cap;
   if (c.warps > 0 && lib->n > 0) {
-    fps::scan_kernel<1, 4, fps::MODE_TOPK, true><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
+    if (lib->compact) fps::scan_kernel<1, 4, fps::MODE_TOPK, true, true><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
+    else fps::scan_kernel<1, 4, fps::MODE_TOPK, true, false><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
     lib->launches++;
   }
   int kp = 1;

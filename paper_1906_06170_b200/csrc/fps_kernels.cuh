@@ -39,6 +39,20 @@ constexpr u32 T_OPEN = 255;   // "accept everything" threshold
 
 enum { MODE_TOPK = 0, MODE_RANGE = 1, MODE_HIST = 2 };
 
+// HBM layout: tiles, each a small structure of arrays
+//   full    (24 B/entry): w0[128] u64 | w1[128] u64 | w2[128] u64                 = 3072 B
+//   compact (21 B/entry): w0[256] u64 | w1[256] u64 | w2lo[256] u32 | w2hi[256] u8 = 5376 B
+// One warp iteration of the single-query scan (32 lanes x 4 entries) reads
+// one full tile (or half a compact one): its loads fall in one 3-5 KB span.
+// (compact tiles hold 256 entries so a tile, 5376 B, is a whole number of
+// 256 B DRAM interleave chunks, like the 3072 B full tile)
+constexpr int TILE_FULL = 128;
+constexpr int TILE_CMP = 256;
+constexpr u64 TILE_BYTES_FULL = 24 * TILE_FULL;
+constexpr u64 TILE_BYTES_CMP = 21 * TILE_CMP;
+__host__ __device__ __forceinline__ u64 tile_bytes(bool compact) { return compact ? TILE_BYTES_CMP : TILE_BYTES_FULL; }
+__host__ __device__ __forceinline__ u64 tile_entries(bool compact) { return compact ? TILE_CMP : TILE_FULL; }
+
 __host__ __device__ __forceinline__ u64 make_key(u32 d, u64 idx) { return ((u64)d << IDX_BITS) | idx; }
 __host__ __device__ __forceinline__ u32 key_d(u64 key) { return (u32)(key >> IDX_BITS) & 0xffu; }
 
@@ -54,6 +68,34 @@ __device__ __forceinline__ void ld_entries(const u64* p, u64 (&v)[2]) {
 }
 __device__ __forceinline__ void ld_entries(const u64* p, u64 (&v)[1]) {
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v[0]) : "l"(p));
+}
+
+// Compact layout: word 2 is split into a u32 plane (bits 0..31, keys
+// 129..160) and a u8 plane (bits 32..39: keys 161..166 + the 2 low pad bits).
+__device__ __forceinline__ void ld_w2c(const u32* lo, const unsigned char* hi, u64 (&v)[4]) {
+  u32 a, b, c, d, h;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(lo));
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(h) : "l"(hi));
+  v[0] = (u64)a | ((u64)(h & 0xffu) << 32);
+  v[1] = (u64)b | ((u64)((h >> 8) & 0xffu) << 32);
+  v[2] = (u64)c | ((u64)((h >> 16) & 0xffu) << 32);
+  v[3] = (u64)d | ((u64)(h >> 24) << 32);
+}
+__device__ __forceinline__ void ld_w2c(const u32* lo, const unsigned char* hi, u64 (&v)[2]) {
+  u32 a, b;
+  unsigned short h;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(lo));
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(h) : "l"(hi));
+  v[0] = (u64)a | ((u64)(h & 0xffu) << 32);
+  v[1] = (u64)b | ((u64)(h >> 8) << 32);
+}
+__device__ __forceinline__ void ld_w2c(const u32* lo, const unsigned char* hi, u64 (&v)[1]) {
+  u32 a;
+  unsigned short h;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(a) : "l"(lo));
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(h) : "l"(hi));
+  v[0] = (u64)a | ((u64)(h & 0xffu) << 32);
 }
 
 __device__ __forceinline__ u32 dist3(u64 a, u64 b, u64 c, u64 q0, u64 q1, u64 q2) {
@@ -118,9 +160,7 @@ __device__ __forceinline__ u32 warp_kth_bin(const u32* hist, u32 k, int lane, u3
 }
 
 struct ScanArgs {
-  const u64* w0;
-  const u64* w1;
-  const u64* w2;
+  const char* lib;               // tiled library (see TILE_BYTES_*)
   u64 n;           // valid entries on this device
   u64 index_base;  // global index of entry 0
   const u64* queries;  // Q x 3
@@ -195,7 +235,7 @@ struct WarpState {
   u32 cnt[QW];    // buffer fill
 };
 
-template <int QW, int E, int MODE, bool MINQ = false>
+template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
 __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel(const ScanArgs a) {
   extern __shared__ u32 smem[];
   const int lane = threadIdx.x & 31;
@@ -445,10 +485,14 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
   auto load_trip = [&](Trip& t, u64 i0) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const u64 off = (i0 + u) * (32 * E) + (u64)lane * E;
-      ld_entries(a.w0 + off, t.A[u]);
-      ld_entries(a.w1 + off, t.B[u]);
-      ld_entries(a.w2 + off, t.C[u]);
+      const u64 first = (i0 + u) * (32 * E) + (u64)lane * E;
+      constexpr u64 TL = CMP ? TILE_CMP : TILE_FULL;
+      const char* tb = a.lib + (first / TL) * (CMP ? TILE_BYTES_CMP : TILE_BYTES_FULL);
+      const u64 r = first % TL;
+      ld_entries(reinterpret_cast<const u64*>(tb) + r, t.A[u]);
+      ld_entries(reinterpret_cast<const u64*>(tb + 8 * TL) + r, t.B[u]);
+      if (CMP) ld_w2c(reinterpret_cast<const u32*>(tb + 16 * TL) + r, reinterpret_cast<const unsigned char*>(tb + 20 * TL) + r, t.C[u]);
+      else ld_entries(reinterpret_cast<const u64*>(tb + 16 * TL) + r, t.C[u]);
     }
   };
   auto run_trip = [&](const Trip& t, u64 i0) {
@@ -548,10 +592,14 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
   }
   for (; it < it1; ++it) {
     u64 A[E], B[E], C[E];
-    const u64 off = it * (32 * E) + (u64)lane * E;
-    ld_entries(a.w0 + off, A);
-    ld_entries(a.w1 + off, B);
-    ld_entries(a.w2 + off, C);
+    const u64 first = it * (32 * E) + (u64)lane * E;
+    constexpr u64 TL = CMP ? TILE_CMP : TILE_FULL;
+    const char* tb = a.lib + (first / TL) * (CMP ? TILE_BYTES_CMP : TILE_BYTES_FULL);
+    const u64 r = first % TL;
+    ld_entries(reinterpret_cast<const u64*>(tb) + r, A);
+    ld_entries(reinterpret_cast<const u64*>(tb + 8 * TL) + r, B);
+    if (CMP) ld_w2c(reinterpret_cast<const u32*>(tb + 16 * TL) + r, reinterpret_cast<const unsigned char*>(tb + 20 * TL) + r, C);
+    else ld_entries(reinterpret_cast<const u64*>(tb + 16 * TL) + r, C);
     process(A, B, C, it, it >= n_full);
   }
 
@@ -833,27 +881,81 @@ __global__ void merge_kernel(const u64* in_keys, const u32* in_cnt, u32 G, u32 Q
 // ---------------------------------------------------------------------------
 // Library ingestion
 // ---------------------------------------------------------------------------
+// Device view of the tiled library for ingestion / export kernels.
+struct PlanesOut {
+  char* base;
+  int compact;
+  __device__ __forceinline__ u64 te() const { return tile_entries(compact); }
+  __device__ __forceinline__ char* tile(u64 i) const { return base + (i / te()) * tile_bytes(compact); }
+  __device__ __forceinline__ void put(u64 i, u64 a, u64 b, u64 c) const {
+    char* t = tile(i);
+    const u64 T = te(), r = i % T;
+    reinterpret_cast<u64*>(t)[r] = a;
+    reinterpret_cast<u64*>(t + 8 * T)[r] = b;
+    if (compact) {
+      reinterpret_cast<u32*>(t + 16 * T)[r] = (u32)c;
+      reinterpret_cast<unsigned char*>(t + 20 * T)[r] = (unsigned char)(c >> 32);
+    } else {
+      reinterpret_cast<u64*>(t + 16 * T)[r] = c;
+    }
+  }
+  __device__ __forceinline__ void get(u64 i, u64& a, u64& b, u64& c) const {
+    const char* t = tile(i);
+    const u64 T = te(), r = i % T;
+    a = reinterpret_cast<const u64*>(t)[r];
+    b = reinterpret_cast<const u64*>(t + 8 * T)[r];
+    c = compact ? ((u64)reinterpret_cast<const u32*>(t + 16 * T)[r] |
+                   ((u64)reinterpret_cast<const unsigned char*>(t + 20 * T)[r] << 32))
+                : reinterpret_cast<const u64*>(t + 16 * T)[r];
+  }
+};
+
 // rows with `stride` u64 per row, fingerprint words at columns [col0, col0+3)
 // (FPS1 record view: stride 4, col0 1 — scan.py:169; row-major words: 3, 0).
-__global__ void rows_to_planes(const u64* __restrict__ rows, u64 n_rows, int stride, int col0, u64* w0, u64* w1,
-                               u64* w2, u64 dst_off, u32* bad_padding) {
+// bad_padding counts rows that set bits 38.. of word 2 (keys beyond 166).
+__global__ void rows_to_planes(const u64* __restrict__ rows, u64 n_rows, int stride, int col0, PlanesOut o,
+                               u64 dst_off, u32* bad_padding) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += (u64)gridDim.x * blockDim.x) {
     const u64* r = rows + i * stride + col0;
-    u64 a = r[0], b = r[1], c = r[2];
-    w0[dst_off + i] = a;
-    w1[dst_off + i] = b;
-    w2[dst_off + i] = c;
+    const u64 a = r[0], b = r[1], c = r[2];
+    o.put(dst_off + i, a, b, c);
     if (bad_padding && (c >> 38)) atomicAdd(bad_padding, 1u);
   }
 }
 
-__global__ void scatter_rows(const u64* __restrict__ idx, const u64* __restrict__ rows, u64 m, u64* w0, u64* w1,
-                             u64* w2) {
+// Count full-layout entries whose word 2 uses bits 40.. (they need 24 B/entry).
+__global__ void count_wide(const u64* __restrict__ w2, u64 n, u32* wide) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    if (w2[i] >> 40) atomicAdd(wide, 1u);
+}
+
+// Three device planes (full layout) -> library planes.
+__global__ void planes_to_planes(const u64* __restrict__ a, const u64* __restrict__ b, const u64* __restrict__ c,
+                                 u64 n, PlanesOut o) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    o.put(i, a[i], b[i], c[i]);
+}
+
+// Library entries [start, start + m) back to rows (checking / export).
+__global__ void planes_to_rows(PlanesOut o, u64 start, u64 m, u64* __restrict__ rows) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
-    const u64 t = idx[i];
-    w0[t] = rows[3 * i + 0];
-    w1[t] = rows[3 * i + 1];
-    w2[t] = rows[3 * i + 2];
+    u64 x, y, z;
+    o.get(start + i, x, y, z);
+    rows[3 * i + 0] = x;
+    rows[3 * i + 1] = y;
+    rows[3 * i + 2] = z;
+  }
+}
+
+__global__ void scatter_rows(const u64* __restrict__ idx, const u64* __restrict__ rows, u64 m, PlanesOut o,
+                             u32* wide) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+    const u64 c = rows[3 * i + 2];
+    if (o.compact && (c >> 40)) {
+      atomicAdd(wide, 1u);
+      continue;
+    }
+    o.put(idx[i], rows[3 * i + 0], rows[3 * i + 1], c);
   }
 }
 
@@ -864,9 +966,7 @@ __device__ __forceinline__ u64 splitmix64_fin(u64 z) {
 }
 
 struct GenArgs {
-  u64* w0;
-  u64* w1;
-  u64* w2;
+  PlanesOut o;
   u64 n;
   u64 start;     // global index of entry 0
   u64 seed_key;
@@ -892,16 +992,8 @@ __global__ void gen_kernel(const GenArgs a) {
       w[j0 >> 6] |= (u64)b0 << (j0 & 63);
       w[j1 >> 6] |= (u64)b1 << (j1 & 63);
     }
-    a.w0[i] = w[0];
-    a.w1[i] = w[1];
-    a.w2[i] = w[2];
+    a.o.put(i, w[0], w[1], w[2]);
   }
-}
-
-// Reference-order fill of a "padding" tail so vector loads never read garbage:
-__global__ void zero_tail(u64* w0, u64* w1, u64* w2, u64 from, u64 to) {
-  u64 i = from + (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < to) { w0[i] = 0; w1[i] = 0; w2[i] = 0; }
 }
 
 // Truncate sorted range output to the first k per query (large-k path).

@@ -156,26 +156,23 @@ class Library:
         self.close()
 
     # ---- data access ----------------------------------------------------
-    def planes(self) -> tuple[int, int, int, int]:
-        """Device pointers (w0, w1, w2) and the allocated plane length."""
-        p0, p1, p2, na = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_uint64()
-        N.check(N.load().fps_planes(self._h, C.byref(p0), C.byref(p1), C.byref(p2), C.byref(na)), "fps_planes")
-        return p0.value, p1.value, p2.value, na.value
+    def layout(self) -> tuple[bool, int]:
+        """(compact, bytes per entry) of the HBM planes."""
+        c, b = C.c_int(), C.c_uint64()
+        N.check(N.load().fps_layout(self._h, C.byref(c), C.byref(b)), "fps_layout")
+        return bool(c.value), int(b.value)
 
-    def planes_torch(self):
-        """Zero-copy int64 torch views of the three planes (length n)."""
-        import torch
-
-        p0, p1, p2, na = self.planes()
-        full = _torch_from_ptr(p0, 3 * na, self.device)
-        return full[0:self.n], full[na:na + self.n], full[2 * na:2 * na + self.n]
+    def read_entries(self, start: int = 0, count: int | None = None) -> np.ndarray:
+        """Copy entries back as (count, 3) uint64 rows (checking / export)."""
+        count = self.n - start if count is None else count
+        rows = np.empty((count, 3), dtype=np.uint64)
+        if count:
+            N.check(N.load().fps_read_entries(self._h, start, count, rows.ctypes.data), "fps_read_entries")
+        return rows
 
     def words_host(self) -> np.ndarray:
-        """Copy the library back as (n, 3) uint64 (for checking only)."""
-        w0, w1, w2 = self.planes_torch()
-        import torch
-
-        return torch.stack([w0, w1, w2], dim=1).cpu().numpy().view(np.uint64)
+        """The whole library as (n, 3) uint64 (for checking only)."""
+        return self.read_entries()
 
     def write_entries(self, index: np.ndarray, words: np.ndarray) -> None:
         """Overwrite local entries ``index`` with rows of ``words``."""
@@ -282,22 +279,6 @@ def keys_to_hits(keys: np.ndarray, cnt: np.ndarray) -> TopKResult:
     idx = np.where(valid, keys & np.uint64(IDX_MASK), _U64_MAX)
     dist = np.where(valid, (keys >> np.uint64(40)) & np.uint64(0xFF), 0xFFFF).astype(np.uint16)
     return TopKResult(idx.astype(np.uint64), dist, cnt)
-
-
-def _torch_from_ptr(ptr: int, numel: int, device: int):
-    """Wrap raw device memory owned by the library as an int64 torch tensor."""
-    import torch
-
-    class _Holder:
-        __cuda_array_interface__ = {
-            "shape": (numel,),
-            "typestr": "<i8",
-            "data": (ptr, False),
-            "version": 3,
-        }
-
-    with torch.cuda.device(device):
-        return torch.as_tensor(_Holder(), device=f"cuda:{device}")
 
 
 def load_library(source, device: int | None = None, index_base: int = 0) -> Library:

@@ -300,3 +300,30 @@ def test_repeated_calls_are_deterministic():
         again = lib.search_batch(q, 30)
         assert np.array_equal(first.index, again.index) and np.array_equal(first.distance, again.distance)
     assert first.hits(0)[0] == (1, 0)
+
+
+def test_compact_and_full_layouts_agree(monkeypatch):
+    """With FPS_LAYOUT=compact valid fingerprints use the 21-byte tiles; an FPS1
+    record with pad bits beyond bit 39 of word 2 forces the 24-byte layout.
+    Both answer identically to the oracle."""
+    monkeypatch.setenv("FPS_LAYOUT", "compact")
+    seed = 77
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 70_001)
+    q = w[[5, 6, 7]].copy()
+    q[:, 0] ^= np.uint64(0b110)
+    lib = Library.from_words(w)
+    assert lib.layout() == (True, 21)
+    rec = orc.records_from_words(w)
+    rec[100, 3] |= np.uint64(1) << np.uint64(45)  # a pad byte set in the FPS1 record
+    wide = Library.from_records(rec)
+    assert wide.layout() == (False, 24)
+    w_wide = rec[:, 1:].copy()
+    for k in (1, 10, 100):
+        assert lib.search_batch(q, k).hits(0) == oracle_topk(w, q, k)[0]
+        res = wide.search_batch(q, k)
+        exp = oracle_topk(w_wide, q, k)
+        assert [res.hits(i) for i in range(3)] == exp
+    assert np.array_equal(wide.words_host(), w_wide)
+    with pytest.raises(ValueError):
+        lib.write_entries(np.array([3]), np.array([[0, 0, 1 << 41]], dtype=np.uint64))
