@@ -45,7 +45,10 @@ enum fps_status {
   FPS_EPADDING = 4,   /* set bits above key 166: FingerprintError
                          (fingerprint.py:60-61)                              */
   FPS_ECANCELLED = 5, /* cancelled before launch: ScanCancelled (scan.py:190) */
-  FPS_ENODEV = 6      /* no CUDA device: RuntimeError                        */
+  FPS_ENODEV = 6,     /* no CUDA device: RuntimeError                        */
+  FPS_EIO = 7         /* shard file unreadable / bad header / truncated:
+                         ScanError("shard <path>: ...") (scan.py:283-284,
+                         libstore.py:202-212)                                */
 };
 
 /* Input layouts for fps_open. */
@@ -72,6 +75,18 @@ int fps_device_count(int* count);
  * scan does not validate), so pass 0 for them. */
 int fps_open(const uint64_t* words, uint64_t n, int layout, int device, uint64_t index_base, int check_padding,
              fps_lib** out);
+/* Stream FPS1 shard files (libstore.py:5-16) straight into HBM: each file's
+ * 16-byte header is validated (magic "FPS1", version 1, declared count, file
+ * size — the checks of read_shard_header / _iter_blocks, libstore.py:202-212,
+ * scan.py:166-168) before any device work, then records are read in chunks
+ * into pinned buffers, copied asynchronously and transposed on the device
+ * while the next chunk is read. Only the global record range [start,
+ * start + count) of the concatenated shards is loaded (count = UINT64_MAX:
+ * to the end), so each rank of a multi-GPU job streams just its slice.
+ * cids (nullable, count entries) receives the records' CIDs. On FPS_EIO,
+ * fps_last_error() names the shard path. */
+int fps_open_fps1(const char* const* paths, uint32_t n_paths, uint64_t start, uint64_t count, int device,
+                  uint64_t* cids, fps_lib** out);
 /* Same, from three device planes already on `device` (copied). */
 int fps_open_device(const uint64_t* d_w0, const uint64_t* d_w1, const uint64_t* d_w2, uint64_t n, int device,
                     uint64_t index_base, fps_lib** out);

@@ -24,6 +24,7 @@ FPS_ECUDA = 3
 FPS_EPADDING = 4
 FPS_ECANCELLED = 5
 FPS_ENODEV = 6
+FPS_EIO = 7
 
 LAYOUT_ROWS3 = 0
 LAYOUT_FPS1 = 1
@@ -42,6 +43,8 @@ SIGNATURES = {
     "fps_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "fps_open": (C.c_int, [_vp, C.c_uint64, C.c_int, C.c_int, C.c_uint64, C.c_int, C.POINTER(_vp)]),
     "fps_open_device": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int, C.c_uint64, C.POINTER(_vp)]),
+    "fps_open_fps1": (C.c_int, [C.POINTER(C.c_char_p), C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, _vp,
+                                C.POINTER(_vp)]),
     "fps_open_generated": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp, C.c_int, C.c_uint64,
                                      C.POINTER(_vp)]),
     "fps_close": (C.c_int, [_vp]),
@@ -110,6 +113,8 @@ def check(rc: int, what: str) -> None:
         raise ScanCancelled(msg)
     if rc == FPS_ENODEV:
         raise NativeUnavailable(msg)
+    if rc == FPS_EIO:
+        raise ScanError(last_error())  # "shard <path>: ..." like scan.py:283-284
     raise ScanError(msg)
 
 

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cerrno>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -124,7 +125,6 @@ struct fps_lib {
   DevBuf tg, ghist, cand_cnt;
   u32 state_q = 0;
   DevBuf buf, cand, queries, keys, cnt, radius, rkeys, rcount, sort_tmp, sort_out, seg;
-  DevBuf sched;  // 2 x u32 chunk scheduler of the single-query kernels (self-resetting)
   HostBuf h_stage;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
   bool timing = false;
@@ -232,7 +232,6 @@ int ensure_state(fps_lib* L, u32 Q) {
 
 // Restore the clean top-k state after a failed call.
 void reset_state(fps_lib* L) {
-  cudaMemsetAsync(L->sched.p, 0, 16, L->stream);
   if (!L->state_q) return;
   fill_tg(L);
   cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream);
@@ -250,14 +249,6 @@ u32 scan_flags() {
 fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
   fps::ScanArgs a{};
   a.flags = scan_flags();
-  // dynamic chunk claiming measured slower than static contiguous parts on B200
-  // (profiles/r01_experiments.md); kept behind FPS_SCAN_FLAGS bit 4
-  a.sched = (a.flags & 4) ? L->sched.as<u32>() : nullptr;
-  static const u32 chunk = [] {
-    const char* e = std::getenv("FPS_CHUNK");
-    return e ? (u32)std::strtoul(e, nullptr, 0) : 8u;
-  }();
-  a.chunk_iters = chunk;
   a.lib = L->mem;
   a.n = L->n;
   a.index_base = L->index_base;
@@ -514,11 +505,6 @@ int new_lib(int device, u64 index_base, fps_lib** out) {
     delete L;
     return fail(FPS_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
   }
-  if (L->sched.ensure(256) || cudaMemsetAsync(L->sched.p, 0, 256, L->stream) != cudaSuccess) {
-    cudaStreamDestroy(L->stream);
-    delete L;
-    return fail(FPS_ENOMEM, "scheduler allocation");
-  }
   *out = L;
   return FPS_OK;
 }
@@ -529,7 +515,7 @@ void destroy(fps_lib* L) {
   if (L->stream) cudaStreamSynchronize(L->stream);
   if (L->mem) cudaFree(L->mem);
   for (DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt, &L->radius,
-                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->sched})
+                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg})
     b->release();
   L->h_stage.release();
   for (auto& p : L->ev_pool) {
@@ -729,6 +715,111 @@ int fps_open_device(const uint64_t* d_w0, const uint64_t* d_w1, const uint64_t* 
   if (e != cudaSuccess) {
     destroy(L);
     return fail(FPS_ECUDA, std::string("device upload: ") + cudaGetErrorString(e));
+  }
+  *out = L;
+  return FPS_OK;
+}
+
+int fps_open_fps1(const char* const* paths, uint32_t n_paths, uint64_t start, uint64_t count, int device,
+                  uint64_t* cids, fps_lib** out) {
+  if (!out) return fail(FPS_EINVAL, "out is null");
+  *out = nullptr;
+  if (n_paths && !paths) return fail(FPS_EINVAL, "paths is null");
+  // 1. validate every header first (no device work yet): magic, version, count vs size
+  struct ShardFile {
+    std::string path;
+    u64 count;
+  };
+  std::vector<ShardFile> files;
+  u64 total = 0;
+  for (u32 f = 0; f < n_paths; ++f) {
+    const std::string path = paths[f] ? paths[f] : "";
+    FILE* fp = std::fopen(path.c_str(), "rb");
+    if (!fp) return fail(FPS_EIO, "shard " + path + ": " + std::strerror(errno));
+    unsigned char h[16];
+    const size_t got = std::fread(h, 1, 16, fp);
+    std::fseek(fp, 0, SEEK_END);
+    const long long size = std::ftell(fp);
+    std::fclose(fp);
+    if (got < 16) return fail(FPS_EIO, "shard " + path + ": header is " + std::to_string(got) + " bytes, expected 16");
+    if (std::memcmp(h, "FPS1", 4) != 0) return fail(FPS_EIO, "shard " + path + ": bad magic, expected 'FPS1'");
+    const unsigned version = h[4] | (h[5] << 8);
+    if (version != 1)
+      return fail(FPS_EIO, "shard " + path + ": format version " + std::to_string(version) + ", expected 1");
+    u64 n = 0;
+    for (int i = 0; i < 8; ++i) n |= (u64)h[8 + i] << (8 * i);
+    if ((u64)size < 16 + n * 32) {
+      return fail(FPS_EIO, "shard " + path + ": holds " + std::to_string(((u64)size - 16) / 32) +
+                               " records, header declares " + std::to_string(n));
+    }
+    files.push_back({path, n});
+    total += n;
+  }
+  if (start > total) return fail(FPS_EINVAL, "start beyond the last record");
+  const u64 n = std::min<u64>(count, total - start);
+  if (start + n > fps::IDX_MASK) return fail(FPS_EINVAL, "library indices exceed 2^40");
+  fps_lib* L = nullptr;
+  int rc = new_lib(device, start, &L);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  // 2. stream: read chunk i+1 from disk while chunk i is copied and transposed
+  const u64 chunk = 1 << 20;  // records per chunk (32 MiB)
+  HostBuf hb[2];
+  DevBuf db[2];
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b) {
+    if ((rc = hb[b].ensure((size_t)chunk * 32)) || (rc = db[b].ensure((size_t)chunk * 32))) {
+      destroy(L);
+      return rc;
+    }
+    cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+  }
+  // records of the slice use the compact layout only when no record sets bits 40.. of word 2;
+  // decided up front from a full pass would cost a second read, so the 24 B layout is used
+  if ((rc = alloc_planes(L, n, false))) { destroy(L); return rc; }
+  u64 base = 0, dst = 0;  // global index of the current file's first record; entries written
+  int slot = 0;
+  for (const ShardFile& sf : files) {
+    const u64 f0 = base, f1 = base + sf.count;
+    base = f1;
+    const u64 lo = std::max<u64>(f0, start), hi = std::min<u64>(f1, start + n);
+    if (lo >= hi) continue;
+    FILE* fp = std::fopen(sf.path.c_str(), "rb");
+    if (!fp) { destroy(L); return fail(FPS_EIO, "shard " + sf.path + ": " + std::strerror(errno)); }
+    std::fseek(fp, (long)(16 + (lo - f0) * 32), SEEK_SET);
+    for (u64 r = lo; r < hi; r += chunk) {
+      const u64 m = std::min<u64>(chunk, hi - r);
+      cudaEventSynchronize(done[slot]);  // the copy that last used this pinned buffer has finished
+      const size_t got = std::fread(hb[slot].p, 32, m, fp);
+      if (got != m) {
+        std::fclose(fp);
+        destroy(L);
+        return fail(FPS_EIO, "shard " + sf.path + ": truncated while reading");
+      }
+      if (cids) {
+        const u64* rec = hb[slot].as<u64>();
+        for (u64 i = 0; i < m; ++i) cids[dst + i] = rec[4 * i];
+      }
+      cudaMemcpyAsync(db[slot].p, hb[slot].p, m * 32, cudaMemcpyHostToDevice, L->stream);
+      const int blocks = (int)std::min<u64>((m + 255) / 256, 4096);
+      fps::rows_to_planes<<<blocks, 256, 0, L->stream>>>(db[slot].as<u64>(), m, 4, 1, L->out(), dst, nullptr);
+      L->launches++;
+      cudaEventRecord(done[slot], L->stream);
+      dst += m;
+      slot ^= 1;
+    }
+    std::fclose(fp);
+  }
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(done[b]);
+    hb[b].release();
+    db[b].release();
+  }
+  if (e != cudaSuccess) {
+    destroy(L);
+    return fail(FPS_ECUDA, std::string("shard upload: ") + cudaGetErrorString(e));
   }
   *out = L;
   return FPS_OK;

@@ -25,6 +25,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef FPS_QW1_MINB
+#define FPS_QW1_MINB 2  // CTAs per SM the single-query kernels are register-limited for
+#endif
+
 namespace fps {
 
 typedef unsigned long long u64;
@@ -171,11 +175,9 @@ struct ScanArgs {
   u32 cap;         // MODE_TOPK: per-(warp, query) buffer capacity
   u32 n_qg;        // query groups (ceil(Q / QW))
   u32 flags;       // experiment knobs (FPS_SCAN_FLAGS): 1 = no global publish, 2 = no tg refresh,
-                   // 4 = dynamic chunk claiming
+                   // 32 = select without programmatic dependent launch
   u32 gstride;     // words between consecutive ghist bins / tg replicas (spreads hot lines over L2 slices)
   u32 tg_rep;      // replicas of tg[q] (all receive every atomicMin; warp g reads replica g % tg_rep)
-  u32* sched;      // QW == 1: {next chunk, warps done}; zero between launches (the last warp resets it)
-  u32 chunk_iters; // iterations per dynamically claimed chunk
   u32 pub_every;   // only library parts with part % pub_every == 0 publish to ghist
   u64 n_parts;     // library parts
   u64 iters;       // ceil(n / (32*E))
@@ -236,7 +238,7 @@ struct WarpState {
 };
 
 template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
-__global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 3))) scan_kernel(const ScanArgs a) {
   extern __shared__ u32 smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -504,71 +506,11 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
       prefetch_tg();
     }
   };
-  if (QW == 1 && a.sched != nullptr) {
-    // HBM-bound single-query scan. Warps claim chunks of chunk_iters
-    // iterations from a global counter (dynamic balance: no straggler parts);
-    // claims only grow, so every warp still walks the library in ascending
-    // index order and the exact tie rule of the filter holds. The next claim
-    // is issued a whole chunk before it is needed, and the next iteration's
-    // loads are in flight while the current one is processed.
-    const u64 CH = a.chunk_iters;
-    const u64 n_chunks = (a.iters + CH - 1) / CH;
-    auto claim = [&]() -> u32 { return lane == 0 ? atomicAdd(a.sched, 1u) : 0u; };
-    u32 pend = claim();
-    u64 cur = __shfl_sync(FULL, pend, 0);
-    pend = claim();
-    u64 nxt = n_chunks;  // resolved from `pend` at the first chunk switch
-    bool have_pend = true;
-    auto advance = [&](u64& i, u64& e) -> bool {
-      if (++i < e) return true;
-      if (have_pend) { nxt = __shfl_sync(FULL, pend, 0); have_pend = false; }
-      if (nxt >= n_chunks) return false;
-      i = nxt * CH;
-      e = i + CH < a.iters ? i + CH : a.iters;
-      pend = claim();
-      have_pend = true;
-      return true;
-    };
-    auto step = [&](const Trip& t, u64 i) {
-      if (i < n_full) run_trip(t, i);
-      else process(t.A[0], t.B[0], t.C[0], i, true);
-    };
-    if (cur < n_chunks) {
-      u64 i = cur * CH;
-      u64 e = i + CH < a.iters ? i + CH : a.iters;
-      Trip P, R;
-      load_trip(P, i);
-      while (true) {
-        u64 ni = i, ne = e;
-        bool more = advance(ni, ne);
-        if (more) load_trip(R, ni);
-        step(P, i);
-        if (!more) break;
-        i = ni;
-        e = ne;
-        ni = i;
-        ne = e;
-        more = advance(ni, ne);
-        if (more) load_trip(P, ni);
-        step(R, i);
-        if (!more) break;
-        i = ni;
-        e = ne;
-      }
-    } else if (have_pend) {
-      (void)__shfl_sync(FULL, pend, 0);
-    }
-    it = it1;  // the static tail loop below has nothing left to do
-    fence_acq_rel_gpu();
-    if (lane == 0) {
-      const u32 done = atomicAdd(a.sched + 1, 1u);
-      if (done == (u32)(a.n_qg * a.n_parts) - 1) {
-        a.sched[0] = 0;
-        a.sched[1] = 0;
-      }
-    }
-  } else if (QW == 1) {
-    // static parts, software-pipelined (used when no scheduler is supplied)
+  if (QW == 1) {
+    // HBM-bound single-query scan over a static contiguous part, software-pipelined:
+    // the next iteration's loads are in flight while the current one is processed.
+    // (Dynamic chunk claiming and narrower per-warp parts measured slower on
+    // B200: profiles/r01_experiments.md.)
     Trip P, R;
     if (it + U <= it_main) load_trip(P, it);
     while (it + U <= it_main) {
@@ -621,7 +563,6 @@ __global__ void __launch_bounds__(256, (QW >= 4 || QW == 1 ? 2 : 3)) scan_kernel
     for (int j = 0; j < QW; ++j) {
       const u32 qi = qg * QW + j;
       if (qi >= a.Q) continue;
-      if (a.flags & 16) continue;  // experiment: skip the survivor flush (wrong results)
       if (ws->cnt[j] > a.k) compact(j);
       const u32 n = ws->cnt[j];
       const u32 t = *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));

@@ -113,6 +113,29 @@ class Library:
         return cls(h.value, rec[:, 0].copy())
 
     @classmethod
+    def from_fps1(cls, paths, start: int = 0, count: int | None = None, device: int | None = None,
+                  with_cids: bool = True) -> "Library":
+        """Stream FPS1 shard files (in order) into HBM; only records
+        [start, start + count) of their concatenation are loaded (one rank's
+        slice). Headers are validated first: a bad shard raises ScanError
+        naming its path (scan.py:283-284)."""
+        paths = [str(p) for p in paths]
+        arr = (C.c_char_p * max(1, len(paths)))(*[p.encode() for p in paths])
+        total = None
+        if with_cids or count is None:
+            total = sum(_fps1_count(p) for p in paths)
+        n = (total - start) if count is None else count
+        if total is not None:
+            n = max(0, min(n, total - start))
+        cids = np.empty(n, dtype=np.uint64) if with_cids else None
+        h = C.c_void_p()
+        dev = cls._device(device) if paths else cls._device(device)
+        N.check(N.load().fps_open_fps1(arr, len(paths), start, n if count is not None or total is not None
+                                       else (1 << 64) - 1, dev, cids.ctypes.data if cids is not None else None,
+                                       C.byref(h)), "fps_open_fps1")
+        return cls(h.value, cids)
+
+    @classmethod
     def from_device_planes(cls, w0, w1, w2, device: int | None = None, index_base: int = 0) -> "Library":
         """Copy three device planes (torch int64/uint64 tensors or pointers)."""
         n = int(w0.numel()) if hasattr(w0, "numel") else None
@@ -281,6 +304,15 @@ def keys_to_hits(keys: np.ndarray, cnt: np.ndarray) -> TopKResult:
     return TopKResult(idx.astype(np.uint64), dist, cnt)
 
 
+def _fps1_count(path) -> int:
+    """Record count declared by an FPS1 header (validated again by the C loader)."""
+    with open(path, "rb") as f:
+        head = f.read(16)
+    if len(head) < 16 or head[:4] != b"FPS1":
+        return 0  # the loader reports the precise error
+    return int.from_bytes(head[8:16], "little")
+
+
 def load_library(source, device: int | None = None, index_base: int = 0) -> Library:
     """Upload a library once: an (n, 3) word array, an (n, 4) FPS1 record
     array, a ShardManifest / library directory (FPS1 shards), or a Library."""
@@ -293,8 +325,7 @@ def load_library(source, device: int | None = None, index_base: int = 0) -> Libr
     from . import libstore
 
     manifest = source if hasattr(source, "shards") else libstore.load_manifest(Path(source))
-    records = libstore.read_manifest_records(manifest)
-    return Library.from_records(records, device, index_base)
+    return Library.from_fps1([s.path for s in manifest.shards], device=device)
 
 
 def load_libraries(sources: Sequence, device: int | None = None) -> list[Library]:

@@ -106,6 +106,7 @@ class _Resident:
 
 
 _cache: dict[tuple, _Resident] = {}
+_CACHE_MAX = 8
 _cache_lock = threading.Lock()
 
 
@@ -129,21 +130,25 @@ def _resident(manifest, device: int | None) -> _Resident:
         hit = _cache.get(key)
         if hit is not None:
             return hit
-        records = []
-        offsets = [0]
+        # header pre-check in shard order, so the first bad shard is the one reported
         for shard in manifest.shards:
             try:
-                rec = libstore.read_shard_records(shard)
+                with open(shard.path, "rb") as f:
+                    libstore.read_shard_header(f, shard.path)
             except (OSError, LibstoreError) as exc:
                 raise ScanError(f"shard {shard.path}: {exc}") from exc
-            records.append(rec)
-            offsets.append(offsets[-1] + len(rec))
-        allrec = np.concatenate(records) if records else np.zeros((0, 4), dtype="<u8")
-        lib = Library.from_records(allrec, device)
-        cids = allrec[:, 0].copy()
+        lib = Library.from_fps1([s.path for s in manifest.shards], device=device)
+        offsets = [0]
+        for shard in manifest.shards:
+            with open(shard.path, "rb") as f:
+                offsets.append(offsets[-1] + libstore.read_shard_header(f, shard.path))
+        cids = lib.cids
         monotone = bool(np.all(cids[1:] > cids[:-1])) if len(cids) > 1 else True
         res = _Resident(lib=lib, cids=cids, cid_monotone=monotone, offsets=offsets)
         _cache[key] = res
+        while len(_cache) > _CACHE_MAX:  # bounded HBM use: evict the oldest library
+            old = next(iter(_cache))
+            _cache.pop(old).lib.close()
         return res
 
 

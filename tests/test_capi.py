@@ -79,3 +79,32 @@ def test_null_handle_rejected(lib):
     q = np.zeros((1, 3), dtype=np.uint64)
     assert lib.fps_topk(None, q.ctypes.data, 1, 5, None, None, cnt.ctypes.data) == _native.FPS_EINVAL
     assert b"null" in lib.fps_last_error()
+
+
+def test_fps1_loader_reports_bad_shards_without_a_gpu(lib, tmp_path):
+    """Shard headers are validated before any device work: bad magic, wrong
+    version and truncation come back as FPS_EIO naming the path (the
+    reference's ScanError("shard <path>: ...") contract, scan.py:283-284)."""
+    import ctypes
+
+    from paper_1906_06170_b200 import _native
+
+    good = tmp_path / "good.fps"
+    good.write_bytes(b"FPS1" + (1).to_bytes(2, "little") + b"\0\0" + (2).to_bytes(8, "little") + b"\0" * 64)
+    cases = {
+        "magic.fps": b"NOPE" + b"\0" * 12,
+        "version.fps": b"FPS1" + (2).to_bytes(2, "little") + b"\0\0" + (0).to_bytes(8, "little"),
+        "trunc.fps": b"FPS1" + (1).to_bytes(2, "little") + b"\0\0" + (5).to_bytes(8, "little") + b"\0" * 40,
+        "short.fps": b"FPS1",
+    }
+    for name, data in cases.items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        arr = (ctypes.c_char_p * 2)(str(good).encode(), str(p).encode())
+        h = ctypes.c_void_p()
+        rc = lib.fps_open_fps1(arr, 2, 0, 2**64 - 1, 0, None, ctypes.byref(h))
+        assert rc == _native.FPS_EIO, name
+        msg = lib.fps_last_error().decode()
+        assert msg.startswith("shard ") and name in msg, msg
+    arr = (ctypes.c_char_p * 1)(str(tmp_path / "missing.fps").encode())
+    assert lib.fps_open_fps1(arr, 1, 0, 2**64 - 1, 0, None, ctypes.byref(ctypes.c_void_p())) == _native.FPS_EIO

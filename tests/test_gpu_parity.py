@@ -327,3 +327,31 @@ def test_compact_and_full_layouts_agree(monkeypatch):
     assert np.array_equal(wide.words_host(), w_wide)
     with pytest.raises(ValueError):
         lib.write_entries(np.array([3]), np.array([[0, 0, 1 << 41]], dtype=np.uint64))
+
+
+def test_fps1_streaming_loader(tmp_path):
+    """FPS1 shards stream straight into HBM; any record slice of the
+    concatenation (a rank's shard) loads with its global index base."""
+    seed = 1234
+    thr = synth.beta_thresholds(seed)
+    n = 2_500_011  # > 2 loader chunks
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 300_000)
+    w = np.concatenate([w] * 8 + [w[:n - 8 * len(w)]])
+    cids = np.arange(7, 7 + 3 * n, 3, dtype=np.uint64)
+    mpath = orc.write_fps1_library(tmp_path, w, 3, cids=cids)
+    paths = sorted(str(p) for p in tmp_path.glob("shard-*.fps"))
+    lib = Library.from_fps1(paths)
+    assert lib.n == n and lib.index_base == 0
+    assert np.array_equal(lib.words_host(), w)
+    assert np.array_equal(lib.cids, cids)
+    start, count = 833_000, 900_001  # crosses a shard boundary
+    part = Library.from_fps1(paths, start=start, count=count)
+    assert part.index_base == start and part.n == count
+    assert np.array_equal(part.words_host(), w[start:start + count])
+    assert np.array_equal(part.cids, cids[start:start + count])
+    q = w[start + 5].copy()
+    assert part.search(q, 5)[0] == (start + 5, 0)
+    from paper_1906_06170_b200 import libstore
+
+    via_manifest = scan.search(libstore.load_manifest(mpath.parent), tuple(int(x) for x in q), scan.SearchParams(n=3))
+    assert via_manifest.hits[0].distance == 0
