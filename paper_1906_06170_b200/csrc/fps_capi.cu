@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/fps.h"
+#include "fps_bitslice.cuh"
 #include "fps_kernels.cuh"
 
 using fps::u32;
@@ -40,6 +41,13 @@ int fail(int code, const std::string& msg) {
       return fail(e_ == cudaErrorMemoryAllocation ? FPS_ENOMEM : FPS_ECUDA,                     \
                   std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
     }                                                                                           \
+  } while (0)
+
+// launch check that names the kernel in the error message
+#define LAUNCH_CHECK(name)                                                                      \
+  do {                                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                                        \
+    if (e_ != cudaSuccess) return fail(FPS_ECUDA, std::string(name) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
 constexpr int WPB = 8;  // warps per CTA in the scan kernels
@@ -125,9 +133,13 @@ struct fps_lib {
   DevBuf tg, ghist, cand_cnt;
   u32 state_q = 0;
   DevBuf buf, cand, queries, keys, cnt, radius, rkeys, rcount, sort_tmp, sort_out, seg;
+  // bit-plane copy of the library for the multi-query scans (built on first use)
+  DevBuf bs, bsq;
+  int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
   HostBuf h_stage;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
   bool timing = false;
+  bool timing_suspend = false;  // helper passes (e.g. the bit-slice seed) are not timed
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   size_t ev_used = 0;
   fps::PlanesOut out() const { return fps::PlanesOut{mem, compact ? 1 : 0}; }
@@ -176,12 +188,13 @@ void pick_shape(u32 Q, int* qw, int* e) {
 }
 
 template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
-Config make_config(const fps_lib* L, u32 Q, u32 k) {
+Config make_config(const fps_lib* L, u32 Q, u32 k, u64 n_prefix = 0) {
   Config c{};
   c.qw = QW;
   c.e = E;
   c.n_qg = (Q + QW - 1) / QW;
-  c.iters = (L->n + 32 * E - 1) / (32 * E);
+  const u64 n = n_prefix ? n_prefix : L->n;
+  c.iters = (n + 32 * E - 1) / (32 * E);
   const u64 slots = (u64)L->sms * max_ctas_per_sm<QW, E, MODE, MINQ, CMP>() * WPB;
   u64 parts = std::max<u64>(1, slots / c.n_qg);
   const u64 min_iters = (QW == 1) ? 8 : 2;  // keep per-warp parts long enough to amortise warm-up
@@ -278,7 +291,7 @@ cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* ca
 
 // Record an event pair around the next scan-kernel launch when timing is on.
 std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
-  if (!L->timing) return nullptr;
+  if (!L->timing || L->timing_suspend) return nullptr;
   if (L->ev_used == L->ev_pool.size()) {
     cudaEvent_t a, b;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
@@ -288,14 +301,16 @@ std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
 }
 
 template <int QW, int E, bool CMP>
-int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only) {
-  Config c = make_config<QW, E, fps::MODE_TOPK, false, CMP>(L, Q, k);
+int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
+               u64 n_prefix = 0) {
+  Config c = make_config<QW, E, fps::MODE_TOPK, false, CMP>(L, Q, k, n_prefix);
   int rc;
   if ((rc = ensure_state(L, Q))) return rc;
   if ((rc = L->buf.ensure(c.warps * QW * (size_t)c.cap * 8))) return rc;
   if ((rc = L->cand.ensure((size_t)Q * c.cand_cap * 8))) return rc;
   if (prepare_only) return FPS_OK;
   fps::ScanArgs a = base_args(L, d_q, Q);
+  if (n_prefix) a.n = n_prefix;
   a.k = k;
   a.cap = c.cap;
   a.n_qg = c.n_qg;
@@ -334,9 +349,11 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
     cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr_set = true;
   }
+  LAUNCH_CHECK("scan_kernel<topk>");
   CUDA_TRY(launch_select(Q, sel_smem, s, a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, a.tg_rep, k,
                          d_keys, d_cnt, !(a.flags & 32)));
   L->launches++;
+  LAUNCH_CHECK("select_kernel");
   if (std::getenv("FPS_DEBUG")) {
     unsigned long long t[12] = {0};
     cudaStreamSynchronize(s);
@@ -349,8 +366,159 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   return FPS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// bit-sliced multi-query path (fps_bitslice.cuh)
+// ---------------------------------------------------------------------------
+constexpr u32 BS_MIN_Q = 32;  // below this the POPC kernels (query words in registers) win
+
+size_t bs_smem() {
+  return 2 * (fps::BS_TILE_BYTES + 128) + 16 + fps::BS_QPC * sizeof(fps::BsQuery) +
+         (size_t)fps::BS_WARPS * fps::BS_QPW * fps::HB * 4 + fps::BS_WARPS * sizeof(fps::WarpState<fps::BS_QPW>) +
+         (size_t)fps::BS_WARPS * fps::BS_QPW * 10 * 4;
+}
+
+// Build (once) the bit-plane copy; libraries with pad bits past key 166 stay on the POPC path.
+int bs_ensure(fps_lib* L) {
+  if (L->bs_state) return FPS_OK;
+  const u64 tiles = (L->n + fps::BS_TILE_ENTRIES - 1) / fps::BS_TILE_ENTRIES;
+  int rc;
+  if ((rc = L->bs.ensure((size_t)std::max<u64>(tiles, 1) * fps::BS_TILE_BYTES))) {
+    cudaGetLastError();
+    L->bs_state = -1;  // not enough memory for the copy: keep the POPC scan
+    return FPS_OK;
+  }
+  DevBuf wide;
+  if ((rc = wide.ensure(4))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L->bs.p, 0, L->bs.bytes, L->stream));
+  CUDA_TRY(cudaMemsetAsync(wide.p, 0, 4, L->stream));
+  const u64 nblocks = (L->n + 31) / 32;
+  const int grid = (int)std::min<u64>((nblocks * 32 + 255) / 256, (u64)L->sms * 32);
+  fps::bs_build_kernel<<<std::max(grid, 1), 256, 0, L->stream>>>(L->out(), L->n, L->bs.as<u32>(), wide.as<u32>());
+  L->launches++;
+  u32 nwide = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, L->stream));
+  CUDA_TRY(cudaStreamSynchronize(L->stream));
+  L->bs_state = nwide ? -1 : 1;
+  if (nwide) L->bs.release();
+  return FPS_OK;
+}
+
+bool bs_wanted(fps_lib* L, u32 Q) {
+  const char* e = std::getenv("FPS_BITSLICE");
+  if (e && std::string(e) == "0") return false;
+  if (Q < BS_MIN_Q || L->n < fps::BS_TILE_ENTRIES) return false;
+  if (bs_ensure(L) != FPS_OK) return false;
+  return L->bs_state == 1;
+}
+
+fps::BsArgs bs_args(fps_lib* L, u32 Q, u64* n_parts_out) {
+  fps::BsArgs b{};
+  b.bs = L->bs.as<u32>();
+  b.n = L->n;
+  b.index_base = L->index_base;
+  b.qs = reinterpret_cast<const fps::BsQuery*>(L->bsq.p);
+  b.Q = Q;
+  b.n_qg = (Q + fps::BS_QPC - 1) / fps::BS_QPC;
+  b.tiles = (L->n + fps::BS_TILE_ENTRIES - 1) / fps::BS_TILE_ENTRIES;
+  static int ctas_per_sm = 0;
+  if (!ctas_per_sm) {
+    const size_t sm = bs_smem();
+    cudaFuncSetAttribute(fps::bs_scan_kernel<fps::MODE_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(fps::bs_scan_kernel<fps::MODE_RANGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fps::bs_scan_kernel<fps::MODE_TOPK>,
+                                                  fps::BS_WARPS * 32, sm);
+    ctas_per_sm = std::max(1, ctas_per_sm);
+  }
+  const u64 slots = (u64)L->sms * ctas_per_sm;
+  u64 parts = std::max<u64>(1, slots / b.n_qg);
+  parts = std::min<u64>(parts, std::max<u64>(1, b.tiles / 4));  // >= 4 tiles per CTA
+  b.n_parts = parts;
+  *n_parts_out = parts;
+  return b;
+}
+
+int bs_prep(fps_lib* L, const u64* d_q, u32 Q, cudaStream_t s) {
+  int rc;
+  if ((rc = L->bsq.ensure((size_t)Q * sizeof(fps::BsQuery)))) return rc;
+  fps::bs_prep_queries<<<(Q + 127) / 128, 128, 0, s>>>(d_q, Q, reinterpret_cast<fps::BsQuery*>(L->bsq.p));
+  L->launches++;
+  LAUNCH_CHECK("bs_prep_queries");
+  return FPS_OK;
+}
+
+template <bool CMP>
+int topk_bs(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only) {
+  int rc;
+  // 1. seed: exact top-k of a library prefix with the POPC scan -> tg[q] bound
+  const u64 seed_n = std::min<u64>(L->n, 1 << 18);
+  L->timing_suspend = true;
+  rc = topk_fused<8, 2, CMP>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n);
+  L->timing_suspend = false;
+  if (rc) return rc;
+  u64 parts = 0;
+  fps::BsArgs b = bs_args(L, Q, &parts);
+  const u64 ctas = (u64)b.n_qg * parts;
+  const u32 cap = (std::max<u32>(2 * k, k + 1024) + 31) / 32 * 32;
+  const u64 cand_cap = parts * (u64)k;
+  if ((rc = L->buf.ensure(ctas * fps::BS_WARPS * fps::BS_QPW * (size_t)cap * 8))) return rc;
+  if ((rc = L->cand.ensure((size_t)Q * cand_cap * 8))) return rc;
+  if ((rc = L->bsq.ensure((size_t)Q * sizeof(fps::BsQuery)))) return rc;
+  if (prepare_only) return FPS_OK;
+  fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q),
+                                                   ghist_stride(Q));
+  L->launches++;
+  LAUNCH_CHECK("bs_seed_tg");
+  if ((rc = bs_prep(L, d_q, Q, s))) return rc;
+  b.qs = reinterpret_cast<const fps::BsQuery*>(L->bsq.p);  // (re)allocated by bs_prep
+  // 2. bit-sliced scan of the whole library
+  b.k = k;
+  b.cap = cap;
+  b.tg = L->tg.as<u32>();
+  b.tg_rep = tg_replicas(Q);
+  b.gstride = ghist_stride(Q);
+  b.buf = L->buf.as<u64>();
+  b.cand = L->cand.as<u64>();
+  b.cand_cnt = L->cand_cnt.as<u32>();
+  b.cand_cap = cand_cap;
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::bs_scan_kernel<fps::MODE_TOPK><<<(unsigned)ctas, fps::BS_WARPS * 32, bs_smem(), s>>>(b);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  LAUNCH_CHECK("bs_scan_kernel<topk>");
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, b.cand, b.cand_cnt, cand_cap, b.tg, L->ghist.as<u32>(),
+                         ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt, false));
+  L->launches++;
+  LAUNCH_CHECK("select_kernel (bit-slice)");
+  return FPS_OK;
+}
+
+int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u64* d_out, u64 cap, u64* d_count,
+             cudaStream_t s) {
+  int rc;
+  if ((rc = bs_prep(L, d_q, Q, s))) return rc;
+  u64 parts = 0;
+  fps::BsArgs b = bs_args(L, Q, &parts);
+  b.radius = d_radius;
+  b.out = d_out;
+  b.out_cnt = d_count;
+  b.out_cap = cap;
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::bs_scan_kernel<fps::MODE_RANGE><<<(unsigned)((u64)b.n_qg * parts), fps::BS_WARPS * 32, bs_smem(), s>>>(b);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return FPS_OK;
+}
+
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
                   bool prepare_only) {
+  if (bs_wanted(L, Q))
+    return L->compact ? topk_bs<true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only)
+                      : topk_bs<false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   int qw, e;
   pick_shape(Q, &qw, &e);
   if (L->compact) {
@@ -383,6 +551,8 @@ int launch_plain(fps_lib* L, fps::ScanArgs a, cudaStream_t s) {
 
 template <int MODE>
 int plain_dispatch(fps_lib* L, const fps::ScanArgs& a, cudaStream_t s) {
+  if (MODE == fps::MODE_RANGE && bs_wanted(L, a.Q))
+    return range_bs(L, a.queries, a.Q, a.radius, a.out, a.out_cap, a.out_cnt, s);
   int qw, e;
   pick_shape(a.Q, &qw, &e);
   if (L->compact) {
@@ -515,7 +685,7 @@ void destroy(fps_lib* L) {
   if (L->stream) cudaStreamSynchronize(L->stream);
   if (L->mem) cudaFree(L->mem);
   for (DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt, &L->radius,
-                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg})
+                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->bs, &L->bsq})
     b->release();
   L->h_stage.release();
   for (auto& p : L->ev_pool) {
