@@ -123,6 +123,17 @@ class ClockSampler(threading.Thread):
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def roofline_model(workload: str) -> dict:
+    """Per-kernel instruction-mix constants measured once with ncu (profiles/roofline_model.json)."""
+    p = ROOT / "profiles" / "roofline_model.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(workload, {})
+        except Exception:
+            return {}
+    return {}
+
+
 def traffic_for(workload: str):
     """dram bytes per scan-kernel launch from the committed ncu --set full capture."""
     p = ROOT / "profiles" / "traffic.json"
@@ -403,6 +414,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     # roofline of the scan kernel
     peaks = measured_peaks()
     compact, bpe = lib.layout()
+    kernel = lib.last_kernel
     if plan.radius is None and Q <= 4:
         bound = "hbm"
         bytes_per_launch = float(bpe) * count
@@ -410,23 +422,35 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         peak = float(peaks.get("hbm_gbs", 6650.0))
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic_for(args.workload), "peak_source": peaks["_source"],
-                "algorithmic_bytes_per_launch": bytes_per_launch, "scan_kernel_ms": scan_avg_ms,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "scan_kernel_ms": scan_avg_ms, "kernel": kernel,
                 "nominal_8tbs_frac": achieved / 8000.0}
     else:
         sm = props.multi_processor_count
         mhz = clocks["sm_mhz"] or float(peaks.get("sm_max_mhz", 1965.0))
-        # binding pipe of the instruction mix: the POPC (XU) pipe at 16 lanes/clk/SM;
-        # Q >= 2 kernels issue 4 POPC per comparison (carry-save), Q == 1 issues 6
-        per_cmp = POPC_PER_CMP_CSA if Q >= 2 else POPC_PER_CMP_NAIVE
-        peak = sm * POPC_PER_SM_CLK / per_cmp * mhz * 1e6 / 1e9  # G comparisons/s
-        naive = sm * POPC_PER_SM_CLK / POPC_PER_CMP_NAIVE * mhz * 1e6 / 1e9
         achieved = Q * count / (scan_avg_ms / 1e3) / 1e9
-        roof = {"bound": "popc", "achieved": achieved, "peak": peak, "unit": "Gcmp/s", "frac": achieved / peak,
-                "traffic": traffic_for(args.workload),
-                "peak_source": f"{sm} SMs x 16 POPC/clk/SM (measured) / {per_cmp:.0f} POPC per comparison x "
-                               f"{mhz:.0f} MHz (median SM clock in the timed region)",
-                "naive_6popc_peak": naive, "naive_6popc_frac": achieved / naive,
-                "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": float(bpe) * count}
+        naive = sm * POPC_PER_SM_CLK / POPC_PER_CMP_NAIVE * mhz * 1e6 / 1e9
+        model = roofline_model(args.workload)
+        if kernel == "bit-sliced multi-query scan" and model.get("alu_warp_instr_per_cmp"):
+            # ALU-pipe bound: 2 warp-instructions/clk/SM issue on the ALU pipe;
+            # ALU instructions per comparison of this kernel measured by ncu
+            per = float(model["alu_warp_instr_per_cmp"])
+            peak = sm * 2.0 * mhz * 1e6 / per / 1e9
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gcmp/s", "frac": achieved / peak,
+                    "traffic": traffic_for(args.workload),
+                    "peak_source": f"{sm} SMs x 2 ALU warp-instructions/clk x {mhz:.0f} MHz / {per:.4f} ALU "
+                                   f"warp-instructions per comparison (ncu, {model.get('source', 'profiles')})"}
+        else:
+            # binding pipe of the POPC formulation: XU at 16 lanes/clk/SM;
+            # Q >= 2 kernels issue 4 POPC per comparison (carry-save), Q == 1 issues 6
+            per_cmp = POPC_PER_CMP_CSA if Q >= 2 else POPC_PER_CMP_NAIVE
+            peak = sm * POPC_PER_SM_CLK / per_cmp * mhz * 1e6 / 1e9  # G comparisons/s
+            roof = {"bound": "popc", "achieved": achieved, "peak": peak, "unit": "Gcmp/s", "frac": achieved / peak,
+                    "traffic": traffic_for(args.workload),
+                    "peak_source": f"{sm} SMs x 16 POPC/clk/SM (measured) / {per_cmp:.0f} POPC per comparison x "
+                                   f"{mhz:.0f} MHz (median SM clock in the timed region)"}
+        roof.update({"naive_6popc_peak": naive, "naive_6popc_frac": achieved / naive,
+                     "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": float(bpe) * count,
+                     "kernel": kernel})
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

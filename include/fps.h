@@ -144,6 +144,10 @@ int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream);
  * d_in_keys G x Q x k (each row sorted, UINT64_MAX pads), d_in_cnt G x Q. */
 int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_t G, uint32_t Q, uint32_t k,
                     uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream);
+/* Kernel family of the last scan on this handle (reporting / tests):
+ * 1 single-query HBM scan, 2 multi-query POPC scan, 3 bit-sliced multi-query
+ * scan, 4 large-k (histogram + range + sort) path. */
+int fps_last_kernel(const fps_lib* lib);
 /* Number of kernels launched by this handle so far (evidence counter). */
 uint64_t fps_launch_count(const fps_lib* lib);
 /* Scan-kernel timing for roofline reporting: when enabled, every scan-kernel

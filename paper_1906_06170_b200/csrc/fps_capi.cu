@@ -138,6 +138,7 @@ struct fps_lib {
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
   HostBuf h_stage;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
+  int last_kernel = 0;  // fps_last_kernel
   bool timing = false;
   bool timing_suspend = false;  // helper passes (e.g. the bit-slice seed) are not timed
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -516,11 +517,14 @@ int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u
 
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
                   bool prepare_only) {
-  if (bs_wanted(L, Q))
+  if (bs_wanted(L, Q)) {
+    L->last_kernel = 3;
     return L->compact ? topk_bs<true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only)
                       : topk_bs<false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  }
   int qw, e;
   pick_shape(Q, &qw, &e);
+  L->last_kernel = qw == 1 ? 1 : 2;
   if (L->compact) {
     if (qw == 1) return topk_fused<1, 4, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
     if (qw == 2) return topk_fused<2, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
@@ -551,10 +555,13 @@ int launch_plain(fps_lib* L, fps::ScanArgs a, cudaStream_t s) {
 
 template <int MODE>
 int plain_dispatch(fps_lib* L, const fps::ScanArgs& a, cudaStream_t s) {
-  if (MODE == fps::MODE_RANGE && bs_wanted(L, a.Q))
+  if (MODE == fps::MODE_RANGE && bs_wanted(L, a.Q)) {
+    L->last_kernel = 3;
     return range_bs(L, a.queries, a.Q, a.radius, a.out, a.out_cap, a.out_cnt, s);
+  }
   int qw, e;
   pick_shape(a.Q, &qw, &e);
+  L->last_kernel = qw == 1 ? 1 : 2;
   if (L->compact) {
     if (qw == 1) return launch_plain<1, 4, MODE, true>(L, a, s);
     if (qw == 2) return launch_plain<2, 2, MODE, true>(L, a, s);
@@ -713,6 +720,7 @@ void unpack_topk(const u64* keys, const u32* cnt, u32 Q, u32 k, uint64_t* out_id
 // threshold T_q -> range collection with radius T_q -> sort -> first k.
 int topk_large(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt) {
   int rc;
+  L->last_kernel = 4;
   if ((rc = ensure_state(L, Q))) return rc;
   CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, (size_t)Q * fps::HB * 4, L->stream));
   fps::ScanArgs a = base_args(L, d_q, Q);
@@ -1285,6 +1293,8 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
 }
 
 uint64_t fps_launch_count(const fps_lib* lib) { return lib ? lib->launches.load() : 0; }
+
+int fps_last_kernel(const fps_lib* lib) { return lib ? lib->last_kernel : 0; }
 
 int fps_timing(fps_lib* lib, int enable) {
   if (int rc = check_lib(lib)) return rc;

@@ -214,6 +214,13 @@ class Library:
         N.check(N.load().fps_timing_read(self._h, C.byref(t), C.byref(c)), "fps_timing_read")
         return t.value, c.value
 
+    KERNELS = {0: "none", 1: "single-query HBM scan", 2: "multi-query POPC scan", 3: "bit-sliced multi-query scan",
+               4: "large-k histogram/range/sort"}
+
+    @property
+    def last_kernel(self) -> str:
+        return self.KERNELS.get(int(N.load().fps_last_kernel(self._h)), "unknown")
+
     @property
     def launches(self) -> int:
         return int(N.load().fps_launch_count(self._h))
