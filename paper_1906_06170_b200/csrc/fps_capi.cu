@@ -28,6 +28,9 @@ using fps::u64;
 namespace {
 
 thread_local std::string g_err;
+// bumped by every device (re)allocation: CUDA graphs captured before it may
+// hold stale pointers and are re-captured
+std::atomic<u64> g_alloc_gen{0};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -63,6 +66,7 @@ struct DevBuf {
     bytes = 0;
     size_t b = std::max<size_t>(want, 256);
     cudaError_t e = cudaMalloc(&p, b);
+    g_alloc_gen++;
     if (e != cudaSuccess) {
       cudaGetLastError();
       return fail(FPS_ENOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
@@ -72,6 +76,7 @@ struct DevBuf {
   }
   void release() {
     if (p) cudaFree(p);
+    if (p) g_alloc_gen++;
     p = nullptr;
     bytes = 0;
   }
@@ -139,6 +144,16 @@ struct fps_lib {
   HostBuf h_stage;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
   int last_kernel = 0;  // fps_last_kernel
+  // host-API top-k calls replayed as one CUDA graph per (Q, k):
+  // H2D queries -> scan -> select -> D2H, captured once
+  struct TopkGraph {
+    u32 Q = 0, k = 0;
+    u64 gen = 0;
+    cudaGraphExec_t exec = nullptr;
+    HostBuf hq, hout;
+    DevBuf dq, dkeys, dcnt;
+  };
+  std::vector<TopkGraph*> graphs;
   bool timing = false;
   bool timing_suspend = false;  // helper passes (e.g. the bit-slice seed) are not timed
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -695,6 +710,15 @@ void destroy(fps_lib* L) {
                     &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->bs, &L->bsq})
     b->release();
   L->h_stage.release();
+  for (auto* gr : L->graphs) {
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    gr->hq.release();
+    gr->hout.release();
+    gr->dq.release();
+    gr->dkeys.release();
+    gr->dcnt.release();
+    delete gr;
+  }
   for (auto& p : L->ev_pool) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
@@ -1127,6 +1151,83 @@ int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t
   return rc;
 }
 
+namespace {
+
+bool graphs_enabled(const fps_lib* L) {
+  static const bool off = [] {
+    const char* e = std::getenv("FPS_GRAPHS");
+    return (e && std::string(e) == "0") || std::getenv("FPS_DEBUG") != nullptr;
+  }();
+  return !off && !L->timing;
+}
+
+// Replay (capturing on first use) the whole host-API top-k call for (Q, k).
+// Returns FPS_OK with results in gr->hout, or an error (the caller falls back).
+int topk_graph(fps_lib* L, const uint64_t* queries, u32 Q, u32 k, fps_lib::TopkGraph** out) {
+  fps_lib::TopkGraph* gr = nullptr;
+  for (auto* x : L->graphs)
+    if (x->Q == Q && x->k == k) gr = x;
+  int rc;
+  if (!gr) {
+    if (L->graphs.size() >= 8) {  // bounded cache: drop the oldest
+      auto* old = L->graphs.front();
+      if (old->exec) cudaGraphExecDestroy(old->exec);
+      old->hq.release(); old->hout.release(); old->dq.release(); old->dkeys.release(); old->dcnt.release();
+      delete old;
+      L->graphs.erase(L->graphs.begin());
+    }
+    gr = new fps_lib::TopkGraph();
+    gr->Q = Q;
+    gr->k = k;
+    L->graphs.push_back(gr);
+    if ((rc = gr->hq.ensure((size_t)Q * 24)) || (rc = gr->hout.ensure((size_t)Q * k * 8 + (size_t)Q * 4)) ||
+        (rc = gr->dq.ensure((size_t)Q * 24)) || (rc = gr->dkeys.ensure((size_t)Q * k * 8)) ||
+        (rc = gr->dcnt.ensure((size_t)Q * 4)))
+      return rc;
+  }
+  if (!gr->exec || gr->gen != g_alloc_gen.load()) {
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    gr->exec = nullptr;
+    // every scratch buffer must exist before capture (no allocation inside it)
+    if ((rc = topk_dispatch(L, gr->dq.as<u64>(), Q, k, gr->dkeys.as<u64>(), gr->dcnt.as<u32>(), L->stream, true)))
+      return rc;
+    CUDA_TRY(cudaStreamSynchronize(L->stream));
+    const u64 gen = g_alloc_gen.load();
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(L->stream, cudaStreamCaptureModeThreadLocal));
+    cudaMemcpyAsync(gr->dq.p, gr->hq.p, (size_t)Q * 24, cudaMemcpyHostToDevice, L->stream);
+    rc = topk_dispatch(L, gr->dq.as<u64>(), Q, k, gr->dkeys.as<u64>(), gr->dcnt.as<u32>(), L->stream, false);
+    cudaMemcpyAsync(gr->hout.p, gr->dkeys.p, (size_t)Q * k * 8, cudaMemcpyDeviceToHost, L->stream);
+    cudaMemcpyAsync(gr->hout.as<char>() + (size_t)Q * k * 8, gr->dcnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost,
+                    L->stream);
+    cudaError_t e = cudaStreamEndCapture(L->stream, &graph);
+    if (rc || e != cudaSuccess || g_alloc_gen.load() != gen) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      return rc ? rc : fail(FPS_ECUDA, "graph capture failed");
+    }
+    e = cudaGraphInstantiate(&gr->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      gr->exec = nullptr;
+      return fail(FPS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    gr->gen = gen;
+  }
+  std::memcpy(gr->hq.p, queries, (size_t)Q * 24);
+  CUDA_TRY(cudaGraphLaunch(gr->exec, L->stream));
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e != cudaSuccess) {
+    reset_state(L);
+    return fail(FPS_ECUDA, std::string("top-k graph: ") + cudaGetErrorString(e));
+  }
+  *out = gr;
+  return FPS_OK;
+}
+
+}  // namespace
+
 int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx, uint16_t* out_dist,
              uint32_t* out_cnt) {
   if (int rc = check_lib(lib)) return rc;
@@ -1138,6 +1239,16 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
   std::lock_guard<std::mutex> lk(lib->mu);
   DeviceGuard g(lib->device);
   int rc;
+  if (k <= KMAX_FUSED && graphs_enabled(lib)) {
+    fps_lib::TopkGraph* gr = nullptr;
+    if (topk_graph(lib, queries, Q, k, &gr) == FPS_OK) {
+      const u64* hk = gr->hout.as<u64>();
+      const u32* hc = reinterpret_cast<const u32*>(gr->hout.as<char>() + (size_t)Q * k * 8);
+      unpack_topk(hk, hc, Q, k, out_idx, out_dist, out_cnt);
+      return FPS_OK;
+    }
+    cudaGetLastError();  // fall through to the stream path
+  }
   if ((rc = stage_queries(lib, queries, Q))) return rc;
   if ((rc = lib->keys.ensure((size_t)Q * k * 8)) || (rc = lib->cnt.ensure((size_t)Q * 4))) return rc;
   if (k <= KMAX_FUSED) {
