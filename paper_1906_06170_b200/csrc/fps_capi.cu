@@ -142,6 +142,11 @@ struct fps_lib {
   DevBuf bs, bsq;
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
   HostBuf h_stage;
+  // mapped pinned result buffer of the single-query host path (written by the
+  // select kernel over PCIe: no D2H copy) and its device alias
+  void* hmap = nullptr;
+  void* dmap = nullptr;
+  size_t hmap_bytes = 0;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
   int last_kernel = 0;  // fps_last_kernel
   // host-API top-k calls replayed as one CUDA graph per (Q, k):
@@ -318,7 +323,7 @@ std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
 
 template <int QW, int E, bool CMP>
 int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
-               u64 n_prefix = 0) {
+               u64 n_prefix = 0, const u64* h_qin = nullptr) {
   Config c = make_config<QW, E, fps::MODE_TOPK, false, CMP>(L, Q, k, n_prefix);
   int rc;
   if ((rc = ensure_state(L, Q))) return rc;
@@ -326,6 +331,12 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   if ((rc = L->cand.ensure((size_t)Q * c.cand_cap * 8))) return rc;
   if (prepare_only) return FPS_OK;
   fps::ScanArgs a = base_args(L, d_q, Q);
+  if (h_qin) {  // single query passed by value (host API): no H2D copy
+    a.queries = nullptr;
+    a.qin[0] = h_qin[0];
+    a.qin[1] = h_qin[1];
+    a.qin[2] = h_qin[2];
+  }
   if (n_prefix) a.n = n_prefix;
   a.k = k;
   a.cap = c.cap;
@@ -710,6 +721,7 @@ void destroy(fps_lib* L) {
                     &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->bs, &L->bsq})
     b->release();
   L->h_stage.release();
+  if (L->hmap) cudaFreeHost(L->hmap);
   for (auto* gr : L->graphs) {
     if (gr->exec) cudaGraphExecDestroy(gr->exec);
     gr->hq.release();
@@ -1153,6 +1165,17 @@ int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t
 
 namespace {
 
+// Host wait for a synchronous call: spin on cudaStreamQuery (a short scan
+// finishes in tens of microseconds, and a blocking sync adds wake-up latency).
+cudaError_t wait_stream(cudaStream_t s) {
+  static const bool block = std::getenv("FPS_BLOCKING_SYNC") != nullptr;
+  if (block) return cudaStreamSynchronize(s);
+  for (;;) {
+    cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+  }
+}
+
 bool graphs_enabled(const fps_lib* L) {
   static const bool off = [] {
     const char* e = std::getenv("FPS_GRAPHS");
@@ -1217,7 +1240,7 @@ int topk_graph(fps_lib* L, const uint64_t* queries, u32 Q, u32 k, fps_lib::TopkG
   }
   std::memcpy(gr->hq.p, queries, (size_t)Q * 24);
   CUDA_TRY(cudaGraphLaunch(gr->exec, L->stream));
-  cudaError_t e = cudaStreamSynchronize(L->stream);
+  cudaError_t e = wait_stream(L->stream);
   if (e != cudaSuccess) {
     reset_state(L);
     return fail(FPS_ECUDA, std::string("top-k graph: ") + cudaGetErrorString(e));
@@ -1239,6 +1262,40 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
   std::lock_guard<std::mutex> lk(lib->mu);
   DeviceGuard g(lib->device);
   int rc;
+  if (Q == 1 && k <= KMAX_FUSED && !lib->timing) {
+    // single query: the query travels as a kernel parameter and the select
+    // kernel writes straight into mapped pinned memory -- two launches, no copies
+    const size_t need = (size_t)k * 8 + 64;
+    if (lib->hmap_bytes < need) {
+      if (lib->hmap) cudaFreeHost(lib->hmap);
+      lib->hmap = nullptr;
+      lib->hmap_bytes = 0;
+      if (cudaHostAlloc(&lib->hmap, need, cudaHostAllocMapped) != cudaSuccess ||
+          cudaHostGetDevicePointer(&lib->dmap, lib->hmap, 0) != cudaSuccess) {
+        cudaGetLastError();
+        lib->hmap = nullptr;
+      } else {
+        lib->hmap_bytes = need;
+      }
+    }
+    if (lib->hmap) {
+      u64* dk = reinterpret_cast<u64*>(lib->dmap);
+      u32* dc = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->dmap) + (size_t)k * 8);
+      lib->last_kernel = 1;
+      rc = lib->compact ? topk_fused<1, 4, true>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries))
+                        : topk_fused<1, 4, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
+      if (rc) { reset_state(lib); return rc; }
+      cudaError_t e = wait_stream(lib->stream);
+      if (e != cudaSuccess) {
+        reset_state(lib);
+        return fail(FPS_ECUDA, std::string("top-k: ") + cudaGetErrorString(e));
+      }
+      const u64* hk = reinterpret_cast<const u64*>(lib->hmap);
+      const u32* hc = reinterpret_cast<const u32*>(reinterpret_cast<const char*>(lib->hmap) + (size_t)k * 8);
+      unpack_topk(hk, hc, 1, k, out_idx, out_dist, out_cnt);
+      return FPS_OK;
+    }
+  }
   if (k <= KMAX_FUSED && graphs_enabled(lib)) {
     fps_lib::TopkGraph* gr = nullptr;
     if (topk_graph(lib, queries, Q, k, &gr) == FPS_OK) {

@@ -28,6 +28,12 @@
 #ifndef FPS_QW1_MINB
 #define FPS_QW1_MINB 2  // CTAs per SM the single-query kernels are register-limited for
 #endif
+#ifndef FPS_QW1_U
+#define FPS_QW1_U 1  // single-buffered single-query kernels: iterations loaded per trip
+#endif
+#ifndef FPS_QW1_PIPE
+#define FPS_QW1_PIPE 1  // single-query kernels: 1 = next iteration's loads in flight (double buffer)
+#endif
 
 namespace fps {
 
@@ -167,7 +173,8 @@ struct ScanArgs {
   const char* lib;               // tiled library (see TILE_BYTES_*)
   u64 n;           // valid entries on this device
   u64 index_base;  // global index of entry 0
-  const u64* queries;  // Q x 3
+  const u64* queries;  // Q x 3 (device); nullptr: the single query is inline in qin
+  u64 qin[3];          // inline query words (host API, Q == 1: no H2D copy)
   const unsigned char* radius;  // MODE_RANGE: per-query radius
   u32 Q;
   u32 Qmin;        // MINQ: number of queries the distance is minimised over
@@ -260,9 +267,9 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
   for (int j = 0; j < QW; ++j) {
     u32 qi = qg * QW + j;
     bool ok = qi < a.Q;
-    q0[j] = ok ? a.queries[3 * (u64)qi + 0] : 0;
-    q1[j] = ok ? a.queries[3 * (u64)qi + 1] : 0;
-    q2[j] = ok ? a.queries[3 * (u64)qi + 2] : 0;
+    q0[j] = ok ? (a.queries ? a.queries[3 * (u64)qi + 0] : a.qin[0]) : 0;
+    q1[j] = ok ? (a.queries ? a.queries[3 * (u64)qi + 1] : a.qin[1]) : 0;
+    q2[j] = ok ? (a.queries ? a.queries[3 * (u64)qi + 2] : a.qin[2]) : 0;
     if (MODE == MODE_TOPK) T[j] = ok ? T_OPEN : 0;
     else if (MODE == MODE_RANGE) T[j] = ok ? (u32)a.radius[qi] + 1 : 0;
     else T[j] = ok ? 256 : 0;
@@ -453,7 +460,7 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     }
   };
 
-  constexpr int U = 1;  // iterations per trip (QW == 1 keeps two trips in flight)
+  constexpr int U = (QW == 1 && !FPS_QW1_PIPE) ? FPS_QW1_U : 1;  // iterations per trip
   // loop trips between global-bound refreshes (tg is replicated over L2 slices
   // for small Q, so the single-query kernel can afford one load per trip)
   constexpr int REFRESH = (QW == 1) ? 2 : 8;
@@ -506,7 +513,14 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       prefetch_tg();
     }
   };
-  if (QW == 1) {
+  if (QW == 1 && !FPS_QW1_PIPE) {
+    // single-buffered variant: fewer registers, more resident warps
+    for (; it + U <= it_main; it += U) {
+      Trip t;
+      load_trip(t, it);
+      run_trip(t, it);
+    }
+  } else if (QW == 1) {
     // HBM-bound single-query scan over a static contiguous part, software-pipelined:
     // the next iteration's loads are in flight while the current one is processed.
     // (Dynamic chunk claiming and narrower per-warp parts measured slower on
@@ -625,6 +639,85 @@ __device__ void block_bitonic_sort(u64* s, int n_pow2) {
   }
 }
 
+// Barrier over the first nthreads threads of the CTA (named barrier 1).
+__device__ __forceinline__ void bar_sync_n(u32 nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Bitonic sort of P keys, one per thread t < P (fully unrolled: every stride
+// is a compile-time constant). Strides below 32 exchange through warp
+// shuffles, wider ones through a double-buffered shared array with a
+// P-thread named barrier (one barrier per stage).
+template <u32 P>
+__device__ __forceinline__ u64 bitonic_p(u64 key, u32 t, u64* sh) {
+  int buf = 0;
+#pragma unroll
+  for (u32 size = 2; size <= P; size <<= 1) {
+    const bool up = (t & size) == 0;
+#pragma unroll
+    for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+      u64 other;
+      if (stride >= 32) {
+        u64* b = sh + buf * SEL_THREADS;
+        b[t] = key;
+        bar_sync_n(P);
+        other = b[t ^ stride];
+        buf ^= 1;
+      } else {
+        other = __shfl_xor_sync(FULL, key, stride);
+      }
+      const bool lt = other < key;
+      key = (lt == (((t & stride) == 0) == up)) ? other : key;
+    }
+  }
+  return key;
+}
+
+// Small-select path: the survivors (n <= SEL_THREADS, one key per thread in
+// `my`) that are within the final bound are sorted by the first p = pow2 >= m
+// threads only (p >= 32); when some fall outside the bound they are first
+// compacted through shared memory. The k smallest keys (padded with ~0) go to
+// out; returns m. out == nullptr: warm-up pass (code fetched into the
+// instruction cache while the scan drains).
+__device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u32* s_wcnt, u32 k, u64* out) {
+  const u32 t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const u32 m = (u32)__syncthreads_count(keep);
+  u64 key = keep ? my : ~0ull;
+  if (m != n) {  // uniform: survivors are not exactly threads [0, n) -- compact
+    const u32 bal = __ballot_sync(FULL, keep);
+    if (lane == 0) s_wcnt[w] = __popc(bal);
+    __syncthreads();
+    u32 off = 0;
+#pragma unroll
+    for (int i = 0; i < SEL_THREADS / 32; ++i) off += (i < (int)w) ? s_wcnt[i] : 0;
+    u64* comp = sh + 2 * SEL_THREADS;
+    if (keep) comp[off + __popc(bal & lanemask_lt())] = my;
+    __syncthreads();
+    key = t < m ? comp[t] : ~0ull;
+  }
+#ifdef FPS_SEL_PROBE
+  if (out && t == 0) { g_sel_clock[10] = key; SEL_MARK(8); }
+#endif
+  u32 p = 32;
+  while (p < m) p <<= 1;
+  if (t < p) {
+    switch (p) {
+      case 32: key = bitonic_p<32>(key, t, sh); break;
+      case 64: key = bitonic_p<64>(key, t, sh); break;
+      case 128: key = bitonic_p<128>(key, t, sh); break;
+      case 256: key = bitonic_p<256>(key, t, sh); break;
+      default: key = bitonic_p<512>(key, t, sh); break;
+    }
+#ifdef FPS_SEL_PROBE
+    if (out && t == 0) { g_sel_clock[10] = key; SEL_MARK(9); }
+#endif
+    if (out != nullptr && t < k) out[t] = key;
+  }
+  if (out != nullptr)
+    for (u32 i = p + t; i < k; i += SEL_THREADS) out[i] = ~0ull;
+  return m;
+}
+
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
                                                              u32* ghist, u32 gstride, u32 tg_rep, u32 k,
                                                              u64* out_keys, u32* out_cnt, int reset) {
@@ -632,13 +725,54 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   __shared__ u32 hist[256];
   __shared__ u32 s_nres, s_ntie, s_T, s_m;
   __shared__ u64 s_cut;
-  // launched as a programmatic dependent of the scan: wait for its results
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  SEL_MARK(0);
   const u32 q = blockIdx.x;
-  const u32 n = cand_cnt[q];
   const u64* c = cand + (u64)q * cand_cap;
-  const u32 bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
+  // Launched as a programmatic dependent of the scan. While the scan drains,
+  // run the small-sort code once on dummy keys: after an L2 flush the
+  // kernel's instructions are cold and each first-touch fetch costs ~1 us.
+  __shared__ u32 s_wcnt[SEL_THREADS / 32];
+  u64 my = 0;
+  u32 n = SEL_THREADS, bound = T_OPEN, m_small = 0;
+  u64* dst = nullptr;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // scan results visible
+      SEL_MARK(0);
+      // speculative first-slot read, independent of the count load
+      my = threadIdx.x < cand_cap ? c[threadIdx.x] : ~0ull;
+      n = cand_cnt[q];
+      bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
+      dst = out_keys + (u64)q * k;
+#ifdef FPS_SEL_PROBE
+      if (threadIdx.x == 0) g_sel_clock[1] = my + n + bound;  // wait for the loads
+      SEL_MARK(2);
+#endif
+      if (n > (u32)SEL_THREADS) break;
+    }
+    // common case: every survivor fits one key per thread -- sort the ones
+    // within the bound (unique keys: the first k sorted are the answer)
+    m_small = select_small(my, n, threadIdx.x < n && key_d(my) <= bound, ssel, s_wcnt, k, dst);
+    if (pass == 1) SEL_MARK(3);
+#ifdef FPS_SEL_PROBE
+    if (pass == 1 && threadIdx.x == 0) {
+      g_sel_clock[5] = g_sel_clock[0] + m_small;
+      g_sel_clock[6] = g_sel_clock[0] + bound;
+      g_sel_clock[7] = g_sel_clock[0] + n;
+    }
+#endif
+    __syncthreads();
+  }
+  if (n <= (u32)SEL_THREADS) {
+    if (threadIdx.x == 0) out_cnt[q] = m_small < k ? m_small : k;
+    SEL_MARK(11);
+    if (reset) {
+      for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
+      for (u32 r = threadIdx.x; r < tg_rep; r += blockDim.x) tg[((u64)q * tg_rep + r) * gstride] = T_OPEN;
+      if (threadIdx.x == 0) cand_cnt[q] = 0;
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
   if (threadIdx.x == 0) { s_nres = 0; s_ntie = 0; }
   __syncthreads(); SEL_MARK(1);
