@@ -136,6 +136,7 @@ struct fps_lib {
   // top-k state that must start clean (tg = 255, ghist = 0, cand_cnt = 0);
   // select_kernel restores it after every call
   DevBuf tg, ghist, cand_cnt;
+  DevBuf dyn;  // tail-claim counter of the bulk-copy single-query scan (reset by select_kernel)
   u32 state_q = 0;
   DevBuf buf, cand, queries, keys, cnt, radius, rkeys, rcount, sort_tmp, sort_out, seg;
   // bit-plane copy of the library for the multi-query scans (built on first use)
@@ -182,17 +183,16 @@ struct DeviceGuard {
   }
 };
 
-template <int QW, int E, int MODE>
+template <int QW, int E, int MODE, bool CMP = false>
 size_t scan_smem() {
-  if (MODE == fps::MODE_RANGE) return 0;
-  return (size_t)WPB * (QW * fps::HB * sizeof(u32) + sizeof(fps::WarpState<QW>));
+  return fps::ScanSmem<QW, E, MODE, CMP>::total(WPB);
 }
 
 template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
 int max_ctas_per_sm() {
   static int cached = 0;
   if (cached) return cached;
-  size_t smem = scan_smem<QW, E, MODE>();
+  size_t smem = scan_smem<QW, E, MODE, CMP>();
   auto* k = fps::scan_kernel<QW, E, MODE, MINQ, CMP>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int blocks = 0;
@@ -230,7 +230,7 @@ Config make_config(const fps_lib* L, u32 Q, u32 k, u64 n_prefix = 0) {
     c.cap = cap;
     c.cand_cap = parts * (u64)k;
   }
-  c.smem = scan_smem<QW, E, MODE>();
+  c.smem = scan_smem<QW, E, MODE, CMP>();
   return c;
 }
 
@@ -256,6 +256,8 @@ int ensure_state(fps_lib* L, u32 Q) {
   if ((rc = L->tg.ensure(std::max((size_t)Qa * 4, (size_t)Q * tg_replicas(Q) * ghist_stride(Q) * 4)))) return rc;
   if ((rc = L->ghist.ensure(std::max(gh, (size_t)Qa * fps::HB * 4)))) return rc;
   if ((rc = L->cand_cnt.ensure((size_t)Qa * 4))) return rc;
+  if ((rc = L->dyn.ensure(256))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L->dyn.p, 0, L->dyn.bytes, L->stream));
   CUDA_TRY(fill_tg(L));
   CUDA_TRY(cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream));
   CUDA_TRY(cudaMemsetAsync(L->cand_cnt.p, 0, L->cand_cnt.bytes, L->stream));
@@ -270,6 +272,7 @@ void reset_state(fps_lib* L) {
   fill_tg(L);
   cudaMemsetAsync(L->ghist.p, 0, L->ghist.bytes, L->stream);
   cudaMemsetAsync(L->cand_cnt.p, 0, L->cand_cnt.bytes, L->stream);
+  if (L->dyn.p) cudaMemsetAsync(L->dyn.p, 0, L->dyn.bytes, L->stream);
 }
 
 u32 scan_flags() {
@@ -291,11 +294,31 @@ fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
   return a;
 }
 
+// Dynamic tail of the bulk-copy single-query scan: the first FPS_QW1_DYN_PCT
+// percent of the tiles are split statically over the warps, the rest is
+// claimed in chunks (scan flag 64 disables it). Needs one query group: every
+// warp scans for the same query.
+#ifndef FPS_QW1_DYN_PCT
+#define FPS_QW1_DYN_PCT 100
+#endif
+#ifndef FPS_QW1_DYN_CHUNK
+#define FPS_QW1_DYN_CHUNK 2
+#endif
+template <int QW, int E, int MODE, bool CMP>
+void set_dyn(fps_lib* L, fps::ScanArgs& a) {
+  if (!fps::ScanSmem<QW, E, MODE, CMP>::TMA || MODE != fps::MODE_TOPK || a.n_qg != 1 || (a.flags & 64)) return;
+  if (FPS_QW1_DYN_PCT >= 100 || !L->dyn.p) return;
+  a.dyn_ctr = L->dyn.as<u32>();
+  a.dyn_start = a.iters * FPS_QW1_DYN_PCT / 100;
+  a.dyn_chunk = FPS_QW1_DYN_CHUNK;
+}
+
 // select_kernel launched as a programmatic dependent of the scan kernel: its
 // launch and block scheduling overlap the scan's tail, and griddepcontrol.wait
 // inside it orders it after the scan's completion (and memory flush).
 cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
-                          u32* ghist, u32 gstride, u32 tg_rep, u32 k, u64* out_keys, u32* out_cnt, bool pdl) {
+                          u32* ghist, u32 gstride, u32 tg_rep, u32 k, u64* out_keys, u32* out_cnt, bool pdl,
+                          u32* dyn_ctr = nullptr) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(Q);
   cfg.blockDim = dim3(fps::SEL_THREADS);
@@ -307,7 +330,7 @@ cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* ca
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, fps::select_kernel, cand, cand_cnt, cand_cap, tg, ghist, gstride, tg_rep, k, out_keys,
-                            out_cnt, 1);
+                            out_cnt, 1, dyn_ctr);
 }
 
 // Record an event pair around the next scan-kernel launch when timing is on.
@@ -352,10 +375,28 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   a.cand = L->cand.as<u64>();
   a.cand_cnt = L->cand_cnt.as<u32>();
   a.cand_cap = c.cand_cap;
+  set_dyn<QW, E, fps::MODE_TOPK, CMP>(L, a);
   if (c.warps > 0 && L->n > 0) {
     auto* ev = timing_slot(L);
     if (ev) cudaEventRecord(ev->first, s);
-    fps::scan_kernel<QW, E, fps::MODE_TOPK, false, CMP><<<c.grid, WPB * 32, c.smem, s>>>(a);
+    if (ev) {
+      fps::scan_kernel<QW, E, fps::MODE_TOPK, false, CMP><<<c.grid, WPB * 32, c.smem, s>>>(a);
+    } else {
+      // programmatic dependent of whatever kernel precedes it on the stream
+      // (typically the previous call's select_kernel): launch latency hides
+      // behind that kernel; griddepcontrol.wait in the scan orders the rest
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(c.grid);
+      cfg.blockDim = dim3(WPB * 32);
+      cfg.dynamicSmemBytes = c.smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = (a.flags & 128) ? 0 : 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, fps::scan_kernel<QW, E, fps::MODE_TOPK, false, CMP>, a));
+    }
     if (ev) cudaEventRecord(ev->second, s);
     L->launches++;
   }
@@ -378,7 +419,7 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   }
   LAUNCH_CHECK("scan_kernel<topk>");
   CUDA_TRY(launch_select(Q, sel_smem, s, a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, a.tg_rep, k,
-                         d_keys, d_cnt, !(a.flags & 32)));
+                         d_keys, d_cnt, !(a.flags & 32), a.dyn_ctr));
   L->launches++;
   LAUNCH_CHECK("select_kernel");
   if (std::getenv("FPS_DEBUG")) {
@@ -557,7 +598,7 @@ int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_
     if (qw == 4) return topk_fused<4, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
     return topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   }
-  if (qw == 1) return topk_fused<1, 4, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (qw == 1) return topk_fused<1, FPS_QW1_E, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   if (qw == 2) return topk_fused<2, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   if (qw == 4) return topk_fused<4, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   return topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
@@ -1283,7 +1324,7 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
       u32* dc = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->dmap) + (size_t)k * 8);
       lib->last_kernel = 1;
       rc = lib->compact ? topk_fused<1, 4, true>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries))
-                        : topk_fused<1, 4, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
+                        : topk_fused<1, FPS_QW1_E, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
       if (rc) { reset_state(lib); return rc; }
       cudaError_t e = wait_stream(lib->stream);
       if (e != cudaSuccess) {
@@ -1330,6 +1371,25 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
   return FPS_OK;
 }
 
+#ifdef FPS_SCAN_TRACE
+// debug builds only (not part of include/fps.h): timeline markers
+extern "C" int fps_trace_mark(fps_lib* lib, int slot) {
+  fps::mark_kernel<<<1, 1, 0, lib->stream>>>(slot);
+  return (int)cudaGetLastError();
+}
+extern "C" int fps_trace_read(uint64_t* marks, uint64_t* warps) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(marks, fps::g_mark, 8 * sizeof(u64));
+  return (int)cudaMemcpyFromSymbol(warps, fps::g_scan_trace, sizeof(fps::g_scan_trace));
+}
+extern "C" int fps_trace_clear() {
+  static u64 zeros[16384 * 4];
+  cudaDeviceSynchronize();
+  cudaMemcpyToSymbol(fps::g_mark, zeros, 8 * sizeof(u64));
+  return (int)cudaMemcpyToSymbol(fps::g_scan_trace, zeros, sizeof(zeros));
+}
+#endif
+
 int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx,
                  uint16_t* out_dist, uint32_t* out_cnt) {
   if (int rc = check_lib(lib)) return rc;
@@ -1365,6 +1425,7 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   a.cand = lib->cand.as<u64>();
   a.cand_cnt = lib->cand_cnt.as<u32>();
   a.cand_cap = c.cand_cap;
+  if (!lib->compact) set_dyn<1, 4, fps::MODE_TOPK, false>(lib, a);
   if (c.warps > 0 && lib->n > 0) {
     if (lib->compact) fps::scan_kernel<1, 4, fps::MODE_TOPK, true, true><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
     else fps::scan_kernel<1, 4, fps::MODE_TOPK, true, false><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
@@ -1374,7 +1435,7 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   while (kp < (int)k) kp <<= 1;
   cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, lib->stream, a.cand, a.cand_cnt, c.cand_cap, a.tg,
-                         a.ghist, a.gstride, a.tg_rep, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), true));
+                         a.ghist, a.gstride, a.tg_rep, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), true, a.dyn_ctr));
   lib->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, cudaGetErrorString(e)); }

@@ -31,6 +31,18 @@
 #ifndef FPS_QW1_U
 #define FPS_QW1_U 1  // single-buffered single-query kernels: iterations loaded per trip
 #endif
+#ifndef FPS_QW1_E
+#define FPS_QW1_E 4  // single-query top-k: entries per lane per iteration (4: 256-bit loads, 2: 128-bit)
+#endif
+#ifndef FPS_QW1_TMA
+#define FPS_QW1_TMA 1  // single-query scans stream tiles through a per-warp shared-memory ring (bulk copies)
+#endif
+#ifndef FPS_QW1_STAGES
+#define FPS_QW1_STAGES 2  // tiles in flight per warp in the bulk-copy ring
+#endif
+#ifndef FPS_EXIT_TGP
+#define FPS_EXIT_TGP 1  // single-query scans append survivors under the last prefetched bound
+#endif
 #ifndef FPS_QW1_PIPE
 #define FPS_QW1_PIPE 1  // single-query kernels: 1 = next iteration's loads in flight (double buffer)
 #endif
@@ -188,6 +200,9 @@ struct ScanArgs {
   u32 pub_every;   // only library parts with part % pub_every == 0 publish to ghist
   u64 n_parts;     // library parts
   u64 iters;       // ceil(n / (32*E))
+  u32* dyn_ctr;    // bulk-copy single-query scan: tail chunk counter (nullptr: static parts only)
+  u64 dyn_start;   // first tile of the dynamically claimed tail
+  u64 dyn_chunk;   // tiles per claim
   // MODE_TOPK state (all per query unless noted)
   u32* tg;         // global filter bound: entries with d > tg[q] are not in the top-k
   u32* ghist;      // [Q][HB] distances of published candidates (distinct entries)
@@ -236,6 +251,43 @@ __device__ __forceinline__ u32 tighten_tg(const ScanArgs& a, u32 qi, int lane) {
   return tt;
 }
 
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAIT;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Streaming variant: an L2 evict-first policy, so a library scanned once per
+// call does not displace the small hot scan state (bounds, histograms).
+__device__ __forceinline__ u64 l2_evict_first_policy() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, u32 bytes, u64* bar, u64 pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 // Per-warp slow-path state, kept in shared memory (only touched on inserts).
 template <int QW>
 struct WarpState {
@@ -244,6 +296,35 @@ struct WarpState {
   u32 cnt[QW];    // buffer fill
 };
 
+// Dynamic shared-memory layout of scan_kernel (host and device agree on it):
+// [per-warp histograms][per-warp WarpState] then, for the bulk-copy
+// single-query variant, [per-warp ring of STAGES tiles][per-warp mbarriers]
+// [per-warp slot tile indices].
+template <int QW, int E, int MODE, bool CMP>
+struct ScanSmem {
+  static constexpr bool TMA = (QW == 1 && E == 4 && !CMP && FPS_QW1_TMA != 0);
+  static constexpr int STAGES = FPS_QW1_STAGES;
+  __host__ __device__ static constexpr size_t base(int nwb) {
+    return MODE == MODE_RANGE ? 0 : (size_t)nwb * (QW * HB * sizeof(u32) + sizeof(WarpState<QW>));
+  }
+  __host__ __device__ static constexpr size_t ring_off(int nwb) { return TMA ? (base(nwb) + 127) / 128 * 128 : base(nwb); }
+  __host__ __device__ static constexpr size_t bars_off(int nwb) {
+    return ring_off(nwb) + (TMA ? (size_t)nwb * STAGES * TILE_BYTES_FULL : 0);
+  }
+  __host__ __device__ static constexpr size_t tiles_off(int nwb) { return bars_off(nwb) + (TMA ? (size_t)nwb * STAGES * 8 : 0); }
+  __host__ __device__ static constexpr size_t total(int nwb) { return tiles_off(nwb) + (TMA ? (size_t)nwb * STAGES * 8 : 0); }
+};
+
+#ifdef FPS_SCAN_TRACE
+__device__ u64 g_scan_trace[16384 * 4];  // per warp: start, end (globaltimer ns), SM id, first data
+__device__ u64 g_mark[8];                // marker kernel / select start / select end (globaltimer ns)
+__device__ __forceinline__ u64 gtimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void mark_kernel(int slot) { g_mark[slot] = gtimer(); }
+#endif
 template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
 __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 3))) scan_kernel(const ScanArgs a) {
   extern __shared__ u32 smem[];
@@ -254,7 +335,15 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
   // let a programmatic dependent (select_kernel) launch early; it still waits
   // for this grid to complete before reading its results
   asm volatile("griddepcontrol.launch_dependents;");
+  // launched as a programmatic dependent of the previous call's select_kernel
+  // (host API / graphs): the CTAs get resident while it runs, and wait here
+  // until it has completed (it resets the bounds, histograms and counters)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (g >= (u64)a.n_qg * a.n_parts) return;  // warp-uniform; no block-level sync below
+#ifdef FPS_SCAN_TRACE
+  u64 tr_start, tr_first = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
+#endif
   const u32 qg = (u32)(g % a.n_qg);
   const u64 part = g / a.n_qg;
   const u64 it0 = part * a.iters / a.n_parts;
@@ -460,7 +549,7 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     }
   };
 
-  constexpr int U = (QW == 1 && !FPS_QW1_PIPE) ? FPS_QW1_U : 1;  // iterations per trip
+  constexpr int U = (QW == 1) ? FPS_QW1_U : 1;  // iterations per trip
   // loop trips between global-bound refreshes (tg is replicated over L2 slices
   // for small Q, so the single-query kernel can afford one load per trip)
   constexpr int REFRESH = (QW == 1) ? 2 : 8;
@@ -513,7 +602,111 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       prefetch_tg();
     }
   };
-  if (QW == 1 && !FPS_QW1_PIPE) {
+  using SL = ScanSmem<QW, E, MODE, CMP>;
+  if constexpr (SL::TMA) {
+    // HBM-bound single-query scan. The warp's tiles stream through a
+    // STAGES-deep shared-memory ring filled by the bulk-copy engine (one 3 KB
+    // cp.async.bulk per tile, completion on a per-slot mbarrier), so the bytes
+    // in flight cost no registers. Lane 0 is the producer: it refills a slot
+    // once every lane has consumed it and records the slot's tile index.
+    //
+    // Tile sequence: the warp's static part of the first dyn_start tiles, then
+    // (when dyn_ctr is set) chunks of the remaining tiles claimed from a global
+    // counter -- warps that drew more bandwidth take more of the tail. Claims
+    // are in increasing order, so each warp still sees ascending indices (the
+    // ordered candidate buffers rely on it). The next claim is issued one
+    // chunk ahead so its latency hides behind the copies.
+    constexpr int S = SL::STAGES;
+    constexpr u64 NONE = ~0ull;
+    char* ring = reinterpret_cast<char*>(smem) + SL::ring_off(nwb) + (size_t)wib * S * TILE_BYTES_FULL;
+    u64* bars = reinterpret_cast<u64*>(reinterpret_cast<char*>(smem) + SL::bars_off(nwb)) + wib * S;
+    u64* slot_tile = reinterpret_cast<u64*>(reinterpret_cast<char*>(smem) + SL::tiles_off(nwb)) + wib * S;
+    const u64 pol = l2_evict_first_policy();
+    const bool dyn = a.dyn_ctr != nullptr;
+    const u64 n_static = dyn ? a.dyn_start : a.iters;
+    u64 s_next = part * n_static / a.n_parts, s_end = (part + 1) * n_static / a.n_parts;
+    u64 d_next = 0, d_end = 0;
+    u32 pend = 0;
+    bool has_pend = false;
+    auto claim = [&]() {
+      pend = atomicAdd(a.dyn_ctr, 1u);
+      has_pend = true;
+    };
+    auto next_tile = [&]() -> u64 {
+      if (s_next < s_end) {
+        const u64 t = s_next++;
+        if (s_next == s_end && dyn) claim();
+        return t;
+      }
+      if (d_next >= d_end) {
+        if (!has_pend) return NONE;
+        const u64 c0 = a.dyn_start + (u64)pend * a.dyn_chunk;
+        if (c0 >= a.iters) {
+          has_pend = false;
+          return NONE;
+        }
+        d_next = c0;
+        d_end = c0 + a.dyn_chunk < a.iters ? c0 + a.dyn_chunk : a.iters;
+        claim();
+      }
+      return d_next++;
+    };
+    auto issue = [&](int st) {  // lane 0 only
+      const u64 t = next_tile();
+      slot_tile[st] = t;
+      if (t != NONE) {
+        mbar_expect_tx(&bars[st], (u32)TILE_BYTES_FULL);
+        bulk_g2s_stream(ring + st * TILE_BYTES_FULL, a.lib + t * TILE_BYTES_FULL, (u32)TILE_BYTES_FULL, &bars[st], pol);
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+      }
+    };
+    if (lane == 0) {
+#pragma unroll
+      for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (dyn && s_next == s_end) claim();
+#pragma unroll
+      for (int st = 0; st < S; ++st) issue(st);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (u64 j = 0;; ++j) {
+      const int st = (int)(j % S);
+      mbar_wait(&bars[st], (u32)(j / S) & 1u);
+      const u64 i = *(volatile const u64*)&slot_tile[st];
+      if (i == NONE) break;
+#ifdef FPS_SCAN_TRACE
+      if (j == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
+#endif
+      const u64* tl = reinterpret_cast<const u64*>(ring + st * TILE_BYTES_FULL) + lane * 4;
+      u64 A[4], B[4], C[4];
+      {
+        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(tl);
+        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(tl + 2);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(tl + TILE_FULL);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(tl + TILE_FULL + 2);
+        const ulonglong2 c0 = *reinterpret_cast<const ulonglong2*>(tl + 2 * TILE_FULL);
+        const ulonglong2 c1 = *reinterpret_cast<const ulonglong2*>(tl + 2 * TILE_FULL + 2);
+        A[0] = a0.x; A[1] = a0.y; A[2] = a1.x; A[3] = a1.y;
+        B[0] = b0.x; B[1] = b0.y; B[2] = b1.x; B[3] = b1.y;
+        C[0] = c0.x; C[1] = c0.y; C[2] = c1.x; C[3] = c1.y;
+      }
+      process(*reinterpret_cast<const u64(*)[E]>(A), *reinterpret_cast<const u64(*)[E]>(B),
+              *reinterpret_cast<const u64(*)[E]>(C), i, i >= n_full);
+      __syncwarp();  // every lane's reads of slot st are complete (values consumed)
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(st);
+      }
+      if (MODE == MODE_TOPK && !(a.flags & 2) && ++since_refresh == REFRESH) {
+        since_refresh = 0;
+        apply_tg();
+        prefetch_tg();
+      }
+    }
+    it = it1;
+  } else if (QW == 1 && !FPS_QW1_PIPE) {
     // single-buffered variant: fewer registers, more resident warps
     for (; it + U <= it_main; it += U) {
       Trip t;
@@ -559,6 +752,15 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     process(A, B, C, it, it >= n_full);
   }
 
+#ifdef FPS_SCAN_TRACE
+  if (lane == 0 && g < 16384) {
+    u64 tr_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_end));
+    g_scan_trace[g * 4 + 0] = tr_start;
+    g_scan_trace[g * 4 + 1] = tr_end;
+    g_scan_trace[g * 4 + 3] = tr_first;
+  }
+#endif
   if (MODE == MODE_HIST) {
     __syncwarp();
 #pragma unroll 1
@@ -577,25 +779,46 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     for (int j = 0; j < QW; ++j) {
       const u32 qi = qg * QW + j;
       if (qi >= a.Q) continue;
-      if (ws->cnt[j] > a.k) compact(j);
+      // single query: the bound prefetched during the scan (possibly looser
+      // than the final one -- select re-filters) saves a load at exit
+      const u32 t = (QW == 1 && FPS_EXIT_TGP) ? tgp : *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));
+      // survivors (d <= t) counted from the histogram that mirrors the buffer:
+      // most warps have none and skip reading their buffer back
+      const u32* hj = hist + j * HB;
+      u32 c = 0;
+      for (u32 b = lane; b < (u32)HB; b += 32) c += b <= t ? hj[b] : 0u;
+      c = __reduce_add_sync(FULL, c);
+      if (c == 0) continue;
+      if (c > a.k) compact(j);  // at most k per warp reach the candidate list
       const u32 n = ws->cnt[j];
-      const u32 t = *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));
       const u64* bj = wbuf + (u64)j * a.cap;
-      // survivors: d <= tg (an exact bound on the k-th distance)
-      for (u32 i0 = 0; i0 < n; i0 += 32) {
-        const u32 i = i0 + lane;
-        const u64 key = i < n ? bj[i] : ~0ull;
-        const bool keep = i < n && key_d(key) <= t;
-        const u32 kb = __ballot_sync(FULL, keep);
-        const u32 nk = __popc(kb);
-        if (nk == 0) continue;
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(a.cand_cnt + qi, nk);
-        base = __shfl_sync(FULL, base, 0);
-        if (keep) a.cand[(u64)qi * a.cand_cap + base + __popc(kb & lanemask_lt())] = key;
+      // survivors: d <= tg (an exact bound on the k-th distance); four
+      // independent loads per lane in flight
+      for (u32 i0 = 0; i0 < n; i0 += 128) {
+        u64 kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const u32 i = i0 + u * 32 + lane;
+          kk[u] = i < n ? bj[i] : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const u32 i = i0 + u * 32 + lane;
+          const bool keep = i < n && key_d(kk[u]) <= t;
+          const u32 kb = __ballot_sync(FULL, keep);
+          const u32 nk = __popc(kb);
+          if (nk == 0) continue;
+          u32 base = 0;
+          if (lane == 0) base = atomicAdd(a.cand_cnt + qi, nk);
+          base = __shfl_sync(FULL, base, 0);
+          if (keep) a.cand[(u64)qi * a.cand_cap + base + __popc(kb & lanemask_lt())] = kk[u];
+        }
       }
     }
   }
+#ifdef FPS_SCAN_TRACE
+  if (lane == 0 && g < 16384) g_scan_trace[g * 4 + 2] = gtimer();
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -720,11 +943,15 @@ __device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u
 
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
                                                              u32* ghist, u32 gstride, u32 tg_rep, u32 k,
-                                                             u64* out_keys, u32* out_cnt, int reset) {
+                                                             u64* out_keys, u32* out_cnt, int reset,
+                                                             u32* dyn_ctr) {
   extern __shared__ u64 ssel[];  // [k_pow2] result + [SEL_ECAP] ties
   __shared__ u32 hist[256];
   __shared__ u32 s_nres, s_ntie, s_T, s_m;
   __shared__ u64 s_cut;
+  // the next call's scan may be launched as a programmatic dependent: let its
+  // CTAs become resident now (they wait for this grid to finish)
+  asm volatile("griddepcontrol.launch_dependents;");
   const u32 q = blockIdx.x;
   const u64* c = cand + (u64)q * cand_cap;
   // Launched as a programmatic dependent of the scan. While the scan drains,
@@ -739,6 +966,9 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
     if (pass == 1) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // scan results visible
       SEL_MARK(0);
+#ifdef FPS_SCAN_TRACE
+      if (threadIdx.x == 0 && q == 0) g_mark[2] = gtimer();
+#endif
       // speculative first-slot read, independent of the count load
       my = threadIdx.x < cand_cap ? c[threadIdx.x] : ~0ull;
       n = cand_cnt[q];
@@ -765,11 +995,15 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   }
   if (n <= (u32)SEL_THREADS) {
     if (threadIdx.x == 0) out_cnt[q] = m_small < k ? m_small : k;
+#ifdef FPS_SCAN_TRACE
+    if (threadIdx.x == 0 && q == 0) g_mark[3] = gtimer();
+#endif
     SEL_MARK(11);
     if (reset) {
       for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
       for (u32 r = threadIdx.x; r < tg_rep; r += blockDim.x) tg[((u64)q * tg_rep + r) * gstride] = T_OPEN;
       if (threadIdx.x == 0) cand_cnt[q] = 0;
+      if (dyn_ctr && q == 0 && threadIdx.x == 0) *dyn_ctr = 0;
     }
     return;
   }
@@ -914,6 +1148,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
     for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
     for (u32 r = threadIdx.x; r < tg_rep; r += blockDim.x) tg[((u64)q * tg_rep + r) * gstride] = T_OPEN;
     if (threadIdx.x == 0) cand_cnt[q] = 0;
+    if (dyn_ctr && q == 0 && threadIdx.x == 0) *dyn_ctr = 0;
   }
 }
 

@@ -51,7 +51,18 @@ class RangeResult:
                          self.distance.astype(np.int64)], axis=1)
 
 
-@dataclass(frozen=True)
+_U64 = np.dtype(np.uint64)
+_topk = None
+
+
+def _topk_fn():
+    global _topk
+    if _topk is None:
+        _topk = N.load().fps_topk
+    return _topk
+
+
+@dataclass(slots=True)
 class TopKResult:
     """Per-query top-k: row q holds count[q] valid (index, distance) pairs."""
 
@@ -228,16 +239,31 @@ class Library:
     # ---- queries ----------------------------------------------------------
     def search_batch(self, queries, k: int) -> TopKResult:
         """Per-query top-k, one independent search per query (config 4)."""
-        q = as_query_words(queries)
+        if (type(queries) is np.ndarray and queries.dtype == _U64 and queries.ndim == 2
+                and queries.shape[1] == 3 and queries.flags.c_contiguous):
+            q = queries  # fast path: padding bits are validated by fps_topk (FPS_EPADDING)
+        else:
+            q = as_query_words(queries)
         if k < 1:
             raise ValueError("n must be >= 1")
         Q = len(q)
-        idx = np.empty((Q, k), dtype=np.uint64)
-        dist = np.empty((Q, k), dtype=np.uint16)
-        cnt = np.zeros(Q, dtype=np.uint32)
+        # one host block for the three outputs: a single allocation and one
+        # address lookup per call (this is on the latency-critical path)
+        blk = np.empty(Q * k * 10 + Q * 4 + 8, dtype=np.uint8)
+        base = C.addressof(C.c_char.from_buffer(blk))
+        idx = np.ndarray((Q, k), np.uint64, blk, 0)
+        dist = np.ndarray((Q, k), np.uint16, blk, Q * k * 8)
+        cnt = np.ndarray((Q,), np.uint32, blk, Q * k * 10)
         if Q:
-            N.check(N.load().fps_topk(self._h, q.ctypes.data, Q, k, idx.ctypes.data, dist.ctypes.data,
-                                      cnt.ctypes.data), "fps_topk")
+            try:
+                qp = C.addressof(C.c_char.from_buffer(q))
+            except (TypeError, ValueError):  # read-only query array
+                qp = q.ctypes.data
+            rc = _topk_fn()(self._h, qp, Q, k, base, base + Q * k * 8, base + Q * k * 10)
+            if rc:
+                N.check(rc, "fps_topk")
+        else:
+            cnt[:] = 0
         return TopKResult(idx, dist, cnt)
 
     def search(self, query, k: int) -> list[tuple[int, int]]:
