@@ -294,23 +294,20 @@ fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
   return a;
 }
 
-// Dynamic tail of the bulk-copy single-query scan: the first FPS_QW1_DYN_PCT
-// percent of the tiles are split statically over the warps, the rest is
-// claimed in chunks (scan flag 64 disables it). Needs one query group: every
-// warp scans for the same query.
-#ifndef FPS_QW1_DYN_PCT
-#define FPS_QW1_DYN_PCT 100
-#endif
-#ifndef FPS_QW1_DYN_CHUNK
-#define FPS_QW1_DYN_CHUNK 2
-#endif
+// Dynamic tail of the bulk-copy single-query scan. Warps draw unequal HBM
+// bandwidth (their static parts finish ~10 % apart on a 95 M library), so on
+// long scans the second half of the tiles is claimed in 8-tile chunks from a
+// global counter. Short scans (< 128 tiles per warp) stay static: the claim
+// traffic there costs more than the imbalance (profiles/r01_experiments.md).
+// Scan flag 64 disables it. Needs one query group: every warp scans for the
+// same query.
 template <int QW, int E, int MODE, bool CMP>
 void set_dyn(fps_lib* L, fps::ScanArgs& a) {
   if (!fps::ScanSmem<QW, E, MODE, CMP>::TMA || MODE != fps::MODE_TOPK || a.n_qg != 1 || (a.flags & 64)) return;
-  if (FPS_QW1_DYN_PCT >= 100 || !L->dyn.p) return;
+  if (!L->dyn.p || a.iters < 128 * a.n_parts) return;
   a.dyn_ctr = L->dyn.as<u32>();
-  a.dyn_start = a.iters * FPS_QW1_DYN_PCT / 100;
-  a.dyn_chunk = FPS_QW1_DYN_CHUNK;
+  a.dyn_start = a.iters / 2;
+  a.dyn_chunk = 8;
 }
 
 // select_kernel launched as a programmatic dependent of the scan kernel: its
