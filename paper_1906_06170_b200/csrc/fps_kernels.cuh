@@ -339,6 +339,12 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
   // (host API / graphs): the CTAs get resident while it runs, and wait here
   // until it has completed (it resets the bounds, histograms and counters)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  using SL = ScanSmem<QW, E, MODE, CMP>;
+  __shared__ u32 s_cta_next;  // bulk-copy scan: next tile of the CTA's run (CTA-dynamic mode)
+  if constexpr (SL::TMA) {
+    if (threadIdx.x == 0) s_cta_next = 0;
+    __syncthreads();  // the only block-level barrier: before any warp leaves
+  }
   if (g >= (u64)a.n_qg * a.n_parts) return;  // warp-uniform; no block-level sync below
 #ifdef FPS_SCAN_TRACE
   u64 tr_start, tr_first = 0;
@@ -602,7 +608,6 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       prefetch_tg();
     }
   };
-  using SL = ScanSmem<QW, E, MODE, CMP>;
   if constexpr (SL::TMA) {
     // HBM-bound single-query scan. The warp's tiles stream through a
     // STAGES-deep shared-memory ring filled by the bulk-copy engine (one 3 KB
@@ -625,6 +630,18 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     const bool dyn = a.dyn_ctr != nullptr;
     const u64 n_static = dyn ? a.dyn_start : a.iters;
     u64 s_next = part * n_static / a.n_parts, s_end = (part + 1) * n_static / a.n_parts;
+    // CTA-dynamic (short scans, one query group): the CTA's warps take the
+    // tiles of the CTA's contiguous run one at a time from a shared counter,
+    // so warps that draw more bandwidth take more tiles.
+    const bool cta_dyn = !dyn && a.n_qg == 1 && !(a.flags & 256);
+    u64 cta_lo = 0, cta_hi = 0;
+    if (cta_dyn) {
+      const u64 w0 = (u64)blockIdx.x * nwb;
+      const u64 nv = (a.n_parts - w0) < (u64)nwb ? (a.n_parts - w0) : (u64)nwb;
+      cta_lo = w0 * a.iters / a.n_parts;
+      cta_hi = (w0 + nv) * a.iters / a.n_parts;
+      s_next = s_end = 0;
+    }
     u64 d_next = 0, d_end = 0;
     u32 pend = 0;
     bool has_pend = false;
@@ -633,6 +650,10 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       has_pend = true;
     };
     auto next_tile = [&]() -> u64 {
+      if (cta_dyn) {
+        const u64 t = cta_lo + atomicAdd(&s_cta_next, 1u);
+        return t < cta_hi ? t : NONE;
+      }
       if (s_next < s_end) {
         const u64 t = s_next++;
         if (s_next == s_end && dyn) claim();

@@ -99,3 +99,22 @@ def test_config3_sharded_merge_full_size():
     torch.cuda.synchronize()
     res = keys_to_hits(out_k.cpu().numpy().view(np.uint64), out_c.cpu().numpy().astype(np.uint32))
     assert res.hits(0) == lib.search(q[0], k)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_scan_schedules_agree(name, monkeypatch):
+    """The single-query bulk-copy scan has three tile schedules -- static
+    per-warp parts, CTA-dynamic (shared counter) and the global dynamic tail
+    (long scans only) -- selected per call; FPS_SCAN_FLAGS 64 / 256 switch the
+    dynamic ones off. Every schedule returns the oracle's exact list, for
+    several queries and k values (ties at the k-th distance included)."""
+    plan, lib, q, w = full(name)
+    rng = np.random.default_rng(7)
+    queries = [q[0], w[int(rng.integers(len(w)))], w[int(rng.integers(len(w)))]]
+    for k in (1, 10, 100, 1000):
+        want = [oracle_lists(w, np.asarray(qq).reshape(1, 3), k)[0] for qq in queries]
+        for flags in ("0", "64", "256", "320"):
+            monkeypatch.setenv("FPS_SCAN_FLAGS", flags)
+            for qq, exp in zip(queries, want):
+                assert lib.search(qq, k) == exp, (flags, k)
+    monkeypatch.delenv("FPS_SCAN_FLAGS")
