@@ -32,7 +32,16 @@ constexpr int BS_TILE_ENTRIES = 1024;        // 32 blocks of 32 entries
 constexpr int BS_TILE_WORDS = BS_PLANES * 32;
 constexpr u32 BS_TILE_BYTES = BS_TILE_WORDS * 4;  // 22,272 B
 constexpr int BS_LIST = 88;                  // max plane indices per query (83 rounded to 8)
-constexpr int BS_QPW = 4;                    // queries per warp
+#ifndef FPS_BS_QPW
+#define FPS_BS_QPW 4
+#endif
+#ifndef FPS_BS_DUAL
+#define FPS_BS_DUAL 0  // two carry-save accumulators per (query, block)
+#endif
+#ifndef FPS_BS_MINB
+#define FPS_BS_MINB 3
+#endif
+constexpr int BS_QPW = FPS_BS_QPW;           // queries per warp
 constexpr int BS_WARPS = 8;
 constexpr int BS_QPC = BS_QPW * BS_WARPS;    // queries per CTA
 
@@ -169,7 +178,7 @@ __device__ __forceinline__ u32 bs_pass_mask(const u32 (&A)[8], const u32 (&C)[8]
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(BS_WARPS * 32, 1) bs_scan_kernel(const BsArgs a) {
+__global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(const BsArgs a) {
   extern __shared__ __align__(128) unsigned char bsm[];
   u32* tiles = reinterpret_cast<u32*>(bsm);                          // 2 x (BS_TILE_WORDS + 32 zero words)
   u64* bars = reinterpret_cast<u64*>(bsm + 2 * (BS_TILE_BYTES + 128));  // 2 mbarriers
@@ -259,39 +268,87 @@ __global__ void __launch_bounds__(BS_WARPS * 32, 1) bs_scan_kernel(const BsArgs 
         if (jj == j) Tj = T[jj];
       if (Tj == 0) continue;  // padding slot or nothing can pass
       const BsQuery& qq = sq[wid * BS_QPW + j];
-      // carry-save count of the listed planes: ones..s64 = binary digits
+      // carry-save count of the listed planes: ones..s64 = binary digits.
+      // Two independent accumulators (even / odd 8-plane chunks) give the
+      // LOP3 chains twice the instruction-level parallelism; they are summed
+      // once per (query, block) with a 7-bit bit-sliced add.
       u32 ones = 0, twos = 0, fours = 0, eights = 0, s16 = 0, s32 = 0, s64 = 0;
+      u32 ones2 = 0, twos2 = 0, fours2 = 0, eights2 = 0, s162 = 0, s322 = 0, s642 = 0;
       const char* lane_base = reinterpret_cast<const char*>(tile) + 4 * lane;
-      for (u32 c0 = 0; c0 < qq.len; c0 += 8) {
-        const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
-        const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
-        const u32 off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-        u32 d[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) d[i] = *reinterpret_cast<const u32*>(lane_base + off[i]);
-        u32 twosA, twosB, foursA, foursB, eightsA;
 #define CSA(h, l, x, y)              \
   do {                               \
     const u32 u_ = l ^ x;            \
     h = (l & x) | (u_ & y);          \
     l = u_ ^ y;                      \
   } while (0)
-        CSA(twosA, ones, d[0], d[1]);
-        CSA(twosB, ones, d[2], d[3]);
-        CSA(foursA, twos, twosA, twosB);
-        CSA(twosA, ones, d[4], d[5]);
-        CSA(twosB, ones, d[6], d[7]);
-        CSA(foursB, twos, twosA, twosB);
-        CSA(eightsA, fours, foursA, foursB);
-#undef CSA
-        u32 c1 = eights & eightsA;
-        eights ^= eightsA;
-        u32 c2 = s16 & c1;
-        s16 ^= c1;
-        u32 c3 = s32 & c2;
-        s32 ^= c2;
-        s64 ^= c3;
+#define CSA8(d, ones, twos, fours, eights, s16, s32, s64) \
+  do {                                                     \
+    u32 twosA, twosB, foursA, foursB, eightsA;             \
+    CSA(twosA, ones, d[0], d[1]);                          \
+    CSA(twosB, ones, d[2], d[3]);                          \
+    CSA(foursA, twos, twosA, twosB);                       \
+    CSA(twosA, ones, d[4], d[5]);                          \
+    CSA(twosB, ones, d[6], d[7]);                          \
+    CSA(foursB, twos, twosA, twosB);                       \
+    CSA(eightsA, fours, foursA, foursB);                   \
+    u32 c1 = eights & eightsA;                             \
+    eights ^= eightsA;                                     \
+    u32 c2 = s16 & c1;                                     \
+    s16 ^= c1;                                             \
+    u32 c3 = s32 & c2;                                     \
+    s32 ^= c2;                                             \
+    s64 ^= c3;                                             \
+  } while (0)
+      u32 c0 = 0;
+#if FPS_BS_DUAL
+      for (; c0 + 16 <= qq.len; c0 += 16) {
+        const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
+        const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
+        const uint4 o2 = *reinterpret_cast<const uint4*>(qq.list + c0 + 8);
+        const uint4 o3 = *reinterpret_cast<const uint4*>(qq.list + c0 + 12);
+        const u32 off0[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        const u32 off1[8] = {o2.x, o2.y, o2.z, o2.w, o3.x, o3.y, o3.z, o3.w};
+        u32 d0[8], d1[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          d0[i] = *reinterpret_cast<const u32*>(lane_base + off0[i]);
+          d1[i] = *reinterpret_cast<const u32*>(lane_base + off1[i]);
+        }
+        CSA8(d0, ones, twos, fours, eights, s16, s32, s64);
+        CSA8(d1, ones2, twos2, fours2, eights2, s162, s322, s642);
       }
+#endif
+      for (; c0 < qq.len; c0 += 8) {
+        const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
+        const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
+        const u32 off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        u32 d[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d[i] = *reinterpret_cast<const u32*>(lane_base + off[i]);
+        CSA8(d, ones, twos, fours, eights, s16, s32, s64);
+      }
+#undef CSA8
+#undef CSA
+#if FPS_BS_DUAL
+      {  // (ones..s64) += (ones2..s642): ripple-carry over the 7 digit planes
+        u32 cy = ones & ones2;
+        ones ^= ones2;
+#define ADDBIT(x, y)                            \
+  do {                                          \
+    const u32 t_ = x ^ y;                       \
+    const u32 n_ = (x & y) | (cy & t_);         \
+    x = t_ ^ cy;                                \
+    cy = n_;                                    \
+  } while (0)
+        ADDBIT(twos, twos2);
+        ADDBIT(fours, fours2);
+        ADDBIT(eights, eights2);
+        ADDBIT(s16, s162);
+        ADDBIT(s32, s322);
+        s64 ^= s642 ^ cy;  // the count is < 128: no carry out
+#undef ADDBIT
+      }
+#endif
       // pass mask: sign of X + (|q| - T), X = |a| - 2c (sparse) or 2c - |a|
       // (dense); a warp-uniform branch picks the operand order (no selects)
       const u32 C[8] = {0, ones, twos, fours, eights, s16, s32, s64};  // 2c

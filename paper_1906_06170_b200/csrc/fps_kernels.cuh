@@ -43,6 +43,9 @@
 #ifndef FPS_EXIT_TGP
 #define FPS_EXIT_TGP 1  // single-query scans append survivors under the last prefetched bound
 #endif
+#ifndef FPS_SEL_WARM
+#define FPS_SEL_WARM 0  // select_kernel runs its sort once on dummy keys while the scan drains
+#endif
 #ifndef FPS_QW1_PIPE
 #define FPS_QW1_PIPE 1  // single-query kernels: 1 = next iteration's loads in flight (double buffer)
 #endif
@@ -847,7 +850,7 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
 // One CTA per query. Resets the per-query scan state (tg, ghist, cand_cnt) so
 // the next call starts clean without a memset launch.
 // ---------------------------------------------------------------------------
-constexpr int SEL_THREADS = 512;
+constexpr int SEL_THREADS = 1024;
 
 // Number of keys in s[0, n) smaller than x; four independent counters keep
 // the dependent add chain short (shared-memory broadcast reads).
@@ -950,7 +953,8 @@ __device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u
       case 64: key = bitonic_p<64>(key, t, sh); break;
       case 128: key = bitonic_p<128>(key, t, sh); break;
       case 256: key = bitonic_p<256>(key, t, sh); break;
-      default: key = bitonic_p<512>(key, t, sh); break;
+      case 512: key = bitonic_p<512>(key, t, sh); break;
+      default: key = bitonic_p<1024>(key, t, sh); break;
     }
 #ifdef FPS_SEL_PROBE
     if (out && t == 0) { g_sel_clock[10] = key; SEL_MARK(9); }
@@ -983,7 +987,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   u32 n = SEL_THREADS, bound = T_OPEN, m_small = 0;
   u64* dst = nullptr;
 #pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = FPS_SEL_WARM ? 0 : 1; pass < 2; ++pass) {
     if (pass == 1) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // scan results visible
       SEL_MARK(0);
