@@ -35,9 +35,6 @@ constexpr int BS_LIST = 88;                  // max plane indices per query (83 
 #ifndef FPS_BS_QPW
 #define FPS_BS_QPW 4
 #endif
-#ifndef FPS_BS_DUAL
-#define FPS_BS_DUAL 0  // two carry-save accumulators per (query, block)
-#endif
 #ifndef FPS_BS_MINB
 #define FPS_BS_MINB 3
 #endif
@@ -268,12 +265,10 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
         if (jj == j) Tj = T[jj];
       if (Tj == 0) continue;  // padding slot or nothing can pass
       const BsQuery& qq = sq[wid * BS_QPW + j];
-      // carry-save count of the listed planes: ones..s64 = binary digits.
-      // Two independent accumulators (even / odd 8-plane chunks) give the
-      // LOP3 chains twice the instruction-level parallelism; they are summed
-      // once per (query, block) with a 7-bit bit-sliced add.
+      // carry-save count of the listed planes: ones..s64 = binary digits
+      // (a second, interleaved accumulator for more ILP measured slower:
+      // profiles/r01_experiments.md)
       u32 ones = 0, twos = 0, fours = 0, eights = 0, s16 = 0, s32 = 0, s64 = 0;
-      u32 ones2 = 0, twos2 = 0, fours2 = 0, eights2 = 0, s162 = 0, s322 = 0, s642 = 0;
       const char* lane_base = reinterpret_cast<const char*>(tile) + 4 * lane;
 #define CSA(h, l, x, y)              \
   do {                               \
@@ -300,24 +295,6 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
     s64 ^= c3;                                             \
   } while (0)
       u32 c0 = 0;
-#if FPS_BS_DUAL
-      for (; c0 + 16 <= qq.len; c0 += 16) {
-        const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
-        const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
-        const uint4 o2 = *reinterpret_cast<const uint4*>(qq.list + c0 + 8);
-        const uint4 o3 = *reinterpret_cast<const uint4*>(qq.list + c0 + 12);
-        const u32 off0[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-        const u32 off1[8] = {o2.x, o2.y, o2.z, o2.w, o3.x, o3.y, o3.z, o3.w};
-        u32 d0[8], d1[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          d0[i] = *reinterpret_cast<const u32*>(lane_base + off0[i]);
-          d1[i] = *reinterpret_cast<const u32*>(lane_base + off1[i]);
-        }
-        CSA8(d0, ones, twos, fours, eights, s16, s32, s64);
-        CSA8(d1, ones2, twos2, fours2, eights2, s162, s322, s642);
-      }
-#endif
       for (; c0 < qq.len; c0 += 8) {
         const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
         const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
@@ -329,26 +306,6 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
       }
 #undef CSA8
 #undef CSA
-#if FPS_BS_DUAL
-      {  // (ones..s64) += (ones2..s642): ripple-carry over the 7 digit planes
-        u32 cy = ones & ones2;
-        ones ^= ones2;
-#define ADDBIT(x, y)                            \
-  do {                                          \
-    const u32 t_ = x ^ y;                       \
-    const u32 n_ = (x & y) | (cy & t_);         \
-    x = t_ ^ cy;                                \
-    cy = n_;                                    \
-  } while (0)
-        ADDBIT(twos, twos2);
-        ADDBIT(fours, fours2);
-        ADDBIT(eights, eights2);
-        ADDBIT(s16, s162);
-        ADDBIT(s32, s322);
-        s64 ^= s642 ^ cy;  // the count is < 128: no carry out
-#undef ADDBIT
-      }
-#endif
       // pass mask: sign of X + (|q| - T), X = |a| - 2c (sparse) or 2c - |a|
       // (dense); a warp-uniform branch picks the operand order (no selects)
       const u32 C[8] = {0, ones, twos, fours, eights, s16, s32, s64};  // 2c
