@@ -125,6 +125,12 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
 int fps_range(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t** out_keys,
               uint64_t* n_out);
 void fps_free(void* p);
+/* Split n range keys into the three result columns (query, index, distance)
+ * in one pass on the host -- the reference has no range op; this
+ * builds the columns its RangeResult-style result needs without numpy
+ * temporaries. Pure host code: callable without a GPU. */
+void fps_range_unpack(const uint64_t* keys, uint64_t n, uint32_t* out_query, uint64_t* out_index,
+                      uint16_t* out_dist);
 
 /* ---- stream-ordered device API (benchmarks, CUDA graphs, multi-GPU) ---- */
 /* Allocate scratch for (Q, k) so that fps_topk_async does not allocate. */

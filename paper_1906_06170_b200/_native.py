@@ -56,6 +56,7 @@ SIGNATURES = {
     "fps_topk_min": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "fps_range": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.POINTER(_vp), _u64p]),
     "fps_free": (None, [_vp]),
+    "fps_range_unpack": (None, [_vp, C.c_uint64, _vp, _vp, _vp]),
     "fps_topk_prepare": (C.c_int, [_vp, C.c_uint32, C.c_uint32]),
     "fps_topk_async": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "fps_range_async": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _vp, C.c_uint64, _vp, _vp]),

@@ -1499,6 +1499,16 @@ int fps_range(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* 
 
 void fps_free(void* p) { std::free(p); }
 
+void fps_range_unpack(const uint64_t* keys, uint64_t n, uint32_t* out_query, uint64_t* out_index,
+                      uint16_t* out_dist) {
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t x = keys[i];
+    out_query[i] = (uint32_t)(x >> 48);
+    out_index[i] = x & fps::IDX_MASK;
+    out_dist[i] = (uint16_t)((x >> fps::IDX_BITS) & 0xffu);
+  }
+}
+
 int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream) {
   if (lib) {
     std::lock_guard<std::mutex> lk(lib->mu);

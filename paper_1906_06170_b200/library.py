@@ -296,13 +296,16 @@ class Library:
             return RangeResult.from_keys(np.zeros(0, np.uint64))
         N.check(N.load().fps_range(self._h, q.ctypes.data, Q, rad.ctypes.data, C.byref(out), C.byref(n_out)),
                 "fps_range")
+        m = n_out.value
+        query = np.empty(m, np.uint32)
+        index = np.empty(m, np.uint64)
+        distance = np.empty(m, np.uint16)
         try:
-            m = n_out.value
-            keys = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_uint64)), shape=(m,)).copy() if m else \
-                np.zeros(0, np.uint64)
+            if m:  # one native pass instead of numpy shift/mask temporaries
+                N.load().fps_range_unpack(out, m, query.ctypes.data, index.ctypes.data, distance.ctypes.data)
         finally:
             N.load().fps_free(out)
-        return RangeResult.from_keys(keys)
+        return RangeResult(query=query, index=index, distance=distance)
 
     # ---- stream-ordered device API --------------------------------------
     def topk_prepare(self, Q: int, k: int) -> None:

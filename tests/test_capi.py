@@ -108,3 +108,21 @@ def test_fps1_loader_reports_bad_shards_without_a_gpu(lib, tmp_path):
         assert msg.startswith("shard ") and name in msg, msg
     arr = (ctypes.c_char_p * 1)(str(tmp_path / "missing.fps").encode())
     assert lib.fps_open_fps1(arr, 1, 0, 2**64 - 1, 0, None, ctypes.byref(ctypes.c_void_p())) == _native.FPS_EIO
+
+
+def test_range_unpack_matches_key_layout(lib):
+    """fps_range_unpack (host code, no GPU) splits (q << 48 | d << 40 | idx)
+    keys exactly like RangeResult.from_keys."""
+    from paper_1906_06170_b200.library import RangeResult
+
+    rng = np.random.default_rng(3)
+    n = 10_001
+    q = rng.integers(0, 65535, n, dtype=np.uint64)
+    d = rng.integers(0, 167, n, dtype=np.uint64)
+    idx = rng.integers(0, 1 << 40, n, dtype=np.uint64)
+    keys = (q << np.uint64(48)) | (d << np.uint64(40)) | idx
+    oq, oi, od = np.empty(n, np.uint32), np.empty(n, np.uint64), np.empty(n, np.uint16)
+    lib.fps_range_unpack(keys.ctypes.data, n, oq.ctypes.data, oi.ctypes.data, od.ctypes.data)
+    ref = RangeResult.from_keys(keys)
+    assert np.array_equal(oq, ref.query) and np.array_equal(oi, ref.index) and np.array_equal(od, ref.distance)
+    assert np.array_equal(oq, q.astype(np.uint32)) and np.array_equal(od, d.astype(np.uint16))
