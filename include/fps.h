@@ -132,6 +132,29 @@ void fps_free(void* p);
 void fps_range_unpack(const uint64_t* keys, uint64_t n, uint32_t* out_query, uint64_t* out_index,
                       uint16_t* out_dist);
 
+/* ---- library builder (host only, no GPU) ---- */
+/* 64-bit FNV-1a over n bytes, resumable: replaces libstore.fnv1a_64
+ * (libstore.py:93-98). Start with value = 0xcbf29ce484222325. */
+uint64_t fps_fnv1a64(const void* data, uint64_t n, uint64_t value);
+/* FNV-1a of a file's bytes from `offset` to EOF (validate_manifest's record
+ * region checksum, libstore.py:383-390). FPS_EIO if unreadable. */
+int fps_fnv1a64_file(const char* path, uint64_t offset, uint64_t* out);
+/* libstore.build_shards (libstore.py:243-272): parse `<CID>\t<bits>` lines
+ * (parse_library_line, :136-155; parse_bitstring, fingerprint.py:112-134;
+ * whitespace-only lines skipped but counted), pack FPS1 records and write
+ * shard_count contiguous shards `out_dir/shard-NNN.fps` (split_sizes).
+ * Input is either text_path (whole file, universal newlines like Python's
+ * text mode) or the buffer text[0, len) cut into n_lines lines at
+ * line_offsets[0..n_lines]. out_counts / out_checksums have shard_count
+ * slots (record count, FNV-1a of the record region); *out_total = records.
+ * A malformed line returns FPS_EINVAL with its 1-based number in *err_line
+ * and its bytes at [*err_off, *err_off + *err_len) of the input, and writes
+ * no file. threads <= 0: all hardware threads. */
+int fps_build_shards(const char* text, uint64_t len, const uint64_t* line_offsets, uint64_t n_lines,
+                     const char* text_path, uint32_t shard_count, const char* out_dir, int threads,
+                     uint64_t* out_counts, uint64_t* out_checksums, uint64_t* out_total, uint64_t* err_line,
+                     uint64_t* err_off, uint64_t* err_len);
+
 /* ---- stream-ordered device API (benchmarks, CUDA graphs, multi-GPU) ---- */
 /* Allocate scratch for (Q, k) so that fps_topk_async does not allocate. */
 int fps_topk_prepare(fps_lib* lib, uint32_t Q, uint32_t k);

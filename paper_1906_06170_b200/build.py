@@ -26,7 +26,8 @@ def nvcc() -> str:
 
 
 def sources() -> list[Path]:
-    return sorted(SRC.glob("*.cu")) + sorted(SRC.glob("*.cuh")) + [PKG.parent / "include" / "fps.h"]
+    return (sorted(SRC.glob("*.cu")) + sorted(SRC.glob("*.cuh")) + sorted(SRC.glob("*.cpp"))
+            + [PKG.parent / "include" / "fps.h"])
 
 
 def up_to_date() -> bool:
@@ -40,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return OUT
     cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-           "-o", str(OUT) + ".tmp", str(SRC / "fps_capi.cu")]
+           "-Xcompiler", "-pthread", "-o", str(OUT) + ".tmp", str(SRC / "fps_capi.cu"), str(SRC / "fps_ingest.cpp")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

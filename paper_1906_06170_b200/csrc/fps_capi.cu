@@ -839,6 +839,9 @@ int topk_large(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
 
 }  // namespace
 
+// error message setter for the host-only ingestion code (fps_ingest.cpp)
+void fps_set_last_error(const std::string& msg) { g_err = msg; }
+
 extern "C" {
 
 int fps_version(void) { return FPS_ABI_VERSION; }

@@ -47,6 +47,25 @@ class LibstoreError(Exception):
     """Base class for library storage failures."""
 
 
+class LineFormatError(LibstoreError):
+    """A text library line is malformed; carries the 1-based line number when known."""
+
+    def __init__(self, message: str, line_number: int | None = None):
+        self.line_number = line_number
+        prefix = f"line {line_number}: " if line_number is not None else ""
+        super().__init__(prefix + message)
+
+
+class MissingTab(LineFormatError):
+    def __init__(self, line_number: int | None = None):
+        super().__init__("expected `<CID>\\t<bitstring>`, no tab found", line_number)
+
+
+class BadCid(LineFormatError):
+    def __init__(self, raw: str, line_number: int | None = None):
+        super().__init__(f"bad CID {raw!r}: must be a decimal integer in 1..2^64-1", line_number)
+
+
 class ShardFileError(LibstoreError):
     """A shard file failed structural validation; carries the offending path."""
 
@@ -60,6 +79,10 @@ class BadMagic(ShardFileError):
 
 
 class VersionMismatch(ShardFileError):
+    pass
+
+
+class ChecksumMismatch(ShardFileError):
     pass
 
 
