@@ -297,7 +297,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     stream = torch.cuda.current_stream(dev).cuda_stream
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 << 20) or (126 << 20)
-    lib_bytes = 24 * count
+    lib_bytes = lib.layout()[1] * count
     # A library larger than L2 is its own flush: the single-query scan streams
     # it with an L2 evict-first policy, so K steps run back to back between one
     # event pair (no reuse across steps). Smaller libraries get an explicit

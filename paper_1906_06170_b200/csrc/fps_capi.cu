@@ -305,9 +305,10 @@ template <int QW, int E, int MODE, bool CMP>
 void set_dyn(fps_lib* L, fps::ScanArgs& a) {
   if (!fps::ScanSmem<QW, E, MODE, CMP>::TMA || MODE != fps::MODE_TOPK || a.n_qg != 1 || (a.flags & 64)) return;
   if (!L->dyn.p || a.iters < 128 * a.n_parts) return;
+  constexpr u64 SUB = fps::ScanSmem<QW, E, MODE, CMP>::SUB;  // iterations per tile (the kernel's work unit)
   a.dyn_ctr = L->dyn.as<u32>();
-  a.dyn_start = a.iters / 2;
-  a.dyn_chunk = 8;
+  a.dyn_start = (a.iters + SUB - 1) / SUB / 2;
+  a.dyn_chunk = std::max<u64>(1, 8 / SUB);
 }
 
 // select_kernel launched as a programmatic dependent of the scan kernel: its
@@ -701,12 +702,13 @@ int stage_queries(fps_lib* L, const uint64_t* queries, u32 Q) {
   return FPS_OK;
 }
 
-// The compact 21 B/entry tiles read 12.5 % fewer bytes but measured slower on
-// B200 (C3: 357 vs 341 us; profiles/r01_experiments.md), so the 24 B tiles are
-// the default and compact is opt-in (FPS_LAYOUT=compact).
+// The compact 21 B/entry tiles (word 2 as u32 + u8) read 12.5 % fewer bytes;
+// with the bulk-copy scan they are faster in every config (C3 scan 319 ->
+// 289 us, profiles/r01_experiments.md), so they are the default whenever no
+// entry uses bits 40.. of word 2. FPS_LAYOUT=full forces the 24 B tiles.
 bool force_full_layout() {
   const char* e = std::getenv("FPS_LAYOUT");
-  return !(e && std::string(e) == "compact");
+  return e && std::string(e) == "full";
 }
 
 int alloc_planes(fps_lib* L, u64 n, bool compact) {
@@ -1076,6 +1078,40 @@ int fps_open_fps1(const char* const* paths, uint32_t n_paths, uint64_t start, ui
     destroy(L);
     return fail(FPS_ECUDA, std::string("shard upload: ") + cudaGetErrorString(e));
   }
+  // The records streamed into 24 B tiles (their word-2 width is unknown up
+  // front); re-tile to the 21 B layout when no record needs bits 40.. .
+  if (n > 0 && !force_full_layout()) {
+    DevBuf wide;
+    if ((rc = wide.ensure(4))) { destroy(L); return rc; }
+    CUDA_TRY(cudaMemsetAsync(wide.p, 0, 4, L->stream));
+    const int blocks = (int)std::min<u64>((n + 255) / 256, (u64)L->sms * 16);
+    fps::count_wide_lib<<<blocks, 256, 0, L->stream>>>(L->out(), n, wide.as<u32>());
+    u32 nwide = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, L->stream));
+    CUDA_TRY(cudaStreamSynchronize(L->stream));
+    if (nwide == 0) {
+      const fps::PlanesOut full = L->out();
+      char* old_mem = L->mem;
+      const u64 old_alloc = L->n_alloc;
+      L->mem = nullptr;
+      if ((rc = alloc_planes(L, n, true)) == FPS_OK) {
+        fps::retile_kernel<<<blocks, 256, 0, L->stream>>>(full, L->out(), n);
+        L->launches += 2;
+        e = cudaStreamSynchronize(L->stream);
+        cudaFree(old_mem);
+        if (e != cudaSuccess) {
+          destroy(L);
+          return fail(FPS_ECUDA, std::string("re-tiling: ") + cudaGetErrorString(e));
+        }
+      } else {  // no room for a second copy: keep the 24 B tiles
+        cudaGetLastError();
+        L->mem = old_mem;
+        L->compact = false;
+        L->n = n;
+        L->n_alloc = old_alloc;
+      }
+    }
+  }
   *out = L;
   return FPS_OK;
 }
@@ -1425,7 +1461,8 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   a.cand = lib->cand.as<u64>();
   a.cand_cnt = lib->cand_cnt.as<u32>();
   a.cand_cap = c.cand_cap;
-  if (!lib->compact) set_dyn<1, 4, fps::MODE_TOPK, false>(lib, a);
+  if (lib->compact) set_dyn<1, 4, fps::MODE_TOPK, true>(lib, a);
+  else set_dyn<1, 4, fps::MODE_TOPK, false>(lib, a);
   if (c.warps > 0 && lib->n > 0) {
     if (lib->compact) fps::scan_kernel<1, 4, fps::MODE_TOPK, true, true><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
     else fps::scan_kernel<1, 4, fps::MODE_TOPK, true, false><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);

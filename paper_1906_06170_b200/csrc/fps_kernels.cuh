@@ -305,14 +305,16 @@ struct WarpState {
 // [per-warp slot tile indices].
 template <int QW, int E, int MODE, bool CMP>
 struct ScanSmem {
-  static constexpr bool TMA = (QW == 1 && E == 4 && !CMP && FPS_QW1_TMA != 0);
+  static constexpr bool TMA = (QW == 1 && E == 4 && FPS_QW1_TMA != 0);
   static constexpr int STAGES = FPS_QW1_STAGES;
+  static constexpr u64 SLOT = CMP ? TILE_BYTES_CMP : TILE_BYTES_FULL;  // one library tile per ring slot
+  static constexpr int SUB = CMP ? TILE_CMP / 128 : TILE_FULL / 128;   // 128-entry iterations per tile
   __host__ __device__ static constexpr size_t base(int nwb) {
     return MODE == MODE_RANGE ? 0 : (size_t)nwb * (QW * HB * sizeof(u32) + sizeof(WarpState<QW>));
   }
   __host__ __device__ static constexpr size_t ring_off(int nwb) { return TMA ? (base(nwb) + 127) / 128 * 128 : base(nwb); }
   __host__ __device__ static constexpr size_t bars_off(int nwb) {
-    return ring_off(nwb) + (TMA ? (size_t)nwb * STAGES * TILE_BYTES_FULL : 0);
+    return ring_off(nwb) + (TMA ? (size_t)nwb * STAGES * SLOT : 0);
   }
   __host__ __device__ static constexpr size_t tiles_off(int nwb) { return bars_off(nwb) + (TMA ? (size_t)nwb * STAGES * 8 : 0); }
   __host__ __device__ static constexpr size_t total(int nwb) { return tiles_off(nwb) + (TMA ? (size_t)nwb * STAGES * 8 : 0); }
@@ -625,13 +627,16 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     // ordered candidate buffers rely on it). The next claim is issued one
     // chunk ahead so its latency hides behind the copies.
     constexpr int S = SL::STAGES;
+    constexpr u64 SLOT = SL::SLOT;
+    constexpr int SUB = SL::SUB;
     constexpr u64 NONE = ~0ull;
-    char* ring = reinterpret_cast<char*>(smem) + SL::ring_off(nwb) + (size_t)wib * S * TILE_BYTES_FULL;
+    char* ring = reinterpret_cast<char*>(smem) + SL::ring_off(nwb) + (size_t)wib * S * SLOT;
     u64* bars = reinterpret_cast<u64*>(reinterpret_cast<char*>(smem) + SL::bars_off(nwb)) + wib * S;
     u64* slot_tile = reinterpret_cast<u64*>(reinterpret_cast<char*>(smem) + SL::tiles_off(nwb)) + wib * S;
     const u64 pol = l2_evict_first_policy();
+    const u64 n_tiles = (a.iters + SUB - 1) / SUB;  // work unit: one library tile
     const bool dyn = a.dyn_ctr != nullptr;
-    const u64 n_static = dyn ? a.dyn_start : a.iters;
+    const u64 n_static = dyn ? a.dyn_start : n_tiles;
     u64 s_next = part * n_static / a.n_parts, s_end = (part + 1) * n_static / a.n_parts;
     // CTA-dynamic (short scans, one query group): the CTA's warps take the
     // tiles of the CTA's contiguous run one at a time from a shared counter,
@@ -641,8 +646,8 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     if (cta_dyn) {
       const u64 w0 = (u64)blockIdx.x * nwb;
       const u64 nv = (a.n_parts - w0) < (u64)nwb ? (a.n_parts - w0) : (u64)nwb;
-      cta_lo = w0 * a.iters / a.n_parts;
-      cta_hi = (w0 + nv) * a.iters / a.n_parts;
+      cta_lo = w0 * n_tiles / a.n_parts;
+      cta_hi = (w0 + nv) * n_tiles / a.n_parts;
       s_next = s_end = 0;
     }
     u64 d_next = 0, d_end = 0;
@@ -665,12 +670,12 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       if (d_next >= d_end) {
         if (!has_pend) return NONE;
         const u64 c0 = a.dyn_start + (u64)pend * a.dyn_chunk;
-        if (c0 >= a.iters) {
+        if (c0 >= n_tiles) {
           has_pend = false;
           return NONE;
         }
         d_next = c0;
-        d_end = c0 + a.dyn_chunk < a.iters ? c0 + a.dyn_chunk : a.iters;
+        d_end = c0 + a.dyn_chunk < n_tiles ? c0 + a.dyn_chunk : n_tiles;
         claim();
       }
       return d_next++;
@@ -679,8 +684,8 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       const u64 t = next_tile();
       slot_tile[st] = t;
       if (t != NONE) {
-        mbar_expect_tx(&bars[st], (u32)TILE_BYTES_FULL);
-        bulk_g2s_stream(ring + st * TILE_BYTES_FULL, a.lib + t * TILE_BYTES_FULL, (u32)TILE_BYTES_FULL, &bars[st], pol);
+        mbar_expect_tx(&bars[st], (u32)SLOT);
+        bulk_g2s_stream(ring + st * SLOT, a.lib + t * SLOT, (u32)SLOT, &bars[st], pol);
       } else {
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
       }
@@ -698,26 +703,41 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     for (u64 j = 0;; ++j) {
       const int st = (int)(j % S);
       mbar_wait(&bars[st], (u32)(j / S) & 1u);
-      const u64 i = *(volatile const u64*)&slot_tile[st];
-      if (i == NONE) break;
+      const u64 t = *(volatile const u64*)&slot_tile[st];
+      if (t == NONE) break;
 #ifdef FPS_SCAN_TRACE
       if (j == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
 #endif
-      const u64* tl = reinterpret_cast<const u64*>(ring + st * TILE_BYTES_FULL) + lane * 4;
-      u64 A[4], B[4], C[4];
-      {
-        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(tl);
-        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(tl + 2);
-        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(tl + TILE_FULL);
-        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(tl + TILE_FULL + 2);
-        const ulonglong2 c0 = *reinterpret_cast<const ulonglong2*>(tl + 2 * TILE_FULL);
-        const ulonglong2 c1 = *reinterpret_cast<const ulonglong2*>(tl + 2 * TILE_FULL + 2);
+      const char* tb = ring + st * SLOT;
+#pragma unroll
+      for (int h = 0; h < SUB; ++h) {
+        const u64 i = t * SUB + h;  // 128-entry iteration
+        if (SUB > 1 && i >= a.iters) break;
+        u64 A[4], B[4], C[4];
+        constexpr int TL = CMP ? TILE_CMP : TILE_FULL;
+        const u64* w0 = reinterpret_cast<const u64*>(tb) + h * 128 + lane * 4;
+        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(w0);
+        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(w0 + 2);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(w0 + TL);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(w0 + TL + 2);
         A[0] = a0.x; A[1] = a0.y; A[2] = a1.x; A[3] = a1.y;
         B[0] = b0.x; B[1] = b0.y; B[2] = b1.x; B[3] = b1.y;
-        C[0] = c0.x; C[1] = c0.y; C[2] = c1.x; C[3] = c1.y;
+        if constexpr (CMP) {
+          // word 2 as a u32 plane (keys 129..160) + a u8 plane (keys 161..166 + 2 pad bits)
+          const uint4 lo = *reinterpret_cast<const uint4*>(tb + 16 * TL + 4 * (h * 128 + lane * 4));
+          const u32 hi = *reinterpret_cast<const u32*>(tb + 20 * TL + (h * 128 + lane * 4));
+          C[0] = (u64)lo.x | ((u64)(hi & 0xffu) << 32);
+          C[1] = (u64)lo.y | ((u64)((hi >> 8) & 0xffu) << 32);
+          C[2] = (u64)lo.z | ((u64)((hi >> 16) & 0xffu) << 32);
+          C[3] = (u64)lo.w | ((u64)(hi >> 24) << 32);
+        } else {
+          const ulonglong2 c0 = *reinterpret_cast<const ulonglong2*>(w0 + 2 * TL);
+          const ulonglong2 c1 = *reinterpret_cast<const ulonglong2*>(w0 + 2 * TL + 2);
+          C[0] = c0.x; C[1] = c0.y; C[2] = c1.x; C[3] = c1.y;
+        }
+        process(*reinterpret_cast<const u64(*)[E]>(A), *reinterpret_cast<const u64(*)[E]>(B),
+                *reinterpret_cast<const u64(*)[E]>(C), i, i >= n_full);
       }
-      process(*reinterpret_cast<const u64(*)[E]>(A), *reinterpret_cast<const u64(*)[E]>(B),
-              *reinterpret_cast<const u64(*)[E]>(C), i, i >= n_full);
       __syncwarp();  // every lane's reads of slot st are complete (values consumed)
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1262,6 +1282,24 @@ __global__ void rows_to_planes(const u64* __restrict__ rows, u64 n_rows, int str
 __global__ void count_wide(const u64* __restrict__ w2, u64 n, u32* wide) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
     if (w2[i] >> 40) atomicAdd(wide, 1u);
+}
+
+// Library entries that use bits 40.. of word 2 (they need the 24 B tiles).
+__global__ void count_wide_lib(PlanesOut src, u64 n, u32* wide) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    u64 a, b, c;
+    src.get(i, a, b, c);
+    if (c >> 40) atomicAdd(wide, 1u);
+  }
+}
+
+// Re-tile a library (24 B tiles -> 21 B tiles after loading, when it fits).
+__global__ void retile_kernel(PlanesOut src, PlanesOut dst, u64 n) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    u64 a, b, c;
+    src.get(i, a, b, c);
+    dst.put(i, a, b, c);
+  }
 }
 
 // Three device planes (full layout) -> library planes.

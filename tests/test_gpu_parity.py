@@ -329,6 +329,40 @@ def test_compact_and_full_layouts_agree(monkeypatch):
         lib.write_entries(np.array([3]), np.array([[0, 0, 1 << 41]], dtype=np.uint64))
 
 
+def test_fps1_loader_retiles_to_compact(tmp_path, monkeypatch):
+    """FPS1 records stream into 24 B tiles and are re-tiled to the 21 B layout
+    when no record uses bits 40.. of word 2; a record with such a pad bit keeps
+    the 24 B tiles (and is counted, as the reference counts it); FPS_LAYOUT=full
+    forces them. Every layout answers like the oracle."""
+    seed = 4321
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 200_003)
+    q = w[[11, 12]].copy()
+    q[:, 1] ^= np.uint64(0b1011)
+    orc.write_fps1_library(tmp_path / "ok", w, 2)
+    paths = sorted(str(p) for p in (tmp_path / "ok").glob("shard-*.fps"))
+    lib = Library.from_fps1(paths)
+    assert lib.layout() == (True, 21)
+    assert np.array_equal(lib.words_host(), w)
+    for k in (1, 10, 100):
+        assert [lib.search_batch(q, k).hits(i) for i in range(2)] == oracle_topk(w, q, k)
+    monkeypatch.setenv("FPS_LAYOUT", "full")
+    full = Library.from_fps1(paths)
+    assert full.layout() == (False, 24)
+    assert full.search_batch(q, 10).hits(0) == lib.search_batch(q, 10).hits(0)
+    monkeypatch.delenv("FPS_LAYOUT")
+    ww = w.copy()
+    ww[777, 2] |= np.uint64(1) << np.uint64(50)  # a pad bit past key 166, beyond the compact word
+    orc.write_fps1_library(tmp_path / "wide", ww, 2)
+    paths = sorted(str(p) for p in (tmp_path / "wide").glob("shard-*.fps"))
+    wide = Library.from_fps1(paths)
+    assert wide.layout() == (False, 24)
+    qq = w[777:778].copy()  # the record's pad bit counts as one differing key
+    assert wide.search(qq, 3) == oracle_topk(ww, qq, 3)[0]
+    assert wide.search(qq, 1)[0] == (777, 1)
+    assert [wide.search_batch(q, 10).hits(i) for i in range(2)] == oracle_topk(ww, q, 10)
+
+
 def test_fps1_streaming_loader(tmp_path):
     """FPS1 shards stream straight into HBM; any record slice of the
     concatenation (a rank's shard) loads with its global index base."""
