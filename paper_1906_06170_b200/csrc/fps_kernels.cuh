@@ -340,11 +340,14 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
   // let a programmatic dependent (select_kernel) launch early; it still waits
   // for this grid to complete before reading its results
   asm volatile("griddepcontrol.launch_dependents;");
-  // launched as a programmatic dependent of the previous call's select_kernel
-  // (host API / graphs): the CTAs get resident while it runs, and wait here
-  // until it has completed (it resets the bounds, histograms and counters)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   using SL = ScanSmem<QW, E, MODE, CMP>;
+  // Launched as a programmatic dependent of the previous call's select_kernel
+  // (host API / graphs): the CTAs get resident while it runs and wait until it
+  // has completed (it resets the bounds, histograms and counters) before
+  // touching that state. The bulk-copy scan first puts its first library
+  // tiles in flight -- the library is read-only -- so the HBM ramp overlaps
+  // the previous select.
+  if constexpr (!SL::TMA) asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ u32 s_cta_next;  // bulk-copy scan: next tile of the CTA's run (CTA-dynamic mode)
   if constexpr (SL::TMA) {
     if (threadIdx.x == 0) s_cta_next = 0;
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       for (int j = 0; j < QW; ++j) refresh_tg(j);
     }
   };
-  if (MODE == MODE_TOPK && !(a.flags & 2)) prefetch_tg();
+  if (MODE == MODE_TOPK && !(a.flags & 2) && !SL::TMA) prefetch_tg();
   // Only the globally last iteration can hold entries >= n; the main range is
   // scanned without per-entry masking.
   const u64 it_main = it1 < n_full ? it1 : n_full;
@@ -690,10 +693,21 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
       }
     };
+    // first tiles before the dependency wait, when no global claim is needed
+    // for them (the tail counter belongs to the previous call until it ends)
+    const bool pre = cta_dyn || s_end - s_next > (u64)S;
     if (lane == 0) {
 #pragma unroll
       for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (pre) {
+#pragma unroll
+        for (int st = 0; st < S; ++st) issue(st);
+      }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (MODE == MODE_TOPK && !(a.flags & 2)) prefetch_tg();
+    if (lane == 0 && !pre) {
       if (dyn && s_next == s_end) claim();
 #pragma unroll
       for (int st = 0; st < S; ++st) issue(st);
