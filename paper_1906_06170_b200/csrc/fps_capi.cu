@@ -390,7 +390,9 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
       cfg.stream = s;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = (a.flags & 128) ? 0 : 1;
+      // (long scans with the global tail measured faster without it: C3
+      // 306 vs 291-297 us; short ones faster with it: C2 48.3 vs 50.3 us)
+      attr[0].val.programmaticStreamSerializationAllowed = ((a.flags & 128) || a.dyn_ctr) ? 0 : 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       CUDA_TRY(cudaLaunchKernelEx(&cfg, fps::scan_kernel<QW, E, fps::MODE_TOPK, false, CMP>, a));
