@@ -28,18 +28,28 @@ namespace fps {
 
 constexpr int BS_PLANES = 174;               // 166 key planes + 8 popcount planes
 constexpr int BS_ZERO = 174;                 // index of an all-zero plane (padding)
-constexpr int BS_TILE_ENTRIES = 1024;        // 32 blocks of 32 entries
-constexpr int BS_TILE_WORDS = BS_PLANES * 32;
-constexpr u32 BS_TILE_BYTES = BS_TILE_WORDS * 4;  // 22,272 B
+#ifndef FPS_BS_BPL
+#define FPS_BS_BPL 2
+#endif
+constexpr int BS_BPL = FPS_BS_BPL;           // 32-entry blocks per lane (one LDS.64 reads a plane of both)
+static_assert(BS_BPL == 2, "the scan reads both blocks of a lane with one 64-bit shared load");
+constexpr int BS_BLOCKS = 32 * BS_BPL;       // blocks per tile
+constexpr int BS_TILE_ENTRIES = 32 * BS_BLOCKS;
+constexpr int BS_TILE_WORDS = BS_PLANES * BS_BLOCKS;
+constexpr u32 BS_TILE_BYTES = BS_TILE_WORDS * 4;  // 44,544 B at 2 blocks per lane
+constexpr u32 BS_PLANE_BYTES = BS_BLOCKS * 4;
 constexpr int BS_LIST = 88;                  // max plane indices per query (83 rounded to 8)
 #ifndef FPS_BS_QPW
 #define FPS_BS_QPW 4
 #endif
 #ifndef FPS_BS_MINB
-#define FPS_BS_MINB 3
+#define FPS_BS_MINB 1
 #endif
 constexpr int BS_QPW = FPS_BS_QPW;           // queries per warp
-constexpr int BS_WARPS = 8;
+#ifndef FPS_BS_WARPS
+#define FPS_BS_WARPS 16
+#endif
+constexpr int BS_WARPS = FPS_BS_WARPS;
 constexpr int BS_QPC = BS_QPW * BS_WARPS;    // queries per CTA
 
 // ---------------------------------------------------------------------------
@@ -57,18 +67,18 @@ __global__ void bs_build_kernel(PlanesOut lib, u64 n, u32* __restrict__ bs, u32*
     // bits past key 166 (FPS1 pad bytes) are not represented in the planes:
     // such libraries keep using the POPC scan, which counts them like the reference
     if (w[2] >> 38) atomicAdd(wide, 1u);
-    u32* tile = bs + (blk / 32) * BS_TILE_WORDS;
-    const u32 b = (u32)(blk % 32);
+    u32* tile = bs + (blk / BS_BLOCKS) * BS_TILE_WORDS;
+    const u32 b = (u32)(blk % BS_BLOCKS);
 #pragma unroll 2
     for (int p = 0; p < 166; ++p) {
       const u32 m = __ballot_sync(FULL, (w[p >> 6] >> (p & 63)) & 1);
-      if (lane == 0) tile[p * 32 + b] = m;
+      if (lane == 0) tile[p * BS_BLOCKS + b] = m;
     }
     const u32 pc = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2] & ((1ull << 38) - 1)));
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const u32 m = __ballot_sync(FULL, (pc >> k) & 1);
-      if (lane == 0) tile[(166 + k) * 32 + b] = m;
+      if (lane == 0) tile[(166 + k) * BS_BLOCKS + b] = m;
     }
   }
 }
@@ -79,7 +89,7 @@ struct BsQuery {
   u32 dense;   // 1: list = zero keys (count |a AND NOT q|)
   u32 len;     // list length, multiple of 8
   u32 pad;
-  u32 list[BS_LIST];  // byte offsets (plane * 128) of the planes to count, padded with the zero plane
+  u32 list[BS_LIST];  // byte offsets (plane * BS_PLANE_BYTES) of the planes to count, padded with the zero plane
 };
 
 __global__ void bs_prep_queries(const u64* __restrict__ q, u32 Q, BsQuery* __restrict__ out) {
@@ -93,10 +103,10 @@ __global__ void bs_prep_queries(const u64* __restrict__ q, u32 Q, BsQuery* __res
   u32 len = 0;
   for (int p = 0; p < 166; ++p) {
     const u32 bit = (u32)(((p < 64 ? w0 : p < 128 ? w1 : w2) >> (p & 63)) & 1);
-    if (bit != r.dense) r.list[len++] = (u32)p * 128u;
+    if (bit != r.dense) r.list[len++] = (u32)p * BS_PLANE_BYTES;
   }
-  while (len % 8) r.list[len++] = (u32)BS_ZERO * 128u;
-  for (u32 i = len; i < BS_LIST; ++i) r.list[i] = (u32)BS_ZERO * 128u;
+  while (len % 8) r.list[len++] = (u32)BS_ZERO * BS_PLANE_BYTES;
+  for (u32 i = len; i < BS_LIST; ++i) r.list[i] = (u32)BS_ZERO * BS_PLANE_BYTES;
   r.len = len;
   r.pad = 0;
   out[qi] = r;
@@ -177,8 +187,8 @@ __device__ __forceinline__ u32 bs_pass_mask(const u32 (&A)[8], const u32 (&C)[8]
 template <int MODE>
 __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(const BsArgs a) {
   extern __shared__ __align__(128) unsigned char bsm[];
-  u32* tiles = reinterpret_cast<u32*>(bsm);                          // 2 x (BS_TILE_WORDS + 32 zero words)
-  u64* bars = reinterpret_cast<u64*>(bsm + 2 * (BS_TILE_BYTES + 128));  // 2 mbarriers
+  u32* tiles = reinterpret_cast<u32*>(bsm);  // 2 x (BS_TILE_WORDS + a zero plane)
+  u64* bars = reinterpret_cast<u64*>(bsm + 2 * (BS_TILE_BYTES + BS_PLANE_BYTES));  // 2 mbarriers
   BsQuery* sq = reinterpret_cast<BsQuery*>(bars + 2);                 // [BS_QPC]
   u32* hist_all = reinterpret_cast<u32*>(sq + BS_QPC);               // [BS_WARPS][BS_QPW][HB] (TOPK)
   WarpState<BS_QPW>* ws_all = reinterpret_cast<WarpState<BS_QPW>*>(hist_all + BS_WARPS * BS_QPW * HB);
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
     else { sq[i].pop = 0; sq[i].dense = 0; sq[i].len = 0; }
   }
   for (int b = 0; b < 2; ++b)
-    for (int i = threadIdx.x; i < 32; i += blockDim.x) tiles[b * (BS_TILE_WORDS + 32) + BS_TILE_WORDS + i] = 0;
+    for (int i = threadIdx.x; i < BS_BLOCKS; i += blockDim.x) tiles[b * (BS_TILE_WORDS + BS_BLOCKS) + BS_TILE_WORDS + i] = 0;
   u32* hist = hist_all + wid * BS_QPW * HB;
   WarpState<BS_QPW>* ws = ws_all + wid;
   if (MODE == MODE_TOPK) {
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
 
   auto issue = [&](u64 t, int b) {
     mbar_expect_tx(&bars[b], BS_TILE_BYTES);
-    bulk_g2s(tiles + b * (BS_TILE_WORDS + 32), a.bs + t * BS_TILE_WORDS, BS_TILE_BYTES, &bars[b]);
+    bulk_g2s(tiles + b * (BS_TILE_WORDS + BS_BLOCKS), a.bs + t * BS_TILE_WORDS, BS_TILE_BYTES, &bars[b]);
   };
   if (threadIdx.x == 0) {
     if (t0 < t1) issue(t0, 0);
@@ -248,14 +258,23 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
     const int b = (int)((t - t0) & 1);
     mbar_wait(&bars[b], phase[b]);
     phase[b] ^= 1;
-    const u32* tile = tiles + b * (BS_TILE_WORDS + 32);
-    // popcount planes of this lane's block (shared by every query)
-    u32 A[8];
+    const u32* tile = tiles + b * (BS_TILE_WORDS + BS_BLOCKS);
+    // popcount planes of this lane's blocks (shared by every query)
+    u32 A[BS_BPL][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) A[i] = tile[(166 + i) * 32 + lane];
-    const u64 blk_first = t * BS_TILE_ENTRIES + (u64)lane * 32;  // local index of this lane's bit 0
+    for (int i = 0; i < 8; ++i) {
+      const uint2 v = *reinterpret_cast<const uint2*>(tile + (166 + i) * BS_BLOCKS + lane * BS_BPL);
+      A[0][i] = v.x;
+      A[1][i] = v.y;
+    }
+    const u64 blk_first = t * BS_TILE_ENTRIES + (u64)lane * 32 * BS_BPL;  // local index of this lane's bit 0
     // entries past n (last tile) never pass: mask them out
-    const u32 valid = blk_first >= a.n ? 0u : (a.n - blk_first >= 32 ? FULL : ((1u << (a.n - blk_first)) - 1u));
+    u32 valid[BS_BPL];
+#pragma unroll
+    for (int h = 0; h < BS_BPL; ++h) {
+      const u64 f = blk_first + 32 * h;
+      valid[h] = f >= a.n ? 0u : (a.n - f >= 32 ? FULL : ((1u << (a.n - f)) - 1u));
+    }
 
 #pragma unroll 1
     for (int j = 0; j < BS_QPW; ++j) {
@@ -265,66 +284,77 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
         if (jj == j) Tj = T[jj];
       if (Tj == 0) continue;  // padding slot or nothing can pass
       const BsQuery& qq = sq[wid * BS_QPW + j];
-      // carry-save count of the listed planes: ones..s64 = binary digits
-      // (a second, interleaved accumulator for more ILP measured slower:
-      // profiles/r01_experiments.md)
-      u32 ones = 0, twos = 0, fours = 0, eights = 0, s16 = 0, s32 = 0, s64 = 0;
-      const char* lane_base = reinterpret_cast<const char*>(tile) + 4 * lane;
+      // carry-save count of the listed planes for both blocks: ones..s64 =
+      // binary digits (two independent chains per lane)
+      u32 ones[BS_BPL], twos[BS_BPL], fours[BS_BPL], eights[BS_BPL], s16[BS_BPL], s32[BS_BPL], s64[BS_BPL];
+#pragma unroll
+      for (int h = 0; h < BS_BPL; ++h) ones[h] = twos[h] = fours[h] = eights[h] = s16[h] = s32[h] = s64[h] = 0;
+      const char* lane_base = reinterpret_cast<const char*>(tile) + 4 * BS_BPL * lane;
 #define CSA(h, l, x, y)              \
   do {                               \
     const u32 u_ = l ^ x;            \
     h = (l & x) | (u_ & y);          \
     l = u_ ^ y;                      \
   } while (0)
-#define CSA8(d, ones, twos, fours, eights, s16, s32, s64) \
-  do {                                                     \
-    u32 twosA, twosB, foursA, foursB, eightsA;             \
-    CSA(twosA, ones, d[0], d[1]);                          \
-    CSA(twosB, ones, d[2], d[3]);                          \
-    CSA(foursA, twos, twosA, twosB);                       \
-    CSA(twosA, ones, d[4], d[5]);                          \
-    CSA(twosB, ones, d[6], d[7]);                          \
-    CSA(foursB, twos, twosA, twosB);                       \
-    CSA(eightsA, fours, foursA, foursB);                   \
-    u32 c1 = eights & eightsA;                             \
-    eights ^= eightsA;                                     \
-    u32 c2 = s16 & c1;                                     \
-    s16 ^= c1;                                             \
-    u32 c3 = s32 & c2;                                     \
-    s32 ^= c2;                                             \
-    s64 ^= c3;                                             \
-  } while (0)
-      u32 c0 = 0;
-      for (; c0 < qq.len; c0 += 8) {
+      for (u32 c0 = 0; c0 < qq.len; c0 += 8) {
         const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
         const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
         const u32 off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-        u32 d[8];
+        u32 d[BS_BPL][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) d[i] = *reinterpret_cast<const u32*>(lane_base + off[i]);
-        CSA8(d, ones, twos, fours, eights, s16, s32, s64);
+        for (int i = 0; i < 8; ++i) {
+          const uint2 v = *reinterpret_cast<const uint2*>(lane_base + off[i]);
+          d[0][i] = v.x;
+          d[1][i] = v.y;
+        }
+#pragma unroll
+        for (int h = 0; h < BS_BPL; ++h) {
+          u32 twosA, twosB, foursA, foursB, eightsA;
+          CSA(twosA, ones[h], d[h][0], d[h][1]);
+          CSA(twosB, ones[h], d[h][2], d[h][3]);
+          CSA(foursA, twos[h], twosA, twosB);
+          CSA(twosA, ones[h], d[h][4], d[h][5]);
+          CSA(twosB, ones[h], d[h][6], d[h][7]);
+          CSA(foursB, twos[h], twosA, twosB);
+          CSA(eightsA, fours[h], foursA, foursB);
+          const u32 c1 = eights[h] & eightsA;
+          eights[h] ^= eightsA;
+          const u32 c2 = s16[h] & c1;
+          s16[h] ^= c1;
+          const u32 c3 = s32[h] & c2;
+          s32[h] ^= c2;
+          s64[h] ^= c3;
+        }
       }
-#undef CSA8
 #undef CSA
       // pass mask: sign of X + (|q| - T), X = |a| - 2c (sparse) or 2c - |a|
       // (dense); a warp-uniform branch picks the operand order (no selects)
-      const u32 C[8] = {0, ones, twos, fours, eights, s16, s32, s64};  // 2c
       const u32* wm = wmask + j * 10;
-      const u32 m = (qq.dense ? bs_pass_mask<true>(A, C, wm) : bs_pass_mask<false>(A, C, wm)) & valid;
-      if (!__any_sync(FULL, m)) continue;
+      u32 m[BS_BPL];
+#pragma unroll
+      for (int h = 0; h < BS_BPL; ++h) {
+        const u32 C[8] = {0, ones[h], twos[h], fours[h], eights[h], s16[h], s32[h], s64[h]};  // 2c
+        m[h] = (qq.dense ? bs_pass_mask<true>(A[h], C, wm) : bs_pass_mask<false>(A[h], C, wm)) & valid[h];
+      }
+      if (!__any_sync(FULL, m[0] | m[1])) continue;
 
       // ---- slow path: exact distances of the passing entries, in index order
+      // (bit e of mm = entry blk_first + e; the lane's blocks are consecutive)
+      const u64 mm = (u64)m[0] | ((u64)m[1] << 32);
       const u32 qi = qg * BS_QPC + wid * BS_QPW + j;
-      const u32 cntl = __popc(m);
+      const u32 cntl = (u32)__popcll(mm);
       const u32 incl = warp_incl_scan(cntl, lane);
       const u32 total = __shfl_sync(FULL, incl, 31);
       auto dist_of_bit = [&](int e) -> u32 {
+        const int h = e >> 5, bit = e & 31;
         u32 av = 0, cv = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) av |= ((A[i] >> e) & 1u) << i;
-        const u32 cbits[7] = {ones, twos, fours, eights, s16, s32, s64};
+        for (int i = 0; i < 8; ++i) av |= (((h ? A[1][i] : A[0][i]) >> bit) & 1u) << i;
+        const u32 cb[7] = {h ? ones[1] : ones[0], h ? twos[1] : twos[0], h ? fours[1] : fours[0],
+                           h ? eights[1] : eights[0], h ? s16[1] : s16[0], h ? s32[1] : s32[0],
+                           h ? s64[1] : s64[0]};
 #pragma unroll
-        for (int i = 0; i < 7; ++i) cv |= ((cbits[i] >> e) & 1u) << i;
+        for (int i = 0; i < 7; ++i) cv |= ((cb[i] >> bit) & 1u) << i;
         return qq.dense ? qq.pop - av + 2 * cv : av + qq.pop - 2 * cv;
       };
       if (MODE == MODE_RANGE) {
@@ -332,8 +362,8 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
         if (lane == 31) base = atomicAdd(a.out_cnt, (u64)total);
         base = __shfl_sync(FULL, base, 31);
         u64 pos = base + incl - cntl;
-        for (u32 mm = m; mm; mm &= mm - 1) {
-          const int e = __ffs(mm) - 1;
+        for (u64 rest = mm; rest; rest &= rest - 1) {
+          const int e = __ffsll((long long)rest) - 1;
           if (pos < a.out_cap)
             a.out[pos] = ((u64)qi << 48) | make_key(dist_of_bit(e), a.index_base + blk_first + e);
           ++pos;
@@ -377,8 +407,8 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
 #ifdef FPS_BS_DEBUG
       if (cnt0 + total > a.cap) { printf("BS overflow cnt0 %u total %u cap %u\n", cnt0, total, a.cap); __trap(); }
 #endif
-      for (u32 mm = m; mm; mm &= mm - 1) {
-        const int e = __ffs(mm) - 1;
+      for (u64 rest = mm; rest; rest &= rest - 1) {
+        const int e = __ffsll((long long)rest) - 1;
         const u32 d = dist_of_bit(e);
 #ifdef FPS_BS_DEBUG
         if (d >= HB || d >= Tj) { printf("BS bad d %u T %u pop %u dense %u lane %d e %d\n", d, Tj, qq.pop, qq.dense, lane, e); __trap(); }

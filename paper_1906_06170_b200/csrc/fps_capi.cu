@@ -440,7 +440,7 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
 constexpr u32 BS_MIN_Q = 32;  // below this the POPC kernels (query words in registers) win
 
 size_t bs_smem() {
-  return 2 * (fps::BS_TILE_BYTES + 128) + 16 + fps::BS_QPC * sizeof(fps::BsQuery) +
+  return 2 * (fps::BS_TILE_BYTES + fps::BS_PLANE_BYTES) + 16 + fps::BS_QPC * sizeof(fps::BsQuery) +
          (size_t)fps::BS_WARPS * fps::BS_QPW * fps::HB * 4 + fps::BS_WARPS * sizeof(fps::WarpState<fps::BS_QPW>) +
          (size_t)fps::BS_WARPS * fps::BS_QPW * 10 * 4;
 }
