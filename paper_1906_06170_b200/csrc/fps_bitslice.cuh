@@ -16,9 +16,13 @@
 // Roughly 150 LOP3/LDS per 32 x 32 = 1024 comparisons per warp instruction
 // stream, versus ~4.5 k instructions (4 k POPC-pipe slots) for the POPC scan.
 //
-// Tiles of 1024 entries (32 blocks) are streamed into shared memory with the
-// Blackwell bulk-copy engine (cp.async.bulk + mbarrier, double buffered);
-// the 8 warps of a CTA share each tile and split the CTA's query group.
+// Tiles of 2048 entries (64 blocks, 44.5 KB) are streamed into shared memory
+// with the Blackwell bulk-copy engine (cp.async.bulk + mbarrier, double
+// buffered); the 16 warps of a CTA (one CTA per SM) share each tile and split
+// the CTA's 64 queries. A lane owns two consecutive blocks: one 64-bit shared
+// load fetches a plane word of both, so the plane-address arithmetic and the
+// loads are amortised over 64 entries and the two carry-save chains
+// interleave (C4: 46.0 -> 33.7 ms against one block per lane).
 // Results go through the same per-(warp, query) ordered candidate buffers,
 // exact tie rule and select_kernel as the POPC scan (fps_kernels.cuh).
 #pragma once
