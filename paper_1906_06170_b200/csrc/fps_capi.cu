@@ -598,7 +598,7 @@ int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_
     if (qw == 4) return topk_fused<4, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
     return topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   }
-  if (qw == 1) return topk_fused<1, FPS_QW1_E, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
+  if (qw == 1) return topk_fused<1, 4, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   if (qw == 2) return topk_fused<2, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   if (qw == 4) return topk_fused<4, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
   return topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only);
@@ -1362,7 +1362,7 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
       u32* dc = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->dmap) + (size_t)k * 8);
       lib->last_kernel = 1;
       rc = lib->compact ? topk_fused<1, 4, true>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries))
-                        : topk_fused<1, FPS_QW1_E, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
+                        : topk_fused<1, 4, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
       if (rc) { reset_state(lib); return rc; }
       cudaError_t e = wait_stream(lib->stream);
       if (e != cudaSuccess) {

@@ -28,26 +28,11 @@
 #ifndef FPS_QW1_MINB
 #define FPS_QW1_MINB 2  // CTAs per SM the single-query kernels are register-limited for
 #endif
-#ifndef FPS_QW1_U
-#define FPS_QW1_U 1  // single-buffered single-query kernels: iterations loaded per trip
-#endif
-#ifndef FPS_QW1_E
-#define FPS_QW1_E 4  // single-query top-k: entries per lane per iteration (4: 256-bit loads, 2: 128-bit)
-#endif
 #ifndef FPS_QW1_TMA
 #define FPS_QW1_TMA 1  // single-query scans stream tiles through a per-warp shared-memory ring (bulk copies)
 #endif
 #ifndef FPS_QW1_STAGES
 #define FPS_QW1_STAGES 2  // tiles in flight per warp in the bulk-copy ring
-#endif
-#ifndef FPS_EXIT_TGP
-#define FPS_EXIT_TGP 1  // single-query scans append survivors under the last prefetched bound
-#endif
-#ifndef FPS_SEL_WARM
-#define FPS_SEL_WARM 0  // select_kernel runs its sort once on dummy keys while the scan drains
-#endif
-#ifndef FPS_QW1_PIPE
-#define FPS_QW1_PIPE 1  // single-query kernels: 1 = next iteration's loads in flight (double buffer)
 #endif
 
 namespace fps {
@@ -563,7 +548,7 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
     }
   };
 
-  constexpr int U = (QW == 1) ? FPS_QW1_U : 1;  // iterations per trip
+  constexpr int U = 1;  // iterations per trip
   // loop trips between global-bound refreshes (tg is replicated over L2 slices
   // for small Q, so the single-query kernel can afford one load per trip)
   constexpr int REFRESH = (QW == 1) ? 2 : 8;
@@ -764,32 +749,6 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       }
     }
     it = it1;
-  } else if (QW == 1 && !FPS_QW1_PIPE) {
-    // single-buffered variant: fewer registers, more resident warps
-    for (; it + U <= it_main; it += U) {
-      Trip t;
-      load_trip(t, it);
-      run_trip(t, it);
-    }
-  } else if (QW == 1) {
-    // HBM-bound single-query scan over a static contiguous part, software-pipelined:
-    // the next iteration's loads are in flight while the current one is processed.
-    // (Dynamic chunk claiming and narrower per-warp parts measured slower on
-    // B200: profiles/r01_experiments.md.)
-    Trip P, R;
-    if (it + U <= it_main) load_trip(P, it);
-    while (it + U <= it_main) {
-      const bool more = it + 2 * U <= it_main;
-      if (more) load_trip(R, it + U);
-      run_trip(P, it);
-      it += U;
-      if (!more) break;
-      const bool more2 = it + 2 * U <= it_main;
-      if (more2) load_trip(P, it + U);
-      run_trip(R, it);
-      it += U;
-      if (!more2) break;
-    }
   } else {
     for (; it + U <= it_main; it += U) {
       Trip t;
@@ -839,7 +798,7 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
       if (qi >= a.Q) continue;
       // single query: the bound prefetched during the scan (possibly looser
       // than the final one -- select re-filters) saves a load at exit
-      const u32 t = (QW == 1 && FPS_EXIT_TGP) ? tgp : *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));
+      const u32 t = (QW == 1) ? tgp : *(volatile const u32*)tgrep(a, qi, (u32)(g % a.tg_rep));
       // survivors (d <= t) counted from the histogram that mirrors the buffer:
       // most warps have none and skip reading their buffer back
       const u32* hj = hist + j * HB;
@@ -958,8 +917,7 @@ __device__ __forceinline__ u64 bitonic_p(u64 key, u32 t, u64* sh) {
 // `my`) that are within the final bound are sorted by the first p = pow2 >= m
 // threads only (p >= 32); when some fall outside the bound they are first
 // compacted through shared memory. The k smallest keys (padded with ~0) go to
-// out; returns m. out == nullptr: warm-up pass (code fetched into the
-// instruction cache while the scan drains).
+// out; returns m.
 __device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u32* s_wcnt, u32 k, u64* out) {
   const u32 t = threadIdx.x, lane = t & 31, w = t >> 5;
   const u32 m = (u32)__syncthreads_count(keep);
@@ -977,7 +935,7 @@ __device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u
     key = t < m ? comp[t] : ~0ull;
   }
 #ifdef FPS_SEL_PROBE
-  if (out && t == 0) { g_sel_clock[10] = key; SEL_MARK(8); }
+  if (t == 0) { g_sel_clock[10] = key; SEL_MARK(8); }
 #endif
   u32 p = 32;
   while (p < m) p <<= 1;
@@ -991,12 +949,11 @@ __device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u
       default: key = bitonic_p<1024>(key, t, sh); break;
     }
 #ifdef FPS_SEL_PROBE
-    if (out && t == 0) { g_sel_clock[10] = key; SEL_MARK(9); }
+    if (t == 0) { g_sel_clock[10] = key; SEL_MARK(9); }
 #endif
-    if (out != nullptr && t < k) out[t] = key;
+    if (t < k) out[t] = key;
   }
-  if (out != nullptr)
-    for (u32 i = p + t; i < k; i += SEL_THREADS) out[i] = ~0ull;
+  for (u32 i = p + t; i < k; i += SEL_THREADS) out[i] = ~0ull;
   return m;
 }
 
@@ -1013,38 +970,29 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   asm volatile("griddepcontrol.launch_dependents;");
   const u32 q = blockIdx.x;
   const u64* c = cand + (u64)q * cand_cap;
-  // Launched as a programmatic dependent of the scan. While the scan drains,
-  // run the small-sort code once on dummy keys: after an L2 flush the
-  // kernel's instructions are cold and each first-touch fetch costs ~1 us.
+  // launched as a programmatic dependent of the scan: wait for its results
   __shared__ u32 s_wcnt[SEL_THREADS / 32];
-  u64 my = 0;
-  u32 n = SEL_THREADS, bound = T_OPEN, m_small = 0;
-  u64* dst = nullptr;
-#pragma unroll 1
-  for (int pass = FPS_SEL_WARM ? 0 : 1; pass < 2; ++pass) {
-    if (pass == 1) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");  // scan results visible
-      SEL_MARK(0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  SEL_MARK(0);
 #ifdef FPS_SCAN_TRACE
-      if (threadIdx.x == 0 && q == 0) g_mark[2] = gtimer();
+  if (threadIdx.x == 0 && q == 0) g_mark[2] = gtimer();
 #endif
-      // speculative first-slot read, independent of the count load
-      my = threadIdx.x < cand_cap ? c[threadIdx.x] : ~0ull;
-      n = cand_cnt[q];
-      bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
-      dst = out_keys + (u64)q * k;
+  // speculative first-slot read, independent of the count load
+  const u64 my = threadIdx.x < cand_cap ? c[threadIdx.x] : ~0ull;
+  const u32 n = cand_cnt[q];
+  const u32 bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
 #ifdef FPS_SEL_PROBE
-      if (threadIdx.x == 0) g_sel_clock[1] = my + n + bound;  // wait for the loads
-      SEL_MARK(2);
+  if (threadIdx.x == 0) g_sel_clock[1] = my + n + bound;  // wait for the loads
+  SEL_MARK(2);
 #endif
-      if (n > (u32)SEL_THREADS) break;
-    }
+  u32 m_small = 0;
+  if (n <= (u32)SEL_THREADS) {
     // common case: every survivor fits one key per thread -- sort the ones
     // within the bound (unique keys: the first k sorted are the answer)
-    m_small = select_small(my, n, threadIdx.x < n && key_d(my) <= bound, ssel, s_wcnt, k, dst);
-    if (pass == 1) SEL_MARK(3);
+    m_small = select_small(my, n, threadIdx.x < n && key_d(my) <= bound, ssel, s_wcnt, k, out_keys + (u64)q * k);
+    SEL_MARK(3);
 #ifdef FPS_SEL_PROBE
-    if (pass == 1 && threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
       g_sel_clock[5] = g_sel_clock[0] + m_small;
       g_sel_clock[6] = g_sel_clock[0] + bound;
       g_sel_clock[7] = g_sel_clock[0] + n;
