@@ -389,3 +389,31 @@ def test_fps1_streaming_loader(tmp_path):
 
     via_manifest = scan.search(libstore.load_manifest(mpath.parent), tuple(int(x) for x in q), scan.SearchParams(n=3))
     assert via_manifest.hits[0].distance == 0
+
+
+@pytest.mark.parametrize("n", [2048, 2049, 2080, 2081, 4095, 70_001, 132_127])
+def test_bitslice_tails_and_query_groups(n):
+    """Q >= 32 runs the bit-sliced kernel: 2,048-entry tiles, two 32-entry
+    blocks per lane. Library sizes around the tile / block / lane-pair
+    boundaries, two query groups (Q = 70 > 64 per CTA), sparse and dense
+    queries (|q| > 83 counts the zero keys), top-k and range: all equal the
+    oracle."""
+    seed = 9000 + n
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, n)
+    rng = np.random.default_rng(n)
+    Q = 70
+    q = w[rng.integers(0, n, Q)].copy()
+    q[:, 0] ^= rng.integers(0, 2**16, Q).astype(np.uint64) << np.uint64(1)
+    dense = np.array([~np.uint64(0), ~np.uint64(0), np.uint64((1 << 38) - 1)], dtype=np.uint64)
+    q[:8] = dense ^ q[:8] & np.uint64(0x0F0F0F0F)  # mostly-ones queries
+    q[:8, 2] &= np.uint64((1 << 38) - 1)
+    lib = Library.from_words(w)
+    for k in (1, 10, 100):
+        res = lib.search_batch(q, k)
+        exp = oracle_topk(w, q, k)
+        for i in range(Q):
+            assert res.hits(i) == exp[i], (n, k, i)
+    assert lib.last_kernel == "bit-sliced multi-query scan"
+    r = lib.range_search(q[:40], 12)
+    assert np.array_equal(r.rows(), orc.c_range(w, q[:40], 12))
