@@ -46,14 +46,17 @@ def gather_topk(keys: torch.Tensor, cnt: torch.Tensor, k: int, merge: MergeFn, g
     cnt = cnt.contiguous()
     if world == 1:
         return merge(keys.unsqueeze(0), cnt.unsqueeze(0), k)
+    # one collective per call: keys and counts travel in a single int64 buffer
+    Q = cnt.numel()
+    packed = torch.cat([keys.reshape(-1).view(torch.int64), cnt.to(torch.int64)])
     if rank == dst:
-        kl = [torch.empty_like(keys) for _ in range(world)]
-        cl = [torch.empty_like(cnt) for _ in range(world)]
-        dist.gather(keys, kl, dst=dst, group=group)
-        dist.gather(cnt, cl, dst=dst, group=group)
-        return merge(torch.stack(kl), torch.stack(cl), k)
-    dist.gather(keys, None, dst=dst, group=group)
-    dist.gather(cnt, None, dst=dst, group=group)
+        bufs = [torch.empty_like(packed) for _ in range(world)]
+        dist.gather(packed, bufs, dst=dst, group=group)
+        allp = torch.stack(bufs)  # (G, Q*k + Q)
+        kk = allp[:, :Q * k].reshape(world, *keys.shape).view(keys.dtype)
+        cc = allp[:, Q * k:].to(cnt.dtype)
+        return merge(kk.contiguous(), cc.contiguous(), k)
+    dist.gather(packed, None, dst=dst, group=group)
     return None
 
 
