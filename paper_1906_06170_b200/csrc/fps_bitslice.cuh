@@ -300,29 +300,60 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
     h = (l & x) | (u_ & y);          \
     l = u_ ^ y;                      \
   } while (0)
-      for (u32 c0 = 0; c0 < qq.len; c0 += 8) {
-        const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c0);
-        const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c0 + 4);
+      // 8 listed planes of both blocks -> the eights-weight carry of each
+      // block (ones/twos/fours absorb the rest)
+      auto load8 = [&](u32 c, u32 (&d)[BS_BPL][8]) {
+        const uint4 o0 = *reinterpret_cast<const uint4*>(qq.list + c);
+        const uint4 o1 = *reinterpret_cast<const uint4*>(qq.list + c + 4);
         const u32 off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-        u32 d[BS_BPL][8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const uint2 v = *reinterpret_cast<const uint2*>(lane_base + off[i]);
           d[0][i] = v.x;
           d[1][i] = v.y;
         }
+      };
+      auto tree8 = [&](const u32 (&d)[BS_BPL][8], u32 (&e8)[BS_BPL]) {
 #pragma unroll
         for (int h = 0; h < BS_BPL; ++h) {
-          u32 twosA, twosB, foursA, foursB, eightsA;
+          u32 twosA, twosB, foursA, foursB;
           CSA(twosA, ones[h], d[h][0], d[h][1]);
           CSA(twosB, ones[h], d[h][2], d[h][3]);
           CSA(foursA, twos[h], twosA, twosB);
           CSA(twosA, ones[h], d[h][4], d[h][5]);
           CSA(twosB, ones[h], d[h][6], d[h][7]);
           CSA(foursB, twos[h], twosA, twosB);
-          CSA(eightsA, fours[h], foursA, foursB);
-          const u32 c1 = eights[h] & eightsA;
-          eights[h] ^= eightsA;
+          CSA(e8[h], fours[h], foursA, foursB);
+        }
+      };
+      u32 c0 = 0;
+      // 16 planes per step: two 8-plane trees and one more carry-save adder
+      // at weight 8 (35 LOP3 per 16 planes instead of 42)
+      for (; c0 + 16 <= qq.len; c0 += 16) {
+        u32 d[BS_BPL][8], e8a[BS_BPL], e8b[BS_BPL];
+        load8(c0, d);
+        tree8(d, e8a);
+        load8(c0 + 8, d);
+        tree8(d, e8b);
+#pragma unroll
+        for (int h = 0; h < BS_BPL; ++h) {
+          u32 e16;
+          CSA(e16, eights[h], e8a[h], e8b[h]);
+          const u32 c2 = s16[h] & e16;
+          s16[h] ^= e16;
+          const u32 c3 = s32[h] & c2;
+          s32[h] ^= c2;
+          s64[h] ^= c3;
+        }
+      }
+      if (c0 < qq.len) {  // a last group of 8 (lists are padded to multiples of 8)
+        u32 d[BS_BPL][8], e8[BS_BPL];
+        load8(c0, d);
+        tree8(d, e8);
+#pragma unroll
+        for (int h = 0; h < BS_BPL; ++h) {
+          const u32 c1 = eights[h] & e8[h];
+          eights[h] ^= e8[h];
           const u32 c2 = s16[h] & c1;
           s16[h] ^= c1;
           const u32 c3 = s32[h] & c2;
