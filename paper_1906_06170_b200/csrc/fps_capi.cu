@@ -301,14 +301,20 @@ fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
 // traffic there costs more than the imbalance (profiles/r01_experiments.md).
 // Scan flag 64 disables it. Needs one query group: every warp scans for the
 // same query.
+#ifndef FPS_DYN_STATIC_PCT
+#define FPS_DYN_STATIC_PCT 50  // share of the tiles split statically before the global tail
+#endif
+#ifndef FPS_DYN_CHUNK_ITERS
+#define FPS_DYN_CHUNK_ITERS 12  // 128-entry iterations per tail claim (6 compact tiles; 4 -> contention, 24 -> coarse tail)
+#endif
 template <int QW, int E, int MODE, bool CMP>
 void set_dyn(fps_lib* L, fps::ScanArgs& a) {
   if (!fps::ScanSmem<QW, E, MODE, CMP>::TMA || MODE != fps::MODE_TOPK || a.n_qg != 1 || (a.flags & 64)) return;
   if (!L->dyn.p || a.iters < 128 * a.n_parts) return;
   constexpr u64 SUB = fps::ScanSmem<QW, E, MODE, CMP>::SUB;  // iterations per tile (the kernel's work unit)
   a.dyn_ctr = L->dyn.as<u32>();
-  a.dyn_start = (a.iters + SUB - 1) / SUB / 2;
-  a.dyn_chunk = std::max<u64>(1, 8 / SUB);
+  a.dyn_start = (a.iters + SUB - 1) / SUB * FPS_DYN_STATIC_PCT / 100;
+  a.dyn_chunk = std::max<u64>(1, FPS_DYN_CHUNK_ITERS / SUB);
 }
 
 // select_kernel launched as a programmatic dependent of the scan kernel: its
