@@ -304,13 +304,16 @@ fps::ScanArgs base_args(const fps_lib* L, const u64* d_q, u32 Q) {
 #ifndef FPS_DYN_STATIC_PCT
 #define FPS_DYN_STATIC_PCT 50  // share of the tiles split statically before the global tail
 #endif
+#ifndef FPS_DYN_MIN_ITERS
+#define FPS_DYN_MIN_ITERS 128  // per-warp iterations below which a scan uses the CTA-dynamic schedule
+#endif
 #ifndef FPS_DYN_CHUNK_ITERS
 #define FPS_DYN_CHUNK_ITERS 12  // 128-entry iterations per tail claim (6 compact tiles; 4 -> contention, 24 -> coarse tail)
 #endif
 template <int QW, int E, int MODE, bool CMP>
 void set_dyn(fps_lib* L, fps::ScanArgs& a) {
   if (!fps::ScanSmem<QW, E, MODE, CMP>::TMA || MODE != fps::MODE_TOPK || a.n_qg != 1 || (a.flags & 64)) return;
-  if (!L->dyn.p || a.iters < 128 * a.n_parts) return;
+  if (!L->dyn.p || a.iters < FPS_DYN_MIN_ITERS * a.n_parts) return;
   constexpr u64 SUB = fps::ScanSmem<QW, E, MODE, CMP>::SUB;  // iterations per tile (the kernel's work unit)
   a.dyn_ctr = L->dyn.as<u32>();
   a.dyn_start = (a.iters + SUB - 1) / SUB * FPS_DYN_STATIC_PCT / 100;
