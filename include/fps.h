@@ -125,6 +125,13 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
 int fps_range(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t** out_keys,
               uint64_t* n_out);
 void fps_free(void* p);
+/* Range search in two calls, results straight into caller-owned columns
+ * (no library-allocated buffer): fps_range_begin scans, sorts by (q,
+ * distance, index) and leaves the n hits on the device; fps_range_fetch
+ * copies them through a pinned double buffer and splits them into
+ * query / index / distance columns of n entries. Same hits as fps_range. */
+int fps_range_begin(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t* n_out);
+int fps_range_fetch(fps_lib* lib, uint32_t* out_query, uint64_t* out_index, uint16_t* out_dist, uint64_t n);
 /* Split n range keys into the three result columns (query, index, distance)
  * in one pass on the host -- the reference has no range op; this
  * builds the columns its RangeResult-style result needs without numpy

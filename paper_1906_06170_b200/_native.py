@@ -57,6 +57,8 @@ SIGNATURES = {
     "fps_range": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.POINTER(_vp), _u64p]),
     "fps_free": (None, [_vp]),
     "fps_range_unpack": (None, [_vp, C.c_uint64, _vp, _vp, _vp]),
+    "fps_range_begin": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _u64p]),
+    "fps_range_fetch": (C.c_int, [_vp, _vp, _vp, _vp, C.c_uint64]),
     "fps_fnv1a64": (C.c_uint64, [_vp, C.c_uint64, C.c_uint64]),
     "fps_fnv1a64_file": (C.c_int, [C.c_char_p, C.c_uint64, _u64p]),
     "fps_build_shards": (C.c_int, [_vp, C.c_uint64, _vp, C.c_uint64, C.c_char_p, C.c_uint32, C.c_char_p, C.c_int,

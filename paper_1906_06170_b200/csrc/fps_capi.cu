@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fps.h"
@@ -143,6 +144,8 @@ struct fps_lib {
   DevBuf bs, bsq;
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
   HostBuf h_stage;
+  HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
+  u64 range_pending = 0;  // sorted range keys left on the device by fps_range_begin
   // mapped pinned result buffer of the single-query host path (written by the
   // select kernel over PCIe: no D2H copy) and its device alias
   void* hmap = nullptr;
@@ -1549,6 +1552,67 @@ int fps_range(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* 
 }
 
 void fps_free(void* p) { std::free(p); }
+
+int fps_range_begin(fps_lib* lib, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t* n_out) {
+  if (int rc = check_lib(lib)) return rc;
+  if (!n_out) return fail(FPS_EINVAL, "null output");
+  *n_out = 0;
+  if (Q > 65535) return fail(FPS_EINVAL, "at most 65535 queries per range call");
+  if (Q && (!queries || !radius)) return fail(FPS_EINVAL, "null argument");
+  for (u32 q = 0; q < Q; ++q)
+    if (queries[3 * (u64)q + 2] >> 38) return fail(FPS_EPADDING, "padding bits above key 166 must be zero");
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  lib->range_pending = 0;
+  if (Q == 0) return FPS_OK;
+  int rc;
+  if ((rc = stage_queries(lib, queries, Q))) return rc;
+  if ((rc = lib->radius.ensure(Q))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(lib->radius.p, radius, Q, cudaMemcpyHostToDevice, lib->stream));
+  u64 hits = 0;
+  if ((rc = range_collect(lib, lib->queries.as<u64>(), Q, lib->radius.as<unsigned char>(), &hits, 0))) return rc;
+  if ((rc = sort_keys(lib, lib->rkeys.as<u64>(), hits, lib->stream))) return rc;
+  lib->range_pending = hits;
+  *n_out = hits;
+  return FPS_OK;
+}
+
+int fps_range_fetch(fps_lib* lib, uint32_t* out_query, uint64_t* out_index, uint16_t* out_dist, uint64_t n) {
+  if (int rc = check_lib(lib)) return rc;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  if (n != lib->range_pending) return fail(FPS_EINVAL, "fps_range_fetch: n does not match fps_range_begin");
+  if (n && (!out_query || !out_index || !out_dist)) return fail(FPS_EINVAL, "null argument");
+  // pinned double buffer: chunk c + 1 copies while chunk c is split into
+  // columns (host threads measured slower: spawning them costs more than the
+  // split, which is bounded by first-touch faults on the fresh columns)
+  constexpr u64 CH = 1 << 17;  // keys per chunk (1 MiB)
+  int rc;
+  if (n && ((rc = lib->h_range[0].ensure(CH * 8)) || (rc = lib->h_range[1].ensure(CH * 8)))) return rc;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  const u64* src = lib->rkeys.as<u64>();
+  auto issue = [&](u64 c) {
+    const u64 lo = c * CH, m = std::min<u64>(CH, n - lo);
+    cudaMemcpyAsync(lib->h_range[c & 1].p, src + lo, m * 8, cudaMemcpyDeviceToHost, lib->stream);
+    cudaEventRecord(ev[c & 1], lib->stream);
+  };
+  const u64 chunks = (n + CH - 1) / CH;
+  if (chunks) issue(0);
+  cudaError_t e = cudaSuccess;
+  for (u64 c = 0; c < chunks && e == cudaSuccess; ++c) {
+    e = cudaEventSynchronize(ev[c & 1]);
+    if (c + 1 < chunks) issue(c + 1);
+    const u64 lo = c * CH, m = std::min<u64>(CH, n - lo);
+    fps_range_unpack(reinterpret_cast<const uint64_t*>(lib->h_range[c & 1].p), m, out_query + lo, out_index + lo,
+                     out_dist + lo);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(lib->stream);
+  for (auto& x : ev) cudaEventDestroy(x);
+  lib->range_pending = 0;
+  if (e != cudaSuccess) return fail(FPS_ECUDA, std::string("range fetch: ") + cudaGetErrorString(e));
+  return FPS_OK;
+}
 
 void fps_range_unpack(const uint64_t* keys, uint64_t n, uint32_t* out_query, uint64_t* out_index,
                       uint16_t* out_dist) {

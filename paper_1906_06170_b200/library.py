@@ -290,21 +290,19 @@ class Library:
         if np.any(r < 0):
             raise ValueError("radius must be >= 0")
         rad = np.ascontiguousarray(np.minimum(r, 254).astype(np.uint8))
-        out = C.c_void_p()
         n_out = C.c_uint64()
         if Q == 0:
             return RangeResult.from_keys(np.zeros(0, np.uint64))
-        N.check(N.load().fps_range(self._h, q.ctypes.data, Q, rad.ctypes.data, C.byref(out), C.byref(n_out)),
-                "fps_range")
+        lib = N.load()
+        # scan + device sort, then the sorted hits straight into the result
+        # columns through a pinned double buffer (no intermediate key array)
+        N.check(lib.fps_range_begin(self._h, q.ctypes.data, Q, rad.ctypes.data, C.byref(n_out)), "fps_range_begin")
         m = n_out.value
         query = np.empty(m, np.uint32)
         index = np.empty(m, np.uint64)
         distance = np.empty(m, np.uint16)
-        try:
-            if m:  # one native pass instead of numpy shift/mask temporaries
-                N.load().fps_range_unpack(out, m, query.ctypes.data, index.ctypes.data, distance.ctypes.data)
-        finally:
-            N.load().fps_free(out)
+        N.check(lib.fps_range_fetch(self._h, query.ctypes.data, index.ctypes.data, distance.ctypes.data, m),
+                "fps_range_fetch")
         return RangeResult(query=query, index=index, distance=distance)
 
     # ---- stream-ordered device API --------------------------------------
