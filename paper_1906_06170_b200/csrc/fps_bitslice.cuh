@@ -49,7 +49,7 @@ constexpr int BS_LIST = 88;                  // max plane indices per query (83 
 #ifndef FPS_BS_MINB
 #define FPS_BS_MINB 1
 #endif
-constexpr int BS_QPW = FPS_BS_QPW;           // queries per warp
+constexpr int BS_QPW = FPS_BS_QPW;           // queries per warp (the maximum; small batches use 1 or 2)
 #ifndef FPS_BS_WARPS
 #define FPS_BS_WARPS 16
 #endif
@@ -188,14 +188,15 @@ __device__ __forceinline__ u32 bs_pass_mask(const u32 (&A)[8], const u32 (&C)[8]
   return bs_sign_after_add_m(X, wm);
 }
 
-template <int MODE>
+template <int MODE, int QPW>
 __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(const BsArgs a) {
+  constexpr int QPC = QPW * BS_WARPS;  // queries per CTA
   extern __shared__ __align__(128) unsigned char bsm[];
   u32* tiles = reinterpret_cast<u32*>(bsm);  // 2 x (BS_TILE_WORDS + a zero plane)
   u64* bars = reinterpret_cast<u64*>(bsm + 2 * (BS_TILE_BYTES + BS_PLANE_BYTES));  // 2 mbarriers
-  BsQuery* sq = reinterpret_cast<BsQuery*>(bars + 2);                 // [BS_QPC]
-  u32* hist_all = reinterpret_cast<u32*>(sq + BS_QPC);               // [BS_WARPS][BS_QPW][HB] (TOPK)
-  WarpState<BS_QPW>* ws_all = reinterpret_cast<WarpState<BS_QPW>*>(hist_all + BS_WARPS * BS_QPW * HB);
+  BsQuery* sq = reinterpret_cast<BsQuery*>(bars + 2);                 // [QPC]
+  u32* hist_all = reinterpret_cast<u32*>(sq + QPC);               // [BS_WARPS][QPW][HB] (TOPK)
+  WarpState<QPW>* ws_all = reinterpret_cast<WarpState<QPW>*>(hist_all + BS_WARPS * QPW * HB);
   // per (warp, slot): bit masks of (|q| - T) mod 2^10, refreshed whenever T changes
   u32* wmask_all = reinterpret_cast<u32*>(ws_all + BS_WARPS);
 
@@ -206,18 +207,18 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
   const u64 g = (u64)blockIdx.x * BS_WARPS + wid;  // global warp id (buffers)
 
   // queries of this CTA
-  for (int i = threadIdx.x; i < BS_QPC; i += blockDim.x) {
-    const u32 qi = qg * BS_QPC + i;
+  for (int i = threadIdx.x; i < QPC; i += blockDim.x) {
+    const u32 qi = qg * QPC + i;
     if (qi < a.Q) sq[i] = a.qs[qi];
     else { sq[i].pop = 0; sq[i].dense = 0; sq[i].len = 0; }
   }
   for (int b = 0; b < 2; ++b)
     for (int i = threadIdx.x; i < BS_BLOCKS; i += blockDim.x) tiles[b * (BS_TILE_WORDS + BS_BLOCKS) + BS_TILE_WORDS + i] = 0;
-  u32* hist = hist_all + wid * BS_QPW * HB;
-  WarpState<BS_QPW>* ws = ws_all + wid;
+  u32* hist = hist_all + wid * QPW * HB;
+  WarpState<QPW>* ws = ws_all + wid;
   if (MODE == MODE_TOPK) {
-    for (int i = lane; i < BS_QPW * HB; i += 32) hist[i] = 0;
-    if (lane < BS_QPW) { ws->town[lane] = T_OPEN; ws->pubd[lane] = 0; ws->cnt[lane] = 0; }
+    for (int i = lane; i < QPW * HB; i += 32) hist[i] = 0;
+    if (lane < QPW) { ws->town[lane] = T_OPEN; ws->pubd[lane] = 0; ws->cnt[lane] = 0; }
   }
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -227,10 +228,10 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
   __syncthreads();
 
   // per-slot thresholds (accept d < T)
-  u32 T[BS_QPW];
+  u32 T[QPW];
 #pragma unroll
-  for (int j = 0; j < BS_QPW; ++j) {
-    const u32 qi = qg * BS_QPC + wid * BS_QPW + j;
+  for (int j = 0; j < QPW; ++j) {
+    const u32 qi = qg * QPC + wid * QPW + j;
     if (qi >= a.Q) T[j] = 0;
     else if (MODE == MODE_RANGE) T[j] = (u32)a.radius[qi] + 1;
     else {
@@ -238,15 +239,15 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
       T[j] = (t < T_OPEN ? t : T_OPEN - 1) + 1;
     }
   }
-  u64* wbuf = (MODE == MODE_TOPK) ? a.buf + g * BS_QPW * (u64)a.cap : nullptr;
-  u32* wmask = wmask_all + wid * BS_QPW * 10;
+  u64* wbuf = (MODE == MODE_TOPK) ? a.buf + g * QPW * (u64)a.cap : nullptr;
+  u32* wmask = wmask_all + wid * QPW * 10;
   auto set_wmask = [&](int j, u32 Tj) {
-    const u32 w = (u32)((int)sq[wid * BS_QPW + j].pop - (int)Tj) & 0x3ffu;
+    const u32 w = (u32)((int)sq[wid * QPW + j].pop - (int)Tj) & 0x3ffu;
     if (lane < 10) wmask[j * 10 + lane] = ((w >> lane) & 1u) ? FULL : 0u;
     __syncwarp();
   };
 #pragma unroll
-  for (int j = 0; j < BS_QPW; ++j) set_wmask(j, T[j]);
+  for (int j = 0; j < QPW; ++j) set_wmask(j, T[j]);
 
   auto issue = [&](u64 t, int b) {
     mbar_expect_tx(&bars[b], BS_TILE_BYTES);
@@ -281,13 +282,13 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
     }
 
 #pragma unroll 1
-    for (int j = 0; j < BS_QPW; ++j) {
+    for (int j = 0; j < QPW; ++j) {
       u32 Tj = 0;
 #pragma unroll
-      for (int jj = 0; jj < BS_QPW; ++jj)
+      for (int jj = 0; jj < QPW; ++jj)
         if (jj == j) Tj = T[jj];
       if (Tj == 0) continue;  // padding slot or nothing can pass
-      const BsQuery& qq = sq[wid * BS_QPW + j];
+      const BsQuery& qq = sq[wid * QPW + j];
       // carry-save count of the listed planes for both blocks: ones..s64 =
       // binary digits (two independent chains per lane)
       u32 ones[BS_BPL], twos[BS_BPL], fours[BS_BPL], eights[BS_BPL], s16[BS_BPL], s32[BS_BPL], s64[BS_BPL];
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
       // ---- slow path: exact distances of the passing entries, in index order
       // (bit e of mm = entry blk_first + e; the lane's blocks are consecutive)
       const u64 mm = (u64)m[0] | ((u64)m[1] << 32);
-      const u32 qi = qg * BS_QPC + wid * BS_QPW + j;
+      const u32 qi = qg * QPC + wid * QPW + j;
       const u32 cntl = (u32)__popcll(mm);
       const u32 incl = warp_incl_scan(cntl, lane);
       const u32 total = __shfl_sync(FULL, incl, 31);
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
         const u32 tt = warp_kth_bin(hj, a.k, lane, &less);
         const u32 nt = tt < Tj ? tt : Tj;
 #pragma unroll
-        for (int jj = 0; jj < BS_QPW; ++jj)
+        for (int jj = 0; jj < QPW; ++jj)
           if (jj == j) T[jj] = nt;
         set_wmask(j, nt);
         if (lane == 0) ws->town[j] = tt;
@@ -472,8 +473,8 @@ __global__ void __launch_bounds__(BS_WARPS * 32, FPS_BS_MINB) bs_scan_kernel(con
 
   if (MODE == MODE_TOPK) {
 #pragma unroll 1
-    for (int j = 0; j < BS_QPW; ++j) {
-      const u32 qi = qg * BS_QPC + wid * BS_QPW + j;
+    for (int j = 0; j < QPW; ++j) {
+      const u32 qi = qg * QPC + wid * QPW + j;
       if (qi >= a.Q) continue;
       u32* hj = hist + j * HB;
       u64* bj = wbuf + (u64)j * a.cap;

@@ -449,12 +449,55 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
 // ---------------------------------------------------------------------------
 // bit-sliced multi-query path (fps_bitslice.cuh)
 // ---------------------------------------------------------------------------
-constexpr u32 BS_MIN_Q = 32;  // below this the POPC kernels (query words in registers) win
+// Batches from 2 queries take the bit-sliced kernel: on the 95.4 M library it
+// beats the POPC kernels at every Q >= 2 (Q = 2: 0.38 vs 0.46 ms, Q = 8: 0.51
+// vs 1.22 ms, Q = 32: 1.20 vs 4.48 ms; tools/q_sweep.py). FPS_BS_MIN_Q
+// overrides, FPS_BITSLICE=0 disables it.
+u32 bs_min_q() {
+  static u32 v = []() {
+    const char* e = std::getenv("FPS_BS_MIN_Q");
+    return e ? (u32)std::max(1, std::atoi(e)) : 2u;
+  }();
+  return v;
+}
 
-size_t bs_smem() {
-  return 2 * (fps::BS_TILE_BYTES + fps::BS_PLANE_BYTES) + 16 + fps::BS_QPC * sizeof(fps::BsQuery) +
-         (size_t)fps::BS_WARPS * fps::BS_QPW * fps::HB * 4 + fps::BS_WARPS * sizeof(fps::WarpState<fps::BS_QPW>) +
-         (size_t)fps::BS_WARPS * fps::BS_QPW * 10 * 4;
+// Queries per warp of the bit-sliced kernel: small batches spread one or two
+// queries over every warp of a CTA instead of four over a quarter of them.
+u32 bs_qpw(u32 Q) { return Q <= (u32)fps::BS_WARPS ? 1u : Q <= 2u * fps::BS_WARPS ? 2u : (u32)fps::BS_QPW; }
+
+template <int QPW>
+size_t bs_smem_t() {
+  return 2 * (fps::BS_TILE_BYTES + fps::BS_PLANE_BYTES) + 16 + (size_t)QPW * fps::BS_WARPS * sizeof(fps::BsQuery) +
+         (size_t)fps::BS_WARPS * QPW * fps::HB * 4 + fps::BS_WARPS * sizeof(fps::WarpState<QPW>) +
+         (size_t)fps::BS_WARPS * QPW * 10 * 4;
+}
+size_t bs_smem(u32 qpw) { return qpw == 1 ? bs_smem_t<1>() : qpw == 2 ? bs_smem_t<2>() : bs_smem_t<fps::BS_QPW>(); }
+
+template <int MODE, int QPW>
+int bs_ctas_per_sm() {
+  static int cached = 0;
+  if (!cached) {
+    const size_t sm = bs_smem_t<QPW>();
+    cudaFuncSetAttribute(fps::bs_scan_kernel<MODE, QPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, fps::bs_scan_kernel<MODE, QPW>, fps::BS_WARPS * 32, sm);
+    cached = std::max(1, cached);
+  }
+  return cached;
+}
+
+template <int MODE>
+cudaError_t bs_launch(u32 qpw, u64 ctas, cudaStream_t s, const fps::BsArgs& b) {
+  if (qpw == 1) {
+    bs_ctas_per_sm<MODE, 1>();
+    fps::bs_scan_kernel<MODE, 1><<<(unsigned)ctas, fps::BS_WARPS * 32, bs_smem_t<1>(), s>>>(b);
+  } else if (qpw == 2) {
+    bs_ctas_per_sm<MODE, 2>();
+    fps::bs_scan_kernel<MODE, 2><<<(unsigned)ctas, fps::BS_WARPS * 32, bs_smem_t<2>(), s>>>(b);
+  } else {
+    bs_ctas_per_sm<MODE, fps::BS_QPW>();
+    fps::bs_scan_kernel<MODE, fps::BS_QPW><<<(unsigned)ctas, fps::BS_WARPS * 32, bs_smem_t<fps::BS_QPW>(), s>>>(b);
+  }
+  return cudaGetLastError();
 }
 
 // Build (once) the bit-plane copy; libraries with pad bits past key 166 stay on the POPC path.
@@ -486,29 +529,24 @@ int bs_ensure(fps_lib* L) {
 bool bs_wanted(fps_lib* L, u32 Q) {
   const char* e = std::getenv("FPS_BITSLICE");
   if (e && std::string(e) == "0") return false;
-  if (Q < BS_MIN_Q || L->n < fps::BS_TILE_ENTRIES) return false;
+  if (Q < bs_min_q() || L->n < fps::BS_TILE_ENTRIES) return false;
   if (bs_ensure(L) != FPS_OK) return false;
   return L->bs_state == 1;
 }
 
-fps::BsArgs bs_args(fps_lib* L, u32 Q, u64* n_parts_out) {
+fps::BsArgs bs_args(fps_lib* L, u32 Q, u32 qpw, u64* n_parts_out) {
   fps::BsArgs b{};
   b.bs = L->bs.as<u32>();
   b.n = L->n;
   b.index_base = L->index_base;
   b.qs = reinterpret_cast<const fps::BsQuery*>(L->bsq.p);
   b.Q = Q;
-  b.n_qg = (Q + fps::BS_QPC - 1) / fps::BS_QPC;
+  const u32 qpc = qpw * fps::BS_WARPS;
+  b.n_qg = (Q + qpc - 1) / qpc;
   b.tiles = (L->n + fps::BS_TILE_ENTRIES - 1) / fps::BS_TILE_ENTRIES;
-  static int ctas_per_sm = 0;
-  if (!ctas_per_sm) {
-    const size_t sm = bs_smem();
-    cudaFuncSetAttribute(fps::bs_scan_kernel<fps::MODE_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(fps::bs_scan_kernel<fps::MODE_RANGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fps::bs_scan_kernel<fps::MODE_TOPK>,
-                                                  fps::BS_WARPS * 32, sm);
-    ctas_per_sm = std::max(1, ctas_per_sm);
-  }
+  const int ctas_per_sm = qpw == 1 ? bs_ctas_per_sm<fps::MODE_TOPK, 1>()
+                          : qpw == 2 ? bs_ctas_per_sm<fps::MODE_TOPK, 2>()
+                                     : bs_ctas_per_sm<fps::MODE_TOPK, fps::BS_QPW>();
   const u64 slots = (u64)L->sms * ctas_per_sm;
   u64 parts = std::max<u64>(1, slots / b.n_qg);
   parts = std::min<u64>(parts, std::max<u64>(1, b.tiles / 4));  // >= 4 tiles per CTA
@@ -536,11 +574,12 @@ int topk_bs(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, c
   L->timing_suspend = false;
   if (rc) return rc;
   u64 parts = 0;
-  fps::BsArgs b = bs_args(L, Q, &parts);
+  const u32 qpw = bs_qpw(Q);
+  fps::BsArgs b = bs_args(L, Q, qpw, &parts);
   const u64 ctas = (u64)b.n_qg * parts;
   const u32 cap = (std::max<u32>(2 * k, k + 1024) + 31) / 32 * 32;
   const u64 cand_cap = parts * (u64)k;
-  if ((rc = L->buf.ensure(ctas * fps::BS_WARPS * fps::BS_QPW * (size_t)cap * 8))) return rc;
+  if ((rc = L->buf.ensure(ctas * fps::BS_WARPS * qpw * (size_t)cap * 8))) return rc;
   if ((rc = L->cand.ensure((size_t)Q * cand_cap * 8))) return rc;
   if ((rc = L->bsq.ensure((size_t)Q * sizeof(fps::BsQuery)))) return rc;
   if (prepare_only) return FPS_OK;
@@ -562,7 +601,7 @@ int topk_bs(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, c
   b.cand_cap = cand_cap;
   auto* ev = timing_slot(L);
   if (ev) cudaEventRecord(ev->first, s);
-  fps::bs_scan_kernel<fps::MODE_TOPK><<<(unsigned)ctas, fps::BS_WARPS * 32, bs_smem(), s>>>(b);
+  CUDA_TRY(bs_launch<fps::MODE_TOPK>(qpw, ctas, s, b));
   if (ev) cudaEventRecord(ev->second, s);
   L->launches++;
   LAUNCH_CHECK("bs_scan_kernel<topk>");
@@ -580,17 +619,17 @@ int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u
   int rc;
   if ((rc = bs_prep(L, d_q, Q, s))) return rc;
   u64 parts = 0;
-  fps::BsArgs b = bs_args(L, Q, &parts);
+  const u32 qpw = bs_qpw(Q);
+  fps::BsArgs b = bs_args(L, Q, qpw, &parts);
   b.radius = d_radius;
   b.out = d_out;
   b.out_cnt = d_count;
   b.out_cap = cap;
   auto* ev = timing_slot(L);
   if (ev) cudaEventRecord(ev->first, s);
-  fps::bs_scan_kernel<fps::MODE_RANGE><<<(unsigned)((u64)b.n_qg * parts), fps::BS_WARPS * 32, bs_smem(), s>>>(b);
+  CUDA_TRY(bs_launch<fps::MODE_RANGE>(qpw, (u64)b.n_qg * parts, s, b));
   if (ev) cudaEventRecord(ev->second, s);
   L->launches++;
-  CUDA_TRY(cudaGetLastError());
   return FPS_OK;
 }
 

@@ -147,8 +147,14 @@ def test_topk_tail_sizes(n):
         assert lib.search(q[0], k) == oracle_topk(w, q, k)[0]
 
 
-@pytest.mark.parametrize("Q", [1, 2, 3, 4, 5, 7, 8, 9, 16, 33])
-def test_topk_query_counts(Q):
+@pytest.mark.parametrize("popc", [False, True])
+@pytest.mark.parametrize("Q", [1, 2, 3, 4, 5, 7, 8, 9, 16, 17, 33])
+def test_topk_query_counts(Q, popc, monkeypatch):
+    """Q >= 2 takes the bit-sliced kernel (1, 2 or 4 queries per warp by Q);
+    FPS_BITSLICE=0 keeps the POPC kernels (QW = 2/4/8 query words in
+    registers) covered too."""
+    if popc:
+        monkeypatch.setenv("FPS_BITSLICE", "0")
     seed = 4242 + Q
     thr = synth.beta_thresholds(seed)
     w = orc.generate_words(synth.seed_key(seed), thr, 0, 200_000)
@@ -231,8 +237,11 @@ def test_fps1_padding_scanned_as_stored():
     assert got[-1] == (7, 8)
 
 
+@pytest.mark.parametrize("popc", [False, True])
 @pytest.mark.parametrize("radius", [0, 3, 6, 40])
-def test_range_vs_oracle(radius):
+def test_range_vs_oracle(radius, popc, monkeypatch):
+    if popc:  # the POPC kernels instead of the bit-sliced one
+        monkeypatch.setenv("FPS_BITSLICE", "0")
     seed = 99
     thr = synth.beta_thresholds(seed)
     w = orc.generate_words(synth.seed_key(seed), thr, 0, 250_000)
