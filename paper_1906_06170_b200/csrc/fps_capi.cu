@@ -142,6 +142,7 @@ struct fps_lib {
   DevBuf buf, cand, queries, keys, cnt, radius, rkeys, rcount, sort_tmp, sort_out, seg;
   // bit-plane copy of the library for the multi-query scans (built on first use)
   DevBuf bs, bsq;
+  DevBuf mq;  // min-over-queries merge scratch (fps_topk_min on the batched kernel)
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -1493,6 +1494,40 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   int rc;
   if ((rc = stage_queries(lib, queries, Q))) return rc;
   if ((rc = lib->keys.ensure((size_t)k * 8)) || (rc = lib->cnt.ensure(4))) return rc;
+  if (Q >= 2 && bs_wanted(lib, Q)) {
+    // Per-query top-k on the batched (bit-sliced) kernel, then the min merge:
+    // the global top-k by min_q distance is contained in the union of the
+    // per-query top-k lists (an entry's best query ranks it no lower than the
+    // global order does), and its score is its smallest listed distance.
+    const u64 n = (u64)Q * k;
+    if ((rc = lib->mq.ensure(n * 8 * 3 + (size_t)Q * 4 + 16))) return rc;
+    u64* pk = lib->mq.as<u64>();  // per-query keys
+    u64* tmp = pk + n;
+    u64* out = tmp + n;
+    u32* pc = reinterpret_cast<u32*>(out + n);
+    u32* firsts = pc + Q;
+    if ((rc = topk_dispatch(lib, lib->queries.as<u64>(), Q, k, pk, pc, lib->stream, false))) {
+      reset_state(lib);
+      return rc;
+    }
+    const int blocks = (int)std::min<u64>((n + 255) / 256, 4096);
+    fps::minq_flip<<<blocks, 256, 0, lib->stream>>>(pk, pc, Q, k, tmp);
+    if ((rc = sort_keys(lib, tmp, n, lib->stream))) return rc;
+    CUDA_TRY(cudaMemsetAsync(firsts, 0, 4, lib->stream));
+    fps::minq_first<<<blocks, 256, 0, lib->stream>>>(tmp, n, out, firsts);
+    if ((rc = sort_keys(lib, out, n, lib->stream))) return rc;
+    lib->launches += 2;
+    if ((rc = lib->h_stage.ensure((size_t)k * 8 + 4))) return rc;
+    u64* hk = lib->h_stage.as<u64>();
+    u32* hc = reinterpret_cast<u32*>(lib->h_stage.as<char>() + (size_t)k * 8);
+    CUDA_TRY(cudaMemcpyAsync(hk, out, (size_t)k * 8, cudaMemcpyDeviceToHost, lib->stream));
+    CUDA_TRY(cudaMemcpyAsync(hc, firsts, 4, cudaMemcpyDeviceToHost, lib->stream));
+    cudaError_t e = cudaStreamSynchronize(lib->stream);
+    if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, std::string("top-k min: ") + cudaGetErrorString(e)); }
+    *hc = std::min<u32>(*hc, k);
+    unpack_topk(hk, hc, 1, k, out_idx, out_dist, out_cnt);
+    return FPS_OK;
+  }
   Config c = lib->compact ? make_config<1, 4, fps::MODE_TOPK, true, true>(lib, 1, k)
                           : make_config<1, 4, fps::MODE_TOPK, true, false>(lib, 1, k);
   if ((rc = ensure_state(lib, 1))) return rc;

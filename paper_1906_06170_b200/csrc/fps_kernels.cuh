@@ -1331,6 +1331,29 @@ __global__ void gen_kernel(const GenArgs a) {
   }
 }
 
+// Min-over-queries merge of Q per-query top-k lists (batch_search on the
+// batched kernel): every listed entry becomes (index << 8 | distance) so one
+// sort groups an entry's appearances with its smallest distance first.
+__global__ void minq_flip(const u64* __restrict__ keys, const u32* __restrict__ cnt, u32 Q, u32 k,
+                          u64* __restrict__ out) {
+  const u64 n = (u64)Q * k;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u32 q = (u32)(i / k), r = (u32)(i % k);
+    const u64 key = keys[i];
+    out[i] = r < cnt[q] ? (((key & IDX_MASK) << 8) | key_d(key)) : ~0ull;
+  }
+}
+// After that sort: keep each entry's first (minimum-distance) appearance as a
+// (distance << 40 | index) key, everything else ~0; *firsts counts the kept.
+__global__ void minq_first(const u64* __restrict__ sorted, u64 n, u64* __restrict__ out, u32* firsts) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u64 x = sorted[i];
+    const bool first = x != ~0ull && (i == 0 || (sorted[i - 1] >> 8) != (x >> 8));
+    out[i] = first ? make_key((u32)(x & 0xffu), x >> 8) : ~0ull;
+    if (first) atomicAdd(firsts, 1u);
+  }
+}
+
 // Truncate sorted range output to the first k per query (large-k path).
 __global__ void truncate_kernel(const u64* sorted, const u64* seg_off, u32 Q, u32 k, u64* out_keys, u32* out_cnt) {
   const u32 q = blockIdx.x;

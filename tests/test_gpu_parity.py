@@ -426,3 +426,25 @@ def test_bitslice_tails_and_query_groups(n):
     assert lib.last_kernel == "bit-sliced multi-query scan"
     r = lib.range_search(q[:40], 12)
     assert np.array_equal(r.rows(), orc.c_range(w, q[:40], 12))
+
+
+@pytest.mark.parametrize("popc", [False, True])
+@pytest.mark.parametrize("Q", [2, 5, 40])
+def test_batch_min_on_the_batched_kernel(Q, popc, monkeypatch):
+    """batch_search (min over queries, one top-k; scan.py:306-318): per-query
+    top-k on the bit-sliced kernel + the on-device min merge, or the
+    single-pass POPC min kernel (FPS_BITSLICE=0). Both equal the oracle,
+    including entries that several queries list and distance ties."""
+    if popc:
+        monkeypatch.setenv("FPS_BITSLICE", "0")
+    seed = 515 + Q
+    thr = synth.beta_thresholds(seed)
+    w = orc.generate_words(synth.seed_key(seed), thr, 0, 150_000)
+    rng = np.random.default_rng(Q)
+    src = rng.integers(0, len(w), Q)
+    src[1] = src[0]  # two queries near the same entry: shared hits
+    q = w[src].copy()
+    q[:, 0] ^= rng.integers(0, 2**12, Q).astype(np.uint64) << np.uint64(1)
+    lib = Library.from_words(w)
+    for k in (1, 10, 100, 1000):
+        assert lib.search_min(q, k) == orc.batch_min_topk(w, q, k), (Q, k)
