@@ -138,6 +138,15 @@ class ClockSampler(threading.Thread):
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def plane_scan_planes(q) -> int:
+    """Planes the single-query plane scan reads (fps_planeq.cuh): the 8
+    popcount planes + the query's set keys (or zero keys when |q| > 83)."""
+    w = [int(x) for x in q]
+    pop = sum(bin(x).count("1") for x in w)
+    pop166 = bin(w[0]).count("1") + bin(w[1]).count("1") + bin(w[2] & ((1 << 38) - 1)).count("1")
+    return 8 + (166 - pop166 if pop > 83 else pop166)
+
+
 def roofline_model(workload: str) -> dict:
     """Per-kernel instruction-mix constants measured once with ncu (profiles/roofline_model.json)."""
     p = ROOT / "profiles" / "roofline_model.json"
@@ -297,14 +306,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     stream = torch.cuda.current_stream(dev).cuda_stream
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 << 20) or (126 << 20)
-    lib_bytes = lib.layout()[1] * count
-    # A library larger than L2 is its own flush: the single-query scan streams
-    # it with an L2 evict-first policy, so K steps run back to back between one
-    # event pair (no reuse across steps). Smaller libraries get an explicit
-    # flush between steps, outside per-step events.
-    flush = (not args.no_flush) and lib_bytes <= l2
-    flush_buf = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev) if flush else None
-    clean_buf = torch.ones(max(2 * l2, 256 << 20) // 8, dtype=torch.int64, device=dev) if flush else None
+    flush_buf = clean_buf = None
 
     def flush_l2():
         # write a buffer larger than L2 (evicts the library), then read another
@@ -350,6 +352,23 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # Library bytes one step reads: the whole tiled library, or for the
+    # single-query plane scan only the planes of the query (8 popcount planes +
+    # min(|q|, 166 - |q|) key planes, 1 bit per entry each).
+    kernel = lib.last_kernel
+    compact, bpe = lib.layout()
+    if kernel == "single-query plane scan":
+        bytes_per_launch = float(count) * plane_scan_planes(queries[0]) / 8.0
+    else:
+        bytes_per_launch = float(bpe) * count
+    # Bytes read per step larger than L2 are their own flush: the scans stream
+    # with an L2 evict-first policy, so K steps run back to back between one
+    # event pair. Smaller ones (C1; C2 on the plane scan) get an explicit flush
+    # between steps, outside per-step events.
+    flush = (not args.no_flush) and bytes_per_launch <= l2
+    if flush:
+        flush_buf = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+        clean_buf = torch.ones(max(2 * l2, 256 << 20) // 8, dtype=torch.int64, device=dev)
     launches0 = lib.launches
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -440,11 +459,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
 
     # roofline of the scan kernel
     peaks = measured_peaks()
-    compact, bpe = lib.layout()
-    kernel = lib.last_kernel
     if plan.radius is None and Q <= 4:
-        bound = "hbm"
-        bytes_per_launch = float(bpe) * count
         achieved = bytes_per_launch / (scan_avg_ms / 1e3) / 1e9
         peak = float(peaks.get("hbm_gbs", 6650.0))
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -488,7 +503,11 @@ def run_ours(args, rank: int, local_rank: int, world: int):
                          "lines are left)" if flush else
                    "library larger than L2 and streamed with an L2 evict-first policy: no flush, the K steps "
                    "run back to back between one event pair",
-                   "layout": (f"tiles of 128 entries, SoA inside a tile, {bpe} B/entry "
+                   "layout": (f"plane-major bit planes (1 bit/entry/plane); the query reads "
+                              f"{plane_scan_planes(queries[0])} of 174 planes = "
+                              f"{plane_scan_planes(queries[0]) / 8:.3f} B/entry"
+                              if kernel == "single-query plane scan" else
+                              f"tiles of 128 entries, SoA inside a tile, {bpe} B/entry "
                               f"({'compact: word 2 as u32 + u8' if compact else 'full: 3 x u64'})")},
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

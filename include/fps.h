@@ -182,7 +182,8 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
                     uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream);
 /* Kernel family of the last scan on this handle (reporting / tests):
  * 1 single-query HBM scan, 2 multi-query POPC scan, 3 bit-sliced multi-query
- * scan, 4 large-k (histogram + range + sort) path. */
+ * scan, 4 large-k (histogram + range + sort) path, 5 single-query plane scan
+ * (reads only the bit planes the query needs). */
 int fps_last_kernel(const fps_lib* lib);
 /* Number of kernels launched by this handle so far (evidence counter). */
 uint64_t fps_launch_count(const fps_lib* lib);

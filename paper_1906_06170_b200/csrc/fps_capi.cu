@@ -22,6 +22,7 @@
 #include "../../include/fps.h"
 #include "fps_bitslice.cuh"
 #include "fps_kernels.cuh"
+#include "fps_planeq.cuh"
 
 using fps::u32;
 using fps::u64;
@@ -144,6 +145,10 @@ struct fps_lib {
   DevBuf bs, bsq;
   DevBuf mq;  // min-over-queries merge scratch (fps_topk_min on the batched kernel)
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
+  // plane-major copy for the single-query plane scan (built on first use)
+  DevBuf pm;
+  int pm_state = 0;  // as bs_state
+  u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
   u64 range_pending = 0;  // sorted range keys left on the device by fps_range_begin
@@ -634,8 +639,152 @@ int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u
   return FPS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// single-query plane scan (fps_planeq.cuh)
+// ---------------------------------------------------------------------------
+// Build (once) the plane-major copy; libraries with pad bits past key 166 keep
+// the POPC scan (it counts them, like the reference).
+int pm_ensure(fps_lib* L) {
+  if (L->pm_state) return FPS_OK;
+  const u64 steps = std::max<u64>(1, (L->n + fps::PQ_STEP - 1) / fps::PQ_STEP);
+  // plane stride: whole steps, an odd number of 256 B chunks (planes read
+  // side by side do not start on the same DRAM interleave phase)
+  u64 stride_chunks = steps | 1;
+  L->pm_stride = stride_chunks * fps::PQ_WORDS;
+  int rc;
+  if ((rc = L->pm.ensure((size_t)fps::BS_PLANES * L->pm_stride * 4))) {
+    cudaGetLastError();
+    L->pm_state = -1;
+    return FPS_OK;
+  }
+  DevBuf wide;
+  if ((rc = wide.ensure(4))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L->pm.p, 0, L->pm.bytes, L->stream));
+  CUDA_TRY(cudaMemsetAsync(wide.p, 0, 4, L->stream));
+  const u64 nblocks = (L->n + 31) / 32;
+  const int grid = (int)std::min<u64>((nblocks * 32 + 255) / 256, (u64)L->sms * 32);
+  fps::pm_build_kernel<<<std::max(grid, 1), 256, 0, L->stream>>>(L->out(), L->n, L->pm.as<u32>(), L->pm_stride,
+                                                                 wide.as<u32>());
+  L->launches++;
+  LAUNCH_CHECK("pm_build_kernel");
+  u32 nwide = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, L->stream));
+  CUDA_TRY(cudaStreamSynchronize(L->stream));
+  L->pm_state = nwide ? -1 : 1;
+  if (nwide) L->pm.release();
+  return FPS_OK;
+}
+
+bool pq_wanted(fps_lib* L) {
+  const char* e = std::getenv("FPS_PLANEQ");  // "0": the POPC scan (tests cover both)
+  if ((e && std::string(e) == "0") || L->n == 0) return false;
+  if (pm_ensure(L) != FPS_OK) return false;
+  return L->pm_state == 1;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+// Stage positions of a query: 8 popcount planes + its listed planes padded to 8.
+u32 pq_positions(const u64* q) {
+  const u32 pop = (u32)(__builtin_popcountll(q[0]) + __builtin_popcountll(q[1]) + __builtin_popcountll(q[2]));
+  const u32 pop166 = (u32)(__builtin_popcountll(q[0]) + __builtin_popcountll(q[1]) +
+                           __builtin_popcountll(q[2] & ((1ull << 38) - 1)));
+  const u32 m = pop > 83 ? 166 - pop166 : pop166;
+  return 8 + (m + 7) / 8 * 8;
+}
+
+int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
+            bool prepare_only) {
+  int rc;
+  const int nwb = std::max(1, std::min(16, env_int("FPS_PQ_WARPS", 8)));
+  const int stages = std::max(1, std::min(fps::PQ_SMAX, env_int("FPS_PQ_STAGES", 2)));
+  // ring per warp: `stages` stages of a typical list (48 positions = up to
+  // 40 listed planes); wider lists fold warps in the kernel; with the query
+  // on the host the ring is sized to it exactly
+  const u32 np = h_qin ? pq_positions(h_qin) : 48;
+  // (capped by the shared memory of one CTA; at least two stages of the
+  // widest list over the whole CTA)
+  const u32 ring_cap = (u32)((fps::pq_smem(nwb, 0) > 0 ? (200u * 1024 - (u32)fps::pq_smem(nwb, 0)) : 0) / nwb) / 256 * 256;
+  u32 ring = std::min<u32>((u32)stages * np * fps::PQ_CHUNK, ring_cap);
+  ring = std::max<u32>(ring, (u32)((2 * fps::PQ_NPMAX * fps::PQ_CHUNK + nwb - 1) / nwb + 255) / 256 * 256);
+  const size_t smem = fps::pq_smem(nwb, ring);
+  if (smem > 226 * 1024) return fail(FPS_EINVAL, "plane scan: shared memory ring too large (FPS_PQ_WARPS/STAGES)");
+  const u64 steps = (L->n + fps::PQ_STEP - 1) / fps::PQ_STEP;
+  const u64 grid = std::max<u64>(1, std::min<u64>((u64)L->sms, steps));
+  const u64 warps = grid * nwb;
+  const u32 cap = (std::max<u32>(2 * k, k + fps::PQ_STEP) + 31) / 32 * 32;
+  const u64 cand_cap = warps * (u64)k;
+  if ((rc = ensure_state(L, 1))) return rc;
+  if ((rc = L->buf.ensure(warps * (size_t)cap * 8))) return rc;
+  if ((rc = L->cand.ensure(cand_cap * 8))) return rc;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {  // (the kernel's static shared memory comes on top)
+    CUDA_TRY(cudaFuncSetAttribute(fps::pq_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  if (prepare_only) return FPS_OK;
+  fps::PqArgs a{};
+  a.pm = L->pm.as<u32>();
+  a.pstride = L->pm_stride;
+  a.n = L->n;
+  a.index_base = L->index_base;
+  a.queries = h_qin ? nullptr : d_q;
+  if (h_qin) { a.qin[0] = h_qin[0]; a.qin[1] = h_qin[1]; a.qin[2] = h_qin[2]; }
+  a.k = k;
+  a.cap = cap;
+  a.n_steps = steps;
+  a.ring_bytes = ring;
+  a.pub_every = (u32)std::max<u64>(1, warps / 512);
+  a.flags = scan_flags();
+  a.tg = L->tg.as<u32>();
+  a.ghist = L->ghist.as<u32>();
+  a.gstride = ghist_stride(1);
+  a.tg_rep = tg_replicas(1);
+  a.buf = L->buf.as<u64>();
+  a.cand = L->cand.as<u64>();
+  a.cand_cnt = L->cand_cnt.as<u32>();
+  a.cand_cap = cand_cap;
+  L->last_kernel = 5;
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(nwb * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (ev || (a.flags & 128)) ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, fps::pq_scan_kernel, a));
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  LAUNCH_CHECK("pq_scan_kernel");
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  static bool sel_attr = false;
+  if (!sel_attr) {
+    cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    sel_attr = true;
+  }
+  CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, s, a.cand, a.cand_cnt, cand_cap, a.tg, a.ghist,
+                         a.gstride, a.tg_rep, k, d_keys, d_cnt, !(a.flags & 32)));
+  L->launches++;
+  LAUNCH_CHECK("select_kernel (plane scan)");
+  if (std::getenv("FPS_DEBUG"))
+    std::fprintf(stderr, "[fps] plane scan: grid=%llu warps/CTA=%d ring=%u smem=%zu\n", (unsigned long long)grid, nwb,
+                 ring, smem);
+  return FPS_OK;
+}
+
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
                   bool prepare_only) {
+  if (Q == 1 && pq_wanted(L)) return topk_pq(L, d_q, nullptr, k, d_keys, d_cnt, s, prepare_only);
   if (bs_wanted(L, Q)) {
     L->last_kernel = 3;
     return L->compact ? topk_bs<true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only)
@@ -1266,6 +1415,11 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
   u32 nwide = 0;
   CUDA_TRY(cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, lib->stream));
   CUDA_TRY(cudaStreamSynchronize(lib->stream));
+  // the bit-plane copies are derived from the entries: rebuild on next use
+  lib->bs.release();
+  lib->bs_state = 0;
+  lib->pm.release();
+  lib->pm_state = 0;
   if (nwide) return fail(FPS_EINVAL, "entry sets bits 40.. of word 2; the library uses the compact layout");
   return FPS_OK;
 }
@@ -1413,7 +1567,8 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
       u64* dk = reinterpret_cast<u64*>(lib->dmap);
       u32* dc = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->dmap) + (size_t)k * 8);
       lib->last_kernel = 1;
-      rc = lib->compact ? topk_fused<1, 4, true>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries))
+      rc = pq_wanted(lib) ? topk_pq(lib, nullptr, reinterpret_cast<const u64*>(queries), k, dk, dc, lib->stream, false)
+         : lib->compact ? topk_fused<1, 4, true>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries))
                         : topk_fused<1, 4, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
       if (rc) { reset_state(lib); return rc; }
       cudaError_t e = wait_stream(lib->stream);

@@ -210,14 +210,17 @@ struct ScanArgs {
 // the cumulative count up to T reaches k, no entry with d > T can be in the
 // top-k and tg[q] = min(tg[q], T) is exact. Reads of ghist see monotone
 // counters, so any snapshot is a valid lower count.
-__device__ __forceinline__ u32* gbin(const ScanArgs& a, u32 qi, u32 b) {
+template <class A>
+__device__ __forceinline__ u32* gbin(const A& a, u32 qi, u32 b) {
   return a.ghist + ((u64)qi * HB + b) * a.gstride;
 }
-__device__ __forceinline__ u32* tgrep(const ScanArgs& a, u32 qi, u32 r) {
+template <class A>
+__device__ __forceinline__ u32* tgrep(const A& a, u32 qi, u32 r) {
   return a.tg + ((u64)qi * a.tg_rep + r) * a.gstride;
 }
 
-__device__ __forceinline__ u32 tighten_tg(const ScanArgs& a, u32 qi, int lane) {
+template <class A>
+__device__ __forceinline__ u32 tighten_tg(const A& a, u32 qi, int lane) {
   u32 hv[7], s = 0;
 #pragma unroll
   for (int i = 0; i < 7; ++i) { hv[i] = *(volatile const u32*)gbin(a, qi, lane * 7 + i); s += hv[i]; }

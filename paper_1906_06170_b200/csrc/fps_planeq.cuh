@@ -1,0 +1,474 @@
+// fps_planeq.cuh — single-query scan that reads only the bit planes the query
+// needs (configs 1-3, the HBM-bound path).
+//
+// The distance contract is the reference's (scan.py:137-143): d = sum over the
+// three words of popcount(entry XOR query). With the library stored as bit
+// planes (plane p of a 32-entry block = one u32 whose bit e is key p+1 of
+// entry e; planes 166..173 = the entry's popcount |a|, bit by bit):
+//   d = |a| + |q| - 2 |a AND q|          (c counted over the query's set keys)
+//   d = |q| - |a| + 2 |a AND NOT q|      (dense queries, |q| > 83: zero keys)
+// so one query needs only its m = min(|q|, 166 - |q|) listed planes plus the
+// 8 popcount planes: (8 + m) / 8 bytes per entry instead of 21-24 B for the
+// whole fingerprint. MACCS-like queries (|q| ~ 38 keys) read 5.75 B/entry —
+// the HBM stream, which bounds the single-query scan, shrinks ~3.7x.
+//
+// Layout (plane-major): plane p occupies pstride u32 words from pm + p *
+// pstride; word w is 32-entry block w. A warp step covers 2,048 entries (64
+// words = 256 B of every listed plane; a lane owns two consecutive blocks and
+// reads both with one 64-bit shared load, as in fps_bitslice.cuh).
+//
+// Per warp, a ring of S stages in shared memory is filled by the bulk-copy
+// engine: for a stage, lane l issues the 256 B cp.async.bulk copies of stage
+// positions l, l+32, l+64 (position 0..7 = popcount planes, 8.. = the query's
+// list), all completing on the stage's mbarrier. The count c runs through the
+// carry-save adder tree of the multi-query kernel; the pass mask is the sign
+// plane of X + (|q| - T) with X = |a| - 2c (or 2c - |a|).
+//
+// Selection is the single-query POPC scan's (fps_kernels.cuh): per-warp
+// ordered candidate buffer with its distance histogram and the exact tie
+// rule, sampled warps publishing witnesses into ghist, the global bound tg,
+// survivors d <= tg to the flat list, then select_kernel. A warp's first step
+// has no bound yet: instead of buffering all 2,048 entries it binary-searches
+// (bit-sliced counts, no per-entry work) the smallest T with k entries d < T
+// in that step and buffers exactly those — its own k-th distance is then
+// T - 1, which is what the tie rule needs.
+#pragma once
+#include "fps_bitslice.cuh"
+
+namespace fps {
+
+constexpr int PQ_STEP = 2048;                   // entries per warp step
+constexpr int PQ_WORDS = PQ_STEP / 32;          // u32 words of one plane per step
+constexpr u32 PQ_CHUNK = PQ_WORDS * 4;          // 256 B per plane per step
+constexpr int PQ_NPMAX = 8 + BS_LIST;           // stage positions: popcount planes + padded list
+constexpr int PQ_SMAX = 4;                      // ring stages per warp (at most)
+constexpr u64 PQ_NONE = ~0ull;
+
+// Plane-major copy of the library: one warp per 32-entry block, plane p =
+// ballot of key p+1; lane (p mod 32) stores it. Libraries with bits past key
+// 166 (FPS1 pad bytes) are flagged in *wide and keep the POPC scan.
+__global__ void pm_build_kernel(PlanesOut lib, u64 n, u32* __restrict__ pm, u64 pstride, u32* wide) {
+  const int lane = threadIdx.x & 31;
+  const u64 nblocks = (n + 31) / 32;
+  for (u64 blk = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; blk < nblocks;
+       blk += ((u64)gridDim.x * blockDim.x) >> 5) {
+    const u64 i = blk * 32 + lane;
+    u64 w[3] = {0, 0, 0};
+    if (i < n) lib.get(i, w[0], w[1], w[2]);
+    if (w[2] >> 38) atomicAdd(wide, 1u);
+    u32 mine[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < 166; ++p) {
+      const u32 m = __ballot_sync(FULL, (u32)(w[p >> 6] >> (p & 63)) & 1u);
+      if ((p & 31) == lane) mine[p >> 5] = m;
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const int p = c * 32 + lane;
+      if (p < 166) pm[(u64)p * pstride + blk] = mine[c];
+    }
+    const u32 pc = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2] & ((1ull << 38) - 1)));
+    u32 pcm = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const u32 m = __ballot_sync(FULL, (pc >> b) & 1u);
+      if (lane == b) pcm = m;
+    }
+    if (lane < 8) pm[(u64)(166 + lane) * pstride + blk] = pcm;
+  }
+}
+
+struct PqArgs {
+  const u32* pm;        // plane-major planes (174 x pstride words)
+  u64 pstride;          // words per plane (>= 64 * n_steps; padding words are zero)
+  u64 n;                // valid entries
+  u64 index_base;
+  const u64* queries;   // the query (3 words) on the device; nullptr: inline in qin
+  u64 qin[3];
+  u32 k, cap;           // top-k, per-warp buffer capacity (>= k + PQ_STEP)
+  u64 n_steps;          // ceil(n / PQ_STEP)
+  u32 ring_bytes;       // shared-memory ring per warp (before warps are folded, see below)
+  u32 pub_every;        // warps with g % pub_every == 0 publish witnesses
+  u32 flags;            // FPS_SCAN_FLAGS: 1 = no publishing, 2 = no tg refresh
+  u32* tg;
+  u32* ghist;
+  u32 gstride, tg_rep;
+  u64* buf;             // [warps][cap]
+  u64* cand;            // [cand_cap] survivors of the query
+  u32* cand_cnt;
+  u64 cand_cap;
+};
+
+// Dynamic shared memory: [warps][ring_bytes] ring | [warps][PQ_SMAX] mbarriers
+// | [warps][PQ_SMAX] slot steps | [warps][HB] histograms | [warps] WarpState.
+__host__ __device__ inline size_t pq_smem(int nwb, u32 ring_bytes) {
+  return (size_t)nwb * ring_bytes + (size_t)nwb * PQ_SMAX * 16 + (size_t)nwb * HB * 4 +
+         (size_t)nwb * sizeof(WarpState<1>);
+}
+
+__global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
+  extern __shared__ __align__(128) unsigned char pqs[];
+  // the select kernel may launch now; it waits for this grid before reading
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  __shared__ u32 s_list[PQ_NPMAX];  // source plane of each stage position (BS_ZERO: zero padding)
+  __shared__ u32 s_np, s_nc, s_pop, s_dense, s_next;
+
+  // ---- the query's plane list (read-only inputs: safe before the dependency wait)
+  if (wib == 0) {
+    const u64 q0 = a.queries ? a.queries[0] : a.qin[0];
+    const u64 q1 = a.queries ? a.queries[1] : a.qin[1];
+    const u64 q2 = a.queries ? a.queries[2] : a.qin[2];
+    // |q| over all 192 bits (pad bits of a query count once each; the
+    // library's are zero on this path), as the POPC distance does
+    const u32 pop = (u32)(__popcll(q0) + __popcll(q1) + __popcll(q2));
+    const u32 dense = pop > 83 ? 1u : 0u;
+    u32 base = 0;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const int p = c * 32 + lane;
+      const u64 wv = c < 2 ? q0 : (c < 4 ? q1 : q2);
+      const u32 bit = (u32)(wv >> (p & 63)) & 1u;
+      const bool sel = p < 166 && bit != dense;
+      const u32 bal = __ballot_sync(FULL, sel);
+      if (sel) s_list[8 + base + __popc(bal & lanemask_lt())] = (u32)p;
+      base += __popc(bal);
+    }
+    const u32 mpad = (base + 7) & ~7u;
+    if (lane < 8) s_list[lane] = 166 + lane;
+    for (u32 i = 8 + base + lane; i < 8 + mpad; i += 32) s_list[i] = BS_ZERO;
+    if (lane == 0) {
+      s_np = 8 + mpad;
+      s_nc = 8 + base;
+      s_pop = pop;
+      s_dense = dense;
+      s_next = 0;
+    }
+  }
+  __syncthreads();  // the only block-level barrier
+  const u32 np = s_np, nc = s_nc, pop = s_pop;
+  const bool dense = s_dense != 0;
+  const u32 stage_bytes = np * PQ_CHUNK;
+  // Fold warps until every active warp has >= 2 stages (wide lists on a ring
+  // sized for typical ones): warp wib < nact owns `fold` consecutive rings.
+  u32 fold = 1;
+  while (fold < (u32)nwb && (a.ring_bytes * fold) / stage_bytes < 2) fold <<= 1;
+  const u32 nact = (u32)nwb / fold;
+  if ((u32)wib >= nact) return;
+  const u32 rbytes = a.ring_bytes * fold;
+  const u32 S = min((u32)PQ_SMAX, rbytes / stage_bytes);
+
+  char* ring = reinterpret_cast<char*>(pqs) + (size_t)wib * rbytes;
+  u64* bars = reinterpret_cast<u64*>(pqs + (size_t)nwb * a.ring_bytes) + wib * PQ_SMAX;
+  u64* slot_step = reinterpret_cast<u64*>(pqs + (size_t)nwb * a.ring_bytes) + nwb * PQ_SMAX + wib * PQ_SMAX;
+  u32* hist = reinterpret_cast<u32*>(reinterpret_cast<u64*>(pqs + (size_t)nwb * a.ring_bytes) + 2 * nwb * PQ_SMAX) +
+              wib * HB;
+  WarpState<1>* ws = reinterpret_cast<WarpState<1>*>(
+                         reinterpret_cast<u32*>(reinterpret_cast<u64*>(pqs + (size_t)nwb * a.ring_bytes) +
+                                                2 * nwb * PQ_SMAX) + nwb * HB) + wib;
+  const u64 g = (u64)blockIdx.x * nact + wib;  // global warp id (buffers, publishing)
+
+  // zero padding positions of every slot (never written by the copies)
+  for (u32 st = 0; st < S; ++st) {
+    u32* sp = reinterpret_cast<u32*>(ring + st * stage_bytes);
+    for (u32 i = nc * PQ_WORDS + lane; i < np * PQ_WORDS; i += 32) sp[i] = 0;
+  }
+  const u32* src[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const u32 pos = lane + 32 * r;
+    src[r] = pos < nc ? a.pm + (u64)s_list[pos] * a.pstride : nullptr;
+  }
+  for (int i = lane; i < HB; i += 32) hist[i] = 0;
+  if (lane == 0) {
+    ws->town[0] = T_OPEN;
+    ws->pubd[0] = 0;
+    ws->cnt[0] = 0;
+    for (u32 st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // CTA-dynamic schedule: the CTA owns a contiguous run of steps; its warps
+  // claim them one at a time (each warp sees ascending steps: the ordered
+  // buffers rely on it) so warps that draw more bandwidth take more.
+  const u64 cta_lo = (u64)blockIdx.x * a.n_steps / gridDim.x;
+  const u64 cta_hi = ((u64)blockIdx.x + 1) * a.n_steps / gridDim.x;
+  const u64 pol = l2_evict_first_policy();
+  auto issue = [&](u32 st) {
+    u64 t = 0;
+    if (lane == 0) {
+      t = cta_lo + atomicAdd(&s_next, 1u);
+      if (t >= cta_hi) t = PQ_NONE;
+      slot_step[st] = t;
+      if (t == PQ_NONE) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+      else mbar_expect_tx(&bars[st], nc * PQ_CHUNK);
+    }
+    t = __shfl_sync(FULL, t, 0);
+    if (t == PQ_NONE) return;
+    char* dst = ring + st * stage_bytes;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const u32 pos = lane + 32 * r;
+      if (pos < nc) bulk_g2s_stream(dst + pos * PQ_CHUNK, src[r] + t * PQ_WORDS, PQ_CHUNK, &bars[st], pol);
+    }
+  };
+  for (u32 st = 0; st < S; ++st) issue(st);
+  // ---- everything below touches the per-call state the previous select resets
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  u64* wbuf = a.buf + g * (u64)a.cap;
+  u32 T = T_OPEN;  // accept d < T
+  u32 tgp = (a.flags & 2) ? T_OPEN : *(volatile const u32*)tgrep(a, 0, (u32)(g % a.tg_rep));
+  const bool publisher = !(a.flags & 1) && (g % a.pub_every) == 0;
+
+  auto compact = [&]() {  // ordered compaction to the k best (buffer is in index order)
+    const u32 n0 = ws->cnt[0];
+    u32 less;
+    const u32 tt = warp_kth_bin(hist, a.k, lane, &less);
+    const u32 mk = a.k - less;
+    u32 outp = 0, ties = 0;
+    for (u32 i0 = 0; i0 < n0; i0 += 32) {
+      const u32 i = i0 + lane;
+      const bool vld = i < n0;
+      const u64 key = vld ? wbuf[i] : ~0ull;
+      const u32 d = key_d(key);
+      const bool lt = vld && d < tt, tie = vld && d == tt;
+      const u32 tb = __ballot_sync(FULL, tie);
+      const bool keep = lt || (tie && ties + __popc(tb & lanemask_lt()) < mk);
+      const u32 kb = __ballot_sync(FULL, keep);
+      const u32 pp = outp + __popc(kb & lanemask_lt());
+      __syncwarp();
+      if (keep) wbuf[pp] = key;
+      outp += __popc(kb);
+      ties += __popc(tb);
+    }
+    for (u32 bb = lane; bb < HB; bb += 32) {
+      if (bb > tt) hist[bb] = 0;
+      else if (bb == tt) hist[bb] = mk;
+    }
+    if (lane == 0) ws->cnt[0] = outp;
+    __syncwarp();
+  };
+
+#pragma unroll 1
+  for (u64 j = 0;; ++j) {
+    const u32 st = (u32)(j % S);
+    mbar_wait(&bars[st], (u32)(j / S) & 1u);
+    const u64 t = *(volatile const u64*)&slot_step[st];
+    if (t == PQ_NONE) break;
+    // the bound prefetched one step ago
+    {
+      const u32 tl = (tgp < T_OPEN ? tgp : T_OPEN - 1) + 1;
+      T = tl < T ? tl : T;
+    }
+    const char* stage = ring + st * stage_bytes;
+    const char* lb = stage + 8 * lane;  // this lane's two words (8 B) of every position
+    u32 A[BS_BPL][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint2 v = *reinterpret_cast<const uint2*>(lb + i * PQ_CHUNK);
+      A[0][i] = v.x;
+      A[1][i] = v.y;
+    }
+    const u64 blk_first = t * PQ_STEP + (u64)lane * 64;  // local index of bit 0 of this lane's first block
+    u32 valid[BS_BPL];
+#pragma unroll
+    for (int h = 0; h < BS_BPL; ++h) {
+      const u64 f = blk_first + 32 * h;
+      valid[h] = f >= a.n ? 0u : (a.n - f >= 32 ? FULL : ((1u << (a.n - f)) - 1u));
+    }
+    // carry-save count of the listed planes (positions 8 .. np-1)
+    u32 ones[BS_BPL], twos[BS_BPL], fours[BS_BPL], eights[BS_BPL], s16[BS_BPL], s32[BS_BPL], s64[BS_BPL];
+#pragma unroll
+    for (int h = 0; h < BS_BPL; ++h) ones[h] = twos[h] = fours[h] = eights[h] = s16[h] = s32[h] = s64[h] = 0;
+#define CSA(h, l, x, y)   \
+  do {                    \
+    const u32 u_ = l ^ x; \
+    h = (l & x) | (u_ & y); \
+    l = u_ ^ y;           \
+  } while (0)
+    const char* lp = lb + 8 * PQ_CHUNK;
+    auto load8 = [&](u32 c, u32 (&d)[BS_BPL][8]) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint2 v = *reinterpret_cast<const uint2*>(lp + (c + i) * PQ_CHUNK);
+        d[0][i] = v.x;
+        d[1][i] = v.y;
+      }
+    };
+    auto tree8 = [&](const u32 (&d)[BS_BPL][8], u32 (&e8)[BS_BPL]) {
+#pragma unroll
+      for (int h = 0; h < BS_BPL; ++h) {
+        u32 twosA, twosB, foursA, foursB;
+        CSA(twosA, ones[h], d[h][0], d[h][1]);
+        CSA(twosB, ones[h], d[h][2], d[h][3]);
+        CSA(foursA, twos[h], twosA, twosB);
+        CSA(twosA, ones[h], d[h][4], d[h][5]);
+        CSA(twosB, ones[h], d[h][6], d[h][7]);
+        CSA(foursB, twos[h], twosA, twosB);
+        CSA(e8[h], fours[h], foursA, foursB);
+      }
+    };
+    const u32 mlen = np - 8;
+    u32 c0 = 0;
+#pragma unroll 1
+    for (; c0 + 16 <= mlen; c0 += 16) {
+      u32 d[BS_BPL][8], e8a[BS_BPL], e8b[BS_BPL];
+      load8(c0, d);
+      tree8(d, e8a);
+      load8(c0 + 8, d);
+      tree8(d, e8b);
+#pragma unroll
+      for (int h = 0; h < BS_BPL; ++h) {
+        u32 e16;
+        CSA(e16, eights[h], e8a[h], e8b[h]);
+        const u32 c2 = s16[h] & e16;
+        s16[h] ^= e16;
+        const u32 c3 = s32[h] & c2;
+        s32[h] ^= c2;
+        s64[h] ^= c3;
+      }
+    }
+    if (c0 < mlen) {
+      u32 d[BS_BPL][8], e8[BS_BPL];
+      load8(c0, d);
+      tree8(d, e8);
+#pragma unroll
+      for (int h = 0; h < BS_BPL; ++h) {
+        const u32 c1 = eights[h] & e8[h];
+        eights[h] ^= e8[h];
+        const u32 c2 = s16[h] & c1;
+        s16[h] ^= c1;
+        const u32 c3 = s32[h] & c2;
+        s32[h] ^= c2;
+        s64[h] ^= c3;
+      }
+    }
+#undef CSA
+    // every lane is done reading this slot: refill it with the step S ahead
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(st);
+    if (!(a.flags & 2)) tgp = *(volatile const u32*)tgrep(a, 0, (u32)(g % a.tg_rep));  // applied next step
+
+    // X = P - N over 10 bits: (P, N) = (|a|, 2c) sparse, (2c, |a|) dense
+    u32 X[BS_BPL][10];
+#pragma unroll
+    for (int h = 0; h < BS_BPL; ++h) {
+      const u32 C[8] = {0, ones[h], twos[h], fours[h], eights[h], s16[h], s32[h], s64[h]};  // 2c
+      u32 cy = FULL;
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        const u32 p = i < 8 ? (dense ? C[i] : A[h][i]) : 0u;
+        const u32 nn = ~(i < 8 ? (dense ? A[h][i] : C[i]) : 0u);
+        X[h][i] = p ^ nn ^ cy;
+        cy = (p & nn) | (cy & (p ^ nn));
+      }
+    }
+    // entries with d < Tq: sign plane of X + (|q| - Tq)
+    auto pass = [&](int h, u32 Tq) -> u32 {
+      return bs_sign_after_add(X[h], (pop - Tq) & 0x3ffu) & valid[h];
+    };
+    if (T >= T_OPEN) {
+      // no bound yet (the warp's first step before any witness was
+      // published): smallest T with >= k entries d < T in this step
+      u32 nv = __popc(valid[0]) + __popc(valid[1]);
+      nv = __reduce_add_sync(FULL, nv);
+      if (nv >= a.k) {
+        u32 lo = 0, hi = 256;  // count(d < lo) < k <= count(d < hi)
+#pragma unroll 1
+        while (hi - lo > 1) {
+          const u32 mid = (lo + hi) >> 1;
+          const u32 c = __reduce_add_sync(FULL, (u32)(__popc(pass(0, mid)) + __popc(pass(1, mid))));
+          if (c >= a.k) hi = mid;
+          else lo = mid;
+        }
+        T = hi;
+      }
+    }
+    const u32 m0 = pass(0, T), m1 = pass(1, T);
+    if (!__any_sync(FULL, m0 | m1)) continue;
+
+    // ---- slow path: exact distances of the passing entries, in index order
+    const u64 mm = (u64)m0 | ((u64)m1 << 32);
+    const u32 cntl = (u32)__popcll(mm);
+    const u32 incl = warp_incl_scan(cntl, lane);
+    const u32 total = __shfl_sync(FULL, incl, 31);
+    auto dist_of_bit = [&](int e) -> u32 {
+      const int h = e >> 5, bit = e & 31;
+      u32 av = 0, cv = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av |= (((h ? A[1][i] : A[0][i]) >> bit) & 1u) << i;
+      const u32 cb[7] = {h ? ones[1] : ones[0], h ? twos[1] : twos[0], h ? fours[1] : fours[0],
+                         h ? eights[1] : eights[0], h ? s16[1] : s16[0], h ? s32[1] : s32[0],
+                         h ? s64[1] : s64[0]};
+#pragma unroll
+      for (int i = 0; i < 7; ++i) cv |= ((cb[i] >> bit) & 1u) << i;
+      return dense ? pop - av + 2 * cv : av + pop - 2 * cv;
+    };
+    if (ws->cnt[0] + total > a.cap) compact();
+    const u32 cnt0 = ws->cnt[0];
+    u32 pos = cnt0 + incl - cntl;
+    for (u64 rest = mm; rest; rest &= rest - 1) {
+      const int e = __ffsll((long long)rest) - 1;
+      const u32 d = dist_of_bit(e);
+      wbuf[pos++] = make_key(d, a.index_base + blk_first + e);
+      atomicAdd(hist + d, 1u);
+    }
+    __syncwarp();
+    if (lane == 0) ws->cnt[0] = cnt0 + total;
+    __syncwarp();
+    if (cnt0 + total < a.k) continue;
+    u32 less;
+    const u32 town = warp_kth_bin(hist, a.k, lane, &less);
+    if (lane == 0) ws->town[0] = town;
+    u32 nt = town;
+    if (publisher) {
+      if (!ws->pubd[0]) {
+        // first publication: every buffered candidate with d <= town
+        for (u32 b = lane; b <= town && b < HB; b += 32) {
+          const u32 cb = hist[b];
+          if (cb) atomicAdd(gbin(a, 0, b), cb);
+        }
+      } else {
+        // later: the entries just inserted with d <= town
+        for (u64 rest = mm; rest; rest &= rest - 1) {
+          const u32 d = dist_of_bit(__ffsll((long long)rest) - 1);
+          if (d <= town) atomicAdd(gbin(a, 0, d), 1u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ws->pubd[0] = 1;
+      __syncwarp();
+      const u32 tt = tighten_tg(a, 0, lane);
+      const u32 lim = (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
+      nt = town < lim ? town : lim;
+    }
+    T = nt < T ? nt : T;
+    __syncwarp();
+  }
+
+  // ---- survivors (d <= the last prefetched bound) to the flat list
+  const u32 tb = tgp;
+  u32 c = 0;
+  for (u32 b = lane; b < (u32)HB; b += 32) c += b <= tb ? hist[b] : 0u;
+  c = __reduce_add_sync(FULL, c);
+  if (c == 0) return;
+  if (c > a.k) compact();
+  const u32 n0 = ws->cnt[0];
+  for (u32 i0 = 0; i0 < n0; i0 += 32) {
+    const u32 i = i0 + lane;
+    const u64 key = i < n0 ? wbuf[i] : ~0ull;
+    const bool keep = i < n0 && key_d(key) <= tb;
+    const u32 kb = __ballot_sync(FULL, keep);
+    const u32 nk = __popc(kb);
+    if (nk == 0) continue;
+    u32 base = 0;
+    if (lane == 0) base = atomicAdd(a.cand_cnt, nk);
+    base = __shfl_sync(FULL, base, 0);
+    if (keep) a.cand[base + __popc(kb & lanemask_lt())] = key;
+  }
+}
+
+}  // namespace fps

@@ -448,3 +448,92 @@ def test_batch_min_on_the_batched_kernel(Q, popc, monkeypatch):
     lib = Library.from_words(w)
     for k in (1, 10, 100, 1000):
         assert lib.search_min(q, k) == orc.batch_min_topk(w, q, k), (Q, k)
+
+
+# ---------------------------------------------------------------- single-query plane scan
+def _dev_topk(lib, q, k):
+    """fps_topk_async with the query on the device (the plane count is not known to the host)."""
+    import torch
+
+    dq = torch.from_numpy(np.ascontiguousarray(q[:1]).view(np.int64).copy()).cuda()
+    keys = torch.empty((1, k), dtype=torch.int64, device="cuda")
+    cnt = torch.empty((1,), dtype=torch.int32, device="cuda")
+    lib.topk_prepare(1, k)
+    lib.topk_async(dq, 1, k, keys, cnt, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return keys_to_hits(keys.cpu().numpy().view(np.uint64), cnt.cpu().numpy()).hits(0)
+
+
+def _query_with_pop(rng, pop):
+    bits = rng.choice(np.arange(1, 166), size=pop, replace=False)  # key 1 (bit 0) stays clear
+    q = np.zeros(3, dtype=np.uint64)
+    for b in bits:
+        q[b // 64] |= np.uint64(1) << np.uint64(b % 64)
+    return q
+
+
+@pytest.mark.parametrize("n", [1, 31, 2047, 2048, 2049, 4097, 100_003])
+def test_plane_scan_sizes_and_query_densities(n, monkeypatch):
+    """Q = 1 reads only the query's planes (|q| <= 83: set keys, else zero
+    keys): both host (query inline) and device query paths, list lengths on
+    both sides of the 8-plane padding and of the dense switch, against the
+    oracle and the POPC scan (FPS_PLANEQ=0)."""
+    seed = 9000 + n
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(n)
+    for pop in (0, 1, 8, 9, 38, 83, 84, 120, 165):
+        q = _query_with_pop(rng, pop)
+        for k in (1, 10, 100):
+            exp = oracle_topk(w, q[None], k)[0]
+            assert lib.search(q, k) == exp, (n, pop, k)
+            assert lib.last_kernel == "single-query plane scan"
+            assert _dev_topk(lib, q[None], k) == exp, (n, pop, k)
+    monkeypatch.setenv("FPS_PLANEQ", "0")
+    q = _query_with_pop(rng, 40)
+    assert lib.search(q, 10) == oracle_topk(w, q[None], 10)[0]
+    assert lib.last_kernel == "single-query HBM scan"
+
+
+@pytest.mark.parametrize("warps,stages", [(1, 1), (4, 2), (8, 1), (8, 4), (16, 2)])
+def test_plane_scan_ring_shapes(warps, stages, monkeypatch):
+    """Warps per CTA x ring stages (wide lists fold warps to keep >= 2 stages)."""
+    monkeypatch.setenv("FPS_PQ_WARPS", str(warps))
+    monkeypatch.setenv("FPS_PQ_STAGES", str(stages))
+    seed = 77
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, 300_001)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(warps * 10 + stages)
+    for pop in (20, 60, 83, 100):
+        q = _query_with_pop(rng, pop)
+        for k in (10, 1024):
+            exp = oracle_topk(w, q[None], k)[0]
+            assert lib.search(q, k) == exp, (warps, stages, pop, k)
+            assert _dev_topk(lib, q[None], k) == exp, (warps, stages, pop, k)
+
+
+def test_plane_copy_follows_entry_writes():
+    """The plane copies are derived from the entries: a write invalidates them."""
+    seed = 31
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, 50_000)
+    lib = Library.from_words(w)
+    q = w[123].copy()
+    assert lib.search(q, 3) == oracle_topk(w, q[None], 3)[0]
+    qq = np.stack([q, w[7]])
+    lib.search_batch(qq, 3)  # builds the bit-slice tiles too
+    lib.write_entries(np.array([40_000], dtype=np.uint64), q[None])
+    w[40_000] = q
+    assert lib.search(q, 3) == oracle_topk(w, q[None], 3)[0]
+    res = lib.search_batch(qq, 3)
+    exp = oracle_topk(w, qq, 3)
+    assert [res.hits(0), res.hits(1)] == exp
+    assert (40_000, 0) in res.hits(0)
+
+
+def test_plane_scan_not_used_with_pad_bits():
+    rec = np.zeros((3000, 4), dtype=np.uint64)
+    rec[:, 0] = np.arange(1, 3001)
+    rec[5, 3] = np.uint64(1) << np.uint64(45)
+    lib = Library.from_records(rec)
+    assert lib.search(np.zeros(3, dtype=np.uint64), 3000)[-1] == (5, 1)
+    assert lib.last_kernel == "single-query HBM scan"
