@@ -647,11 +647,11 @@ int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u
 // the POPC scan (it counts them, like the reference).
 int pm_ensure(fps_lib* L) {
   if (L->pm_state) return FPS_OK;
-  const u64 steps = std::max<u64>(1, (L->n + fps::PQ_STEP - 1) / fps::PQ_STEP);
+  const u64 steps = std::max<u64>(1, (L->n + 32 * fps::PQ_STRIDE_WORDS - 1) / (32 * fps::PQ_STRIDE_WORDS));
   // plane stride: whole steps, an odd number of 256 B chunks (planes read
   // side by side do not start on the same DRAM interleave phase)
   u64 stride_chunks = steps | 1;
-  L->pm_stride = stride_chunks * fps::PQ_WORDS;
+  L->pm_stride = stride_chunks * fps::PQ_STRIDE_WORDS;
   int rc;
   if ((rc = L->pm.ensure((size_t)fps::BS_PLANES * L->pm_stride * 4))) {
     cudaGetLastError();
@@ -700,7 +700,14 @@ u32 pq_positions(const u64* q) {
 int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
             bool prepare_only) {
   int rc;
-  const int nwb = std::max(1, std::min(16, env_int("FPS_PQ_WARPS", 8)));
+  // Shape (tools/pq_sweep.py): long scans run 16 warps x one 32-entry block
+  // per lane (more warps consuming the ring: C3 101 vs 107 us), short ones
+  // 8 warps x two blocks per lane (C2 28.0 vs 32.2 us per call).
+  const bool long_scan = L->n >= (32u << 20);
+  const int bpl = env_int("FPS_PQ_BPL", long_scan ? 1 : 2) == 1 ? 1 : 2;  // 32-entry blocks per lane
+  const u32 chunk = bpl == 1 ? fps::PqStep<1>::CHUNK : fps::PqStep<2>::CHUNK;
+  const u64 step_entries = bpl == 1 ? fps::PqStep<1>::ENTRIES : fps::PqStep<2>::ENTRIES;
+  const int nwb = std::max(1, std::min(16, env_int("FPS_PQ_WARPS", long_scan ? 16 : 8)));
   const int stages = std::max(1, std::min(fps::PQ_SMAX, env_int("FPS_PQ_STAGES", 2)));
   // ring per warp: `stages` stages of a typical list (48 positions = up to
   // 40 listed planes); wider lists fold warps in the kernel; with the query
@@ -708,23 +715,29 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   const u32 np = h_qin ? pq_positions(h_qin) : 48;
   // (capped by the shared memory of one CTA; at least two stages of the
   // widest list over the whole CTA)
-  const u32 ring_cap = (u32)((fps::pq_smem(nwb, 0) > 0 ? (200u * 1024 - (u32)fps::pq_smem(nwb, 0)) : 0) / nwb) / 256 * 256;
-  u32 ring = std::min<u32>((u32)stages * np * fps::PQ_CHUNK, ring_cap);
-  ring = std::max<u32>(ring, (u32)((2 * fps::PQ_NPMAX * fps::PQ_CHUNK + nwb - 1) / nwb + 255) / 256 * 256);
+  const u32 budget = (u32)env_int("FPS_PQ_SMEM_KB", 210) * 1024;
+  const u32 ring_cap = (u32)((budget - (u32)fps::pq_smem(nwb, 0)) / nwb) / 256 * 256;
+  u32 ring = std::min<u32>((u32)stages * np * chunk, ring_cap);
+  ring = std::max<u32>(ring, (u32)((2 * fps::PQ_NPMAX * chunk + nwb - 1) / nwb + 255) / 256 * 256);
   const size_t smem = fps::pq_smem(nwb, ring);
   if (smem > 226 * 1024) return fail(FPS_EINVAL, "plane scan: shared memory ring too large (FPS_PQ_WARPS/STAGES)");
-  const u64 steps = (L->n + fps::PQ_STEP - 1) / fps::PQ_STEP;
+  const u64 steps = (L->n + step_entries - 1) / step_entries;
   const u64 grid = std::max<u64>(1, std::min<u64>((u64)L->sms, steps));
   const u64 warps = grid * nwb;
-  const u32 cap = (std::max<u32>(2 * k, k + fps::PQ_STEP) + 31) / 32 * 32;
+  const u32 cap = (std::max<u32>(2 * k, k + (u32)step_entries) + 31) / 32 * 32;
   const u64 cand_cap = warps * (u64)k;
   if ((rc = ensure_state(L, 1))) return rc;
   if ((rc = L->buf.ensure(warps * (size_t)cap * 8))) return rc;
   if ((rc = L->cand.ensure(cand_cap * 8))) return rc;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {  // (the kernel's static shared memory comes on top)
-    CUDA_TRY(cudaFuncSetAttribute(fps::pq_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
+  const int copy = env_int("FPS_PQ_COPY", 1);  // 1: cp.async 16 B per lane (default, measured faster), 0: bulk copies
+  const int kv = (copy == 1 ? 1 : 0) * 2 + (bpl == 2 ? 1 : 0);
+  void (*const kerns[4])(fps::PqArgs) = {fps::pq_scan_kernel<0, 1>, fps::pq_scan_kernel<0, 2>,
+                                         fps::pq_scan_kernel<1, 1>, fps::pq_scan_kernel<1, 2>};
+  auto* kern = kerns[kv];
+  static size_t smem_set[4] = {0, 0, 0, 0};
+  if (smem > smem_set[kv]) {  // (the kernel's static shared memory comes on top)
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set[kv] = smem;
   }
   if (prepare_only) return FPS_OK;
   fps::PqArgs a{};
@@ -761,7 +774,7 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   attr[0].val.programmaticStreamSerializationAllowed = (ev || (a.flags & 128)) ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, fps::pq_scan_kernel, a));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
   if (ev) cudaEventRecord(ev->second, s);
   L->launches++;
   LAUNCH_CHECK("pq_scan_kernel");
@@ -1627,11 +1640,16 @@ extern "C" int fps_trace_read(uint64_t* marks, uint64_t* warps) {
   cudaMemcpyFromSymbol(marks, fps::g_mark, 8 * sizeof(u64));
   return (int)cudaMemcpyFromSymbol(warps, fps::g_scan_trace, sizeof(fps::g_scan_trace));
 }
+extern "C" int fps_trace_phases(uint64_t* ph) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(ph, fps::g_pq_phase, sizeof(fps::g_pq_phase));
+}
 extern "C" int fps_trace_clear() {
-  static u64 zeros[16384 * 4];
+  static u64 zeros[16384 * 8];
   cudaDeviceSynchronize();
   cudaMemcpyToSymbol(fps::g_mark, zeros, 8 * sizeof(u64));
-  return (int)cudaMemcpyToSymbol(fps::g_scan_trace, zeros, sizeof(zeros));
+  cudaMemcpyToSymbol(fps::g_pq_phase, zeros, sizeof(fps::g_pq_phase));
+  return (int)cudaMemcpyToSymbol(fps::g_scan_trace, zeros, sizeof(fps::g_scan_trace));
 }
 #endif
 

@@ -37,9 +37,14 @@
 
 namespace fps {
 
-constexpr int PQ_STEP = 2048;                   // entries per warp step
-constexpr int PQ_WORDS = PQ_STEP / 32;          // u32 words of one plane per step
-constexpr u32 PQ_CHUNK = PQ_WORDS * 4;          // 256 B per plane per step
+// A warp step covers 1,024 x BPL entries: BPL consecutive 32-entry blocks per
+// lane, i.e. 32 x BPL u32 words = 128 x BPL bytes of every listed plane.
+template <int BPL> struct PqStep {
+  static constexpr u32 WORDS = 32 * BPL;       // u32 words of one plane per step
+  static constexpr u32 CHUNK = WORDS * 4;      // bytes of one plane per step
+  static constexpr u64 ENTRIES = 32ull * WORDS;
+};
+constexpr u32 PQ_STRIDE_WORDS = 64;             // plane stride granule (whole steps at BPL <= 2)
 constexpr int PQ_NPMAX = 8 + BS_LIST;           // stage positions: popcount planes + padded list
 constexpr int PQ_SMAX = 4;                      // ring stages per warp (at most)
 constexpr u64 PQ_NONE = ~0ull;
@@ -106,13 +111,29 @@ __host__ __device__ inline size_t pq_smem(int nwb, u32 ring_bytes) {
          (size_t)nwb * sizeof(WarpState<1>);
 }
 
+// COPY 0: per-plane 256 B cp.async.bulk (TMA engine); 1: 16 B cp.async
+// (LDGSTS) per lane, two planes per warp instruction, completion through
+// cp.async.mbarrier.arrive.noinc on the same stage barriers.
+#ifdef FPS_SCAN_TRACE
+__device__ u64 g_pq_phase[16384 * 8];  // per warp, first step: CSA done, refill issued, bound, mask, inserted, published
+#endif
+template <int COPY, int BPL>
 __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
+  constexpr u32 PQ_WORDS = PqStep<BPL>::WORDS, PQ_CHUNK = PqStep<BPL>::CHUNK;
+  constexpr u64 PQ_STEP = PqStep<BPL>::ENTRIES;
+  constexpr u32 LPP = 8 * BPL;      // cp.async: lanes per position (16 B each)
+  constexpr u32 PPI = 32 / LPP;     // positions per warp instruction (512 B)
   extern __shared__ __align__(128) unsigned char pqs[];
   // the select kernel may launch now; it waits for this grid before reading
   asm volatile("griddepcontrol.launch_dependents;");
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+#ifdef FPS_SCAN_TRACE
+  u64 tr_start = gtimer(), tr_first = 0, tr_step1 = 0;
+  bool ph_done = false;
+#endif
   __shared__ u32 s_list[PQ_NPMAX];  // source plane of each stage position (BS_ZERO: zero padding)
   __shared__ u32 s_np, s_nc, s_pop, s_dense, s_next;
+  __shared__ const u32* s_base[PQ_NPMAX];  // plane base of each copied position (COPY 1)
 
   // ---- the query's plane list (read-only inputs: safe before the dependency wait)
   if (wib == 0) {
@@ -145,7 +166,10 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       s_next = 0;
     }
   }
-  __syncthreads();  // the only block-level barrier
+  __syncthreads();
+  if (COPY == 1)
+    for (u32 i = threadIdx.x; i < s_nc; i += blockDim.x) s_base[i] = a.pm + (u64)s_list[i] * a.pstride;
+  __syncthreads();  // the last block-level barrier
   const u32 np = s_np, nc = s_nc, pop = s_pop;
   const bool dense = s_dense != 0;
   const u32 stage_bytes = np * PQ_CHUNK;
@@ -184,7 +208,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     ws->town[0] = T_OPEN;
     ws->pubd[0] = 0;
     ws->cnt[0] = 0;
-    for (u32 st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+    for (u32 st = 0; st < S; ++st) mbar_init(&bars[st], COPY == 1 ? 32u : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -195,16 +219,45 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   const u64 cta_lo = (u64)blockIdx.x * a.n_steps / gridDim.x;
   const u64 cta_hi = ((u64)blockIdx.x + 1) * a.n_steps / gridDim.x;
   const u64 pol = l2_evict_first_policy();
+  const u32 half = (u32)lane / LPP;  // position within a cp.async group
   auto issue = [&](u32 st) {
     u64 t = 0;
     if (lane == 0) {
       t = cta_lo + atomicAdd(&s_next, 1u);
       if (t >= cta_hi) t = PQ_NONE;
       slot_step[st] = t;
-      if (t == PQ_NONE) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
-      else mbar_expect_tx(&bars[st], nc * PQ_CHUNK);
+      if (COPY == 0) {
+        if (t == PQ_NONE) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+        else mbar_expect_tx(&bars[st], nc * PQ_CHUNK);
+      }
     }
     t = __shfl_sync(FULL, t, 0);
+    if (COPY == 1) {
+      if (t != PQ_NONE) {
+        // one instruction moves 512 B: lanes [LPP*j, LPP*j + LPP) copy 16 B
+        // each of position PPI*i + j; source = plane base + a per-stage offset
+        u32 dst = smem_u32(ring + st * stage_bytes) + half * PQ_CHUNK + (lane % LPP) * 16;
+        const u64 off = t * PQ_CHUNK + (lane % LPP) * 16;
+        const u64* bp = reinterpret_cast<const u64*>(s_base) + half;
+        const u32 ngrp = nc / PPI;
+#pragma unroll 4
+        for (u32 i = 0; i < ngrp; ++i) {
+          const char* sp = reinterpret_cast<const char*>(bp[PPI * i]) + off;
+          asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(sp), "l"(pol)
+                       : "memory");
+          dst += PPI * PQ_CHUNK;
+        }
+        if (half < nc % PPI) {
+          const char* sp = reinterpret_cast<const char*>(bp[PPI * ngrp]) + off;
+          asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(sp), "l"(pol)
+                       : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+      }
+      return;
+    }
     if (t == PQ_NONE) return;
     char* dst = ring + st * stage_bytes;
 #pragma unroll
@@ -219,8 +272,35 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
 
   u64* wbuf = a.buf + g * (u64)a.cap;
   u32 T = T_OPEN;  // accept d < T
-  u32 tgp = (a.flags & 2) ? T_OPEN : *(volatile const u32*)tgrep(a, 0, (u32)(g % a.tg_rep));
+  const volatile u32* tgw = tgrep(a, 0, (u32)(g % a.tg_rep));  // this warp's replica of the bound
+  u32 tgp = (a.flags & 2) ? T_OPEN : *tgw;
   const bool publisher = !(a.flags & 1) && (g % a.pub_every) == 0;
+  u32 hv[7];          // published-witness histogram snapshot (deferred tighten)
+  bool tpend = false;
+  // smallest T with >= k published witnesses d <= T -> every replica of tg;
+  // returns the new filter limit (accept d < limit)
+  auto finish_tighten = [&]() -> u32 {
+    tpend = false;
+    u32 sum = 0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) sum += hv[i];
+    const u32 incl = warp_incl_scan(sum, lane);
+    const u32 bal = __ballot_sync(FULL, incl >= a.k);
+    if (!bal) return T_OPEN;
+    const int src = __ffs(bal) - 1;
+    u32 tt = 0;
+    if (lane == src) {
+      u32 cc = incl - sum;
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        if (cc + hv[i] >= a.k) { tt = lane * 7 + i; break; }
+        cc += hv[i];
+      }
+    }
+    tt = __shfl_sync(FULL, tt, src);
+    for (u32 r = lane; r < a.tg_rep; r += 32) atomicMin(tgrep(a, 0, r), tt);
+    return (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
+  };
 
   auto compact = [&]() {  // ordered compaction to the k best (buffer is in index order)
     const u32 n0 = ws->cnt[0];
@@ -252,36 +332,61 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   };
 
 #pragma unroll 1
-  for (u64 j = 0;; ++j) {
-    const u32 st = (u32)(j % S);
-    mbar_wait(&bars[st], (u32)(j / S) & 1u);
+  for (u32 st = 0, ph = 0;; st = (st + 1 == S) ? 0 : st + 1, ph ^= (st == 0) ? 1u : 0u) {
+#ifdef FPS_SCAN_TRACE
+    if (tr_first && !tr_step1) tr_step1 = gtimer();  // (slot 2: end of the first step's compute)
+#endif
+    mbar_wait(&bars[st], ph);
     const u64 t = *(volatile const u64*)&slot_step[st];
     if (t == PQ_NONE) break;
+#ifdef FPS_SCAN_TRACE
+    if (!tr_first) tr_first = gtimer();
+#endif
+    if (a.flags & 512) {  // experiment: stream only (no compute; results are not valid)
+      __syncwarp();
+      issue(st);
+      continue;
+    }
+    if (tpend) {
+      const u32 lim = finish_tighten();
+      T = lim < T ? lim : T;
+    }
     // the bound prefetched one step ago
     {
       const u32 tl = (tgp < T_OPEN ? tgp : T_OPEN - 1) + 1;
       T = tl < T ? tl : T;
     }
     const char* stage = ring + st * stage_bytes;
-    const char* lb = stage + 8 * lane;  // this lane's two words (8 B) of every position
-    u32 A[BS_BPL][8];
+    const char* lb = stage + 4 * BPL * lane;  // this lane's BPL words of every position
+    // one shared load fetches a plane word of all BPL blocks of the lane
+    auto ldp = [&](const char* p, u32* d) {
+      if constexpr (BPL == 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        d[0] = v.x;
+        d[1] = v.y;
+      } else {
+        d[0] = *reinterpret_cast<const u32*>(p);
+      }
+    };
+    u32 A[BPL][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint2 v = *reinterpret_cast<const uint2*>(lb + i * PQ_CHUNK);
-      A[0][i] = v.x;
-      A[1][i] = v.y;
-    }
-    const u64 blk_first = t * PQ_STEP + (u64)lane * 64;  // local index of bit 0 of this lane's first block
-    u32 valid[BS_BPL];
+      u32 v[BPL];
+      ldp(lb + i * PQ_CHUNK, v);
 #pragma unroll
-    for (int h = 0; h < BS_BPL; ++h) {
+      for (int h = 0; h < BPL; ++h) A[h][i] = v[h];
+    }
+    const u64 blk_first = t * PQ_STEP + (u64)lane * 32 * BPL;  // local index of bit 0 of this lane's first block
+    u32 valid[BPL];
+#pragma unroll
+    for (int h = 0; h < BPL; ++h) {
       const u64 f = blk_first + 32 * h;
       valid[h] = f >= a.n ? 0u : (a.n - f >= 32 ? FULL : ((1u << (a.n - f)) - 1u));
     }
     // carry-save count of the listed planes (positions 8 .. np-1)
-    u32 ones[BS_BPL], twos[BS_BPL], fours[BS_BPL], eights[BS_BPL], s16[BS_BPL], s32[BS_BPL], s64[BS_BPL];
+    u32 ones[BPL], twos[BPL], fours[BPL], eights[BPL], s16[BPL], s32[BPL], s64[BPL];
 #pragma unroll
-    for (int h = 0; h < BS_BPL; ++h) ones[h] = twos[h] = fours[h] = eights[h] = s16[h] = s32[h] = s64[h] = 0;
+    for (int h = 0; h < BPL; ++h) ones[h] = twos[h] = fours[h] = eights[h] = s16[h] = s32[h] = s64[h] = 0;
 #define CSA(h, l, x, y)   \
   do {                    \
     const u32 u_ = l ^ x; \
@@ -289,17 +394,18 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     l = u_ ^ y;           \
   } while (0)
     const char* lp = lb + 8 * PQ_CHUNK;
-    auto load8 = [&](u32 c, u32 (&d)[BS_BPL][8]) {
+    auto load8 = [&](u32 c, u32 (&d)[BPL][8]) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const uint2 v = *reinterpret_cast<const uint2*>(lp + (c + i) * PQ_CHUNK);
-        d[0][i] = v.x;
-        d[1][i] = v.y;
+        u32 v[BPL];
+        ldp(lp + (c + i) * PQ_CHUNK, v);
+#pragma unroll
+        for (int h = 0; h < BPL; ++h) d[h][i] = v[h];
       }
     };
-    auto tree8 = [&](const u32 (&d)[BS_BPL][8], u32 (&e8)[BS_BPL]) {
+    auto tree8 = [&](const u32 (&d)[BPL][8], u32 (&e8)[BPL]) {
 #pragma unroll
-      for (int h = 0; h < BS_BPL; ++h) {
+      for (int h = 0; h < BPL; ++h) {
         u32 twosA, twosB, foursA, foursB;
         CSA(twosA, ones[h], d[h][0], d[h][1]);
         CSA(twosB, ones[h], d[h][2], d[h][3]);
@@ -314,13 +420,13 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     u32 c0 = 0;
 #pragma unroll 1
     for (; c0 + 16 <= mlen; c0 += 16) {
-      u32 d[BS_BPL][8], e8a[BS_BPL], e8b[BS_BPL];
+      u32 d[BPL][8], e8a[BPL], e8b[BPL];
       load8(c0, d);
       tree8(d, e8a);
       load8(c0 + 8, d);
       tree8(d, e8b);
 #pragma unroll
-      for (int h = 0; h < BS_BPL; ++h) {
+      for (int h = 0; h < BPL; ++h) {
         u32 e16;
         CSA(e16, eights[h], e8a[h], e8b[h]);
         const u32 c2 = s16[h] & e16;
@@ -331,11 +437,11 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       }
     }
     if (c0 < mlen) {
-      u32 d[BS_BPL][8], e8[BS_BPL];
+      u32 d[BPL][8], e8[BPL];
       load8(c0, d);
       tree8(d, e8);
 #pragma unroll
-      for (int h = 0; h < BS_BPL; ++h) {
+      for (int h = 0; h < BPL; ++h) {
         const u32 c1 = eights[h] & e8[h];
         eights[h] ^= e8[h];
         const u32 c2 = s16[h] & c1;
@@ -346,16 +452,24 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       }
     }
 #undef CSA
+
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 0] = gtimer();
+#endif
     // every lane is done reading this slot: refill it with the step S ahead
     __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (COPY == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 1] = gtimer();
+#endif
     issue(st);
-    if (!(a.flags & 2)) tgp = *(volatile const u32*)tgrep(a, 0, (u32)(g % a.tg_rep));  // applied next step
+    if (!(a.flags & 2)) tgp = *tgw;  // applied next step
 
     // X = P - N over 10 bits: (P, N) = (|a|, 2c) sparse, (2c, |a|) dense
-    u32 X[BS_BPL][10];
+    u32 X[BPL][10];
 #pragma unroll
-    for (int h = 0; h < BS_BPL; ++h) {
+    for (int h = 0; h < BPL; ++h) {
       const u32 C[8] = {0, ones[h], twos[h], fours[h], eights[h], s16[h], s32[h], s64[h]};  // 2c
       u32 cy = FULL;
 #pragma unroll
@@ -370,24 +484,37 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     auto pass = [&](int h, u32 Tq) -> u32 {
       return bs_sign_after_add(X[h], (pop - Tq) & 0x3ffu) & valid[h];
     };
+
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 2] = gtimer();
+#endif
     if (T >= T_OPEN) {
       // no bound yet (the warp's first step before any witness was
       // published): smallest T with >= k entries d < T in this step
-      u32 nv = __popc(valid[0]) + __popc(valid[1]);
+      u32 nv = 0;
+#pragma unroll
+      for (int h = 0; h < BPL; ++h) nv += __popc(valid[h]);
       nv = __reduce_add_sync(FULL, nv);
       if (nv >= a.k) {
         u32 lo = 0, hi = 256;  // count(d < lo) < k <= count(d < hi)
 #pragma unroll 1
         while (hi - lo > 1) {
           const u32 mid = (lo + hi) >> 1;
-          const u32 c = __reduce_add_sync(FULL, (u32)(__popc(pass(0, mid)) + __popc(pass(1, mid))));
+          u32 cl = 0;
+#pragma unroll
+          for (int h = 0; h < BPL; ++h) cl += __popc(pass(h, mid));
+          const u32 c = __reduce_add_sync(FULL, cl);
           if (c >= a.k) hi = mid;
           else lo = mid;
         }
         T = hi;
       }
     }
-    const u32 m0 = pass(0, T), m1 = pass(1, T);
+
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 3] = gtimer();
+#endif
+    const u32 m0 = pass(0, T), m1 = BPL == 2 ? pass(BPL - 1, T) : 0u;
     if (!__any_sync(FULL, m0 | m1)) continue;
 
     // ---- slow path: exact distances of the passing entries, in index order
@@ -396,13 +523,14 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     const u32 incl = warp_incl_scan(cntl, lane);
     const u32 total = __shfl_sync(FULL, incl, 31);
     auto dist_of_bit = [&](int e) -> u32 {
-      const int h = e >> 5, bit = e & 31;
+      const int h = BPL == 2 ? (e >> 5) : 0, bit = e & 31;
+      constexpr int H1 = BPL - 1;
       u32 av = 0, cv = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) av |= (((h ? A[1][i] : A[0][i]) >> bit) & 1u) << i;
-      const u32 cb[7] = {h ? ones[1] : ones[0], h ? twos[1] : twos[0], h ? fours[1] : fours[0],
-                         h ? eights[1] : eights[0], h ? s16[1] : s16[0], h ? s32[1] : s32[0],
-                         h ? s64[1] : s64[0]};
+      for (int i = 0; i < 8; ++i) av |= (((h ? A[H1][i] : A[0][i]) >> bit) & 1u) << i;
+      const u32 cb[7] = {h ? ones[H1] : ones[0], h ? twos[H1] : twos[0], h ? fours[H1] : fours[0],
+                         h ? eights[H1] : eights[0], h ? s16[H1] : s16[0], h ? s32[H1] : s32[0],
+                         h ? s64[H1] : s64[0]};
 #pragma unroll
       for (int i = 0; i < 7; ++i) cv |= ((cb[i] >> bit) & 1u) << i;
       return dense ? pop - av + 2 * cv : av + pop - 2 * cv;
@@ -419,6 +547,10 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     __syncwarp();
     if (lane == 0) ws->cnt[0] = cnt0 + total;
     __syncwarp();
+
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 4] = gtimer();
+#endif
     if (cnt0 + total < a.k) continue;
     u32 less;
     const u32 town = warp_kth_bin(hist, a.k, lane, &less);
@@ -441,16 +573,40 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       __syncwarp();
       if (lane == 0) ws->pubd[0] = 1;
       __syncwarp();
-      const u32 tt = tighten_tg(a, 0, lane);
-      const u32 lim = (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
-      nt = town < lim ? town : lim;
+      // tighten the global bound one step later: the histogram loads are
+      // in flight while the next stage is awaited (an L2 round trip under a
+      // saturated memory system costs microseconds)
+#pragma unroll
+      for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
+      tpend = true;
     }
     T = nt < T ? nt : T;
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 5] = gtimer();
+#endif
+#ifdef FPS_SCAN_TRACE
+    ph_done = true;
+#endif
+
     __syncwarp();
   }
 
-  // ---- survivors (d <= the last prefetched bound) to the flat list
-  const u32 tb = tgp;
+#ifdef FPS_SCAN_TRACE
+  if (lane == 0 && g < 16384) {
+    g_scan_trace[g * 4 + 0] = tr_start;
+    g_scan_trace[g * 4 + 1] = gtimer();
+    g_scan_trace[g * 4 + 3] = tr_first;
+    g_scan_trace[g * 4 + 2] = tr_step1;
+  }
+#endif
+  // ---- survivors (d <= the bound, re-read: short scans end before their
+  // first prefetch sees the witnesses published in the same step) to the flat list
+  if (tpend) finish_tighten();
+  u32 tb = tgp;
+  if (!(a.flags & 2)) {
+    const u32 tf = *tgw;
+    tb = tf < tb ? tf : tb;
+  }
   u32 c = 0;
   for (u32 b = lane; b < (u32)HB; b += 32) c += b <= tb ? hist[b] : 0u;
   c = __reduce_add_sync(FULL, c);

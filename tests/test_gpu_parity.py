@@ -495,9 +495,14 @@ def test_plane_scan_sizes_and_query_densities(n, monkeypatch):
     assert lib.last_kernel == "single-query HBM scan"
 
 
-@pytest.mark.parametrize("warps,stages", [(1, 1), (4, 2), (8, 1), (8, 4), (16, 2)])
-def test_plane_scan_ring_shapes(warps, stages, monkeypatch):
-    """Warps per CTA x ring stages (wide lists fold warps to keep >= 2 stages)."""
+@pytest.mark.parametrize("copy", [0, 1])
+@pytest.mark.parametrize("bpl,warps,stages", [(2, 1, 1), (2, 4, 2), (2, 8, 1), (2, 8, 4), (2, 16, 2), (1, 16, 2),
+                                              (1, 12, 2), (1, 3, 4)])
+def test_plane_scan_ring_shapes(bpl, warps, stages, copy, monkeypatch):
+    """Blocks per lane x warps per CTA x ring stages x copy engine (bulk copies
+    or cp.async); wide lists fold warps to keep >= 2 stages."""
+    monkeypatch.setenv("FPS_PQ_BPL", str(bpl))
+    monkeypatch.setenv("FPS_PQ_COPY", str(copy))
     monkeypatch.setenv("FPS_PQ_WARPS", str(warps))
     monkeypatch.setenv("FPS_PQ_STAGES", str(stages))
     seed = 77

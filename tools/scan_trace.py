@@ -38,6 +38,16 @@ for wl in sys.argv[1:] or ["c2"]:
         if len(fi):
             print("  first tile ", pct(fi))
         print("  loop end   ", pct(en))
-        print("  warp exit  ", pct(en2))
+        print("  warp exit / plane scan: second step start ", pct(en2[t[:, 2] > 0]) if (t[:, 2] > 0).any() else "-")
+        ph = np.zeros(16384 * 8, np.uint64)
+        if hasattr(L, "fps_trace_phases"):
+            L.fps_trace_phases(ph.ctypes.data)
+            ph = ph.reshape(-1, 8).astype(np.int64)[: len(warps) // 4]
+            okr = ph[:, 0] > 0
+            for i, name in enumerate(["csa done", "refill issued", "before bound", "mask", "inserted", "published"]):
+                v = ph[okr, i]
+                v = v[v > 0] - m0
+                if len(v):
+                    print(f"  1st step {name:14s}", pct(v))
         print("  select start %.1f  end %.1f" % ((int(marks[2]) - m0) / 1e3, (int(marks[3]) - m0) / 1e3))
     lib.close()
