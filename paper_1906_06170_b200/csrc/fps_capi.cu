@@ -700,14 +700,15 @@ u32 pq_positions(const u64* q) {
 int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
             bool prepare_only) {
   int rc;
-  // Shape (tools/pq_sweep.py): long scans run 16 warps x one 32-entry block
-  // per lane (more warps consuming the ring: C3 101 vs 107 us), short ones
-  // 8 warps x two blocks per lane (C2 28.0 vs 32.2 us per call).
+  // Shape (tools/pq_sweep.py, profiles/r01_experiments.md): 8 warps x two
+  // 32-entry blocks per lane x 2 ring stages; long scans read the global
+  // bound every 8th step (C3 109.5 -> 95.5 us), short ones every step (the
+  // first steps set it: C2 29.1 vs 33.5 us).
   const bool long_scan = L->n >= (32u << 20);
-  const int bpl = env_int("FPS_PQ_BPL", long_scan ? 1 : 2) == 1 ? 1 : 2;  // 32-entry blocks per lane
+  const int bpl = env_int("FPS_PQ_BPL", 2) == 1 ? 1 : 2;  // 32-entry blocks per lane
   const u32 chunk = bpl == 1 ? fps::PqStep<1>::CHUNK : fps::PqStep<2>::CHUNK;
   const u64 step_entries = bpl == 1 ? fps::PqStep<1>::ENTRIES : fps::PqStep<2>::ENTRIES;
-  const int nwb = std::max(1, std::min(16, env_int("FPS_PQ_WARPS", long_scan ? 16 : 8)));
+  const int nwb = std::max(1, std::min(16, env_int("FPS_PQ_WARPS", 8)));
   const int stages = std::max(1, std::min(fps::PQ_SMAX, env_int("FPS_PQ_STAGES", 2)));
   // ring per warp: `stages` stages of a typical list (48 positions = up to
   // 40 listed planes); wider lists fold warps in the kernel; with the query
@@ -751,6 +752,7 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   a.cap = cap;
   a.n_steps = steps;
   a.ring_bytes = ring;
+  a.refresh = (u32)std::max(1, env_int("FPS_PQ_REFRESH", long_scan ? 8 : 1));
   a.pub_every = (u32)std::max<u64>(1, warps / 512);
   a.flags = scan_flags();
   a.tg = L->tg.as<u32>();

@@ -13,25 +13,28 @@
 // the HBM stream, which bounds the single-query scan, shrinks ~3.7x.
 //
 // Layout (plane-major): plane p occupies pstride u32 words from pm + p *
-// pstride; word w is 32-entry block w. A warp step covers 2,048 entries (64
-// words = 256 B of every listed plane; a lane owns two consecutive blocks and
-// reads both with one 64-bit shared load, as in fps_bitslice.cuh).
+// pstride; word w is 32-entry block w. A warp step covers 1,024 x BPL entries
+// (BPL = 2 by default: a lane owns two consecutive blocks and reads both with
+// one 64-bit shared load, as in fps_bitslice.cuh), i.e. 128 x BPL bytes of
+// every listed plane.
 //
-// Per warp, a ring of S stages in shared memory is filled by the bulk-copy
-// engine: for a stage, lane l issues the 256 B cp.async.bulk copies of stage
-// positions l, l+32, l+64 (position 0..7 = popcount planes, 8.. = the query's
-// list), all completing on the stage's mbarrier. The count c runs through the
-// carry-save adder tree of the multi-query kernel; the pass mask is the sign
-// plane of X + (|q| - T) with X = |a| - 2c (or 2c - |a|).
+// Per warp, a ring of S stages in shared memory: position 0..7 = popcount
+// planes, 8.. = the query's list (zero-padded to a multiple of 8). COPY 1
+// (default) fills a stage with cp.async, 16 B per lane and 512 B per warp
+// instruction, completing on the stage's mbarrier (arrive.noinc per lane);
+// COPY 0 issues one cp.async.bulk per plane chunk (TMA engine), which tops out
+// at ~15 B/clk/SM with 256 B copies. The count c runs through the carry-save
+// adder tree of the multi-query kernel; the pass mask is the sign plane of
+// X + (|q| - T) with X = |a| - 2c (or 2c - |a|).
 //
 // Selection is the single-query POPC scan's (fps_kernels.cuh): per-warp
 // ordered candidate buffer with its distance histogram and the exact tie
 // rule, sampled warps publishing witnesses into ghist, the global bound tg,
 // survivors d <= tg to the flat list, then select_kernel. A warp's first step
-// has no bound yet: instead of buffering all 2,048 entries it binary-searches
-// (bit-sliced counts, no per-entry work) the smallest T with k entries d < T
-// in that step and buffers exactly those — its own k-th distance is then
-// T - 1, which is what the tie rule needs.
+// has no bound yet: it computes the step's distances bit-sliced, finds the
+// k-th smallest by radix select (no per-entry work), publishes witnesses at a
+// few ranks, and holds its entries back one step so they are inserted under
+// the tighter global bound the first wave of witnesses produces.
 #pragma once
 #include "fps_bitslice.cuh"
 
@@ -95,6 +98,7 @@ struct PqArgs {
   u32 ring_bytes;       // shared-memory ring per warp (before warps are folded, see below)
   u32 pub_every;        // warps with g % pub_every == 0 publish witnesses
   u32 flags;            // FPS_SCAN_FLAGS: 1 = no publishing, 2 = no tg refresh
+  u32 refresh;          // steps between reads of the global bound (1 = every step)
   u32* tg;
   u32* ghist;
   u32 gstride, tg_rep;
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   const volatile u32* tgw = tgrep(a, 0, (u32)(g % a.tg_rep));  // this warp's replica of the bound
   u32 tgp = (a.flags & 2) ? T_OPEN : *tgw;
   const bool publisher = !(a.flags & 1) && (g % a.pub_every) == 0;
+  u32 since_refresh = 0;
   u32 hv[7];          // published-witness histogram snapshot (deferred tighten)
   bool tpend = false;
   // smallest T with >= k published witnesses d <= T -> every replica of tg;
@@ -331,6 +336,95 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     __syncwarp();
   };
 
+  // Insert the entries of masks em (bit e of block h = entry bfirst + 32 h + e)
+  // into the ordered buffer with distances dfn(h, bit); then the own bound and,
+  // for new entries of publishers, their witnesses.
+  auto insert = [&](const u32 (&em)[BPL], u64 bfirst, auto&& dfn, bool pub_new) {
+    const u64 mm = (u64)em[0] | (BPL == 2 ? ((u64)em[BPL - 1] << 32) : 0ull);
+    if (!__any_sync(FULL, mm != 0)) return;
+    const u32 cntl = (u32)__popcll(mm);
+    const u32 incl = warp_incl_scan(cntl, lane);
+    const u32 total = __shfl_sync(FULL, incl, 31);
+    if (ws->cnt[0] + total > a.cap) compact();
+    const u32 cnt0 = ws->cnt[0];
+    u32 pos = cnt0 + incl - cntl;
+    for (u64 rest = mm; rest; rest &= rest - 1) {
+      const int e = __ffsll((long long)rest) - 1;
+      const u32 d = dfn(BPL == 2 ? (e >> 5) : 0, e & 31);
+      wbuf[pos++] = make_key(d, a.index_base + bfirst + e);
+      atomicAdd(hist + d, 1u);
+    }
+    __syncwarp();
+    if (lane == 0) ws->cnt[0] = cnt0 + total;
+    __syncwarp();
+    if (cnt0 + total < a.k) return;
+    u32 less;
+    const u32 town = warp_kth_bin(hist, a.k, lane, &less);
+    if (lane == 0) ws->town[0] = town;
+    if (publisher && pub_new) {
+      if (!ws->pubd[0]) {
+        // first publication: every buffered candidate with d <= town
+        for (u32 b = lane; b <= town && b < HB; b += 32) {
+          const u32 cb = hist[b];
+          if (cb) atomicAdd(gbin(a, 0, b), cb);
+        }
+      } else {
+        // later: the entries just inserted with d <= town
+        for (u64 rest = mm; rest; rest &= rest - 1) {
+          const int e = __ffsll((long long)rest) - 1;
+          const u32 d = dfn(BPL == 2 ? (e >> 5) : 0, e & 31);
+          if (d <= town) atomicAdd(gbin(a, 0, d), 1u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ws->pubd[0] = 1;
+      __syncwarp();
+      // tighten the global bound one step later: the histogram loads are
+      // in flight while the next stage is awaited (an L2 round trip under a
+      // saturated memory system costs microseconds)
+#pragma unroll
+      for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
+      tpend = true;
+    }
+    T = town < T ? town : T;
+    __syncwarp();
+  };
+  // first-step entries held back (bit-sliced distances, valid masks)
+  u32 Dsv[BPL][8], vsv[BPL];
+  u64 bsv = 0;
+  u32 Tsv = 256, tlim = T_OPEN;  // their own limit; the last applied global limit
+  bool pending = false;
+  // insert them: d < min(own limit, global limit), no new witnesses (a
+  // publisher already posted the step's)
+  auto flush_pending = [&](bool fresh) {
+    pending = false;
+    u32 lim = Tsv < tlim ? Tsv : tlim;
+    if (fresh && !(a.flags & 2)) {
+      const u32 tf = *tgw;
+      const u32 tl = (tf < T_OPEN ? tf : T_OPEN - 1) + 1;
+      lim = tl < lim ? tl : lim;
+    }
+    u32 em[BPL];
+#pragma unroll
+    for (int h = 0; h < BPL; ++h) {  // D < lim, MSB first over 9 bits (D < 256)
+      u32 lt = 0, eq = FULL;
+#pragma unroll
+      for (int b = 8; b >= 0; --b) {
+        const u32 db = b < 8 ? Dsv[h][b] : 0u;
+        const u32 lb = ((lim >> b) & 1u) ? FULL : 0u;
+        lt |= eq & ~db & lb;
+        eq &= ~(db ^ lb);
+      }
+      em[h] = lt & vsv[h];
+    }
+    insert(em, bsv, [&](int h, int bit) -> u32 {
+      u32 d = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) d |= (((h ? Dsv[BPL - 1][b] : Dsv[0][b]) >> bit) & 1u) << b;
+      return d;
+    }, false);
+  };
+
 #pragma unroll 1
   for (u32 st = 0, ph = 0;; st = (st + 1 == S) ? 0 : st + 1, ph ^= (st == 0) ? 1u : 0u) {
 #ifdef FPS_SCAN_TRACE
@@ -350,12 +444,15 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     if (tpend) {
       const u32 lim = finish_tighten();
       T = lim < T ? lim : T;
+      tlim = lim < tlim ? lim : tlim;
     }
     // the bound prefetched one step ago
     {
       const u32 tl = (tgp < T_OPEN ? tgp : T_OPEN - 1) + 1;
       T = tl < T ? tl : T;
+      tlim = tl < tlim ? tl : tlim;
     }
+    if (pending) flush_pending(false);  // the previous step's held-back entries first (index order)
     const char* stage = ring + st * stage_bytes;
     const char* lb = stage + 4 * BPL * lane;  // this lane's BPL words of every position
     // one shared load fetches a plane word of all BPL blocks of the lane
@@ -454,17 +551,20 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
 #undef CSA
 
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 0] = gtimer();
+    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 0]) g_pq_phase[g * 8 + 0] = gtimer();
 #endif
     // every lane is done reading this slot: refill it with the step S ahead
     __syncwarp();
     if (COPY == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 1] = gtimer();
+    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 1]) g_pq_phase[g * 8 + 1] = gtimer();
 #endif
     issue(st);
-    if (!(a.flags & 2)) tgp = *tgw;  // applied next step
+    if (!(a.flags & 2) && ++since_refresh >= a.refresh) {  // applied at the next step
+      since_refresh = 0;
+      tgp = *tgw;
+    }
 
     // X = P - N over 10 bits: (P, N) = (|a|, 2c) sparse, (2c, |a|) dense
     u32 X[BPL][10];
@@ -484,46 +584,99 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     auto pass = [&](int h, u32 Tq) -> u32 {
       return bs_sign_after_add(X[h], (pop - Tq) & 0x3ffu) & valid[h];
     };
-
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 2] = gtimer();
+    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 2]) g_pq_phase[g * 8 + 2] = gtimer();
 #endif
-    if (T >= T_OPEN) {
-      // no bound yet (the warp's first step before any witness was
-      // published): smallest T with >= k entries d < T in this step
+
+    if (T >= T_OPEN && !pending) {
+      // ---- the warp's first step, no bound known yet. Distances of the
+      // whole step bit-sliced (D = X + |q|), the k-th smallest by radix
+      // select (no per-entry work); publishers post witnesses at the 1st,
+      // 2nd, 4th, 8th and k-th smallest distance. The step's entries are
+      // inserted at the next step, when more witnesses have been published
+      // and the global bound is tighter (typically: far fewer inserts).
+#pragma unroll
+      for (int h = 0; h < BPL; ++h) {
+        u32 cy = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const u32 w = ((pop >> b) & 1u) ? FULL : 0u;
+          Dsv[h][b] = X[h][b] ^ w ^ cy;
+          cy = (X[h][b] & w) | (cy & (X[h][b] ^ w));
+        }
+        vsv[h] = valid[h];
+      }
+#ifdef FPS_SCAN_TRACE
+      if (lane == 0 && g < 16384) g_pq_phase[g * 8 + 6] = gtimer();
+#endif
       u32 nv = 0;
 #pragma unroll
       for (int h = 0; h < BPL; ++h) nv += __popc(valid[h]);
       nv = __reduce_add_sync(FULL, nv);
-      if (nv >= a.k) {
-        u32 lo = 0, hi = 256;  // count(d < lo) < k <= count(d < hi)
-#pragma unroll 1
-        while (hi - lo > 1) {
-          const u32 mid = (lo + hi) >> 1;
-          u32 cl = 0;
+      // r-th smallest distance of the step (1-based, r <= nv), MSB first
+      auto rsel = [&](u32 r) -> u32 {
+        u32 msk[BPL];
 #pragma unroll
-          for (int h = 0; h < BPL; ++h) cl += __popc(pass(h, mid));
-          const u32 c = __reduce_add_sync(FULL, cl);
-          if (c >= a.k) hi = mid;
-          else lo = mid;
+        for (int h = 0; h < BPL; ++h) msk[h] = valid[h];
+        u32 val = 0;
+#pragma unroll
+        for (int b = 7; b >= 0; --b) {
+          u32 c = 0;
+#pragma unroll
+          for (int h = 0; h < BPL; ++h) c += __popc(msk[h] & ~Dsv[h][b]);
+          c = __reduce_add_sync(FULL, c);
+          if (c >= r) {
+#pragma unroll
+            for (int h = 0; h < BPL; ++h) msk[h] &= ~Dsv[h][b];
+          } else {
+            r -= c;
+            val |= 1u << b;
+#pragma unroll
+            for (int h = 0; h < BPL; ++h) msk[h] &= Dsv[h][b];
+          }
         }
-        T = hi;
+        return val;
+      };
+      Tsv = 256;  // fewer than k entries: every one is a candidate
+      if (nv >= a.k) {
+        u32 town1 = 0;
+        if (publisher) {
+          u32 prev = 0;
+#pragma unroll 1
+          for (u32 r = 1;; r = (2 * r < a.k && r < 8) ? 2 * r : a.k) {
+            const u32 tr = rsel(r);
+            if (lane == 0) atomicAdd(gbin(a, 0, tr), r - prev);
+            prev = r;
+            if (r == a.k) { town1 = tr; break; }
+          }
+          if (lane == 0) ws->pubd[0] = 1;
+#pragma unroll
+          for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
+          tpend = true;
+        } else {
+          town1 = rsel(a.k);
+        }
+        // >= k entries of this step have d <= town1 and a smaller index than
+        // any later entry: later entries need d < town1
+        T = town1 < T ? town1 : T;
+        Tsv = town1 + 1;
       }
+#ifdef FPS_SCAN_TRACE
+      if (lane == 0 && g < 16384) g_pq_phase[g * 8 + 7] = gtimer();
+#endif
+      bsv = blk_first;
+      pending = true;
+      __syncwarp();
+      continue;
     }
 
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 3] = gtimer();
+    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 3]) g_pq_phase[g * 8 + 3] = gtimer();
 #endif
-    const u32 m0 = pass(0, T), m1 = BPL == 2 ? pass(BPL - 1, T) : 0u;
-    if (!__any_sync(FULL, m0 | m1)) continue;
-
-    // ---- slow path: exact distances of the passing entries, in index order
-    const u64 mm = (u64)m0 | ((u64)m1 << 32);
-    const u32 cntl = (u32)__popcll(mm);
-    const u32 incl = warp_incl_scan(cntl, lane);
-    const u32 total = __shfl_sync(FULL, incl, 31);
-    auto dist_of_bit = [&](int e) -> u32 {
-      const int h = BPL == 2 ? (e >> 5) : 0, bit = e & 31;
+    u32 em[BPL];
+#pragma unroll
+    for (int h = 0; h < BPL; ++h) em[h] = pass(h, T);
+    insert(em, blk_first, [&](int h, int bit) -> u32 {
       constexpr int H1 = BPL - 1;
       u32 av = 0, cv = 0;
 #pragma unroll
@@ -534,62 +687,14 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
 #pragma unroll
       for (int i = 0; i < 7; ++i) cv |= ((cb[i] >> bit) & 1u) << i;
       return dense ? pop - av + 2 * cv : av + pop - 2 * cv;
-    };
-    if (ws->cnt[0] + total > a.cap) compact();
-    const u32 cnt0 = ws->cnt[0];
-    u32 pos = cnt0 + incl - cntl;
-    for (u64 rest = mm; rest; rest &= rest - 1) {
-      const int e = __ffsll((long long)rest) - 1;
-      const u32 d = dist_of_bit(e);
-      wbuf[pos++] = make_key(d, a.index_base + blk_first + e);
-      atomicAdd(hist + d, 1u);
-    }
-    __syncwarp();
-    if (lane == 0) ws->cnt[0] = cnt0 + total;
-    __syncwarp();
-
+    }, true);
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 4] = gtimer();
-#endif
-    if (cnt0 + total < a.k) continue;
-    u32 less;
-    const u32 town = warp_kth_bin(hist, a.k, lane, &less);
-    if (lane == 0) ws->town[0] = town;
-    u32 nt = town;
-    if (publisher) {
-      if (!ws->pubd[0]) {
-        // first publication: every buffered candidate with d <= town
-        for (u32 b = lane; b <= town && b < HB; b += 32) {
-          const u32 cb = hist[b];
-          if (cb) atomicAdd(gbin(a, 0, b), cb);
-        }
-      } else {
-        // later: the entries just inserted with d <= town
-        for (u64 rest = mm; rest; rest &= rest - 1) {
-          const u32 d = dist_of_bit(__ffsll((long long)rest) - 1);
-          if (d <= town) atomicAdd(gbin(a, 0, d), 1u);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) ws->pubd[0] = 1;
-      __syncwarp();
-      // tighten the global bound one step later: the histogram loads are
-      // in flight while the next stage is awaited (an L2 round trip under a
-      // saturated memory system costs microseconds)
-#pragma unroll
-      for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
-      tpend = true;
-    }
-    T = nt < T ? nt : T;
-#ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !ph_done) g_pq_phase[g * 8 + 5] = gtimer();
-#endif
-#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 5]) g_pq_phase[g * 8 + 5] = gtimer();
     ph_done = true;
 #endif
-
     __syncwarp();
   }
+  if (pending) flush_pending(true);
 
 #ifdef FPS_SCAN_TRACE
   if (lane == 0 && g < 16384) {

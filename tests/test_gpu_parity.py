@@ -542,3 +542,17 @@ def test_plane_scan_not_used_with_pad_bits():
     lib = Library.from_records(rec)
     assert lib.search(np.zeros(3, dtype=np.uint64), 3000)[-1] == (5, 1)
     assert lib.last_kernel == "single-query HBM scan"
+
+
+@pytest.mark.parametrize("refresh", [1, 3, 8])
+def test_plane_scan_bound_refresh_periods(refresh, monkeypatch):
+    """The global bound read every `refresh` steps (long scans: 8)."""
+    monkeypatch.setenv("FPS_PQ_REFRESH", str(refresh))
+    seed = 1234
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, 400_003)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(refresh)
+    for pop in (30, 45):
+        q = _query_with_pop(rng, pop)
+        for k in (10, 100):
+            assert lib.search(q, k) == oracle_topk(w, q[None], k)[0], (refresh, pop, k)

@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round evidence (plane scan refresh): tests, smoke, benches, reference arm, launch list, ncu captures.
+D=gpurun_out/ev2; mkdir -p $D; rm -f $D/*
+python -c "import __graft_entry__ as g; g.build()" > $D/build.log 2>&1 || exit 1
+nvidia-smi > $D/nvidia-smi.txt 2>&1
+timeout 1500 python -m pytest tests -q -m gpu > $D/gpu_tests.log 2>&1; echo "gpu tests rc=$?" >> $D/summary.txt
+tail -2 $D/gpu_tests.log >> $D/summary.txt
+python -c "import __graft_entry__ as g; g.smoke()" > $D/smoke.log 2>&1; echo "smoke rc=$?" >> $D/summary.txt
+timeout 900 python bench.py > $D/bench_default.json 2> $D/bench_default.err; echo "bench default rc=$?" >> $D/summary.txt
+for w in c1 c3 c4 c5; do
+  timeout 900 python bench.py --workload $w > $D/bench_$w.json 2> $D/bench_$w.err; echo "bench $w rc=$?" >> $D/summary.txt
+done
+FPS_PLANEQ=0 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $D/bench_c2_popc.json 2> $D/bench_c2_popc.err
+FPS_PLANEQ=0 timeout 900 python bench.py --workload c3 --no-cpu-baseline > $D/bench_c3_popc.json 2> $D/bench_c3_popc.err
+timeout 900 python bench.py --impl reference --steps 5 --warmup 2 > $D/bench_reference.json 2> $D/bench_reference.err; echo "ref rc=$?" >> $D/summary.txt
+CMD="python bench.py --workload c2 --steps 3 --warmup 2 --no-cpu-baseline"
+$CMD > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $D/launches_c2.csv $CMD > /dev/null 2>&1
+for w in c2 c3 c1; do
+  C="python bench.py --workload $w --steps 3 --warmup 2 --no-cpu-baseline"
+  $C > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"pq_scan_kernel|select_kernel" -s 4 -c 2 -o $D/prof_$w $C > $D/ncu_$w.log 2>&1; echo "ncu $w rc=$?" >> $D/summary.txt
+done
+cat $D/summary.txt

@@ -44,7 +44,7 @@ for wl in sys.argv[1:] or ["c2"]:
             L.fps_trace_phases(ph.ctypes.data)
             ph = ph.reshape(-1, 8).astype(np.int64)[: len(warps) // 4]
             okr = ph[:, 0] > 0
-            for i, name in enumerate(["csa done", "refill issued", "before bound", "mask", "inserted", "published"]):
+            for i, name in enumerate(["csa done", "refill issue", "after X", "mask (2nd)", "-", "inserted(2nd)", "D done", "selected"]):
                 v = ph[okr, i]
                 v = v[v > 0] - m0
                 if len(v):
