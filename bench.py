@@ -420,10 +420,21 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         if plan.radius is None:
             lib.search_batch(qhost, plan.k)
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for _ in range(e2e_steps):
-                res = lib.search_batch(qhost, plan.k)
-            e2e_s = time.perf_counter() - t0
+            if flush:
+                # bytes per call below L2: flush between calls, time each call
+                # alone (the call is synchronous: host query in, host results out)
+                e2e_s = 0.0
+                for _ in range(e2e_steps):
+                    flush_l2()
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    res = lib.search_batch(qhost, plan.k)
+                    e2e_s += time.perf_counter() - t0
+            else:
+                t0 = time.perf_counter()
+                for _ in range(e2e_steps):
+                    res = lib.search_batch(qhost, plan.k)
+                e2e_s = time.perf_counter() - t0
             d2h = Q * plan.k * 8 + Q * 4
         else:
             lib.range_search(qhost, plan.radius)
@@ -511,7 +522,9 @@ def run_ours(args, rank: int, local_rank: int, world: int):
                               f"({'compact: word 2 as u32 + u8' if compact else 'full: 3 x u64'})")},
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps},
+                "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps,
+                "l2": "flushed before every call, calls timed one by one" if (flush and world == 1)
+                      else "calls back to back"},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

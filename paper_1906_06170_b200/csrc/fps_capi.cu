@@ -146,8 +146,9 @@ struct fps_lib {
   DevBuf mq;  // min-over-queries merge scratch (fps_topk_min on the batched kernel)
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
   // plane-major copy for the single-query plane scan (built on first use)
-  DevBuf pm;
+  DevBuf pm, pm_perm, pm_meta;
   int pm_state = 0;  // as bs_state
+  bool pm_sorted = false;  // pm holds the popcount-sorted copy (pm_perm, pm_meta valid)
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -645,8 +646,12 @@ int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u
 // ---------------------------------------------------------------------------
 // Build (once) the plane-major copy; libraries with pad bits past key 166 keep
 // the POPC scan (it counts them, like the reference).
-int pm_ensure(fps_lib* L) {
-  if (L->pm_state) return FPS_OK;
+int pm_ensure(fps_lib* L, bool sorted) {
+  if (L->pm_state && (L->pm_state < 0 || L->pm_sorted == sorted)) return FPS_OK;
+  L->pm.release();
+  L->pm_perm.release();
+  L->pm_meta.release();
+  L->pm_sorted = sorted;
   const u64 steps = std::max<u64>(1, (L->n + 32 * fps::PQ_STRIDE_WORDS - 1) / (32 * fps::PQ_STRIDE_WORDS));
   // plane stride: whole steps, an odd number of 256 B chunks (planes read
   // side by side do not start on the same DRAM interleave phase)
@@ -658,28 +663,57 @@ int pm_ensure(fps_lib* L) {
     L->pm_state = -1;
     return FPS_OK;
   }
-  DevBuf wide;
+  DevBuf wide, keys, sorted_keys, tmp;
   if ((rc = wide.ensure(4))) return rc;
   CUDA_TRY(cudaMemsetAsync(L->pm.p, 0, L->pm.bytes, L->stream));
   CUDA_TRY(cudaMemsetAsync(wide.p, 0, 4, L->stream));
   const u64 nblocks = (L->n + 31) / 32;
   const int grid = (int)std::min<u64>((nblocks * 32 + 255) / 256, (u64)L->sms * 32);
-  fps::pm_build_kernel<<<std::max(grid, 1), 256, 0, L->stream>>>(L->out(), L->n, L->pm.as<u32>(), L->pm_stride,
-                                                                 wide.as<u32>());
+  if (sorted) {
+    // order = entries sorted by (|a|, index): radix sort of |a| << 32 | index on bits 0..39
+    if (L->n > (u64)INT32_MAX) return fail(FPS_EINVAL, "sorted plane copy: more than 2^31 entries on one device");
+    if ((rc = keys.ensure(L->n * 8)) || (rc = sorted_keys.ensure(L->n * 8)) ||
+        (rc = L->pm_perm.ensure(L->n * 4)) || (rc = L->pm_meta.ensure(((L->n + 1023) / 1024) * 2)))
+      return rc;
+    fps::pm_sort_keys_kernel<<<std::max(grid, 1), 256, 0, L->stream>>>(L->out(), L->n, keys.as<u64>());
+    size_t tmp_bytes = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.as<u64>(), sorted_keys.as<u64>(), (int)L->n, 0,
+                                            40, L->stream));
+    if ((rc = tmp.ensure(tmp_bytes))) return rc;
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.as<u64>(), sorted_keys.as<u64>(), (int)L->n, 0,
+                                            40, L->stream));
+    const u64 nb = (L->n + 1023) / 1024;
+    fps::pm_meta_kernel<<<(int)std::min<u64>((nb + 255) / 256, 4096), 256, 0, L->stream>>>(
+        sorted_keys.as<u64>(), L->n, reinterpret_cast<unsigned short*>(L->pm_meta.p));
+    L->launches += 4;
+  }
+  fps::pm_build_kernel<<<std::max(grid, 1), 256, 0, L->stream>>>(
+      L->out(), L->n, L->pm.as<u32>(), L->pm_stride, wide.as<u32>(), sorted ? sorted_keys.as<u64>() : nullptr,
+      sorted ? L->pm_perm.as<u32>() : nullptr);
   L->launches++;
   LAUNCH_CHECK("pm_build_kernel");
   u32 nwide = 0;
   CUDA_TRY(cudaMemcpyAsync(&nwide, wide.p, 4, cudaMemcpyDeviceToHost, L->stream));
   CUDA_TRY(cudaStreamSynchronize(L->stream));
   L->pm_state = nwide ? -1 : 1;
-  if (nwide) L->pm.release();
+  if (nwide) {
+    L->pm.release();
+    L->pm_perm.release();
+    L->pm_meta.release();
+  }
   return FPS_OK;
 }
 
 bool pq_wanted(fps_lib* L) {
   const char* e = std::getenv("FPS_PLANEQ");  // "0": the POPC scan (tests cover both)
   if ((e && std::string(e) == "0") || L->n == 0) return false;
-  if (pm_ensure(L) != FPS_OK) return false;
+  // FPS_PQ_SORTED=1: the popcount-sorted plane copy (SORTED kernels)
+  const char* so = std::getenv("FPS_PQ_SORTED");
+  const bool sorted = so ? std::string(so) == "1" : false;
+  if (pm_ensure(L, sorted) != FPS_OK) {
+    cudaGetLastError();
+    return false;
+  }
   return L->pm_state == 1;
 }
 
@@ -720,10 +754,12 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   const u32 ring_cap = (u32)((budget - (u32)fps::pq_smem(nwb, 0)) / nwb) / 256 * 256;
   u32 ring = std::min<u32>((u32)stages * np * chunk, ring_cap);
   ring = std::max<u32>(ring, (u32)((2 * fps::PQ_NPMAX * chunk + nwb - 1) / nwb + 255) / 256 * 256);
-  const size_t smem = fps::pq_smem(nwb, ring);
-  if (smem > 226 * 1024) return fail(FPS_EINVAL, "plane scan: shared memory ring too large (FPS_PQ_WARPS/STAGES)");
   const u64 steps = (L->n + step_entries - 1) / step_entries;
   const u64 grid = std::max<u64>(1, std::min<u64>((u64)L->sms, steps));
+  const bool srt = L->pm_sorted;
+  const u32 meta_cap = srt ? (u32)((steps + grid - 1) / grid + 1) : 0u;
+  const size_t smem = fps::pq_smem(nwb, ring, meta_cap);
+  if (smem > 226 * 1024) return fail(FPS_EINVAL, "plane scan: shared memory ring too large (FPS_PQ_WARPS/STAGES)");
   const u64 warps = grid * nwb;
   const u32 cap = (std::max<u32>(2 * k, k + (u32)step_entries) + 31) / 32 * 32;
   const u64 cand_cap = warps * (u64)k;
@@ -731,11 +767,12 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   if ((rc = L->buf.ensure(warps * (size_t)cap * 8))) return rc;
   if ((rc = L->cand.ensure(cand_cap * 8))) return rc;
   const int copy = env_int("FPS_PQ_COPY", 1);  // 1: cp.async 16 B per lane (default, measured faster), 0: bulk copies
-  const int kv = (copy == 1 ? 1 : 0) * 2 + (bpl == 2 ? 1 : 0);
-  void (*const kerns[4])(fps::PqArgs) = {fps::pq_scan_kernel<0, 1>, fps::pq_scan_kernel<0, 2>,
-                                         fps::pq_scan_kernel<1, 1>, fps::pq_scan_kernel<1, 2>};
+  const int kv = srt ? 4 + (bpl == 2 ? 1 : 0) : (copy == 1 ? 1 : 0) * 2 + (bpl == 2 ? 1 : 0);
+  void (*const kerns[6])(fps::PqArgs) = {fps::pq_scan_kernel<0, 1, false>, fps::pq_scan_kernel<0, 2, false>,
+                                         fps::pq_scan_kernel<1, 1, false>, fps::pq_scan_kernel<1, 2, false>,
+                                         fps::pq_scan_kernel<1, 1, true>,  fps::pq_scan_kernel<1, 2, true>};
   auto* kern = kerns[kv];
-  static size_t smem_set[4] = {0, 0, 0, 0};
+  static size_t smem_set[6] = {0, 0, 0, 0, 0, 0};
   if (smem > smem_set[kv]) {  // (the kernel's static shared memory comes on top)
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set[kv] = smem;
@@ -753,6 +790,9 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   a.n_steps = steps;
   a.ring_bytes = ring;
   a.refresh = (u32)std::max(1, env_int("FPS_PQ_REFRESH", long_scan ? 8 : 1));
+  a.perm = srt ? L->pm_perm.as<u32>() : nullptr;
+  a.meta = srt ? reinterpret_cast<const unsigned short*>(L->pm_meta.p) : nullptr;
+  a.meta_cap = meta_cap;
   a.pub_every = (u32)std::max<u64>(1, warps / 512);
   a.flags = scan_flags();
   a.tg = L->tg.as<u32>();

@@ -54,15 +54,22 @@ constexpr u64 PQ_NONE = ~0ull;
 
 // Plane-major copy of the library: one warp per 32-entry block, plane p =
 // ballot of key p+1; lane (p mod 32) stores it. Libraries with bits past key
-// 166 (FPS1 pad bytes) are flagged in *wide and keep the POPC scan.
-__global__ void pm_build_kernel(PlanesOut lib, u64 n, u32* __restrict__ pm, u64 pstride, u32* wide) {
+// 166 (FPS1 pad bytes) are flagged in *wide and keep the POPC scan. With
+// `order` (popcount-sorted keys |a| << 32 | index) position j holds entry
+// order[j] and perm[j] records its index.
+__global__ void pm_build_kernel(PlanesOut lib, u64 n, u32* __restrict__ pm, u64 pstride, u32* wide,
+                                const u64* __restrict__ order, u32* __restrict__ perm) {
   const int lane = threadIdx.x & 31;
   const u64 nblocks = (n + 31) / 32;
   for (u64 blk = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; blk < nblocks;
        blk += ((u64)gridDim.x * blockDim.x) >> 5) {
-    const u64 i = blk * 32 + lane;
+    const u64 j = blk * 32 + lane;
     u64 w[3] = {0, 0, 0};
-    if (i < n) lib.get(i, w[0], w[1], w[2]);
+    if (j < n) {
+      const u64 i = order ? (order[j] & 0xffffffffull) : j;
+      if (order) perm[j] = (u32)i;
+      lib.get(i, w[0], w[1], w[2]);
+    }
     if (w[2] >> 38) atomicAdd(wide, 1u);
     u32 mine[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -86,6 +93,25 @@ __global__ void pm_build_kernel(PlanesOut lib, u64 n, u32* __restrict__ pm, u64 
   }
 }
 
+// Sort keys of the popcount-sorted copy: |a| << 32 | index (index < 2^32 on a device).
+__global__ void pm_sort_keys_kernel(PlanesOut lib, u64 n, u64* __restrict__ keys) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    u64 w0, w1, w2;
+    lib.get(i, w0, w1, w2);
+    const u64 pc = (u64)(__popcll(w0) + __popcll(w1) + __popcll(w2 & ((1ull << 38) - 1)));
+    keys[i] = (pc << 32) | i;
+  }
+}
+
+// Popcount range of every 1,024 sorted entries: min | max << 8.
+__global__ void pm_meta_kernel(const u64* __restrict__ sorted, u64 n, unsigned short* __restrict__ meta) {
+  const u64 nb = (n + 1023) / 1024;
+  for (u64 b = (u64)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (u64)gridDim.x * blockDim.x) {
+    const u64 f = b * 1024, l = (f + 1023 < n ? f + 1023 : n - 1);
+    meta[b] = (unsigned short)((sorted[f] >> 32) | ((sorted[l] >> 32) << 8));
+  }
+}
+
 struct PqArgs {
   const u32* pm;        // plane-major planes (174 x pstride words)
   u64 pstride;          // words per plane (>= 64 * n_steps; padding words are zero)
@@ -106,13 +132,19 @@ struct PqArgs {
   u64* cand;            // [cand_cap] survivors of the query
   u32* cand_cnt;
   u64 cand_cap;
+  // popcount-sorted copy (SORTED kernels): sorted position -> local index, and
+  // per 1,024 sorted entries the popcount range (min | max << 8)
+  const u32* perm;
+  const unsigned short* meta;
+  u32 meta_cap;         // steps of a CTA's run the shared-memory copy of meta holds
 };
 
 // Dynamic shared memory: [warps][ring_bytes] ring | [warps][PQ_SMAX] mbarriers
-// | [warps][PQ_SMAX] slot steps | [warps][HB] histograms | [warps] WarpState.
-__host__ __device__ inline size_t pq_smem(int nwb, u32 ring_bytes) {
+// | [warps][PQ_SMAX] slot steps | [warps][HB] histograms | [warps] WarpState
+// | [warps][32] u64 tie scratch | [meta_cap] u16 popcount ranges (SORTED).
+__host__ __device__ inline size_t pq_smem(int nwb, u32 ring_bytes, u32 meta_cap = 0) {
   return (size_t)nwb * ring_bytes + (size_t)nwb * PQ_SMAX * 16 + (size_t)nwb * HB * 4 +
-         (size_t)nwb * sizeof(WarpState<1>);
+         ((size_t)nwb * sizeof(WarpState<1>) + 15) / 16 * 16 + (size_t)nwb * 32 * 8 + (size_t)meta_cap * 2;
 }
 
 // COPY 0: per-plane 256 B cp.async.bulk (TMA engine); 1: 16 B cp.async
@@ -121,8 +153,15 @@ __host__ __device__ inline size_t pq_smem(int nwb, u32 ring_bytes) {
 #ifdef FPS_SCAN_TRACE
 __device__ u64 g_pq_phase[16384 * 8];  // per warp, first step: CSA done, refill issued, bound, mask, inserted, published
 #endif
-template <int COPY, int BPL>
+// SORTED: the plane copy is ordered by popcount |a| (then index). A step whose
+// entries share one |a| (all but ~one per popcount value) skips the popcount
+// planes (|a| is a constant), steps whose |a| range cannot reach the bound
+// (d >= ||a| - |q||) are not read at all, and since a warp no longer meets
+// entries in index order, ties at its own k-th distance are kept and resolved
+// by index (full (d, index) key order) when the buffer is compacted.
+template <int COPY, int BPL, bool SORTED>
 __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
+  static_assert(!SORTED || COPY == 1, "the sorted copy is read with cp.async");
   constexpr u32 PQ_WORDS = PqStep<BPL>::WORDS, PQ_CHUNK = PqStep<BPL>::CHUNK;
   constexpr u64 PQ_STEP = PqStep<BPL>::ENTRIES;
   constexpr u32 LPP = 8 * BPL;      // cp.async: lanes per position (16 B each)
@@ -173,6 +212,29 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   __syncthreads();
   if (COPY == 1)
     for (u32 i = threadIdx.x; i < s_nc; i += blockDim.x) s_base[i] = a.pm + (u64)s_list[i] * a.pstride;
+  // CTA-dynamic schedule: the CTA owns a contiguous run of steps; its warps
+  // claim them one at a time (each warp sees ascending steps: the ordered
+  // buffers rely on it) so warps that draw more bandwidth take more.
+  const u64 cta_lo = (u64)blockIdx.x * a.n_steps / gridDim.x;
+  const u64 cta_hi = ((u64)blockIdx.x + 1) * a.n_steps / gridDim.x;
+  unsigned short* s_meta = reinterpret_cast<unsigned short*>(
+      pqs + pq_smem(nwb, a.ring_bytes) );  // (meta region follows the tie scratch)
+  if (SORTED) {
+    // popcount range of each step of the run: BPL consecutive 1,024-entry blocks
+    for (u64 i = threadIdx.x; i < cta_hi - cta_lo; i += blockDim.x) {
+      u32 lo = 255, hi = 0;
+#pragma unroll
+      for (int h = 0; h < BPL; ++h) {
+        const u64 b = (cta_lo + i) * BPL + h;
+        if (b * 1024 < a.n) {
+          const u32 m = a.meta[b];
+          lo = min(lo, m & 0xffu);
+          hi = max(hi, m >> 8);
+        }
+      }
+      s_meta[i] = (unsigned short)(lo | (hi << 8));
+    }
+  }
   __syncthreads();  // the last block-level barrier
   const u32 np = s_np, nc = s_nc, pop = s_pop;
   const bool dense = s_dense != 0;
@@ -217,18 +279,26 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   }
   __syncwarp();
 
-  // CTA-dynamic schedule: the CTA owns a contiguous run of steps; its warps
-  // claim them one at a time (each warp sees ascending steps: the ordered
-  // buffers rely on it) so warps that draw more bandwidth take more.
-  const u64 cta_lo = (u64)blockIdx.x * a.n_steps / gridDim.x;
-  const u64 cta_hi = ((u64)blockIdx.x + 1) * a.n_steps / gridDim.x;
   const u64 pol = l2_evict_first_policy();
   const u32 half = (u32)lane / LPP;  // position within a cp.async group
+  u32 T = T_OPEN;  // accept d < T
   auto issue = [&](u32 st) {
     u64 t = 0;
+    u32 mt = 0;
     if (lane == 0) {
-      t = cta_lo + atomicAdd(&s_next, 1u);
-      if (t >= cta_hi) t = PQ_NONE;
+      for (;;) {
+        t = cta_lo + atomicAdd(&s_next, 1u);
+        if (t >= cta_hi) {
+          t = PQ_NONE;
+          break;
+        }
+        if (!SORTED) break;
+        // d >= ||a| - |q||: a step whose popcount range stays T away is not read
+        mt = s_meta[t - cta_lo];
+        const u32 lo = mt & 0xffu, hi = mt >> 8;
+        const u32 lb = pop < lo ? lo - pop : (pop > hi ? pop - hi : 0u);
+        if (lb < T) break;
+      }
       slot_step[st] = t;
       if (COPY == 0) {
         if (t == PQ_NONE) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
@@ -238,14 +308,17 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     t = __shfl_sync(FULL, t, 0);
     if (COPY == 1) {
       if (t != PQ_NONE) {
+        // one |a| for the whole step: its popcount planes are not needed
+        mt = __shfl_sync(FULL, mt, 0);
+        const u32 g0 = (SORTED && (mt & 0xffu) == (mt >> 8)) ? 8 / PPI : 0u;
         // one instruction moves 512 B: lanes [LPP*j, LPP*j + LPP) copy 16 B
         // each of position PPI*i + j; source = plane base + a per-stage offset
-        u32 dst = smem_u32(ring + st * stage_bytes) + half * PQ_CHUNK + (lane % LPP) * 16;
+        u32 dst = smem_u32(ring + st * stage_bytes) + half * PQ_CHUNK + (lane % LPP) * 16 + g0 * PPI * PQ_CHUNK;
         const u64 off = t * PQ_CHUNK + (lane % LPP) * 16;
         const u64* bp = reinterpret_cast<const u64*>(s_base) + half;
         const u32 ngrp = nc / PPI;
 #pragma unroll 4
-        for (u32 i = 0; i < ngrp; ++i) {
+        for (u32 i = g0; i < ngrp; ++i) {
           const char* sp = reinterpret_cast<const char*>(bp[PPI * i]) + off;
           asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(sp), "l"(pol)
                        : "memory");
@@ -275,7 +348,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   u64* wbuf = a.buf + g * (u64)a.cap;
-  u32 T = T_OPEN;  // accept d < T
+  u64* tie_scratch = reinterpret_cast<u64*>(pqs + pq_smem(nwb, a.ring_bytes) - (size_t)nwb * 32 * 8) + wib * 32;
   const volatile u32* tgw = tgrep(a, 0, (u32)(g % a.tg_rep));  // this warp's replica of the bound
   u32 tgp = (a.flags & 2) ? T_OPEN : *tgw;
   const bool publisher = !(a.flags & 1) && (g % a.pub_every) == 0;
@@ -307,11 +380,56 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     return (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
   };
 
-  auto compact = [&]() {  // ordered compaction to the k best (buffer is in index order)
+  // Compaction to the k best by (d, index): every entry with d < tt (the
+  // k-th distance), then m = k - count(d < tt) of the ties. In index order
+  // (unsorted copy) those are the first m ties in the buffer; on the sorted
+  // copy the m smallest indices among the ties.
+  auto compact = [&]() {
     const u32 n0 = ws->cnt[0];
     u32 less;
     const u32 tt = warp_kth_bin(hist, a.k, lane, &less);
     const u32 mk = a.k - less;
+    u64 cut = IDX_MASK;  // SORTED: keep ties with index <= cut
+    if (SORTED && hist[tt] > mk) {
+      const u32 ntie = hist[tt];
+      if (ntie <= 32) {
+        u32 tp = 0;
+        for (u32 i0 = 0; i0 < n0; i0 += 32) {
+          const u32 i = i0 + lane;
+          const u64 key = i < n0 ? wbuf[i] : ~0ull;
+          const bool tie = i < n0 && key_d(key) == tt;
+          const u32 tb = __ballot_sync(FULL, tie);
+          if (tie) tie_scratch[tp + __popc(tb & lanemask_lt())] = key & IDX_MASK;
+          tp += __popc(tb);
+        }
+        __syncwarp();
+        const u64 mine = (u32)lane < ntie ? tie_scratch[lane] : ~0ull;
+        u32 rank = 0;
+        for (u32 j = 0; j < ntie; ++j) rank += tie_scratch[j] < mine ? 1u : 0u;
+        const u32 sel = __ballot_sync(FULL, (u32)lane < ntie && rank == mk - 1);
+        cut = __shfl_sync(FULL, mine, __ffs(sel) - 1);
+        __syncwarp();
+      } else {
+        // many ties: the mk-th smallest tie index, MSB first over the buffer
+        u64 pref = 0;
+        u32 r = mk;
+        for (int b = IDX_BITS - 1; b >= 0; --b) {
+          u32 c = 0;
+          for (u32 i0 = 0; i0 < n0; i0 += 32) {
+            const u32 i = i0 + lane;
+            const u64 key = i < n0 ? wbuf[i] : ~0ull;
+            const u64 idx = key & IDX_MASK;
+            const bool ok = i < n0 && key_d(key) == tt && (idx >> (b + 1)) == (pref >> (b + 1)) && !((idx >> b) & 1ull);
+            c += __popc(__ballot_sync(FULL, ok));
+          }
+          if (c < r) {
+            r -= c;
+            pref |= 1ull << b;
+          }
+        }
+        cut = pref;
+      }
+    }
     u32 outp = 0, ties = 0;
     for (u32 i0 = 0; i0 < n0; i0 += 32) {
       const u32 i = i0 + lane;
@@ -320,7 +438,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       const u32 d = key_d(key);
       const bool lt = vld && d < tt, tie = vld && d == tt;
       const u32 tb = __ballot_sync(FULL, tie);
-      const bool keep = lt || (tie && ties + __popc(tb & lanemask_lt()) < mk);
+      const bool keep = lt || (tie && (SORTED ? (key & IDX_MASK) <= cut : ties + __popc(tb & lanemask_lt()) < mk));
       const u32 kb = __ballot_sync(FULL, keep);
       const u32 pp = outp + __popc(kb & lanemask_lt());
       __syncwarp();
@@ -348,11 +466,37 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     if (ws->cnt[0] + total > a.cap) compact();
     const u32 cnt0 = ws->cnt[0];
     u32 pos = cnt0 + incl - cntl;
-    for (u64 rest = mm; rest; rest &= rest - 1) {
-      const int e = __ffsll((long long)rest) - 1;
-      const u32 d = dfn(BPL == 2 ? (e >> 5) : 0, e & 31);
-      wbuf[pos++] = make_key(d, a.index_base + bfirst + e);
-      atomicAdd(hist + d, 1u);
+    if (SORTED) {
+      // eight index lookups in flight at a time (a dependent load per entry
+      // would cost a memory round trip each)
+      for (u64 rest = mm; rest;) {
+        int es[8];
+        u32 li[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          es[j] = -1;
+          if (rest) {
+            es[j] = __ffsll((long long)rest) - 1;
+            rest &= rest - 1;
+            li[j] = __ldg(a.perm + bfirst + es[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (es[j] >= 0) {
+            const u32 d = dfn(BPL == 2 ? (es[j] >> 5) : 0, es[j] & 31);
+            wbuf[pos++] = make_key(d, a.index_base + li[j]);
+            atomicAdd(hist + d, 1u);
+          }
+        }
+      }
+    } else {
+      for (u64 rest = mm; rest; rest &= rest - 1) {
+        const int e = __ffsll((long long)rest) - 1;
+        const u32 d = dfn(BPL == 2 ? (e >> 5) : 0, e & 31);
+        wbuf[pos++] = make_key(d, a.index_base + bfirst + e);
+        atomicAdd(hist + d, 1u);
+      }
     }
     __syncwarp();
     if (lane == 0) ws->cnt[0] = cnt0 + total;
@@ -386,7 +530,9 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
       tpend = true;
     }
-    T = town < T ? town : T;
+    // (sorted order: entries at the own k-th distance may still precede by index)
+    const u32 tn = SORTED ? town + 1 : town;
+    T = tn < T ? tn : T;
     __syncwarp();
   };
   // first-step entries held back (bit-sliced distances, valid masks)
@@ -466,12 +612,20 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       }
     };
     u32 A[BPL][8];
+    const u32 mt = SORTED ? (u32)s_meta[t - cta_lo] : 0u;
+    if (SORTED && (mt & 0xffu) == (mt >> 8)) {  // one popcount for the step
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      u32 v[BPL];
-      ldp(lb + i * PQ_CHUNK, v);
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int h = 0; h < BPL; ++h) A[h][i] = v[h];
+        for (int h = 0; h < BPL; ++h) A[h][i] = ((mt >> i) & 1u) ? FULL : 0u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        u32 v[BPL];
+        ldp(lb + i * PQ_CHUNK, v);
+#pragma unroll
+        for (int h = 0; h < BPL; ++h) A[h][i] = v[h];
+      }
     }
     const u64 blk_first = t * PQ_STEP + (u64)lane * 32 * BPL;  // local index of bit 0 of this lane's first block
     u32 valid[BPL];
@@ -658,7 +812,8 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
         }
         // >= k entries of this step have d <= town1 and a smaller index than
         // any later entry: later entries need d < town1
-        T = town1 < T ? town1 : T;
+        const u32 tn = SORTED ? town1 + 1 : town1;
+        T = tn < T ? tn : T;
         Tsv = town1 + 1;
       }
 #ifdef FPS_SCAN_TRACE

@@ -556,3 +556,69 @@ def test_plane_scan_bound_refresh_periods(refresh, monkeypatch):
         q = _query_with_pop(rng, pop)
         for k in (10, 100):
             assert lib.search(q, k) == oracle_topk(w, q[None], k)[0], (refresh, pop, k)
+
+
+# ---------------------------------------------------------------- popcount-sorted plane copy
+@pytest.mark.parametrize("n", [1, 2047, 2049, 100_003, 300_001])
+def test_sorted_plane_scan_sizes_and_densities(n, monkeypatch):
+    """FPS_PQ_SORTED=1: planes ordered by popcount (uniform-|a| steps skip the
+    popcount planes, out-of-range steps are skipped, ties at the own k-th
+    distance resolved by index)."""
+    monkeypatch.setenv("FPS_PQ_SORTED", "1")
+    seed = 4000 + n
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(n + 1)
+    for pop in (0, 9, 38, 84, 140):
+        q = _query_with_pop(rng, pop)
+        for k in (1, 10, 100, 1024):
+            exp = oracle_topk(w, q[None], k)[0]
+            assert lib.search(q, k) == exp, (n, pop, k)
+            assert _dev_topk(lib, q[None], k) == exp, (n, pop, k)
+    # library entries as queries (planted-like: distance 0 exists)
+    for i in (0, n // 3, n - 1):
+        q = w[i].copy()
+        assert lib.search(q, 10) == oracle_topk(w, q[None], 10)[0]
+
+
+@pytest.mark.parametrize("bpl,warps", [(2, 8), (1, 16), (2, 3)])
+def test_sorted_plane_scan_ties_and_adversarial(bpl, warps, monkeypatch):
+    monkeypatch.setenv("FPS_PQ_SORTED", "1")
+    monkeypatch.setenv("FPS_PQ_BPL", str(bpl))
+    monkeypatch.setenv("FPS_PQ_WARPS", str(warps))
+    # every entry identical: the first k indices, ties overflow the scratch
+    w = np.tile(np.array([[0x1234, 0x5678, 0x9]], dtype=np.uint64), (200_000, 1))
+    lib = Library.from_words(w)
+    for k in (1, 10, 33, 100, 1024):
+        assert lib.search(np.array([0x1234, 0x5678, 0x8], dtype=np.uint64), k) == [(i, 1) for i in range(k)]
+    # two popcount classes interleaved by index, equal distances across classes
+    rng = np.random.default_rng(5)
+    base = np.array([0x0F0F, 0x3, 0x0], dtype=np.uint64)
+    w2 = np.tile(base, (150_000, 1))
+    flip = rng.integers(0, 2, 150_000).astype(bool)
+    w2[flip, 1] ^= np.uint64(0x4)          # one extra key: popcount +1, distance 1
+    w2[~flip, 0] ^= np.uint64(0x1)         # one key fewer: popcount -1, distance 1
+    lib2 = Library.from_words(w2)
+    for k in (5, 64, 500):
+        assert lib2.search(base, k) == oracle_topk(w2, base[None], k)[0]
+    # distances falling with the index
+    n = 120_000
+    w3 = np.zeros((n, 3), dtype=np.uint64)
+    bits = 166 - (np.arange(n) * 166 // n)
+    for i, b in enumerate(bits):
+        v = (1 << int(b)) - 1
+        w3[i] = (v & (2**64 - 1), (v >> 64) & (2**64 - 1), v >> 128)
+    lib3 = Library.from_words(w3)
+    for k in (10, 100, 500):
+        assert lib3.search(np.zeros(3, dtype=np.uint64), k) == oracle_topk(w3, np.zeros((1, 3), np.uint64), k)[0]
+
+
+def test_sorted_plane_scan_config_shapes(monkeypatch):
+    """C1/C2-shaped runs (planted near-duplicates: small bounds prune popcount classes)."""
+    monkeypatch.setenv("FPS_PQ_SORTED", "1")
+    for wl, n in (("c1", 1_000_000), ("c2", 2_000_000)):
+        plan = synth.make_plan(wl, n=n, planted_per_query=200 if wl == "c2" else None)
+        lib, q = synth.build_library(plan)
+        w = lib.words_host()
+        assert lib.search(q[0], plan.k) == oracle_topk(w, q[:1], plan.k)[0]
+        assert _dev_topk(lib, q[:1], plan.k) == oracle_topk(w, q[:1], plan.k)[0]
