@@ -149,6 +149,13 @@ struct fps_lib {
   DevBuf pm, pm_perm, pm_meta;
   int pm_state = 0;  // as bs_state
   bool pm_sorted = false;  // pm holds the popcount-sorted copy (pm_perm, pm_meta valid)
+  // plane-scan knobs (FPS_PQ_*), read from the environment once per handle:
+  // getenv is a linear scan of the environment, and this is the per-call path
+  struct PqKnobs {
+    bool init = false, sorted = false;
+    int bpl = 0, warps = 8, stages = 2, smem_kb = 210, copy = 1, refresh = 0;
+  } pqk;
+  u32 done_seq = 0;  // completion sequence of the single-query host path
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -335,7 +342,7 @@ void set_dyn(fps_lib* L, fps::ScanArgs& a) {
 // inside it orders it after the scan's completion (and memory flush).
 cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
                           u32* ghist, u32 gstride, u32 tg_rep, u32 k, u64* out_keys, u32* out_cnt, bool pdl,
-                          u32* dyn_ctr = nullptr) {
+                          u32* dyn_ctr = nullptr, u32* done_flag = nullptr, u32 done_seq = 0) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(Q);
   cfg.blockDim = dim3(fps::SEL_THREADS);
@@ -347,7 +354,7 @@ cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* ca
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, fps::select_kernel, cand, cand_cnt, cand_cap, tg, ghist, gstride, tg_rep, k, out_keys,
-                            out_cnt, 1, dyn_ctr);
+                            out_cnt, 1, dyn_ctr, done_flag, done_seq);
 }
 
 // Record an event pair around the next scan-kernel launch when timing is on.
@@ -707,20 +714,27 @@ int pm_ensure(fps_lib* L, bool sorted) {
 bool pq_wanted(fps_lib* L) {
   const char* e = std::getenv("FPS_PLANEQ");  // "0": the POPC scan (tests cover both)
   if ((e && std::string(e) == "0") || L->n == 0) return false;
-  // FPS_PQ_SORTED=1: the popcount-sorted plane copy (SORTED kernels)
-  const char* so = std::getenv("FPS_PQ_SORTED");
-  const bool sorted = so ? std::string(so) == "1" : false;
-  if (pm_ensure(L, sorted) != FPS_OK) {
+  if (!L->pqk.init) {
+    auto ev = [](const char* name, int dflt) {
+      const char* v = std::getenv(name);
+      return v ? std::atoi(v) : dflt;
+    };
+    L->pqk.sorted = ev("FPS_PQ_SORTED", 0) == 1;  // the popcount-sorted plane copy (SORTED kernels)
+    L->pqk.bpl = ev("FPS_PQ_BPL", 2) == 1 ? 1 : 2;
+    L->pqk.warps = std::max(1, std::min(16, ev("FPS_PQ_WARPS", 8)));
+    L->pqk.stages = std::max(1, std::min(fps::PQ_SMAX, ev("FPS_PQ_STAGES", 2)));
+    L->pqk.smem_kb = ev("FPS_PQ_SMEM_KB", 210);
+    L->pqk.copy = ev("FPS_PQ_COPY", 1) == 1 ? 1 : 0;
+    L->pqk.refresh = ev("FPS_PQ_REFRESH", 0);
+    L->pqk.init = true;
+  }
+  if (pm_ensure(L, L->pqk.sorted) != FPS_OK) {
     cudaGetLastError();
     return false;
   }
   return L->pm_state == 1;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
 
 // Stage positions of a query: 8 popcount planes + its listed planes padded to 8.
 u32 pq_positions(const u64* q) {
@@ -732,25 +746,25 @@ u32 pq_positions(const u64* q) {
 }
 
 int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
-            bool prepare_only) {
+            bool prepare_only, u32* done_flag = nullptr, u32 done_seq = 0) {
   int rc;
   // Shape (tools/pq_sweep.py, profiles/r01_experiments.md): 8 warps x two
   // 32-entry blocks per lane x 2 ring stages; long scans read the global
   // bound every 8th step (C3 109.5 -> 95.5 us), short ones every step (the
   // first steps set it: C2 29.1 vs 33.5 us).
   const bool long_scan = L->n >= (32u << 20);
-  const int bpl = env_int("FPS_PQ_BPL", 2) == 1 ? 1 : 2;  // 32-entry blocks per lane
+  const int bpl = L->pqk.bpl;  // 32-entry blocks per lane
   const u32 chunk = bpl == 1 ? fps::PqStep<1>::CHUNK : fps::PqStep<2>::CHUNK;
   const u64 step_entries = bpl == 1 ? fps::PqStep<1>::ENTRIES : fps::PqStep<2>::ENTRIES;
-  const int nwb = std::max(1, std::min(16, env_int("FPS_PQ_WARPS", 8)));
-  const int stages = std::max(1, std::min(fps::PQ_SMAX, env_int("FPS_PQ_STAGES", 2)));
+  const int nwb = L->pqk.warps;
+  const int stages = L->pqk.stages;
   // ring per warp: `stages` stages of a typical list (48 positions = up to
   // 40 listed planes); wider lists fold warps in the kernel; with the query
   // on the host the ring is sized to it exactly
   const u32 np = h_qin ? pq_positions(h_qin) : 48;
   // (capped by the shared memory of one CTA; at least two stages of the
   // widest list over the whole CTA)
-  const u32 budget = (u32)env_int("FPS_PQ_SMEM_KB", 210) * 1024;
+  const u32 budget = (u32)L->pqk.smem_kb * 1024;
   const u32 ring_cap = (u32)((budget - (u32)fps::pq_smem(nwb, 0)) / nwb) / 256 * 256;
   u32 ring = std::min<u32>((u32)stages * np * chunk, ring_cap);
   ring = std::max<u32>(ring, (u32)((2 * fps::PQ_NPMAX * chunk + nwb - 1) / nwb + 255) / 256 * 256);
@@ -766,7 +780,7 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   if ((rc = ensure_state(L, 1))) return rc;
   if ((rc = L->buf.ensure(warps * (size_t)cap * 8))) return rc;
   if ((rc = L->cand.ensure(cand_cap * 8))) return rc;
-  const int copy = env_int("FPS_PQ_COPY", 1);  // 1: cp.async 16 B per lane (default, measured faster), 0: bulk copies
+  const int copy = L->pqk.copy;  // 1: cp.async 16 B per lane (default, measured faster), 0: bulk copies
   const int kv = srt ? 4 + (bpl == 2 ? 1 : 0) : (copy == 1 ? 1 : 0) * 2 + (bpl == 2 ? 1 : 0);
   void (*const kerns[6])(fps::PqArgs) = {fps::pq_scan_kernel<0, 1, false>, fps::pq_scan_kernel<0, 2, false>,
                                          fps::pq_scan_kernel<1, 1, false>, fps::pq_scan_kernel<1, 2, false>,
@@ -789,7 +803,7 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   a.cap = cap;
   a.n_steps = steps;
   a.ring_bytes = ring;
-  a.refresh = (u32)std::max(1, env_int("FPS_PQ_REFRESH", long_scan ? 8 : 1));
+  a.refresh = (u32)(L->pqk.refresh > 0 ? L->pqk.refresh : (long_scan ? 8 : 1));
   a.perm = srt ? L->pm_perm.as<u32>() : nullptr;
   a.meta = srt ? reinterpret_cast<const unsigned short*>(L->pm_meta.p) : nullptr;
   a.meta_cap = meta_cap;
@@ -828,10 +842,11 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
     sel_attr = true;
   }
   CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, s, a.cand, a.cand_cnt, cand_cap, a.tg, a.ghist,
-                         a.gstride, a.tg_rep, k, d_keys, d_cnt, !(a.flags & 32)));
+                         a.gstride, a.tg_rep, k, d_keys, d_cnt, !(a.flags & 32), nullptr, done_flag, done_seq));
   L->launches++;
   LAUNCH_CHECK("select_kernel (plane scan)");
-  if (std::getenv("FPS_DEBUG"))
+  static const bool dbg = std::getenv("FPS_DEBUG") != nullptr;
+  if (dbg)
     std::fprintf(stderr, "[fps] plane scan: grid=%llu warps/CTA=%d ring=%u smem=%zu\n", (unsigned long long)grid, nwb,
                  ring, smem);
   return FPS_OK;
@@ -1605,7 +1620,7 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
   if (Q == 1 && k <= KMAX_FUSED && !lib->timing) {
     // single query: the query travels as a kernel parameter and the select
     // kernel writes straight into mapped pinned memory -- two launches, no copies
-    const size_t need = (size_t)k * 8 + 64;
+    const size_t need = (size_t)k * 8 + 64 + 64;  // keys, count, completion flag
     if (lib->hmap_bytes < need) {
       if (lib->hmap) cudaFreeHost(lib->hmap);
       lib->hmap = nullptr;
@@ -1615,6 +1630,8 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
         cudaGetLastError();
         lib->hmap = nullptr;
       } else {
+        std::memset(lib->hmap, 0, need);  // completion flag starts below any sequence number
+        lib->done_seq = 0;
         lib->hmap_bytes = need;
       }
     }
@@ -1622,11 +1639,31 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
       u64* dk = reinterpret_cast<u64*>(lib->dmap);
       u32* dc = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->dmap) + (size_t)k * 8);
       lib->last_kernel = 1;
-      rc = pq_wanted(lib) ? topk_pq(lib, nullptr, reinterpret_cast<const u64*>(queries), k, dk, dc, lib->stream, false)
+      // plane scan: select_kernel posts a sequence number into mapped memory
+      // after the results; the host spins on it (no stream query per spin)
+      u32* hflag = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->hmap) + (size_t)k * 8 + 64);
+      u32* dflag = reinterpret_cast<u32*>(reinterpret_cast<char*>(lib->dmap) + (size_t)k * 8 + 64);
+      const bool pq = pq_wanted(lib);
+      const u32 seq = ++lib->done_seq;
+      rc = pq ? topk_pq(lib, nullptr, reinterpret_cast<const u64*>(queries), k, dk, dc, lib->stream, false, dflag, seq)
          : lib->compact ? topk_fused<1, 4, true>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries))
                         : topk_fused<1, 4, false>(lib, nullptr, 1, k, dk, dc, lib->stream, false, 0, reinterpret_cast<const u64*>(queries));
       if (rc) { reset_state(lib); return rc; }
-      cudaError_t e = wait_stream(lib->stream);
+      cudaError_t e = cudaSuccess;
+      if (pq) {
+        for (u32 spin = 1; *(volatile u32*)hflag != seq; ++spin) {
+          if ((spin & 255) == 0) {  // a failed launch never posts: check the stream now and then
+            e = cudaStreamQuery(lib->stream);
+            if (e == cudaErrorNotReady) { e = cudaSuccess; continue; }
+            if (e != cudaSuccess || *(volatile u32*)hflag == seq) break;
+            e = cudaErrorUnknown;  // stream idle without the flag
+            break;
+          }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+      } else {
+        e = wait_stream(lib->stream);
+      }
       if (e != cudaSuccess) {
         reset_state(lib);
         return fail(FPS_ECUDA, std::string("top-k: ") + cudaGetErrorString(e));

@@ -960,10 +960,21 @@ __device__ __forceinline__ u32 select_small(u64 my, u32 n, bool keep, u64* sh, u
   return m;
 }
 
+// Host-visible completion (single-query host path, one CTA): the results
+// written by every thread, then the sequence number, at system scope.
+__device__ __forceinline__ void post_done(u32* done_flag, u32 done_seq) {
+  if (!done_flag) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *(volatile u32*)done_flag = done_seq;
+  }
+}
+
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
                                                              u32* ghist, u32 gstride, u32 tg_rep, u32 k,
                                                              u64* out_keys, u32* out_cnt, int reset,
-                                                             u32* dyn_ctr) {
+                                                             u32* dyn_ctr, u32* done_flag, u32 done_seq) {
   extern __shared__ u64 ssel[];  // [k_pow2] result + [SEL_ECAP] ties
   __shared__ u32 hist[256];
   __shared__ u32 s_nres, s_ntie, s_T, s_m;
@@ -1015,6 +1026,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
       if (threadIdx.x == 0) cand_cnt[q] = 0;
       if (dyn_ctr && q == 0 && threadIdx.x == 0) *dyn_ctr = 0;
     }
+    post_done(done_flag, done_seq);
     return;
   }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
@@ -1160,6 +1172,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
     if (threadIdx.x == 0) cand_cnt[q] = 0;
     if (dyn_ctr && q == 0 && threadIdx.x == 0) *dyn_ctr = 0;
   }
+  post_done(done_flag, done_seq);
 }
 
 // ---------------------------------------------------------------------------

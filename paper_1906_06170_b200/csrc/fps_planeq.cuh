@@ -768,47 +768,67 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       for (int h = 0; h < BPL; ++h) nv += __popc(valid[h]);
       nv = __reduce_add_sync(FULL, nv);
       // r-th smallest distance of the step (1-based, r <= nv), MSB first
-      auto rsel = [&](u32 r) -> u32 {
-        u32 msk[BPL];
+      // NR radix selects at once (r-th smallest distance of the step, 1-based,
+      // r <= nv), MSB first: the NR warp reductions of a bit are independent
+      // and overlap their latency
+      auto rsel = [&](const auto& rs, auto& out) {
+        constexpr int NR = sizeof(rs) / sizeof(rs[0]);
+        u32 msk[NR][BPL], rr[NR];
 #pragma unroll
-        for (int h = 0; h < BPL; ++h) msk[h] = valid[h];
-        u32 val = 0;
+        for (int j = 0; j < NR; ++j) {
+          rr[j] = rs[j];
+          out[j] = 0;
+#pragma unroll
+          for (int h = 0; h < BPL; ++h) msk[j][h] = valid[h];
+        }
 #pragma unroll
         for (int b = 7; b >= 0; --b) {
-          u32 c = 0;
+          u32 c[NR];
 #pragma unroll
-          for (int h = 0; h < BPL; ++h) c += __popc(msk[h] & ~Dsv[h][b]);
-          c = __reduce_add_sync(FULL, c);
-          if (c >= r) {
+          for (int j = 0; j < NR; ++j) {
+            c[j] = 0;
 #pragma unroll
-            for (int h = 0; h < BPL; ++h) msk[h] &= ~Dsv[h][b];
-          } else {
-            r -= c;
-            val |= 1u << b;
+            for (int h = 0; h < BPL; ++h) c[j] += __popc(msk[j][h] & ~Dsv[h][b]);
+          }
 #pragma unroll
-            for (int h = 0; h < BPL; ++h) msk[h] &= Dsv[h][b];
+          for (int j = 0; j < NR; ++j) c[j] = __reduce_add_sync(FULL, c[j]);
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const bool zero = c[j] >= rr[j];
+            if (!zero) {
+              rr[j] -= c[j];
+              out[j] |= 1u << b;
+            }
+#pragma unroll
+            for (int h = 0; h < BPL; ++h) msk[j][h] &= zero ? ~Dsv[h][b] : Dsv[h][b];
           }
         }
-        return val;
       };
       Tsv = 256;  // fewer than k entries: every one is a candidate
       if (nv >= a.k) {
         u32 town1 = 0;
         if (publisher) {
-          u32 prev = 0;
-#pragma unroll 1
-          for (u32 r = 1;; r = (2 * r < a.k && r < 8) ? 2 * r : a.k) {
-            const u32 tr = rsel(r);
-            if (lane == 0) atomicAdd(gbin(a, 0, tr), r - prev);
-            prev = r;
-            if (r == a.k) { town1 = tr; break; }
+          // witnesses: 1 at the smallest distance, 1 at the 2nd, 2 at the 4th,
+          // k - 4 at the k-th (ranks capped at k)
+          const u32 rs[4] = {1u, min(2u, a.k), min(4u, a.k), a.k};
+          u32 ts[4];
+          rsel(rs, ts);
+          if (lane < 4) {
+            const u32 prev = lane == 0 ? 0u : lane == 1 ? rs[0] : lane == 2 ? rs[1] : rs[2];
+            const u32 tl = lane == 0 ? ts[0] : lane == 1 ? ts[1] : lane == 2 ? ts[2] : ts[3];
+            const u32 rl = lane == 0 ? rs[0] : lane == 1 ? rs[1] : lane == 2 ? rs[2] : rs[3];
+            if (rl > prev) atomicAdd(gbin(a, 0, tl), rl - prev);
           }
+          town1 = ts[3];
           if (lane == 0) ws->pubd[0] = 1;
 #pragma unroll
           for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
           tpend = true;
         } else {
-          town1 = rsel(a.k);
+          const u32 rs[1] = {a.k};
+          u32 ts[1];
+          rsel(rs, ts);
+          town1 = ts[0];
         }
         // >= k entries of this step have d <= town1 and a smaller index than
         // any later entry: later entries need d < town1
