@@ -23,6 +23,7 @@
 #include "fps_bitslice.cuh"
 #include "fps_kernels.cuh"
 #include "fps_planeq.cuh"
+#include "fps_mma.cuh"
 
 using fps::u32;
 using fps::u64;
@@ -156,6 +157,9 @@ struct fps_lib {
     int bpl = 0, warps = 8, stages = 2, smem_kb = 210, copy = 1, refresh = 0;
   } pqk;
   u32 done_seq = 0;  // completion sequence of the single-query host path
+  // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
+  DevBuf mm_apop, mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp;
+  bool mm_apop_ok = false;
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -852,8 +856,131 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   return FPS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// tensor-core multi-query path (fps_mma.cuh), opt-in: FPS_MMA=1
+// ---------------------------------------------------------------------------
+// Large batches take the tensor cores: one 256-query chunk costs ~4.4 ms on
+// the 95.4 M library against ~4.1 ms for 128 queries on the bit-sliced
+// kernel (tools/mma_time.py, tools/q_sweep.py). FPS_MMA=1 forces it for any
+// batch >= 2, FPS_MMA=0 disables it. Not under stream capture: the call
+// checks the candidate lists on the host before its select.
+bool mma_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
+  const char* e = std::getenv("FPS_MMA");
+  const int mode = e ? std::atoi(e) : -1;
+  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M) return false;
+  if (mode != 1 && Q < 192) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
+             bool* fallback) {
+  int rc;
+  *fallback = false;
+  // 1. seed bound: exact top-k of a library prefix (POPC scan)
+  const u64 seed_n = std::min<u64>(L->n, 1 << 18);
+  L->timing_suspend = true;
+  rc = L->compact ? topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n)
+                  : topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n);
+  L->timing_suspend = false;
+  if (rc) return rc;
+  const u32 nchunks = (Q + fps::MM_N - 1) / fps::MM_N;
+  const u64 n_tiles = (L->n + fps::MM_M - 1) / fps::MM_M;
+  const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles));
+  // candidates per query: pairs within the seed bound (~k x N / seed_n expected)
+  const u64 expect = (u64)k * (L->n / std::max<u64>(seed_n, 1) + 1);
+  const u32 cap = (u32)std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
+  if ((rc = L->mm_bop.ensure((size_t)nchunks * fps::MM_B_BYTES)) || (rc = L->mm_ucol.ensure((size_t)nchunks * fps::MM_N * 4)) ||
+      (rc = L->mm_qpop.ensure((size_t)nchunks * fps::MM_N * 4)) || (rc = L->mm_tq.ensure((size_t)Q * 4)) ||
+      (rc = L->mm_qcol.ensure((size_t)nchunks * fps::MM_N * 4)) || (rc = L->mm_keys.ensure((size_t)Q * 8)) ||
+      (rc = L->mm_sorted.ensure((size_t)Q * 8)) ||
+      (rc = L->cand.ensure((size_t)Q * cap * 8)) || (rc = L->mm_apop.ensure(std::max<u64>(L->n, 1))))
+    return rc;
+  static bool attr = false;
+  const size_t smem = fps::MM_B_BYTES + (size_t)fps::MM_STAGES * fps::MM_A_BYTES;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(fps::mma_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  if (prepare_only) return FPS_OK;
+  if (!L->mm_apop_ok) {
+    fps::mm_pop_kernel<<<L->sms * 8, 256, 0, s>>>(L->out(), L->n, L->mm_apop.as<unsigned char>());
+    L->launches++;
+    L->mm_apop_ok = true;
+  }
+  fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
+  fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q), ghist_stride(Q));
+  fps::mm_ukeys_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_q, Q, L->mm_tq.as<u32>(), L->mm_keys.as<u64>());
+  {
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
+    if ((rc = L->mm_tmp.ensure(tb))) return rc;
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(L->mm_tmp.p, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
+  }
+  fps::mm_prep_kernel<<<(nchunks * fps::MM_N + 127) / 128, 128, 0, s>>>(
+      d_q, Q, L->mm_tq.as<u32>(), L->mm_bop.as<unsigned char>(), L->mm_ucol.as<int>(), L->mm_qpop.as<u32>(), nchunks,
+      L->mm_sorted.as<u64>(), L->mm_qcol.as<u32>());
+  L->launches += 5;
+  LAUNCH_CHECK("mm_prep");
+  fps::MmArgs a{};
+  a.lib = L->out();
+  a.n = L->n;
+  a.index_base = L->index_base;
+  a.n_tiles = n_tiles;
+  a.Q = Q;
+  a.nchunks = nchunks;
+  a.parts = parts;
+  a.bop = L->mm_bop.as<unsigned char>();
+  a.ucol = L->mm_ucol.as<int>();
+  a.qpop = L->mm_qpop.as<u32>();
+  a.qcol = L->mm_qcol.as<u32>();
+  a.apop = L->mm_apop.as<unsigned char>();
+  a.cand = L->cand.as<u64>();
+  a.cand_cnt = L->cand_cnt.as<u32>();
+  a.cap = cap;
+  a.mode = 0;
+  a.flags = scan_flags();
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::mma_scan_kernel<<<nchunks * parts, fps::MM_THREADS, smem, s>>>(a);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  LAUNCH_CHECK("mma_scan_kernel");
+  // candidate lists must fit their capacity (else: the bit-sliced kernel)
+  std::vector<u32> cc(Q);
+  CUDA_TRY(cudaMemcpyAsync(cc.data(), L->cand_cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  u32 mx = 0;
+  for (u32 v : cc) mx = std::max(mx, v);
+  if (std::getenv("FPS_DEBUG"))
+    std::fprintf(stderr, "[fps] mma scan: Q=%u chunks=%u parts=%u cap=%u max candidates=%u\n", Q, nchunks, parts, cap, mx);
+  if (mx > cap) {
+    reset_state(L);
+    *fallback = true;
+    return FPS_OK;
+  }
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, a.cand, a.cand_cnt, cap, L->tg.as<u32>(),
+                         L->ghist.as<u32>(), ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt, false));
+  L->launches++;
+  LAUNCH_CHECK("select_kernel (mma)");
+  return FPS_OK;
+}
+
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
                   bool prepare_only) {
+  if (mma_wanted(L, Q, s)) {
+    bool fb = false;
+    L->last_kernel = 6;
+    const int rc = topk_mma(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, &fb);
+    if (rc || !fb) return rc;
+  }
   if (Q == 1 && pq_wanted(L)) return topk_pq(L, d_q, nullptr, k, d_keys, d_cnt, s, prepare_only);
   if (bs_wanted(L, Q)) {
     L->last_kernel = 3;

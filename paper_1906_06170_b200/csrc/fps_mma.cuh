@@ -1,0 +1,330 @@
+// fps_mma.cuh — multi-query scan on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM). Opt-in (FPS_MMA=1).
+//
+// For 0/1 vectors the AND-popcount is a dot product: c = |a AND q| = a . q,
+// and the reference distance (scan.py:137-143, popcount of the XOR of the
+// three full words) is d = |a| + |q| - 2c, with |a|, |q| counted over all
+// 192 bits (pad bits included, as the reference XORs them). So a batch of
+// queries against a library tile is an int8 GEMM with K = 192 (keys 1..166 +
+// pad bits): A = 128 library entries x 192 bytes (0/1), B = 256 queries x 192
+// bytes, D = 128 x 256 int32 in TMEM. The test d <= T_q is
+// 2c + (T_q - |q|) >= |a|.
+//
+// Exactness: T_q is the k-th distance of a seed pass over a library prefix
+// (every seed entry is in the library, so the true k-th distance is <= T_q);
+// every pair with d <= T_q is collected into the query's candidate list and
+// select_kernel keeps the k smallest (distance, index). Lists that overflow
+// their capacity are reported and the batch is recomputed by the bit-sliced
+// kernel.
+//
+// CTA = 9 warps, one CTA per SM: warps 0-3 expand library tiles from the
+// tiled u64 library into the canonical K-major int8 layout (a thread per
+// entry row, nibble -> 4 bytes through a 16-entry table) in a 4-stage
+// shared-memory ring; warp 8 (one lane) issues the MMAs (6 x K=32 per tile)
+// into one of two TMEM accumulators and commits them to mbarriers; warps 4-7
+// (TMEM lane quadrants 0-3) read the accumulators with tcgen05.ld and test
+// 16 columns at a time (max first, exact check only when it can pass).
+#pragma once
+#include "fps_kernels.cuh"
+
+namespace fps {
+
+constexpr int MM_M = 128;          // entries per tile (TMEM lanes)
+constexpr int MM_N = 256;          // queries per CTA chunk (TMEM columns per accumulator)
+constexpr int MM_K = 192;          // bytes per row (3 x 64 bits)
+constexpr int MM_STAGES = 4;
+constexpr u32 MM_A_BYTES = MM_M * MM_K;  // 24 KB
+constexpr u32 MM_B_BYTES = MM_N * MM_K;  // 48 KB
+constexpr int MM_EPI = 8;                 // epilogue warps: 2 per TMEM lane quadrant, each half the columns
+constexpr int MM_THREADS = (4 + MM_EPI + 1) * 32;
+
+// byte (row, k) of a K-major, no-swizzle canonical operand with `rows` rows
+__host__ __device__ __forceinline__ u32 mm_canon(u32 row, u32 k, u32 rows) {
+  return (k / 16) * (rows / 8 * 128) + (row / 8) * 128 + (row % 8) * 16 + (k % 16);
+}
+
+__device__ __forceinline__ u64 mm_desc(u32 saddr, u32 lbo, u32 sbo) {
+  u64 d = (u64)((saddr >> 4) & 0x3fff);
+  d |= (u64)((lbo >> 4) & 0x3fff) << 16;
+  d |= (u64)((sbo >> 4) & 0x3fff) << 32;
+  d |= (u64)1 << 46;  // descriptor version (sm_100); base offset 0, SWIZZLE_NONE
+  return d;
+}
+
+// Query chunk operands, built once per call: B in the canonical layout
+// (queries past Q are zero rows) and per column u = T - |q| (INT_MIN/2: never passes).
+// Columns are ordered by u (sorted keys (u + 2^20) << 32 | query), so the 16
+// columns a thread tests together have nearly the same u and their shared
+// bound (max u) rarely lets a chunk through that no column passes.
+__global__ void mm_ukeys_kernel(const u64* __restrict__ q, u32 Q, const u32* __restrict__ tq, u64* __restrict__ keys) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Q) return;
+  const u32 pop = (u32)(__popcll(q[3 * (u64)i]) + __popcll(q[3 * (u64)i + 1]) + __popcll(q[3 * (u64)i + 2]));
+  keys[i] = ((u64)((int)tq[i] - (int)pop + (1 << 20)) << 32) | i;
+}
+
+__global__ void mm_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __restrict__ tq, unsigned char* __restrict__ bop,
+                               int* __restrict__ ucol, u32* __restrict__ qpop, u32 nchunks,
+                               const u64* __restrict__ order, u32* __restrict__ qcol) {
+  const u32 col = blockIdx.x * blockDim.x + threadIdx.x;  // global column = chunk * 256 + j
+  if (col >= nchunks * MM_N) return;
+  const u32 chunk = col / MM_N, j = col % MM_N;
+  u64 w[3] = {0, 0, 0};
+  const bool ok = col < Q;
+  const u32 qi = ok ? (u32)(order[col] & 0xffffffffu) : 0u;
+  if (ok) { w[0] = q[3 * (u64)qi]; w[1] = q[3 * (u64)qi + 1]; w[2] = q[3 * (u64)qi + 2]; }
+  qcol[col] = qi;
+  unsigned char* b = bop + (u64)chunk * MM_B_BYTES;
+  for (u32 k = 0; k < MM_K; ++k) b[mm_canon(j, k, MM_N)] = (unsigned char)((w[k >> 6] >> (k & 63)) & 1);
+  const u32 pop = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
+  qpop[col] = pop;
+  ucol[col] = ok ? (int)tq[qi] - (int)pop : -(1 << 28);
+}
+
+// |a| of every entry (all 192 bits), one byte each (the epilogue's row term)
+__global__ void mm_pop_kernel(PlanesOut lib, u64 n, unsigned char* __restrict__ pc) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    u64 a, b, c;
+    lib.get(i, a, b, c);
+    pc[i] = (unsigned char)(__popcll(a) + __popcll(b) + __popcll(c));
+  }
+}
+
+// Per query: the seed bound T_q = k-th distance of the seed top-k (255 when
+// the seed holds fewer than k entries: everything is a candidate).
+__global__ void mm_seed_kernel(const u64* __restrict__ keys, const u32* __restrict__ cnt, u32 Q, u32 k, u32* tq) {
+  const u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < Q) tq[q] = cnt[q] >= k ? key_d(keys[(u64)q * k + k - 1]) : 255u;
+}
+
+struct MmArgs {
+  PlanesOut lib;
+  u64 n, index_base;
+  u64 n_tiles;              // ceil(n / 128)
+  u32 Q, nchunks, parts;    // CTA c: chunk c % nchunks, tile range part c / nchunks
+  const unsigned char* bop; // [nchunks][48 KB] canonical B
+  const int* ucol;          // [nchunks * 256]
+  const u32* qpop;          // [nchunks * 256] |q| per column
+  const u32* qcol;          // [nchunks * 256] query of each column
+  const unsigned char* apop;  // [n] |a|
+  u64* cand;                // [Q][cap] keys d << 40 | index
+  u32* cand_cnt;            // [Q]
+  u32 cap;
+  u32 mode;                 // 0 top-k candidates (keys), 1 range hits (query << 48 | key) into out
+  u64* out;
+  u64* out_cnt;
+  u64 out_cap;
+  u32 flags;                // experiments: 4096 = epilogue without tests, 8192 = producer without library loads
+};
+
+__device__ __forceinline__ void mm_bar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mm_bar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mm_bar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n MMW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra MMW;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mm_commit(u64* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a) {
+  extern __shared__ __align__(1024) unsigned char msm[];
+  unsigned char* sB = msm;
+  unsigned char* sA = msm + MM_B_BYTES;  // [MM_STAGES][24 KB]
+  __shared__ __align__(8) u64 full_bar[MM_STAGES], empty_bar[MM_STAGES], tfull[2], tempty[2];
+  __shared__ u32 tmem_base;
+  __shared__ u32 lut[16];
+  __shared__ int s_u[MM_N];
+  __shared__ int s_umax[MM_N / 16];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const u32 chunk = blockIdx.x % a.nchunks;
+  const u64 part = blockIdx.x / a.nchunks;
+  const u64 t0 = part * a.n_tiles / a.parts, t1 = (part + 1) * a.n_tiles / a.parts;
+
+  // ---- setup: B chunk, thresholds, table, barriers, TMEM
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.bop + (u64)chunk * MM_B_BYTES);
+    uint4* dst = reinterpret_cast<uint4*>(sB);
+    for (u32 i = tid; i < MM_B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+  }
+  for (int i = tid; i < MM_N; i += blockDim.x) s_u[i] = a.ucol[chunk * MM_N + i];
+  if (tid < 16) lut[tid] = (tid & 1) | ((tid >> 1) & 1) << 8 | ((tid >> 2) & 1) << 16 | ((tid >> 3) & 1) << 24;
+  if (tid == 0) {
+    for (int s = 0; s < MM_STAGES; ++s) {
+      mm_bar_init(&full_bar[s], 128);
+      mm_bar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mm_bar_init(&tfull[b], 1);
+      mm_bar_init(&tempty[b], MM_EPI * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4 + MM_EPI) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid < MM_N / 16) {
+    int m = s_u[tid * 16];
+    for (int j = 1; j < 16; ++j) m = max(m, s_u[tid * 16 + j]);
+    s_umax[tid] = m;
+  }
+  __syncthreads();
+  const u32 tmem = tmem_base;
+  const u64 ntile = t1 > t0 ? t1 - t0 : 0;
+
+  if (warp < 4) {
+    // ===== producers: thread = entry row of the tile
+    const u32 row = (u32)tid;
+    // the entry of the next tile is loaded while this one is expanded
+    auto load = [&](u64 it, u64 (&w)[3]) {
+      const u64 e = (t0 + it) * MM_M + row;
+      w[0] = w[1] = w[2] = 0;
+      if (it < ntile && e < a.n && !(a.flags & 8192)) {
+        // tiled library (fps_kernels.cuh): shifts instead of PlanesOut's runtime divisions
+        if (a.lib.compact) {
+          const char* tb = a.lib.base + (e >> 8) * TILE_BYTES_CMP;
+          const u64 r = e & 255;
+          w[0] = __ldg(reinterpret_cast<const u64*>(tb) + r);
+          w[1] = __ldg(reinterpret_cast<const u64*>(tb + 8 * TILE_CMP) + r);
+          w[2] = (u64)__ldg(reinterpret_cast<const u32*>(tb + 16 * TILE_CMP) + r) |
+                 ((u64)__ldg(reinterpret_cast<const unsigned char*>(tb + 20 * TILE_CMP) + r) << 32);
+        } else {
+          const u64* tb = reinterpret_cast<const u64*>(a.lib.base + (e >> 7) * TILE_BYTES_FULL);
+          const u64 r = e & 127;
+          w[0] = __ldg(tb + r);
+          w[1] = __ldg(tb + TILE_FULL + r);
+          w[2] = __ldg(tb + 2 * TILE_FULL + r);
+        }
+      }
+    };
+    u64 wn[3];
+    load(0, wn);
+    for (u64 it = 0; it < ntile; ++it) {
+      const int s = (int)(it % MM_STAGES);
+      u64 w[3] = {wn[0], wn[1], wn[2]};
+      load(it + 1, wn);
+      if (it >= MM_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM_STAGES) - 1) & 1u);
+      unsigned char* A = sA + s * MM_A_BYTES;
+#pragma unroll
+      for (int c = 0; c < MM_K / 16; ++c) {
+        const u32 bits = (u32)(w[c >> 2] >> (16 * (c & 3))) & 0xffffu;
+        // 4 bits -> 4 bytes: the shifted copies of a nibble at bits 0/7/14/21
+        // do not overlap, so one multiply spreads them (then keep bit 0 of each byte)
+        uint4 v;
+        v.x = ((bits & 15u) * 0x204081u) & 0x01010101u;
+        v.y = (((bits >> 4) & 15u) * 0x204081u) & 0x01010101u;
+        v.z = (((bits >> 8) & 15u) * 0x204081u) & 0x01010101u;
+        v.w = ((bits >> 12) * 0x204081u) & 0x01010101u;
+        *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mm_bar_arrive(&full_bar[s]);
+    }
+  } else if (warp < 4 + MM_EPI) {
+    // ===== epilogue: warp w reads TMEM lane quadrant w % 4 (rows 32 (w % 4) ..
+    // + 31), columns [half * 128, half * 128 + 128)
+    const u32 quad = (u32)(warp % 4);
+    const u32 half = (u32)(warp - 4) / 4;
+    const u32 row = quad * 32 + lane;
+    for (u64 it = 0; it < ntile; ++it) {
+      const int b = (int)(it & 1);
+      const u64 e = (t0 + it) * MM_M + row;
+      const int apop = e < a.n ? (int)a.apop[e] : (1 << 28);
+      mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * MM_N;
+#pragma unroll 1
+      for (int c0 = (int)half * (MM_N / 2); c0 < (int)(half + 1) * (MM_N / 2); c0 += 64) {
+        u32 r[64];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(r[16 * g + 0]), "=r"(r[16 * g + 1]), "=r"(r[16 * g + 2]), "=r"(r[16 * g + 3]), "=r"(r[16 * g + 4]),
+                "=r"(r[16 * g + 5]), "=r"(r[16 * g + 6]), "=r"(r[16 * g + 7]), "=r"(r[16 * g + 8]), "=r"(r[16 * g + 9]),
+                "=r"(r[16 * g + 10]), "=r"(r[16 * g + 11]), "=r"(r[16 * g + 12]), "=r"(r[16 * g + 13]),
+                "=r"(r[16 * g + 14]), "=r"(r[16 * g + 15])
+              : "r"(taddr + c0 + 16 * g));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (a.flags & 4096) continue;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          u32 m = r[16 * h];
+#pragma unroll
+          for (int j = 1; j < 16; ++j) m = max(m, r[16 * h + j]);
+          const int cb = c0 + 16 * h;
+          if (2 * (int)m + s_umax[cb >> 4] < apop) continue;  // no column of the 16 can pass
+          u32 pm = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pm |= (2 * (int)r[16 * h + j] + s_u[cb + j] >= apop ? 1u : 0u) << j;
+          while (pm) {
+            const int j = __ffs(pm) - 1;
+            pm &= pm - 1;
+            u32 cj = 0;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              if (jj == j) cj = r[16 * h + jj];
+            const u32 col = chunk * MM_N + cb + j;
+            const u32 qi = a.qcol[col];
+            const u32 d = (u32)apop + a.qpop[col] - 2 * cj;
+            const u64 key = make_key(d, a.index_base + e);
+            if (a.mode == 0) {
+              const u32 pos = atomicAdd(a.cand_cnt + qi, 1u);
+              if (pos < a.cap) a.cand[(u64)qi * a.cap + pos] = key;
+            } else {
+              const u64 pos = atomicAdd(a.out_cnt, 1ull);
+              if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mm_bar_arrive(&tempty[b]);
+    }
+  } else {
+    // ===== MMA issuer (one lane)
+    if (lane == 0) {
+      const u32 idesc = (2u << 4) | ((u32)(MM_N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);  // s32 += u8 x u8, K-major
+      const u32 sb = smem_u32(sB);
+      for (u64 it = 0; it < ntile; ++it) {
+        const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
+        if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+        mm_bar_wait(&full_bar[s], (u32)(it / MM_STAGES) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const u32 sa = smem_u32(sA + s * MM_A_BYTES);
+        const u32 dt = tmem + (u32)b * MM_N;
+#pragma unroll
+        for (int ks = 0; ks < MM_K / 32; ++ks) {
+          const u64 da = mm_desc(sa + ks * 2 * (MM_M / 8 * 128), MM_M / 8 * 128, 128);
+          const u64 db = mm_desc(sb + ks * 2 * (MM_N / 8 * 128), MM_N / 8 * 128, 128);
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(dt),
+              "l"(da), "l"(db), "r"(idesc), "r"((u32)(ks > 0)), "r"(0u));
+        }
+        mm_commit(&empty_bar[s]);
+        mm_commit(&tfull[b]);
+      }
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+}  // namespace fps

@@ -226,7 +226,8 @@ class Library:
         return t.value, c.value
 
     KERNELS = {0: "none", 1: "single-query HBM scan", 2: "multi-query POPC scan", 3: "bit-sliced multi-query scan",
-               4: "large-k histogram/range/sort", 5: "single-query plane scan"}
+               4: "large-k histogram/range/sort", 5: "single-query plane scan",
+               6: "tensor-core multi-query scan"}
 
     @property
     def last_kernel(self) -> str:

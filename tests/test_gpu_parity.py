@@ -622,3 +622,60 @@ def test_sorted_plane_scan_config_shapes(monkeypatch):
         w = lib.words_host()
         assert lib.search(q[0], plan.k) == oracle_topk(w, q[:1], plan.k)[0]
         assert _dev_topk(lib, q[:1], plan.k) == oracle_topk(w, q[:1], plan.k)[0]
+
+
+# ---------------------------------------------------------------- tensor-core multi-query path
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 70_001, 300_007])
+def test_mma_multi_query_vs_oracle(n, monkeypatch):
+    """tcgen05 int8 MMA path (FPS_MMA=1): every pair within the seeded bound
+    collected, select keeps the k smallest (distance, index); chunks of 256
+    queries, columns ordered by bound, tails of 128-entry tiles."""
+    monkeypatch.setenv("FPS_MMA", "1")
+    seed = 600 + n
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(n)
+    for Q in (2, 257, 600):
+        q = w[rng.integers(0, n, Q)].copy()
+        q[:, 0] ^= rng.integers(0, 2**24, Q).astype(np.uint64) << np.uint64(1)
+        q[Q // 2] = _query_with_pop(rng, 120)  # a dense query
+        for k in (1, 10, 100):
+            res = lib.search_batch(q, k)
+            exp = oracle_topk(w, q, k)
+            for i in range(Q):
+                assert res.hits(i) == exp[i], (n, Q, k, i)
+
+
+def test_mma_candidate_overflow_falls_back(monkeypatch):
+    """Every entry ties (all within the seed bound): the candidate lists
+    overflow and the call is recomputed by the bit-sliced kernel."""
+    monkeypatch.setenv("FPS_MMA", "1")
+    w = np.tile(np.array([[0x1234, 0x5678, 0x9]], dtype=np.uint64), (300_000, 1))
+    lib = Library.from_words(w)
+    q = np.tile(np.array([[0x1234, 0x5678, 0x8]], dtype=np.uint64), (300, 1))
+    res = lib.search_batch(q, 10)
+    for i in range(300):
+        assert res.hits(i) == [(j, 1) for j in range(10)]
+
+
+def test_mma_pad_bits_counted():
+    """The MMA path covers all 192 bits: FPS1 pad bits count like the reference."""
+    rec = np.zeros((5000, 4), dtype=np.uint64)
+    rec[:, 0] = np.arange(1, 5001)
+    rng = np.random.default_rng(3)
+    rec[:, 1] = rng.integers(0, 2**63, 5000, dtype=np.uint64)
+    rec[17, 3] = np.uint64(0xF) << np.uint64(44)
+    lib = Library.from_records(rec)
+    w = rec[:, 1:].copy()
+    q = w[rng.integers(0, 5000, 256)].copy()
+    q[0] = w[17] & ~(np.uint64(0xF) << np.uint64(44))
+    q[:, 2] &= np.uint64((1 << 38) - 1)
+    import os
+    os.environ["FPS_MMA"] = "1"
+    try:
+        res = lib.search_batch(q, 5)
+    finally:
+        del os.environ["FPS_MMA"]
+    exp = oracle_topk(w, q, 5)
+    for i in range(256):
+        assert res.hits(i) == exp[i]
