@@ -878,54 +878,58 @@ bool mma_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
   return true;
 }
 
-int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
-             bool* fallback) {
-  int rc;
-  *fallback = false;
-  // 1. seed bound: exact top-k of a library prefix (POPC scan)
-  const u64 seed_n = std::min<u64>(L->n, 1 << 18);
-  L->timing_suspend = true;
-  rc = L->compact ? topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n)
-                  : topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n);
-  L->timing_suspend = false;
-  if (rc) return rc;
-  const u32 nchunks = (Q + fps::MM_N - 1) / fps::MM_N;
-  const u64 n_tiles = (L->n + fps::MM_M - 1) / fps::MM_M;
-  const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles));
-  // candidates per query: pairs within the seed bound (~k x N / seed_n expected)
-  const u64 expect = (u64)k * (L->n / std::max<u64>(seed_n, 1) + 1);
-  const u32 cap = (u32)std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
-  if ((rc = L->mm_bop.ensure((size_t)nchunks * fps::MM_B_BYTES)) || (rc = L->mm_ucol.ensure((size_t)nchunks * fps::MM_N * 4)) ||
-      (rc = L->mm_qpop.ensure((size_t)nchunks * fps::MM_N * 4)) || (rc = L->mm_tq.ensure((size_t)Q * 4)) ||
-      (rc = L->mm_qcol.ensure((size_t)nchunks * fps::MM_N * 4)) || (rc = L->mm_keys.ensure((size_t)Q * 8)) ||
-      (rc = L->mm_sorted.ensure((size_t)Q * 8)) ||
-      (rc = L->cand.ensure((size_t)Q * cap * 8)) || (rc = L->mm_apop.ensure(std::max<u64>(L->n, 1))))
-    return rc;
+// accumulator width by batch: the smallest of 64 / 128 / 256 columns that
+// holds the batch in one chunk (the MMA and epilogue work scale with it)
+u32 mma_pick_n(u32 Q) { return Q <= 64 ? 64u : Q <= 128 ? 128u : 256u; }
+
+template <int N>
+int mma_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   static bool attr = false;
-  const size_t smem = fps::MM_B_BYTES + (size_t)fps::MM_STAGES * fps::MM_A_BYTES;
+  const size_t smem = fps::mm_b_bytes(N) + (size_t)fps::MM_STAGES * fps::MM_A_BYTES + (size_t)fps::MM_RAW * fps::MM_RAW_BYTES_MAX;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(fps::mma_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(fps::mma_scan_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::mma_scan_kernel<N><<<ctas, fps::MM_THREADS, smem, s>>>(a);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  LAUNCH_CHECK("mma_scan_kernel");
+  return FPS_OK;
+}
+
+// Shared part of the tensor-core calls: per-query operands from the bound
+// mm_tq[q] (top-k: the seed's k-th distance; range: the radius), columns
+// ordered by u = T - |q|, then the scan. mode 0 appends candidate keys to the
+// per-query lists L->cand (capacity cap); mode 1 appends range hits to out.
+int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
+            cudaStream_t s, bool prepare_only) {
+  int rc;
+  const u32 NN = mma_pick_n(Q);
+  const u32 nchunks = (Q + NN - 1) / NN;
+  const u64 n_tiles = (L->n + fps::MM_M - 1) / fps::MM_M;
+  const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles));
+  if ((rc = L->mm_bop.ensure((size_t)nchunks * fps::mm_b_bytes((int)NN))) ||
+      (rc = L->mm_ucol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_qpop.ensure((size_t)nchunks * NN * 4)) ||
+      (rc = L->mm_qcol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_keys.ensure((size_t)Q * 8)) ||
+      (rc = L->mm_sorted.ensure((size_t)Q * 8)) || (rc = L->mm_apop.ensure(std::max<u64>(L->n, 1))))
+    return rc;
+  size_t tb = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
+  if ((rc = L->mm_tmp.ensure(tb))) return rc;
   if (prepare_only) return FPS_OK;
   if (!L->mm_apop_ok) {
     fps::mm_pop_kernel<<<L->sms * 8, 256, 0, s>>>(L->out(), L->n, L->mm_apop.as<unsigned char>());
     L->launches++;
     L->mm_apop_ok = true;
   }
-  fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
-  fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q), ghist_stride(Q));
   fps::mm_ukeys_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_q, Q, L->mm_tq.as<u32>(), L->mm_keys.as<u64>());
-  {
-    size_t tb = 0;
-    CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
-    if ((rc = L->mm_tmp.ensure(tb))) return rc;
-    CUDA_TRY(cub::DeviceRadixSort::SortKeys(L->mm_tmp.p, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
-  }
-  fps::mm_prep_kernel<<<(nchunks * fps::MM_N + 127) / 128, 128, 0, s>>>(
+  CUDA_TRY(cub::DeviceRadixSort::SortKeys(L->mm_tmp.p, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
+  fps::mm_prep_kernel<<<(nchunks * NN + 127) / 128, 128, 0, s>>>(
       d_q, Q, L->mm_tq.as<u32>(), L->mm_bop.as<unsigned char>(), L->mm_ucol.as<int>(), L->mm_qpop.as<u32>(), nchunks,
-      L->mm_sorted.as<u64>(), L->mm_qcol.as<u32>());
-  L->launches += 5;
+      L->mm_sorted.as<u64>(), L->mm_qcol.as<u32>(), NN);
+  L->launches += 3;
   LAUNCH_CHECK("mm_prep");
   fps::MmArgs a{};
   a.lib = L->out();
@@ -943,14 +947,40 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
   a.cand = L->cand.as<u64>();
   a.cand_cnt = L->cand_cnt.as<u32>();
   a.cap = cap;
-  a.mode = 0;
+  a.mode = mode;
+  a.out = out;
+  a.out_cnt = out_cnt;
+  a.out_cap = out_cap;
   a.flags = scan_flags();
-  auto* ev = timing_slot(L);
-  if (ev) cudaEventRecord(ev->first, s);
-  fps::mma_scan_kernel<<<nchunks * parts, fps::MM_THREADS, smem, s>>>(a);
-  if (ev) cudaEventRecord(ev->second, s);
-  L->launches++;
-  LAUNCH_CHECK("mma_scan_kernel");
+  const u32 ctas = nchunks * parts;
+  if (NN == 64) return mma_launch_n<64>(L, ctas, s, a);
+  if (NN == 128) return mma_launch_n<128>(L, ctas, s, a);
+  return mma_launch_n<256>(L, ctas, s, a);
+}
+
+int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
+             bool* fallback) {
+  int rc;
+  *fallback = false;
+  // 1. seed bound: exact top-k of a library prefix (POPC scan)
+  const u64 seed_n = std::min<u64>(L->n, 1 << 18);
+  L->timing_suspend = true;
+  rc = L->compact ? topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n)
+                  : topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n);
+  L->timing_suspend = false;
+  if (rc) return rc;
+  // candidates per query: pairs within the seed bound (~k x N / seed_n expected)
+  const u64 expect = (u64)k * (L->n / std::max<u64>(seed_n, 1) + 1);
+  const u32 cap = (u32)std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
+  if ((rc = L->mm_tq.ensure((size_t)Q * 4)) || (rc = L->cand.ensure((size_t)Q * cap * 8))) return rc;
+  if (!prepare_only) {
+    fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
+    fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q),
+                                                     ghist_stride(Q));
+    L->launches += 2;
+  }
+  if ((rc = mma_run(L, d_q, Q, 0, cap, nullptr, nullptr, 0, s, prepare_only))) return rc;
+  if (prepare_only) return FPS_OK;
   // candidate lists must fit their capacity (else: the bit-sliced kernel)
   std::vector<u32> cc(Q);
   CUDA_TRY(cudaMemcpyAsync(cc.data(), L->cand_cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, s));
@@ -958,7 +988,7 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
   u32 mx = 0;
   for (u32 v : cc) mx = std::max(mx, v);
   if (std::getenv("FPS_DEBUG"))
-    std::fprintf(stderr, "[fps] mma scan: Q=%u chunks=%u parts=%u cap=%u max candidates=%u\n", Q, nchunks, parts, cap, mx);
+    std::fprintf(stderr, "[fps] mma scan: Q=%u N=%u cap=%u max candidates=%u\n", Q, mma_pick_n(Q), cap, mx);
   if (mx > cap) {
     reset_state(L);
     *fallback = true;
@@ -966,11 +996,39 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
   }
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
-  CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, a.cand, a.cand_cnt, cap, L->tg.as<u32>(),
-                         L->ghist.as<u32>(), ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt, false));
+  CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, L->cand.as<u64>(), L->cand_cnt.as<u32>(), cap,
+                         L->tg.as<u32>(), L->ghist.as<u32>(), ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt,
+                         false));
   L->launches++;
   LAUNCH_CHECK("select_kernel (mma)");
   return FPS_OK;
+}
+
+// Range search on the tensor cores: the bound is the radius itself (exact,
+// no seed); hits go straight to the range output. FPS_MMA=0 disables it,
+// FPS_MMA=1 forces it for any batch >= 2; by default it serves batches of
+// >= FPS_MMA_RANGE_MIN_Q (default 32) queries.
+bool mma_range_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
+  const char* e = std::getenv("FPS_MMA");
+  const int mode = e ? std::atoi(e) : -1;
+  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M) return false;
+  const char* m = std::getenv("FPS_MMA_RANGE_MIN_Q");
+  if (mode != 1 && Q < (u32)(m ? std::atoi(m) : 32)) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+int range_mma(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u64* d_out, u64 cap, u64* d_count,
+              cudaStream_t s) {
+  int rc;
+  if ((rc = L->mm_tq.ensure((size_t)Q * 4))) return rc;
+  fps::mm_radius_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_radius, Q, L->mm_tq.as<u32>());
+  L->launches++;
+  return mma_run(L, d_q, Q, 1, 0, d_out, d_count, cap, s, false);
 }
 
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
@@ -1020,6 +1078,10 @@ int launch_plain(fps_lib* L, fps::ScanArgs a, cudaStream_t s) {
 
 template <int MODE>
 int plain_dispatch(fps_lib* L, const fps::ScanArgs& a, cudaStream_t s) {
+  if (MODE == fps::MODE_RANGE && mma_range_wanted(L, a.Q, s)) {
+    L->last_kernel = 6;
+    return range_mma(L, a.queries, a.Q, a.radius, a.out, a.out_cap, a.out_cnt, s);
+  }
   if (MODE == fps::MODE_RANGE && bs_wanted(L, a.Q)) {
     L->last_kernel = 3;
     return range_bs(L, a.queries, a.Q, a.radius, a.out, a.out_cap, a.out_cnt, s);
@@ -1617,6 +1679,7 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
   lib->bs_state = 0;
   lib->pm.release();
   lib->pm_state = 0;
+  lib->mm_apop_ok = false;  // |a| per entry for the tensor-core path
   if (nwide) return fail(FPS_EINVAL, "entry sets bits 40.. of word 2; the library uses the compact layout");
   return FPS_OK;
 }
@@ -1801,7 +1864,9 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
       return FPS_OK;
     }
   }
-  if (k <= KMAX_FUSED && graphs_enabled(lib)) {
+  // the tensor-core path checks its candidate lists on the host mid-call:
+  // it is not captured (a graph would record the bit-sliced kernel instead)
+  if (k <= KMAX_FUSED && graphs_enabled(lib) && !mma_wanted(lib, Q, lib->stream)) {
     fps_lib::TopkGraph* gr = nullptr;
     if (topk_graph(lib, queries, Q, k, &gr) == FPS_OK) {
       const u64* hk = gr->hout.as<u64>();

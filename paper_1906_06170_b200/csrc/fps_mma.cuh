@@ -30,13 +30,17 @@
 namespace fps {
 
 constexpr int MM_M = 128;          // entries per tile (TMEM lanes)
-constexpr int MM_N = 256;          // queries per CTA chunk (TMEM columns per accumulator)
+constexpr int MM_N = 256;          // queries per CTA chunk (TMEM columns per accumulator), largest shape
+                                   // (mma_scan_kernel<N>: N = 64 / 128 / 256 by batch size)
 constexpr int MM_K = 192;          // bytes per row (3 x 64 bits)
 constexpr int MM_STAGES = 4;
 constexpr u32 MM_A_BYTES = MM_M * MM_K;  // 24 KB
-constexpr u32 MM_B_BYTES = MM_N * MM_K;  // 48 KB
+constexpr u32 MM_B_BYTES = MM_N * MM_K;  // 48 KB (N = 256)
+__host__ __device__ constexpr u32 mm_b_bytes(int n) { return (u32)n * MM_K; }
 constexpr int MM_EPI = 8;                 // epilogue warps: 2 per TMEM lane quadrant, each half the columns
-constexpr int MM_THREADS = (4 + MM_EPI + 1) * 32;
+constexpr int MM_RAW = 8;                 // raw library tiles in flight per CTA (bulk-copy ring)
+constexpr u32 MM_RAW_BYTES_MAX = 24 * 256; // >= tile_bytes(compact) and tile_bytes(full)
+constexpr int MM_THREADS = (4 + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
 
 // byte (row, k) of a K-major, no-swizzle canonical operand with `rows` rows
 __host__ __device__ __forceinline__ u32 mm_canon(u32 row, u32 k, u32 rows) {
@@ -65,20 +69,26 @@ __global__ void mm_ukeys_kernel(const u64* __restrict__ q, u32 Q, const u32* __r
 
 __global__ void mm_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __restrict__ tq, unsigned char* __restrict__ bop,
                                int* __restrict__ ucol, u32* __restrict__ qpop, u32 nchunks,
-                               const u64* __restrict__ order, u32* __restrict__ qcol) {
-  const u32 col = blockIdx.x * blockDim.x + threadIdx.x;  // global column = chunk * 256 + j
-  if (col >= nchunks * MM_N) return;
-  const u32 chunk = col / MM_N, j = col % MM_N;
+                               const u64* __restrict__ order, u32* __restrict__ qcol, u32 NN) {
+  const u32 col = blockIdx.x * blockDim.x + threadIdx.x;  // global column = chunk * NN + j
+  if (col >= nchunks * NN) return;
+  const u32 chunk = col / NN, j = col % NN;
   u64 w[3] = {0, 0, 0};
   const bool ok = col < Q;
   const u32 qi = ok ? (u32)(order[col] & 0xffffffffu) : 0u;
   if (ok) { w[0] = q[3 * (u64)qi]; w[1] = q[3 * (u64)qi + 1]; w[2] = q[3 * (u64)qi + 2]; }
   qcol[col] = qi;
-  unsigned char* b = bop + (u64)chunk * MM_B_BYTES;
-  for (u32 k = 0; k < MM_K; ++k) b[mm_canon(j, k, MM_N)] = (unsigned char)((w[k >> 6] >> (k & 63)) & 1);
+  unsigned char* b = bop + (u64)chunk * mm_b_bytes((int)NN);
+  for (u32 k = 0; k < MM_K; ++k) b[mm_canon(j, k, NN)] = (unsigned char)((w[k >> 6] >> (k & 63)) & 1);
   const u32 pop = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
   qpop[col] = pop;
   ucol[col] = ok ? (int)tq[qi] - (int)pop : -(1 << 28);
+}
+
+// range: the bound of query q is its radius
+__global__ void mm_radius_kernel(const unsigned char* __restrict__ radius, u32 Q, u32* __restrict__ tq) {
+  const u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < Q) tq[q] = radius[q];
 }
 
 // |a| of every entry (all 192 bits), one byte each (the epilogue's row term)
@@ -135,32 +145,49 @@ __device__ __forceinline__ void mm_commit(u64* bar) {
                : "memory");
 }
 
+template <int N>
 __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a) {
+  static_assert(N == 64 || N == 128 || N == 256, "accumulator width");
+  constexpr u32 B_BYTES = mm_b_bytes(N);
+  constexpr u32 TMEM_COLS = 2 * N;         // two accumulators (power of two >= 32)
+  constexpr int CB = N / 2 < 64 ? N / 2 : 64;  // columns an epilogue warp loads per round
   extern __shared__ __align__(1024) unsigned char msm[];
   unsigned char* sB = msm;
-  unsigned char* sA = msm + MM_B_BYTES;  // [MM_STAGES][24 KB]
+  unsigned char* sA = msm + B_BYTES;  // [MM_STAGES][24 KB]
+  char* raw = reinterpret_cast<char*>(msm + B_BYTES + MM_STAGES * MM_A_BYTES);  // [MM_RAW][library tile]
   __shared__ __align__(8) u64 full_bar[MM_STAGES], empty_bar[MM_STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) u64 raw_full[MM_RAW], raw_empty[MM_RAW];
   __shared__ u32 tmem_base;
   __shared__ u32 lut[16];
-  __shared__ int s_u[MM_N];
-  __shared__ int s_umax[MM_N / 16];
+  __shared__ int s_u[N];
+  __shared__ int s_umax[N / 16];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
   const u64 part = blockIdx.x / a.nchunks;
-  const u64 t0 = part * a.n_tiles / a.parts, t1 = (part + 1) * a.n_tiles / a.parts;
+  // CTA work: a contiguous run of library tiles (SUB MMA tiles of 128 entries each)
+  const u32 SUB = a.lib.compact ? TILE_CMP / MM_M : TILE_FULL / MM_M;
+  const u32 RAW_BYTES = (u32)tile_bytes(a.lib.compact);
+  const u64 n_raw = (a.n + tile_entries(a.lib.compact) - 1) / tile_entries(a.lib.compact);
+  const u64 r0 = part * n_raw / a.parts, r1 = (part + 1) * n_raw / a.parts;
+  const u64 nraw = r1 > r0 ? r1 - r0 : 0;
+  const u64 t0 = r0 * SUB;
 
   // ---- setup: B chunk, thresholds, table, barriers, TMEM
   {
-    const uint4* src = reinterpret_cast<const uint4*>(a.bop + (u64)chunk * MM_B_BYTES);
+    const uint4* src = reinterpret_cast<const uint4*>(a.bop + (u64)chunk * B_BYTES);
     uint4* dst = reinterpret_cast<uint4*>(sB);
-    for (u32 i = tid; i < MM_B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+    for (u32 i = tid; i < B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
   }
-  for (int i = tid; i < MM_N; i += blockDim.x) s_u[i] = a.ucol[chunk * MM_N + i];
+  for (int i = tid; i < N; i += blockDim.x) s_u[i] = a.ucol[chunk * N + i];
   if (tid < 16) lut[tid] = (tid & 1) | ((tid >> 1) & 1) << 8 | ((tid >> 2) & 1) << 16 | ((tid >> 3) & 1) << 24;
   if (tid == 0) {
     for (int s = 0; s < MM_STAGES; ++s) {
       mm_bar_init(&full_bar[s], 128);
       mm_bar_init(&empty_bar[s], 1);
+    }
+    for (int r = 0; r < MM_RAW; ++r) {
+      mm_bar_init(&raw_full[r], 1);
+      mm_bar_init(&raw_empty[r], 128);
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
@@ -170,53 +197,48 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   }
   if (warp == 4 + MM_EPI) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(512));
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (tid < MM_N / 16) {
+  if (tid < N / 16) {
     int m = s_u[tid * 16];
     for (int j = 1; j < 16; ++j) m = max(m, s_u[tid * 16 + j]);
     s_umax[tid] = m;
   }
   __syncthreads();
   const u32 tmem = tmem_base;
-  const u64 ntile = t1 > t0 ? t1 - t0 : 0;
+  const u64 ntile = nraw * SUB;
 
   if (warp < 4) {
-    // ===== producers: thread = entry row of the tile
+    // ===== producers: thread = entry row of the tile; the entry's words come
+    // from the raw-tile ring the loader warp fills with bulk copies
     const u32 row = (u32)tid;
-    // the entry of the next tile is loaded while this one is expanded
-    auto load = [&](u64 it, u64 (&w)[3]) {
-      const u64 e = (t0 + it) * MM_M + row;
-      w[0] = w[1] = w[2] = 0;
-      if (it < ntile && e < a.n && !(a.flags & 8192)) {
-        // tiled library (fps_kernels.cuh): shifts instead of PlanesOut's runtime divisions
-        if (a.lib.compact) {
-          const char* tb = a.lib.base + (e >> 8) * TILE_BYTES_CMP;
-          const u64 r = e & 255;
-          w[0] = __ldg(reinterpret_cast<const u64*>(tb) + r);
-          w[1] = __ldg(reinterpret_cast<const u64*>(tb + 8 * TILE_CMP) + r);
-          w[2] = (u64)__ldg(reinterpret_cast<const u32*>(tb + 16 * TILE_CMP) + r) |
-                 ((u64)__ldg(reinterpret_cast<const unsigned char*>(tb + 20 * TILE_CMP) + r) << 32);
-        } else {
-          const u64* tb = reinterpret_cast<const u64*>(a.lib.base + (e >> 7) * TILE_BYTES_FULL);
-          const u64 r = e & 127;
-          w[0] = __ldg(tb + r);
-          w[1] = __ldg(tb + TILE_FULL + r);
-          w[2] = __ldg(tb + 2 * TILE_FULL + r);
-        }
-      }
-    };
-    u64 wn[3];
-    load(0, wn);
     for (u64 it = 0; it < ntile; ++it) {
       const int s = (int)(it % MM_STAGES);
-      u64 w[3] = {wn[0], wn[1], wn[2]};
-      load(it + 1, wn);
+      const u64 r = it / SUB;
+      const u32 sub = (u32)(it % SUB);
+      const int rs = (int)(r % MM_RAW);
+      if (sub == 0) mm_bar_wait(&raw_full[rs], (u32)(r / MM_RAW) & 1u);
+      u64 w[3];
+      {
+        const char* tb = raw + (u64)rs * RAW_BYTES;
+        const u32 e = sub * MM_M + row;
+        if (a.lib.compact) {
+          w[0] = reinterpret_cast<const u64*>(tb)[e];
+          w[1] = reinterpret_cast<const u64*>(tb + 8 * TILE_CMP)[e];
+          w[2] = (u64)reinterpret_cast<const u32*>(tb + 16 * TILE_CMP)[e] |
+                 ((u64)reinterpret_cast<const unsigned char*>(tb + 20 * TILE_CMP)[e] << 32);
+        } else {
+          w[0] = reinterpret_cast<const u64*>(tb)[e];
+          w[1] = reinterpret_cast<const u64*>(tb + 8 * TILE_FULL)[e];
+          w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
+        }
+      }
+      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
       if (it >= MM_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM_A_BYTES;
 #pragma unroll
@@ -234,6 +256,24 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mm_bar_arrive(&full_bar[s]);
     }
+  } else if (warp == 5 + MM_EPI) {
+    // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
+    if (lane == 0 && !(a.flags & 8192)) {
+      const u64 pol = l2_evict_first_policy();
+      for (u64 r = 0; r < nraw; ++r) {
+        const int rs = (int)(r % MM_RAW);
+        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
+        mbar_expect_tx(&raw_full[rs], RAW_BYTES);
+        bulk_g2s_stream(raw + (u64)rs * RAW_BYTES, a.lib.base + (r0 + r) * RAW_BYTES, RAW_BYTES, &raw_full[rs], pol);
+      }
+    } else if (lane == 0) {
+      for (u64 r = 0; r < nraw; ++r) {
+        const int rs = (int)(r % MM_RAW);
+        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
+        mm_bar_arrive(&raw_full[rs]);
+      }
+    }
+    __syncwarp();
   } else if (warp < 4 + MM_EPI) {
     // ===== epilogue: warp w reads TMEM lane quadrant w % 4 (rows 32 (w % 4) ..
     // + 31), columns [half * 128, half * 128 + 128)
@@ -246,12 +286,12 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       const int apop = e < a.n ? (int)a.apop[e] : (1 << 28);
       mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * MM_N;
+      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N;
 #pragma unroll 1
-      for (int c0 = (int)half * (MM_N / 2); c0 < (int)(half + 1) * (MM_N / 2); c0 += 64) {
-        u32 r[64];
+      for (int c0 = (int)half * (N / 2); c0 < (int)(half + 1) * (N / 2); c0 += CB) {
+        u32 r[CB];
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
+        for (int g = 0; g < CB / 16; ++g)
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
               : "=r"(r[16 * g + 0]), "=r"(r[16 * g + 1]), "=r"(r[16 * g + 2]), "=r"(r[16 * g + 3]), "=r"(r[16 * g + 4]),
@@ -262,7 +302,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (a.flags & 4096) continue;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < CB / 16; ++h) {
           u32 m = r[16 * h];
 #pragma unroll
           for (int j = 1; j < 16; ++j) m = max(m, r[16 * h + j]);
@@ -278,7 +318,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj)
               if (jj == j) cj = r[16 * h + jj];
-            const u32 col = chunk * MM_N + cb + j;
+            const u32 col = chunk * N + cb + j;
             const u32 qi = a.qcol[col];
             const u32 d = (u32)apop + a.qpop[col] - 2 * cj;
             const u64 key = make_key(d, a.index_base + e);
@@ -298,7 +338,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   } else {
     // ===== MMA issuer (one lane)
     if (lane == 0) {
-      const u32 idesc = (2u << 4) | ((u32)(MM_N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);  // s32 += u8 x u8, K-major
+      const u32 idesc = (2u << 4) | ((u32)(N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);  // s32 += u8 x u8, K-major
       const u32 sb = smem_u32(sB);
       for (u64 it = 0; it < ntile; ++it) {
         const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
@@ -306,11 +346,11 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         mm_bar_wait(&full_bar[s], (u32)(it / MM_STAGES) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 sa = smem_u32(sA + s * MM_A_BYTES);
-        const u32 dt = tmem + (u32)b * MM_N;
+        const u32 dt = tmem + (u32)b * N;
 #pragma unroll
         for (int ks = 0; ks < MM_K / 32; ++ks) {
           const u64 da = mm_desc(sa + ks * 2 * (MM_M / 8 * 128), MM_M / 8 * 128, 128);
-          const u64 db = mm_desc(sb + ks * 2 * (MM_N / 8 * 128), MM_N / 8 * 128, 128);
+          const u64 db = mm_desc(sb + ks * 2 * (N / 8 * 128), N / 8 * 128, 128);
           asm volatile(
               "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
               " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(dt),
@@ -324,7 +364,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 }  // namespace fps

@@ -635,7 +635,7 @@ def test_mma_multi_query_vs_oracle(n, monkeypatch):
     w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
     lib = Library.from_words(w)
     rng = np.random.default_rng(n)
-    for Q in (2, 257, 600):
+    for Q in (2, 100, 257, 600):  # accumulators of 64 / 128 / 256 columns, 1-3 chunks
         q = w[rng.integers(0, n, Q)].copy()
         q[:, 0] ^= rng.integers(0, 2**24, Q).astype(np.uint64) << np.uint64(1)
         q[Q // 2] = _query_with_pop(rng, 120)  # a dense query
@@ -679,3 +679,49 @@ def test_mma_pad_bits_counted():
     exp = oracle_topk(w, q, 5)
     for i in range(256):
         assert res.hits(i) == exp[i]
+
+
+@pytest.mark.parametrize("n", [127, 129, 70_001, 300_007])
+def test_mma_range_vs_oracle(n, monkeypatch):
+    """Range search on the tensor cores (FPS_MMA=1): the radius is the bound,
+    every pair with d <= r is emitted; 64 / 128 / 256-column accumulators,
+    several chunks, tails of library tiles, a dense query."""
+    monkeypatch.setenv("FPS_MMA", "1")
+    seed = 700 + n
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(n)
+    for Q in (2, 64, 65, 130, 300):
+        q = w[rng.integers(0, n, Q)].copy()
+        q[:, 1] ^= rng.integers(0, 8, Q).astype(np.uint64)
+        q[Q // 2] = _query_with_pop(rng, 120)
+        for radius in (0, 6, 40):
+            r = lib.range_search(q, radius)
+            assert np.array_equal(r.rows(), orc.c_range(w, q, radius)), (n, Q, radius)
+
+
+def test_mma_range_per_query_radius_and_overflow_retry(monkeypatch):
+    """Per-query radii on the tensor-core range path; > 1 M hits: the first
+    pass overflows the output and the call is re-run with a larger buffer."""
+    monkeypatch.setenv("FPS_MMA", "1")
+    w = orc.generate_words(3, np.full(166, 2**31, np.uint64), 0, 400_000)
+    q = w[:40].copy()
+    radii = np.zeros(40, dtype=np.uint8)
+    radii[:5] = [0, 95, 90, 80, 166]
+    radii[5:] = 50
+    lib = Library.from_words(w)
+    r = lib.range_search(q, radii)
+    exp = np.concatenate([orc.c_range(w, q[i:i + 1], int(radii[i])) + np.array([i, 0, 0]) for i in range(40)])
+    assert len(r) > 1 << 20
+    assert np.array_equal(r.rows(), exp)
+
+
+def test_mma_range_default_dispatch_config_shape():
+    """C5-shaped call (64 queries, radius 6, planted near-duplicates) takes the
+    tensor-core range path by default and matches the oracle."""
+    plan = synth.make_plan("c5", n=1_000_000, planted_per_query=300)
+    lib, q = synth.build_library(plan)
+    w = lib.words_host()
+    r = lib.range_search(q, plan.radius)
+    assert lib.last_kernel == "tensor-core multi-query scan"
+    assert np.array_equal(r.rows(), orc.c_range(w, q, plan.radius))
