@@ -717,11 +717,32 @@ def test_mma_range_per_query_radius_and_overflow_retry(monkeypatch):
 
 
 def test_mma_range_default_dispatch_config_shape():
-    """C5-shaped call (64 queries, radius 6, planted near-duplicates) takes the
-    tensor-core range path by default and matches the oracle."""
+    """C5-shaped calls (radius 6, planted near-duplicates): 64 queries take
+    the bit-sliced kernel, 256 the tensor-core range path; both match the oracle."""
     plan = synth.make_plan("c5", n=1_000_000, planted_per_query=300)
     lib, q = synth.build_library(plan)
     w = lib.words_host()
     r = lib.range_search(q, plan.radius)
-    assert lib.last_kernel == "tensor-core multi-query scan"
+    assert lib.last_kernel == "bit-sliced multi-query scan"
     assert np.array_equal(r.rows(), orc.c_range(w, q, plan.radius))
+    q4 = np.concatenate([q, q ^ np.uint64(1), q ^ np.uint64(2), q ^ np.uint64(4)])
+    r = lib.range_search(q4, plan.radius)
+    assert lib.last_kernel == "tensor-core multi-query scan"
+    assert np.array_equal(r.rows(), orc.c_range(w, q4, plan.radius))
+
+
+@pytest.mark.parametrize("Q", [20, 40, 300])
+def test_bitslice_all_ties_buffer_capacity(Q, monkeypatch):
+    """Every entry at the same distance from every query: each warp step of
+    the bit-sliced kernel passes a whole 2,048-entry tile after its buffer was
+    compacted to k, so the per-(warp, query) buffer needs k + one tile (1, 2
+    and 4 queries per warp)."""
+    monkeypatch.setenv("FPS_MMA", "0")
+    w = np.tile(np.array([[0x1234, 0x5678, 0x9]], dtype=np.uint64), (300_000, 1))
+    lib = Library.from_words(w)
+    q = np.tile(np.array([[0x1234, 0x5678, 0x8]], dtype=np.uint64), (Q, 1))
+    for k in (10, 100):
+        res = lib.search_batch(q, k)
+        assert lib.last_kernel == "bit-sliced multi-query scan"
+        for i in range(Q):
+            assert res.hits(i) == [(j, 1) for j in range(k)], (Q, k, i)
