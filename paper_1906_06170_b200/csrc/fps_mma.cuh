@@ -156,6 +156,15 @@ __device__ __forceinline__ void mm_ld32(u32 taddr, u32 (&r)[32]) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+// 32 consecutive TMEM columns, the low 16 bits of each, two per register
+// (column 2i in bits 0-15 of r[i], column 2i+1 in bits 16-31)
+__device__ __forceinline__ void mm_ld32p(u32 taddr, u32 (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ u32 mm_max16(const u32* v) {
   const u32 a0 = max(max(v[0], v[1]), v[2]), a1 = max(max(v[3], v[4]), v[5]), a2 = max(max(v[6], v[7]), v[8]);
   const u32 a3 = max(max(v[9], v[10]), v[11]), a4 = max(max(v[12], v[13]), v[14]);
@@ -292,62 +301,81 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     __syncwarp();
   } else if (warp < 4 + MM_EPI) {
     // ===== epilogue: warp w reads TMEM lane quadrant w % 4 (rows 32 (w % 4) ..
-    // + 31), columns [half * N / 2, (half + 1) * N / 2) in blocks of 32: the
-    // next block's tcgen05.ld is in flight while this one is tested. Common
-    // path per 16 columns: a 3-input max tree and one compare; the exact
-    // per-column test runs only when some lane of the warp can pass (vote).
+    // + 31), columns [half * N / 2, (half + 1) * N / 2). The accumulators are
+    // <= 192, so tcgen05.ld .pack::16b brings two columns per register: the
+    // warp's whole share of the tile is in flight at once (one exposed TMEM
+    // latency per tile) and the accumulator is released before the tests.
+    // Common path per 16 columns: a 16x2 SIMD max tree and one compare; the
+    // exact per-column test runs only when some lane of the warp can pass.
     const u32 quad = (u32)(warp % 4);
     const u32 half = (u32)(warp - 4) / 4;
     const u32 row = quad * 32 + lane;
-    constexpr int NB = N / 2 / 32;  // 32-column blocks per warp
+    constexpr int NC = N / 2;        // columns per warp
+    constexpr int NR = NC / 2;       // packed registers
     for (u64 it = 0; it < ntile; ++it) {
       const int b = (int)(it & 1);
       const u64 e = (t0 + it) * MM_M + row;
       const int apop = e < a.n ? (int)a.apop[e] : (1 << 28);
       mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * (N / 2);
-      u32 r[2][32];
-      mm_ld32(taddr, r[0]);
+      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
+      u32 r[NR];
+#pragma unroll
+      for (int g = 0; g < NR / 16; ++g) mm_ld32p(taddr + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int blk = 0; blk < NB; ++blk) {
-        u32(&cur)[32] = r[blk & 1];
-        if (blk + 1 < NB) mm_ld32(taddr + 32 * (blk + 1), r[(blk + 1) & 1]);
-        if (!(a.flags & 4096)) {
-          const int cb = (int)half * (N / 2) + 32 * blk;
-          const u32 m0 = mm_max16(cur), m1 = mm_max16(cur + 16);
-          const bool p0 = 2 * (int)m0 + s_umax[cb >> 4] >= apop;
-          const bool p1 = 2 * (int)m1 + s_umax[(cb >> 4) + 1] >= apop;
-          if (__any_sync(0xffffffffu, p0 || p1)) {
-            u32 pm = 0;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) pm |= (2 * (int)cur[j] + s_u[cb + j] >= apop ? 1u : 0u) << j;
-            while (pm) {
-              const int j = __ffs(pm) - 1;
-              pm &= pm - 1;
-              u32 cj = 0;
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj)
-                if (jj == j) cj = cur[jj];
-              const u32 col = chunk * N + cb + j;
-              const u32 qi = a.qcol[col];
-              const u32 d = (u32)apop + a.qpop[col] - 2 * cj;
-              const u64 key = make_key(d, a.index_base + e);
-              if (a.mode == 0) {
-                const u32 pos = atomicAdd(a.cand_cnt + qi, 1u);
-                if (pos < a.cap) a.cand[(u64)qi * a.cap + pos] = key;
-              } else {
-                const u64 pos = atomicAdd(a.out_cnt, 1ull);
-                if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
-              }
-            }
-          }
-        }
-        if (blk + 1 < NB) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mm_bar_arrive(&tempty[b]);
+      if (a.flags & 4096) continue;
+      const int cb0 = (int)half * NC;
+      u32 gp = 0;  // groups of 16 columns where some column may pass
+#pragma unroll
+      for (int h = 0; h < NC / 16; ++h) {
+        const u32* v = r + 8 * h;
+        const u32 m2 = __vmaxu2(__vmaxu2(__vmaxu2(v[0], v[1]), __vmaxu2(v[2], v[3])),
+                                __vmaxu2(__vmaxu2(v[4], v[5]), __vmaxu2(v[6], v[7])));
+        const int m = (int)max(m2 & 0xffffu, m2 >> 16);
+        gp |= (2 * m + s_umax[(cb0 >> 4) + h] >= apop ? 1u : 0u) << h;
+      }
+      if (!__any_sync(0xffffffffu, gp != 0)) continue;
+      while (gp) {
+        const int h = __ffs(gp) - 1;
+        gp &= gp - 1;
+        const int cb = cb0 + 16 * h;
+        u32 vv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vv[i] = 0;
+#pragma unroll
+        for (int hh = 0; hh < NC / 16; ++hh)
+          if (hh == h) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vv[i] = r[8 * hh + i];
+          }
+        u32 pm = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int c = (int)((vv[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+          pm |= (2 * c + s_u[cb + j] >= apop ? 1u : 0u) << j;
+        }
+        while (pm) {
+          const int j = __ffs(pm) - 1;
+          pm &= pm - 1;
+          u32 cj = 0;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (jj == j) cj = (vv[jj >> 1] >> (16 * (jj & 1))) & 0xffffu;
+          const u32 col = chunk * N + cb + j;
+          const u32 qi = a.qcol[col];
+          const u32 d = (u32)apop + a.qpop[col] - 2 * cj;
+          const u64 key = make_key(d, a.index_base + e);
+          if (a.mode == 0) {
+            const u32 pos = atomicAdd(a.cand_cnt + qi, 1u);
+            if (pos < a.cap) a.cand[(u64)qi * a.cap + pos] = key;
+          } else {
+            const u64 pos = atomicAdd(a.out_cnt, 1ull);
+            if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
+          }
+        }
+      }
     }
   } else {
     // ===== MMA issuer (one lane)
