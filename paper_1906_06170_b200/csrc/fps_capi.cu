@@ -158,7 +158,7 @@ struct fps_lib {
   } pqk;
   u32 done_seq = 0;  // completion sequence of the single-query host path
   // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
-  DevBuf mm_apop, mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp;
+  DevBuf mm_apop, mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp, mm_priv;
   bool mm_apop_ok = false;
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
@@ -955,6 +955,15 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   a.out_cap = out_cap;
   a.flags = scan_flags();
   const u32 ctas = nchunks * parts;
+  if (mode == 0) {
+    // private per-(CTA, column) candidate lists: ~cap / parts expected per list
+    u64 pcap = std::max<u64>(256, 4 * (u64)cap / 8 / parts + 64);
+    pcap = (pcap + 63) / 64 * 64;
+    while (pcap > 256 && (u64)ctas * NN * pcap * 8 > (1ull << 30)) pcap /= 2;
+    if ((rc = L->mm_priv.ensure((size_t)ctas * NN * pcap * 8))) return rc;
+    a.priv = L->mm_priv.as<u64>();
+    a.pcap = (u32)pcap;
+  }
   if (NN == 64) return mma_launch_n<64>(L, ctas, s, a);
   if (NN == 128) return mma_launch_n<128>(L, ctas, s, a);
   return mma_launch_n<256>(L, ctas, s, a);

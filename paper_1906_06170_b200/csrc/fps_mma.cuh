@@ -37,7 +37,7 @@ constexpr int MM_STAGES = 4;
 constexpr u32 MM_A_BYTES = MM_M * MM_K;  // 24 KB
 constexpr u32 MM_B_BYTES = MM_N * MM_K;  // 48 KB (N = 256)
 __host__ __device__ constexpr u32 mm_b_bytes(int n) { return (u32)n * MM_K; }
-constexpr int MM_EPI = 8;                 // epilogue warps: 2 per TMEM lane quadrant, each half the columns
+constexpr int MM_EPI = 16;                // epilogue warps: 4 per TMEM lane quadrant, each a quarter of the columns
 constexpr int MM_RAW = 8;                 // raw library tiles in flight per CTA (bulk-copy ring)
 constexpr u32 MM_RAW_BYTES_MAX = 24 * 256; // >= tile_bytes(compact) and tile_bytes(full)
 constexpr int MM_THREADS = (4 + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
@@ -125,6 +125,8 @@ struct MmArgs {
   u64* out_cnt;
   u64 out_cap;
   u32 flags;                // experiments: 4096 = epilogue without tests, 8192 = producer without library loads
+  u64* priv;                // top-k: [CTA][N columns][pcap] private candidate lists (no global atomics on the scan path)
+  u32 pcap;
 };
 
 __device__ __forceinline__ void mm_bar_init(u64* bar, u32 count) {
@@ -165,6 +167,11 @@ __device__ __forceinline__ void mm_ld32p(u32 taddr, u32 (&r)[16]) {
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void mm_ld16p(u32 taddr, u32 (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ u32 mm_max16(const u32* v) {
   const u32 a0 = max(max(v[0], v[1]), v[2]), a1 = max(max(v[3], v[4]), v[5]), a2 = max(max(v[6], v[7]), v[8]);
   const u32 a3 = max(max(v[9], v[10]), v[11]), a4 = max(max(v[12], v[13]), v[14]);
@@ -186,6 +193,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   __shared__ u32 lut[16];
   __shared__ int s_u[N];
   __shared__ int s_umax[N / 16];
+  __shared__ u32 s_qcol[N], s_qpop[N], s_pcnt[N];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
   const u64 part = blockIdx.x / a.nchunks;
@@ -203,7 +211,12 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     uint4* dst = reinterpret_cast<uint4*>(sB);
     for (u32 i = tid; i < B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
   }
-  for (int i = tid; i < N; i += blockDim.x) s_u[i] = a.ucol[chunk * N + i];
+  for (int i = tid; i < N; i += blockDim.x) {
+    s_u[i] = a.ucol[chunk * N + i];
+    s_qcol[i] = a.qcol[chunk * N + i];
+    s_qpop[i] = a.qpop[chunk * N + i];
+    s_pcnt[i] = 0;
+  }
   if (tid < 16) lut[tid] = (tid & 1) | ((tid >> 1) & 1) << 8 | ((tid >> 2) & 1) << 16 | ((tid >> 3) & 1) << 24;
   if (tid == 0) {
     for (int s = 0; s < MM_STAGES; ++s) {
@@ -308,20 +321,33 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     // Common path per 16 columns: a 16x2 SIMD max tree and one compare; the
     // exact per-column test runs only when some lane of the warp can pass.
     const u32 quad = (u32)(warp % 4);
-    const u32 half = (u32)(warp - 4) / 4;
+    const u32 half = (u32)(warp - 4) / 4;  // column range of the warp (a quarter)
     const u32 row = quad * 32 + lane;
-    constexpr int NC = N / 2;        // columns per warp
-    constexpr int NR = NC / 2;       // packed registers
+    constexpr int NC = N / (MM_EPI / 4);   // columns per warp
+    constexpr int NR = NC / 2;             // packed registers
+    // |a| of the row two tiles ahead is loaded while this tile is processed
+    // (its global-load latency would otherwise sit on the release path)
+    auto apop_of = [&](u64 t) -> int {
+      const u64 ee = (t0 + t) * MM_M + row;
+      return (t < ntile && ee < a.n) ? (int)__ldg(a.apop + ee) : (1 << 28);
+    };
+    int ap1 = apop_of(0), ap2 = apop_of(1);
     for (u64 it = 0; it < ntile; ++it) {
       const int b = (int)(it & 1);
       const u64 e = (t0 + it) * MM_M + row;
-      const int apop = e < a.n ? (int)a.apop[e] : (1 << 28);
+      const int apop = ap1;
+      ap1 = ap2;
+      ap2 = apop_of(it + 2);
       mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
       u32 r[NR];
+      if constexpr (NR == 8) {
+        mm_ld16p(taddr, *reinterpret_cast<u32(*)[8]>(r));
+      } else {
 #pragma unroll
-      for (int g = 0; g < NR / 16; ++g) mm_ld32p(taddr + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
+        for (int g = 0; g < NR / 16; ++g) mm_ld32p(taddr + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mm_bar_arrive(&tempty[b]);
@@ -363,14 +389,15 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj)
             if (jj == j) cj = (vv[jj >> 1] >> (16 * (jj & 1))) & 0xffffu;
-          const u32 col = chunk * N + cb + j;
-          const u32 qi = a.qcol[col];
-          const u32 d = (u32)apop + a.qpop[col] - 2 * cj;
+          const u32 d = (u32)apop + s_qpop[cb + j] - 2 * cj;
           const u64 key = make_key(d, a.index_base + e);
           if (a.mode == 0) {
-            const u32 pos = atomicAdd(a.cand_cnt + qi, 1u);
-            if (pos < a.cap) a.cand[(u64)qi * a.cap + pos] = key;
+            // the CTA's private list of this column: a shared-memory counter,
+            // a store that nothing waits on; published at the end
+            const u32 pos = atomicAdd(s_pcnt + cb + j, 1u);
+            if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + cb + j) * a.pcap + pos] = key;
           } else {
+            const u32 qi = s_qcol[cb + j];
             const u64 pos = atomicAdd(a.out_cnt, 1ull);
             if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
           }
@@ -406,6 +433,23 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (a.mode == 0) {
+    // publish the private lists: one global atomic per (column, CTA); a list
+    // past its capacity poisons its query's count (> cap: the host falls back)
+    for (int c = warp; c < N; c += MM_THREADS / 32) {
+      const u32 cnt = s_pcnt[c];
+      if (cnt == 0) continue;
+      const u32 qi = s_qcol[c];
+      if (qi >= a.Q || chunk * N + c >= a.Q) continue;
+      u32 base = 0;
+      if (lane == 0) base = atomicAdd(a.cand_cnt + qi, cnt > a.pcap ? a.cap + 1 : cnt);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (cnt > a.pcap) continue;
+      const u64* src = a.priv + ((u64)blockIdx.x * N + c) * a.pcap;
+      for (u32 i = lane; i < cnt; i += 32)
+        if (base + i < a.cap) a.cand[(u64)qi * a.cap + base + i] = src[i];
+    }
+  }
   if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
