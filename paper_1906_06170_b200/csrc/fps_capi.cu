@@ -906,11 +906,12 @@ int mma_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
 // ordered by u = T - |q|, then the scan. mode 0 appends candidate keys to the
 // per-query lists L->cand (capacity cap); mode 1 appends range hits to out.
 int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
-            cudaStream_t s, bool prepare_only) {
+            cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull) {
   int rc;
   const u32 NN = mma_pick_n(Q);
   const u32 nchunks = (Q + NN - 1) / NN;
-  const u64 n_tiles = (L->n + fps::MM_M - 1) / fps::MM_M;
+  n_scan = std::min<u64>(n_scan, L->n);  // entries [0, n_scan) (a prefix pass of the top-k path)
+  const u64 n_tiles = (n_scan + fps::MM_M - 1) / fps::MM_M;
   const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles));
   if ((rc = L->mm_bop.ensure((size_t)nchunks * fps::mm_b_bytes((int)NN))) ||
       (rc = L->mm_ucol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_qpop.ensure((size_t)nchunks * NN * 4)) ||
@@ -935,7 +936,7 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   LAUNCH_CHECK("mm_prep");
   fps::MmArgs a{};
   a.lib = L->out();
-  a.n = L->n;
+  a.n = n_scan;
   a.index_base = L->index_base;
   a.n_tiles = n_tiles;
   a.Q = Q;
@@ -973,45 +974,61 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
              bool* fallback) {
   int rc;
   *fallback = false;
-  // 1. seed bound: exact top-k of a library prefix (POPC scan)
-  const u64 seed_n = std::min<u64>(L->n, 1 << 18);
+  // 1. seed bound: exact top-k of a short library prefix (POPC scan)
+  const char* se = std::getenv("FPS_MMA_SEED");
+  const int seed_log2 = se ? std::atoi(se) : 18;
+  const u64 seed_n = std::min<u64>(L->n, 1ull << seed_log2);
   L->timing_suspend = true;
   rc = L->compact ? topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n)
                   : topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n);
   L->timing_suspend = false;
   if (rc) return rc;
-  // candidates per query: pairs within the seed bound (~k x N / seed_n expected)
-  const u64 expect = (u64)k * (L->n / std::max<u64>(seed_n, 1) + 1);
-  const u32 cap = (u32)std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
-  if ((rc = L->mm_tq.ensure((size_t)Q * 4)) || (rc = L->cand.ensure((size_t)Q * cap * 8))) return rc;
-  if (!prepare_only) {
-    fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
-    fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q),
-                                                     ghist_stride(Q));
-    L->launches += 2;
-  }
-  if ((rc = mma_run(L, d_q, Q, 0, cap, nullptr, nullptr, 0, s, prepare_only))) return rc;
-  if (prepare_only) return FPS_OK;
-  // candidate lists must fit their capacity (else: the bit-sliced kernel)
-  std::vector<u32> cc(Q);
-  CUDA_TRY(cudaMemcpyAsync(cc.data(), L->cand_cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  u32 mx = 0;
-  for (u32 v : cc) mx = std::max(mx, v);
-  if (std::getenv("FPS_DEBUG"))
-    std::fprintf(stderr, "[fps] mma scan: Q=%u N=%u cap=%u max candidates=%u\n", Q, mma_pick_n(Q), cap, mx);
-  if (mx > cap) {
-    reset_state(L);
-    *fallback = true;
-    return FPS_OK;
-  }
+  // 2. on long libraries, a tensor-core pass over a longer prefix first: its
+  //    top-k bound is tighter, so the full pass collects ~16x fewer pairs
+  //    (every pair within a bound is collected: each pass is exact for its range)
+  const char* pe = std::getenv("FPS_MMA_PREFIX");
+  const int pre_log2 = pe ? std::atoi(pe) : 22;
+  const u64 pre_n = (pre_log2 > 0 && L->n >= (8ull << pre_log2)) ? (1ull << pre_log2) : 0;
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
-  CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, L->cand.as<u64>(), L->cand_cnt.as<u32>(), cap,
-                         L->tg.as<u32>(), L->ghist.as<u32>(), ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt,
-                         false));
-  L->launches++;
-  LAUNCH_CHECK("select_kernel (mma)");
+  for (int pass = pre_n ? 0 : 1; pass < 2; ++pass) {
+    const u64 n_scan = pass == 0 ? pre_n : L->n;
+    const u64 bound_n = pass == 0 ? seed_n : (pre_n ? pre_n : seed_n);
+    // candidates per query: pairs within the bound (~k x n_scan / bound_n expected)
+    const u64 expect = (u64)k * (n_scan / std::max<u64>(bound_n, 1) + 1);
+    const u32 cap = (u32)std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
+    if ((rc = L->mm_tq.ensure((size_t)Q * 4)) || (rc = L->cand.ensure((size_t)Q * cap * 8))) return rc;
+    if (!prepare_only) {
+      fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
+      fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q),
+                                                       ghist_stride(Q));
+      L->launches += 2;
+    }
+    if (pass == 0) L->timing_suspend = true;
+    rc = mma_run(L, d_q, Q, 0, cap, nullptr, nullptr, 0, s, prepare_only, n_scan);
+    L->timing_suspend = false;
+    if (rc) return rc;
+    if (prepare_only) continue;
+    // candidate lists must fit their capacity (else: the bit-sliced kernel)
+    std::vector<u32> cc(Q);
+    CUDA_TRY(cudaMemcpyAsync(cc.data(), L->cand_cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    u32 mx = 0;
+    for (u32 v : cc) mx = std::max(mx, v);
+    if (std::getenv("FPS_DEBUG"))
+      std::fprintf(stderr, "[fps] mma scan pass %d: Q=%u N=%u n=%llu cap=%u max candidates=%u\n", pass, Q,
+                   mma_pick_n(Q), (unsigned long long)n_scan, cap, mx);
+    if (mx > cap) {
+      reset_state(L);
+      *fallback = true;
+      return FPS_OK;
+    }
+    CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, L->cand.as<u64>(), L->cand_cnt.as<u32>(), cap,
+                           L->tg.as<u32>(), L->ghist.as<u32>(), ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt,
+                           false));
+    L->launches++;
+    LAUNCH_CHECK("select_kernel (mma)");
+  }
   return FPS_OK;
 }
 

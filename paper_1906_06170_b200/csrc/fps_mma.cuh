@@ -37,7 +37,11 @@ constexpr int MM_STAGES = 4;
 constexpr u32 MM_A_BYTES = MM_M * MM_K;  // 24 KB
 constexpr u32 MM_B_BYTES = MM_N * MM_K;  // 48 KB (N = 256)
 __host__ __device__ constexpr u32 mm_b_bytes(int n) { return (u32)n * MM_K; }
-constexpr int MM_EPI = 16;                // epilogue warps: 4 per TMEM lane quadrant, each a quarter of the columns
+constexpr int MM_EPI = 16;                // epilogue warps: 2 groups (alternate tiles) x 4 lane quadrants x 2 column halves
+#ifndef FPS_MM_SUSPEND_NS
+#define FPS_MM_SUSPEND_NS 20000
+#endif
+constexpr unsigned MM_SUSPEND_NS = FPS_MM_SUSPEND_NS;  // try_wait suspend hint: waiting warps sleep instead of spinning
 constexpr int MM_RAW = 8;                 // raw library tiles in flight per CTA (bulk-copy ring)
 constexpr u32 MM_RAW_BYTES_MAX = 24 * 256; // >= tile_bytes(compact) and tile_bytes(full)
 constexpr int MM_THREADS = (4 + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
@@ -137,9 +141,9 @@ __device__ __forceinline__ void mm_bar_arrive(u64* bar) {
 }
 __device__ __forceinline__ void mm_bar_wait(u64* bar, u32 parity) {
   asm volatile(
-      "{\n .reg .pred p;\n MMW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra MMW;\n}\n" ::"r"(
+      "{\n .reg .pred p;\n MMW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra MMW;\n}\n" ::"r"(
           smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(MM_SUSPEND_NS)
       : "memory");
 }
 __device__ __forceinline__ void mm_commit(u64* bar) {
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], MM_EPI * 32);
+      mm_bar_init(&tempty[b], MM_EPI / 2 * 32);  // one epilogue group per accumulator
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -313,93 +317,95 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     __syncwarp();
   } else if (warp < 4 + MM_EPI) {
-    // ===== epilogue: warp w reads TMEM lane quadrant w % 4 (rows 32 (w % 4) ..
-    // + 31), columns [half * N / 2, (half + 1) * N / 2). The accumulators are
-    // <= 192, so tcgen05.ld .pack::16b brings two columns per register: the
-    // warp's whole share of the tile is in flight at once (one exposed TMEM
-    // latency per tile) and the accumulator is released before the tests.
-    // Common path per 16 columns: a 16x2 SIMD max tree and one compare; the
-    // exact per-column test runs only when some lane of the warp can pass.
-    const u32 quad = (u32)(warp % 4);
-    const u32 half = (u32)(warp - 4) / 4;  // column range of the warp (a quarter)
+    // ===== epilogue: two groups of 8 warps take alternate tiles (group g
+    // always reads accumulator g), so a group has two MMA tiles of time for
+    // its loads and tests and the accumulator it holds is released as soon as
+    // its loads land. Warp (quad, half) of a group reads TMEM lane quadrant
+    // quad (rows 32 quad .. + 31), columns [half * N / 2, (half + 1) * N / 2),
+    // in rounds of <= 64 columns. The accumulators are <= 192, so tcgen05.ld
+    // .pack::16b brings two columns per register. Common path per 16
+    // columns: a 16x2 SIMD max tree and one compare; the exact per-column
+    // test runs only when some lane of the warp can pass.
+    const u32 grp = (u32)(warp - 4) / 8;
+    const u32 wq = (u32)(warp - 4) % 8;
+    const u32 quad = wq % 4, half = wq / 4;
     const u32 row = quad * 32 + lane;
-    constexpr int NC = N / (MM_EPI / 4);   // columns per warp
-    constexpr int NR = NC / 2;             // packed registers
-    // |a| of the row two tiles ahead is loaded while this tile is processed
-    // (its global-load latency would otherwise sit on the release path)
+    constexpr int NC = N / 2;                  // columns per warp
+    constexpr int RC = NC < 64 ? NC : 64;      // columns per round
+    constexpr int NRND = NC / RC;
+    constexpr int RR = RC / 2;                 // packed registers per round
     auto apop_of = [&](u64 t) -> int {
       const u64 ee = (t0 + t) * MM_M + row;
       return (t < ntile && ee < a.n) ? (int)__ldg(a.apop + ee) : (1 << 28);
     };
-    int ap1 = apop_of(0), ap2 = apop_of(1);
-    for (u64 it = 0; it < ntile; ++it) {
-      const int b = (int)(it & 1);
+    // |a| of the group's next tile is loaded while this one is processed
+    int apn = apop_of(grp);
+    for (u64 it = grp; it < ntile; it += 2) {
+      const int b = (int)grp;
       const u64 e = (t0 + it) * MM_M + row;
-      const int apop = ap1;
-      ap1 = ap2;
-      ap2 = apop_of(it + 2);
+      const int apop = apn;
+      apn = apop_of(it + 2);
       mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
-      u32 r[NR];
-      if constexpr (NR == 8) {
-        mm_ld16p(taddr, *reinterpret_cast<u32(*)[8]>(r));
-      } else {
+#pragma unroll 1
+      for (int rnd = 0; rnd < NRND; ++rnd) {
+        u32 r[RR];
+        if constexpr (RR == 16) {
+          mm_ld32p(taddr + RC * rnd, r);
+        } else {
 #pragma unroll
-        for (int g = 0; g < NR / 16; ++g) mm_ld32p(taddr + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
-      }
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mm_bar_arrive(&tempty[b]);
-      if (a.flags & 4096) continue;
-      const int cb0 = (int)half * NC;
-      u32 gp = 0;  // groups of 16 columns where some column may pass
-#pragma unroll
-      for (int h = 0; h < NC / 16; ++h) {
-        const u32* v = r + 8 * h;
-        const u32 m2 = __vmaxu2(__vmaxu2(__vmaxu2(v[0], v[1]), __vmaxu2(v[2], v[3])),
-                                __vmaxu2(__vmaxu2(v[4], v[5]), __vmaxu2(v[6], v[7])));
-        const int m = (int)max(m2 & 0xffffu, m2 >> 16);
-        gp |= (2 * m + s_umax[(cb0 >> 4) + h] >= apop ? 1u : 0u) << h;
-      }
-      if (!__any_sync(0xffffffffu, gp != 0)) continue;
-      while (gp) {
-        const int h = __ffs(gp) - 1;
-        gp &= gp - 1;
-        const int cb = cb0 + 16 * h;
-        u32 vv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) vv[i] = 0;
-#pragma unroll
-        for (int hh = 0; hh < NC / 16; ++hh)
-          if (hh == h) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) vv[i] = r[8 * hh + i];
-          }
-        u32 pm = 0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = (int)((vv[j >> 1] >> (16 * (j & 1))) & 0xffffu);
-          pm |= (2 * c + s_u[cb + j] >= apop ? 1u : 0u) << j;
+          for (int g = 0; g < RR / 16; ++g) mm_ld32p(taddr + RC * rnd + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
         }
-        while (pm) {
-          const int j = __ffs(pm) - 1;
-          pm &= pm - 1;
-          u32 cj = 0;
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (rnd == NRND - 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          mm_bar_arrive(&tempty[b]);
+        }
+        if (a.flags & 4096) continue;
+        const int cb0 = (int)half * NC + RC * rnd;
+        u32 gp = 0;  // groups of 16 columns where some column may pass
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
-            if (jj == j) cj = (vv[jj >> 1] >> (16 * (jj & 1))) & 0xffffu;
-          const u32 d = (u32)apop + s_qpop[cb + j] - 2 * cj;
-          const u64 key = make_key(d, a.index_base + e);
-          if (a.mode == 0) {
-            // the CTA's private list of this column: a shared-memory counter,
-            // a store that nothing waits on; published at the end
-            const u32 pos = atomicAdd(s_pcnt + cb + j, 1u);
-            if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + cb + j) * a.pcap + pos] = key;
-          } else {
-            const u32 qi = s_qcol[cb + j];
-            const u64 pos = atomicAdd(a.out_cnt, 1ull);
-            if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
+        for (int h = 0; h < RC / 16; ++h) {
+          const u32* v = r + 8 * h;
+          const u32 m2 = __vmaxu2(__vmaxu2(__vmaxu2(v[0], v[1]), __vmaxu2(v[2], v[3])),
+                                  __vmaxu2(__vmaxu2(v[4], v[5]), __vmaxu2(v[6], v[7])));
+          const int m = (int)max(m2 & 0xffffu, m2 >> 16);
+          gp |= (2 * m + s_umax[(cb0 >> 4) + h] >= apop ? 1u : 0u) << h;
+        }
+        if (a.flags & 16384) gp = 0;  // experiment: no exact tests (timing only)
+        if (!__any_sync(0xffffffffu, gp != 0)) continue;
+        // exact tests of the flagged groups, straight-line per group (register
+        // indices known at compile time), then one entry per passing column
+#pragma unroll
+        for (int h = 0; h < RC / 16; ++h) {
+          if (!((gp >> h) & 1u)) continue;
+          const int cb = cb0 + 16 * h;
+          u32 pm = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = (int)((r[8 * h + (j >> 1)] >> (16 * (j & 1))) & 0xffffu);
+            pm |= (2 * c + s_u[cb + j] >= apop ? 1u : 0u) << j;
+          }
+          while (pm) {
+            const int j = __ffs(pm) - 1;
+            pm &= pm - 1;
+            u32 cj = 0;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              if (jj == j) cj = (r[8 * h + (jj >> 1)] >> (16 * (jj & 1))) & 0xffffu;
+            const u32 d = (u32)apop + s_qpop[cb + j] - 2 * cj;
+            const u64 key = make_key(d, a.index_base + e);
+            if (a.mode == 0) {
+              // the CTA's private list of this column: a shared-memory counter,
+              // a store that nothing waits on; published at the end
+              const u32 pos = atomicAdd(s_pcnt + cb + j, 1u);
+              if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + cb + j) * a.pcap + pos] = key;
+            } else {
+              const u32 qi = s_qcol[cb + j];
+              const u64 pos = atomicAdd(a.out_cnt, 1ull);
+              if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
+            }
           }
         }
       }

@@ -746,3 +746,26 @@ def test_bitslice_all_ties_buffer_capacity(Q, monkeypatch):
         assert lib.last_kernel == "bit-sliced multi-query scan"
         for i in range(Q):
             assert res.hits(i) == [(j, 1) for j in range(k)], (Q, k, i)
+
+
+@pytest.mark.parametrize("prefix_log2", [12, 14])
+def test_mma_two_pass_prefix_bound(prefix_log2, monkeypatch):
+    """Tensor-core top-k with the prefix pass (a tensor-core top-k of a
+    library prefix tightens the bound of the full pass), forced on a small
+    library: every pair within each pass's bound is collected, so the result
+    is the exact top-k."""
+    monkeypatch.setenv("FPS_MMA", "1")
+    monkeypatch.setenv("FPS_MMA_PREFIX", str(prefix_log2))
+    monkeypatch.setenv("FPS_MMA_SEED", "10")
+    n = 300_007
+    w = orc.generate_words(synth.seed_key(77), synth.beta_thresholds(77), 0, n)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(5)
+    q = w[rng.integers(0, n, 300)].copy()
+    q[:, 0] ^= rng.integers(0, 2**20, 300).astype(np.uint64) << np.uint64(1)
+    q[7] = _query_with_pop(rng, 150)
+    for k in (1, 10, 64):
+        res = lib.search_batch(q, k)
+        exp = oracle_topk(w, q, k)
+        for i in range(300):
+            assert res.hits(i) == exp[i], (prefix_log2, k, i)
