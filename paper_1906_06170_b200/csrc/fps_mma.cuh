@@ -1,29 +1,30 @@
 // fps_mma.cuh — multi-query scan on the 5th-generation tensor cores
-// (tcgen05.mma kind::i8, accumulators in TMEM). Opt-in (FPS_MMA=1).
+// (tcgen05.mma kind::i8, accumulators in TMEM). Default for batches of
+// >= 192 queries (top-k and range); FPS_MMA=0 disables it, FPS_MMA=1 forces it.
 //
 // For 0/1 vectors the AND-popcount is a dot product: c = |a AND q| = a . q,
 // and the reference distance (scan.py:137-143, popcount of the XOR of the
 // three full words) is d = |a| + |q| - 2c, with |a|, |q| counted over all
 // 192 bits (pad bits included, as the reference XORs them). So a batch of
 // queries against a library tile is an int8 GEMM with K = 192 (keys 1..166 +
-// pad bits): A = 128 library entries x 192 bytes (0/1), B = 256 queries x 192
-// bytes, D = 128 x 256 int32 in TMEM. The test d <= T_q is
+// pad bits): A = 128 library entries x 192 bytes (0/1), B = N (64/128/256)
+// queries x 192 bytes, D = 128 x N int32 in TMEM. The test d <= T_q is
 // 2c + (T_q - |q|) >= |a|.
 //
-// Exactness: T_q is the k-th distance of a seed pass over a library prefix
-// (every seed entry is in the library, so the true k-th distance is <= T_q);
-// every pair with d <= T_q is collected into the query's candidate list and
-// select_kernel keeps the k smallest (distance, index). Lists that overflow
-// their capacity are reported and the batch is recomputed by the bit-sliced
-// kernel.
+// Exactness (top-k): T_q is the k-th distance of an exact top-k of a library
+// prefix (every prefix entry is in the library, so the true k-th distance is
+// <= T_q); every pair with d <= T_q is collected into the query's candidate
+// list and select_kernel keeps the k smallest (distance, index). Lists that
+// overflow their capacity are reported and the batch is recomputed by the
+// bit-sliced kernel. Range: T_q is the radius.
 //
-// CTA = 9 warps, one CTA per SM: warps 0-3 expand library tiles from the
-// tiled u64 library into the canonical K-major int8 layout (a thread per
-// entry row, nibble -> 4 bytes through a 16-entry table) in a 4-stage
-// shared-memory ring; warp 8 (one lane) issues the MMAs (6 x K=32 per tile)
-// into one of two TMEM accumulators and commits them to mbarriers; warps 4-7
-// (TMEM lane quadrants 0-3) read the accumulators with tcgen05.ld and test
-// 16 columns at a time (max first, exact check only when it can pass).
+// CTA = 22 warps, one CTA per SM: a loader warp streams library tiles into a
+// raw ring (cp.async.bulk); producer warps 0-3 expand them to the canonical
+// K-major int8 layout (a thread per entry row) in a 4-stage ring; one lane of
+// the MMA warp issues 6 x K=32 MMAs per tile into one of two TMEM
+// accumulators and commits them to mbarriers; 16 epilogue warps (two groups
+// on alternate tiles) read the accumulators with tcgen05.ld .pack::16b and
+// test 16 columns at a time (max first, exact check only when it can pass).
 #pragma once
 #include "fps_kernels.cuh"
 
@@ -44,7 +45,8 @@ constexpr int MM_EPI = 16;                // epilogue warps: 2 groups (alternate
 constexpr unsigned MM_SUSPEND_NS = FPS_MM_SUSPEND_NS;  // try_wait suspend hint: waiting warps sleep instead of spinning
 constexpr int MM_RAW = 8;                 // raw library tiles in flight per CTA (bulk-copy ring)
 constexpr u32 MM_RAW_BYTES_MAX = 24 * 256; // >= tile_bytes(compact) and tile_bytes(full)
-constexpr int MM_THREADS = (4 + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
+constexpr int MM_PROD = 8;                // producer warps: 2 groups (alternate tiles) x 4 (a thread per entry row)
+constexpr int MM_THREADS = (MM_PROD + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
 
 // byte (row, k) of a K-major, no-swizzle canonical operand with `rows` rows
 __host__ __device__ __forceinline__ u32 mm_canon(u32 row, u32 k, u32 rows) {
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     for (int r = 0; r < MM_RAW; ++r) {
       mm_bar_init(&raw_full[r], 1);
-      mm_bar_init(&raw_empty[r], 128);
+      mm_bar_init(&raw_empty[r], 128 * SUB);  // every producer thread that reads the raw tile
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4 + MM_EPI) {
+  if (warp == MM_PROD + MM_EPI) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -255,11 +257,13 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   const u32 tmem = tmem_base;
   const u64 ntile = nraw * SUB;
 
-  if (warp < 4) {
-    // ===== producers: thread = entry row of the tile; the entry's words come
-    // from the raw-tile ring the loader warp fills with bulk copies
-    const u32 row = (u32)tid;
-    for (u64 it = 0; it < ntile; ++it) {
+  if (warp < MM_PROD) {
+    // ===== producers: two groups on alternate tiles, thread = entry row of
+    // the tile; the entry's words come from the raw-tile ring the loader warp
+    // fills with bulk copies
+    const u32 row = (u32)tid % 128;
+    const u32 pg = (u32)warp / 4;
+    for (u64 it = pg; it < ntile; it += 2) {
       const int s = (int)(it % MM_STAGES);
       const u64 r = it / SUB;
       const u32 sub = (u32)(it % SUB);
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
           w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
         }
       }
-      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
+      mm_bar_arrive(&raw_empty[rs]);
       if (it >= MM_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM_A_BYTES;
 #pragma unroll
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mm_bar_arrive(&full_bar[s]);
     }
-  } else if (warp == 5 + MM_EPI) {
+  } else if (warp == MM_PROD + MM_EPI + 1) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
     if (lane == 0 && !(a.flags & 8192)) {
       const u64 pol = l2_evict_first_policy();
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       }
     }
     __syncwarp();
-  } else if (warp < 4 + MM_EPI) {
+  } else if (warp < MM_PROD + MM_EPI) {
     // ===== epilogue: two groups of 8 warps take alternate tiles (group g
     // always reads accumulator g), so a group has two MMA tiles of time for
     // its loads and tests and the accumulator it holds is released as soon as
@@ -326,8 +330,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     // .pack::16b brings two columns per register. Common path per 16
     // columns: a 16x2 SIMD max tree and one compare; the exact per-column
     // test runs only when some lane of the warp can pass.
-    const u32 grp = (u32)(warp - 4) / 8;
-    const u32 wq = (u32)(warp - 4) % 8;
+    const u32 grp = (u32)(warp - MM_PROD) / 8;
+    const u32 wq = (u32)(warp - MM_PROD) % 8;
     const u32 quad = wq % 4, half = wq / 4;
     const u32 row = quad * 32 + lane;
     constexpr int NC = N / 2;                  // columns per warp
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         if (base + i < a.cap) a.cand[(u64)qi * a.cap + base + i] = src[i];
     }
   }
-  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  if (warp == MM_PROD + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 }  // namespace fps
