@@ -45,8 +45,7 @@ constexpr int MM_EPI = 16;                // epilogue warps: 2 groups (alternate
 constexpr unsigned MM_SUSPEND_NS = FPS_MM_SUSPEND_NS;  // try_wait suspend hint: waiting warps sleep instead of spinning
 constexpr int MM_RAW = 8;                 // raw library tiles in flight per CTA (bulk-copy ring)
 constexpr u32 MM_RAW_BYTES_MAX = 24 * 256; // >= tile_bytes(compact) and tile_bytes(full)
-constexpr int MM_PROD = 8;                // producer warps: 2 groups (alternate tiles) x 4 (a thread per entry row)
-constexpr int MM_THREADS = (MM_PROD + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
+constexpr int MM_THREADS = (4 + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
 
 // byte (row, k) of a K-major, no-swizzle canonical operand with `rows` rows
 __host__ __device__ __forceinline__ u32 mm_canon(u32 row, u32 k, u32 rows) {
@@ -231,7 +230,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     for (int r = 0; r < MM_RAW; ++r) {
       mm_bar_init(&raw_full[r], 1);
-      mm_bar_init(&raw_empty[r], 128 * SUB);  // every producer thread that reads the raw tile
+      mm_bar_init(&raw_empty[r], 128);
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
@@ -239,7 +238,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MM_PROD + MM_EPI) {
+  if (warp == 4 + MM_EPI) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -257,13 +256,11 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   const u32 tmem = tmem_base;
   const u64 ntile = nraw * SUB;
 
-  if (warp < MM_PROD) {
-    // ===== producers: two groups on alternate tiles, thread = entry row of
-    // the tile; the entry's words come from the raw-tile ring the loader warp
-    // fills with bulk copies
-    const u32 row = (u32)tid % 128;
-    const u32 pg = (u32)warp / 4;
-    for (u64 it = pg; it < ntile; it += 2) {
+  if (warp < 4) {
+    // ===== producers: thread = entry row of the tile; the entry's words come
+    // from the raw-tile ring the loader warp fills with bulk copies
+    const u32 row = (u32)tid;
+    for (u64 it = 0; it < ntile; ++it) {
       const int s = (int)(it % MM_STAGES);
       const u64 r = it / SUB;
       const u32 sub = (u32)(it % SUB);
@@ -284,7 +281,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
           w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
         }
       }
-      mm_bar_arrive(&raw_empty[rs]);
+      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
       if (it >= MM_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM_A_BYTES;
 #pragma unroll
@@ -302,7 +299,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mm_bar_arrive(&full_bar[s]);
     }
-  } else if (warp == MM_PROD + MM_EPI + 1) {
+  } else if (warp == 5 + MM_EPI) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
     if (lane == 0 && !(a.flags & 8192)) {
       const u64 pol = l2_evict_first_policy();
@@ -320,7 +317,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       }
     }
     __syncwarp();
-  } else if (warp < MM_PROD + MM_EPI) {
+  } else if (warp < 4 + MM_EPI) {
     // ===== epilogue: two groups of 8 warps take alternate tiles (group g
     // always reads accumulator g), so a group has two MMA tiles of time for
     // its loads and tests and the accumulator it holds is released as soon as
@@ -330,8 +327,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     // .pack::16b brings two columns per register. Common path per 16
     // columns: a 16x2 SIMD max tree and one compare; the exact per-column
     // test runs only when some lane of the warp can pass.
-    const u32 grp = (u32)(warp - MM_PROD) / 8;
-    const u32 wq = (u32)(warp - MM_PROD) % 8;
+    const u32 grp = (u32)(warp - 4) / 8;
+    const u32 wq = (u32)(warp - 4) % 8;
     const u32 quad = wq % 4, half = wq / 4;
     const u32 row = quad * 32 + lane;
     constexpr int NC = N / 2;                  // columns per warp
@@ -460,7 +457,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         if (base + i < a.cap) a.cand[(u64)qi * a.cap + base + i] = src[i];
     }
   }
-  if (warp == MM_PROD + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 }  // namespace fps
