@@ -51,14 +51,21 @@ def test_single_query_full_size(name):
         assert [i for i, _ in got] == planted0[:100]
 
 
-def test_config4_full_size():
+def test_config4_full_size(monkeypatch):
     plan, lib, q, w = full("c4")
     res = lib.search_batch(q, plan.k)
+    assert lib.last_kernel == "tensor-core multi-query scan"
     exp = oracle_lists(w, q, plan.k)
     for i in range(plan.Q):
         assert res.hits(i) == exp[i], i
         # the query's source entry is within its flip count
         assert res.hits(i)[0][1] <= len(plan.query_flips[i])
+    # the bit-sliced kernel (FPS_MMA=0) gives the same lists
+    monkeypatch.setenv("FPS_MMA", "0")
+    res2 = lib.search_batch(q, plan.k)
+    assert lib.last_kernel == "bit-sliced multi-query scan"
+    for i in range(plan.Q):
+        assert res2.hits(i) == exp[i], i
 
 
 def test_config5_full_size():
@@ -71,6 +78,15 @@ def test_config5_full_size():
     for i, qi, f in zip(plan.planted_idx, plan.planted_query, plan.planted_flips):
         assert (int(qi), int(i), len(f)) in got
     assert len(rows) >= 640_064
+    # the tensor-core range path (FPS_MMA=1) gives the same triples
+    import os
+    os.environ["FPS_MMA"] = "1"
+    try:
+        r2 = lib.range_search(q, plan.radius)
+        assert lib.last_kernel == "tensor-core multi-query scan"
+    finally:
+        del os.environ["FPS_MMA"]
+    assert np.array_equal(r2.rows(), rows)
 
 
 def test_config3_sharded_merge_full_size():
