@@ -158,8 +158,7 @@ struct fps_lib {
   } pqk;
   u32 done_seq = 0;  // completion sequence of the single-query host path
   // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
-  DevBuf mm_apop, mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp, mm_priv;
-  bool mm_apop_ok = false;
+  DevBuf mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp, mm_priv;
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -870,7 +869,8 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
 bool mma_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
   const char* e = std::getenv("FPS_MMA");
   const int mode = e ? std::atoi(e) : -1;
-  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M) return false;
+  // compact libraries only: the fused test uses K slots 168.. (zero there)
+  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M || !L->compact) return false;
   if (mode != 1 && Q < 192) return false;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
@@ -916,17 +916,13 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   if ((rc = L->mm_bop.ensure((size_t)nchunks * fps::mm_b_bytes((int)NN))) ||
       (rc = L->mm_ucol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_qpop.ensure((size_t)nchunks * NN * 4)) ||
       (rc = L->mm_qcol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_keys.ensure((size_t)Q * 8)) ||
-      (rc = L->mm_sorted.ensure((size_t)Q * 8)) || (rc = L->mm_apop.ensure(std::max<u64>(L->n, 1))))
+      (rc = L->mm_sorted.ensure((size_t)Q * 8)))
     return rc;
   size_t tb = 0;
   CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
   if ((rc = L->mm_tmp.ensure(tb))) return rc;
   if (prepare_only) return FPS_OK;
-  if (!L->mm_apop_ok) {
-    fps::mm_pop_kernel<<<L->sms * 8, 256, 0, s>>>(L->out(), L->n, L->mm_apop.as<unsigned char>());
-    L->launches++;
-    L->mm_apop_ok = true;
-  }
+
   fps::mm_ukeys_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_q, Q, L->mm_tq.as<u32>(), L->mm_keys.as<u64>());
   CUDA_TRY(cub::DeviceRadixSort::SortKeys(L->mm_tmp.p, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
   fps::mm_prep_kernel<<<(nchunks * NN + 127) / 128, 128, 0, s>>>(
@@ -943,10 +939,9 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   a.nchunks = nchunks;
   a.parts = parts;
   a.bop = L->mm_bop.as<unsigned char>();
-  a.ucol = L->mm_ucol.as<int>();
+  a.tcol = L->mm_ucol.as<int>();
   a.qpop = L->mm_qpop.as<u32>();
   a.qcol = L->mm_qcol.as<u32>();
-  a.apop = L->mm_apop.as<unsigned char>();
   a.cand = L->cand.as<u64>();
   a.cand_cnt = L->cand_cnt.as<u32>();
   a.cap = cap;
@@ -1009,15 +1004,21 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
     L->timing_suspend = false;
     if (rc) return rc;
     if (prepare_only) continue;
+    // distances of the collected pairs (the scan stores their indices)
+    fps::mm_fix_kernel<<<dim3(4, Q), 256, 0, s>>>(L->out(), L->index_base, d_q, L->cand.as<u64>(),
+                                                  L->cand_cnt.as<u32>(), cap, nullptr, 0);
+    L->launches++;
+    LAUNCH_CHECK("mm_fix_kernel");
     // candidate lists must fit their capacity (else: the bit-sliced kernel)
     std::vector<u32> cc(Q);
     CUDA_TRY(cudaMemcpyAsync(cc.data(), L->cand_cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     u32 mx = 0;
-    for (u32 v : cc) mx = std::max(mx, v);
+    u64 sum = 0;
+    for (u32 v : cc) mx = std::max(mx, v), sum += v;
     if (std::getenv("FPS_DEBUG"))
-      std::fprintf(stderr, "[fps] mma scan pass %d: Q=%u N=%u n=%llu cap=%u max candidates=%u\n", pass, Q,
-                   mma_pick_n(Q), (unsigned long long)n_scan, cap, mx);
+      std::fprintf(stderr, "[fps] mma scan pass %d: Q=%u N=%u n=%llu cap=%u max candidates=%u total=%llu\n", pass, Q,
+                   mma_pick_n(Q), (unsigned long long)n_scan, cap, mx, (unsigned long long)sum);
     if (mx > cap) {
       reset_state(L);
       *fallback = true;
@@ -1040,7 +1041,7 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
 bool mma_range_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
   const char* e = std::getenv("FPS_MMA");
   const int mode = e ? std::atoi(e) : -1;
-  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M) return false;
+  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M || !L->compact) return false;
   const char* m = std::getenv("FPS_MMA_RANGE_MIN_Q");
   if (mode != 1 && Q < (u32)(m ? std::atoi(m) : 192)) return false;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -1057,7 +1058,12 @@ int range_mma(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, 
   if ((rc = L->mm_tq.ensure((size_t)Q * 4))) return rc;
   fps::mm_radius_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_radius, Q, L->mm_tq.as<u32>());
   L->launches++;
-  return mma_run(L, d_q, Q, 1, 0, d_out, d_count, cap, s, false);
+  if ((rc = mma_run(L, d_q, Q, 1, 0, d_out, d_count, cap, s, false))) return rc;
+  // distances of the hits (the scan stores query and index)
+  fps::mm_fix_kernel<<<L->sms * 4, 256, 0, s>>>(L->out(), L->index_base, d_q, d_out, nullptr, 0, d_count, cap);
+  L->launches++;
+  LAUNCH_CHECK("mm_fix_kernel (range)");
+  return FPS_OK;
 }
 
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
@@ -1708,7 +1714,6 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
   lib->bs_state = 0;
   lib->pm.release();
   lib->pm_state = 0;
-  lib->mm_apop_ok = false;  // |a| per entry for the tensor-core path
   if (nwide) return fail(FPS_EINVAL, "entry sets bits 40.. of word 2; the library uses the compact layout");
   return FPS_OK;
 }

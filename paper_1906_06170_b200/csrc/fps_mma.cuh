@@ -9,7 +9,10 @@
 // queries against a library tile is an int8 GEMM with K = 192 (keys 1..166 +
 // pad bits): A = 128 library entries x 192 bytes (0/1), B = N (64/128/256)
 // queries x 192 bytes, D = 128 x N int32 in TMEM. The test d <= T_q is
-// 2c + (T_q - |q|) >= |a|.
+// folded into the GEMM (compact libraries, whose bits 168.. are zero): B
+// holds 2 x the query bits and, in K slots 168..171, T_q - |q| (three s8
+// parts) and -1; A holds the entry bits and 1, 1, 1, |a|. So D = T_q - d:
+// a pair passes iff D >= 0, and its distance is T_q - D.
 //
 // Exactness (top-k): T_q is the k-th distance of an exact top-k of a library
 // prefix (every prefix entry is in the library, so the true k-th distance is
@@ -34,6 +37,7 @@ constexpr int MM_M = 128;          // entries per tile (TMEM lanes)
 constexpr int MM_N = 256;          // queries per CTA chunk (TMEM columns per accumulator), largest shape
                                    // (mma_scan_kernel<N>: N = 64 / 128 / 256 by batch size)
 constexpr int MM_K = 192;          // bytes per row (3 x 64 bits)
+constexpr int MM_KX = 168;         // first K slot of the fused-test terms (bits 168.. are zero in compact libraries)
 constexpr int MM_STAGES = 4;
 constexpr u32 MM_A_BYTES = MM_M * MM_K;  // 24 KB
 constexpr u32 MM_B_BYTES = MM_N * MM_K;  // 48 KB (N = 256)
@@ -72,8 +76,14 @@ __global__ void mm_ukeys_kernel(const u64* __restrict__ q, u32 Q, const u32* __r
   keys[i] = ((u64)((int)tq[i] - (int)pop + (1 << 20)) << 32) | i;
 }
 
+// B of the fused test (compact libraries: bits 168..191 of every entry and
+// query are zero, so K slots 168..171 are free): B[k] = 2 x bit k of the query
+// (s8), B[168..170] = T - |q| split into three s8 parts, B[171] = -1; the
+// library side sets A[168..170] = 1 and A[171] = |a|. The accumulator is then
+// D = 2c + (T - |q|) - |a| = T - d: the pair passes iff D >= 0, and d = T - D.
+// Padding columns (past Q) get T - |q| = -384: D < 0 for every entry.
 __global__ void mm_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __restrict__ tq, unsigned char* __restrict__ bop,
-                               int* __restrict__ ucol, u32* __restrict__ qpop, u32 nchunks,
+                               int* __restrict__ tcol, u32* __restrict__ qpop, u32 nchunks,
                                const u64* __restrict__ order, u32* __restrict__ qcol, u32 NN) {
   const u32 col = blockIdx.x * blockDim.x + threadIdx.x;  // global column = chunk * NN + j
   if (col >= nchunks * NN) return;
@@ -84,25 +94,23 @@ __global__ void mm_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __re
   if (ok) { w[0] = q[3 * (u64)qi]; w[1] = q[3 * (u64)qi + 1]; w[2] = q[3 * (u64)qi + 2]; }
   qcol[col] = qi;
   unsigned char* b = bop + (u64)chunk * mm_b_bytes((int)NN);
-  for (u32 k = 0; k < MM_K; ++k) b[mm_canon(j, k, NN)] = (unsigned char)((w[k >> 6] >> (k & 63)) & 1);
+  for (u32 k = 0; k < MM_K; ++k) b[mm_canon(j, k, NN)] = (unsigned char)(((w[k >> 6] >> (k & 63)) & 1) * 2);
   const u32 pop = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
   qpop[col] = pop;
-  ucol[col] = ok ? (int)tq[qi] - (int)pop : -(1 << 28);
+  int u = ok ? (int)tq[qi] - (int)pop : -384;
+  for (u32 k = MM_KX; k < MM_KX + 3; ++k) {
+    const int part = u < -128 ? -128 : (u > 127 ? 127 : u);
+    u -= part;
+    b[mm_canon(j, k, NN)] = (unsigned char)(signed char)part;
+  }
+  b[mm_canon(j, MM_KX + 3, NN)] = (unsigned char)(signed char)-1;
+  tcol[col] = ok ? (int)tq[qi] : 0;
 }
 
 // range: the bound of query q is its radius
 __global__ void mm_radius_kernel(const unsigned char* __restrict__ radius, u32 Q, u32* __restrict__ tq) {
   const u32 q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < Q) tq[q] = radius[q];
-}
-
-// |a| of every entry (all 192 bits), one byte each (the epilogue's row term)
-__global__ void mm_pop_kernel(PlanesOut lib, u64 n, unsigned char* __restrict__ pc) {
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    u64 a, b, c;
-    lib.get(i, a, b, c);
-    pc[i] = (unsigned char)(__popcll(a) + __popcll(b) + __popcll(c));
-  }
 }
 
 // Per query: the seed bound T_q = k-th distance of the seed top-k (255 when
@@ -112,16 +120,43 @@ __global__ void mm_seed_kernel(const u64* __restrict__ keys, const u32* __restri
   if (q < Q) tq[q] = cnt[q] >= k ? key_d(keys[(u64)q * k + k - 1]) : 255u;
 }
 
+// Distances of the collected pairs (the scan stores indices only): top-k
+// lists [Q][cap] (counts clamped to cap) or range keys (query << 48 | index).
+__global__ void mm_fix_kernel(PlanesOut lib, u64 index_base, const u64* __restrict__ q, u64* __restrict__ keys,
+                              const u32* __restrict__ cnt, u32 cap, const u64* __restrict__ n_range, u64 range_cap) {
+  if (n_range) {
+    const u64 n = min(*n_range, range_cap);
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+      const u64 k = keys[i];
+      const u64 qi = k >> 48, idx = k & ((1ull << 40) - 1);
+      u64 w0, w1, w2;
+      lib.get(idx - index_base, w0, w1, w2);
+      const u32 d = (u32)(__popcll(w0 ^ q[3 * qi]) + __popcll(w1 ^ q[3 * qi + 1]) + __popcll(w2 ^ q[3 * qi + 2]));
+      keys[i] = (qi << 48) | make_key(d, idx);
+    }
+    return;
+  }
+  const u32 qi = blockIdx.y;
+  const u32 n = min(cnt[qi], cap);
+  const u64 q0 = q[3 * (u64)qi], q1 = q[3 * (u64)qi + 1], q2 = q[3 * (u64)qi + 2];
+  u64* kq = keys + (u64)qi * cap;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 idx = kq[i];
+    u64 w0, w1, w2;
+    lib.get(idx - index_base, w0, w1, w2);
+    kq[i] = make_key((u32)(__popcll(w0 ^ q0) + __popcll(w1 ^ q1) + __popcll(w2 ^ q2)), idx);
+  }
+}
+
 struct MmArgs {
   PlanesOut lib;
   u64 n, index_base;
   u64 n_tiles;              // ceil(n / 128)
   u32 Q, nchunks, parts;    // CTA c: chunk c % nchunks, tile range part c / nchunks
   const unsigned char* bop; // [nchunks][48 KB] canonical B
-  const int* ucol;          // [nchunks * 256]
+  const int* tcol;          // [nchunks * 256] T of each column's query (d = T - D)
   const u32* qpop;          // [nchunks * 256] |q| per column
   const u32* qcol;          // [nchunks * 256] query of each column
-  const unsigned char* apop;  // [n] |a|
   u64* cand;                // [Q][cap] keys d << 40 | index
   u32* cand_cnt;            // [Q]
   u32 cap;
@@ -196,8 +231,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   __shared__ __align__(8) u64 raw_full[MM_RAW], raw_empty[MM_RAW];
   __shared__ u32 tmem_base;
   __shared__ u32 lut[16];
-  __shared__ int s_u[N];
-  __shared__ int s_umax[N / 16];
+  __shared__ int s_t[N];
   __shared__ u32 s_qcol[N], s_qpop[N], s_pcnt[N];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
@@ -217,7 +251,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     for (u32 i = tid; i < B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
   }
   for (int i = tid; i < N; i += blockDim.x) {
-    s_u[i] = a.ucol[chunk * N + i];
+    s_t[i] = a.tcol[chunk * N + i];
     s_qcol[i] = a.qcol[chunk * N + i];
     s_qpop[i] = a.qpop[chunk * N + i];
     s_pcnt[i] = 0;
@@ -247,12 +281,6 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (tid < N / 16) {
-    int m = s_u[tid * 16];
-    for (int j = 1; j < 16; ++j) m = max(m, s_u[tid * 16 + j]);
-    s_umax[tid] = m;
-  }
-  __syncthreads();
   const u32 tmem = tmem_base;
   const u64 ntile = nraw * SUB;
 
@@ -294,6 +322,10 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         v.y = (((bits >> 4) & 15u) * 0x204081u) & 0x01010101u;
         v.z = (((bits >> 8) & 15u) * 0x204081u) & 0x01010101u;
         v.w = ((bits >> 12) * 0x204081u) & 0x01010101u;
+        if (c == MM_KX / 16) {  // bytes 168..171: the fused-test terms 1, 1, 1, |a|
+          const u32 pa = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
+          v.z = 0x00010101u | (pa << 24);
+        }
         *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -323,10 +355,10 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     // its loads and tests and the accumulator it holds is released as soon as
     // its loads land. Warp (quad, half) of a group reads TMEM lane quadrant
     // quad (rows 32 quad .. + 31), columns [half * N / 2, (half + 1) * N / 2),
-    // in rounds of <= 64 columns. The accumulators are <= 192, so tcgen05.ld
-    // .pack::16b brings two columns per register. Common path per 16
-    // columns: a 16x2 SIMD max tree and one compare; the exact per-column
-    // test runs only when some lane of the warp can pass.
+    // in rounds of <= 64 columns. The accumulators D = T - d fit 16 bits, so
+    // tcgen05.ld .pack::16b brings two columns per register. Common path: the
+    // AND of a round's registers (a column passes iff its sign bit is clear);
+    // the per-column extraction runs only for lanes that hold a passing pair.
     const u32 grp = (u32)(warp - 4) / 8;
     const u32 wq = (u32)(warp - 4) % 8;
     const u32 quad = wq % 4, half = wq / 4;
@@ -335,17 +367,9 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     constexpr int RC = NC < 64 ? NC : 64;      // columns per round
     constexpr int NRND = NC / RC;
     constexpr int RR = RC / 2;                 // packed registers per round
-    auto apop_of = [&](u64 t) -> int {
-      const u64 ee = (t0 + t) * MM_M + row;
-      return (t < ntile && ee < a.n) ? (int)__ldg(a.apop + ee) : (1 << 28);
-    };
-    // |a| of the group's next tile is loaded while this one is processed
-    int apn = apop_of(grp);
     for (u64 it = grp; it < ntile; it += 2) {
       const int b = (int)grp;
       const u64 e = (t0 + it) * MM_M + row;
-      const int apop = apn;
-      apn = apop_of(it + 2);
       mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
@@ -364,49 +388,38 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
           mm_bar_arrive(&tempty[b]);
         }
         if (a.flags & 4096) continue;
+        // D = T - d per column (s16 halves): some column passes iff a sign
+        // bit of the AND of all halves is clear
+        u32 t = r[0];
+#pragma unroll
+        for (int i = 1; i < RR; ++i) t &= r[i];
+        bool any = (t & 0x80008000u) != 0x80008000u && e < a.n;
+        if (a.flags & 16384) any = false;  // experiment: no hits (timing only)
+        if (!__any_sync(0xffffffffu, any)) continue;
+        if (!any) continue;
         const int cb0 = (int)half * NC + RC * rnd;
-        u32 gp = 0;  // groups of 16 columns where some column may pass
+        // passing columns as a bit mask (straight-line), then a compact loop:
+        // the hit path stays small (instruction cache) and needs no register
+        // indexing. Keys carry the index only; mm_fix_kernel computes the
+        // distances of the (few) collected pairs from the library words.
+        u64 hm = 0;
 #pragma unroll
-        for (int h = 0; h < RC / 16; ++h) {
-          const u32* v = r + 8 * h;
-          const u32 m2 = __vmaxu2(__vmaxu2(__vmaxu2(v[0], v[1]), __vmaxu2(v[2], v[3])),
-                                  __vmaxu2(__vmaxu2(v[4], v[5]), __vmaxu2(v[6], v[7])));
-          const int m = (int)max(m2 & 0xffffu, m2 >> 16);
-          gp |= (2 * m + s_umax[(cb0 >> 4) + h] >= apop ? 1u : 0u) << h;
+        for (int i = 0; i < RR; ++i) {
+          const u32 nn = ~r[i];
+          hm |= ((u64)((nn >> 15) & 1u) << (2 * i)) | ((u64)(nn >> 31) << (2 * i + 1));
         }
-        if (a.flags & 16384) gp = 0;  // experiment: no exact tests (timing only)
-        if (!__any_sync(0xffffffffu, gp != 0)) continue;
-        // exact tests of the flagged groups, straight-line per group (register
-        // indices known at compile time), then one entry per passing column
-#pragma unroll
-        for (int h = 0; h < RC / 16; ++h) {
-          if (!((gp >> h) & 1u)) continue;
-          const int cb = cb0 + 16 * h;
-          u32 pm = 0;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int c = (int)((r[8 * h + (j >> 1)] >> (16 * (j & 1))) & 0xffffu);
-            pm |= (2 * c + s_u[cb + j] >= apop ? 1u : 0u) << j;
-          }
-          while (pm) {
-            const int j = __ffs(pm) - 1;
-            pm &= pm - 1;
-            u32 cj = 0;
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj)
-              if (jj == j) cj = (r[8 * h + (jj >> 1)] >> (16 * (jj & 1))) & 0xffffu;
-            const u32 d = (u32)apop + s_qpop[cb + j] - 2 * cj;
-            const u64 key = make_key(d, a.index_base + e);
-            if (a.mode == 0) {
-              // the CTA's private list of this column: a shared-memory counter,
-              // a store that nothing waits on; published at the end
-              const u32 pos = atomicAdd(s_pcnt + cb + j, 1u);
-              if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + cb + j) * a.pcap + pos] = key;
-            } else {
-              const u32 qi = s_qcol[cb + j];
-              const u64 pos = atomicAdd(a.out_cnt, 1ull);
-              if (pos < a.out_cap) a.out[pos] = ((u64)qi << 48) | key;
-            }
+        const u64 idx = a.index_base + e;
+        while (hm) {
+          const int c = cb0 + __ffsll((long long)hm) - 1;
+          hm &= hm - 1;
+          if (a.mode == 0) {
+            // the CTA's private list of this column: a shared-memory counter,
+            // a store that nothing waits on; published at the end
+            const u32 pos = atomicAdd(s_pcnt + c, 1u);
+            if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
+          } else {
+            const u64 pos = atomicAdd(a.out_cnt, 1ull);
+            if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
           }
         }
       }
@@ -414,7 +427,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   } else {
     // ===== MMA issuer (one lane)
     if (lane == 0) {
-      const u32 idesc = (2u << 4) | ((u32)(N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);  // s32 += u8 x u8, K-major
+      // s32 += u8 (library) x s8 (queries, fused-test terms), both K-major
+      const u32 idesc = (2u << 4) | (1u << 10) | ((u32)(N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);
       const u32 sb = smem_u32(sB);
       for (u64 it = 0; it < ntile; ++it) {
         const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
