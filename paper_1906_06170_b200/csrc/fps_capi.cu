@@ -971,7 +971,7 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
   *fallback = false;
   // 1. seed bound: exact top-k of a short library prefix (POPC scan)
   const char* se = std::getenv("FPS_MMA_SEED");
-  const int seed_log2 = se ? std::atoi(se) : 18;
+  const int seed_log2 = se ? std::atoi(se) : 16;  // 2^16 .. 2^18: same bound after the prefix pass, cheaper seed
   const u64 seed_n = std::min<u64>(L->n, 1ull << seed_log2);
   L->timing_suspend = true;
   rc = L->compact ? topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n)
