@@ -166,7 +166,11 @@ int fps_build_shards(const char* text, uint64_t len, const uint64_t* line_offset
 /* Allocate scratch for (Q, k) so that fps_topk_async does not allocate. */
 int fps_topk_prepare(fps_lib* lib, uint32_t Q, uint32_t k);
 /* d_queries: Q x 3 on the device; out: d_keys Q x k of (distance << 40 |
- * index) keys (UINT64_MAX pads), d_cnt Q. No host synchronisation. */
+ * index) keys (UINT64_MAX pads), d_cnt Q. No host synchronisation, except on
+ * the tensor-core path (Q >= 192, compact library, stream not capturing):
+ * it waits on the stream once per pass to check its candidate lists for
+ * overflow (then recomputes with the bit-sliced kernel). Under stream
+ * capture the call takes the bit-sliced kernel. */
 int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t k, uint64_t* d_keys,
                    uint32_t* d_cnt, void* stream);
 /* Unsorted range hits into d_out (capacity cap), total count (may exceed cap:
@@ -183,7 +187,8 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
 /* Kernel family of the last scan on this handle (reporting / tests):
  * 1 single-query HBM scan, 2 multi-query POPC scan, 3 bit-sliced multi-query
  * scan, 4 large-k (histogram + range + sort) path, 5 single-query plane scan
- * (reads only the bit planes the query needs). */
+ * (reads only the bit planes the query needs), 6 tensor-core multi-query scan
+ * (tcgen05 int8 GEMM with the distance test folded in). */
 int fps_last_kernel(const fps_lib* lib);
 /* Number of kernels launched by this handle so far (evidence counter). */
 uint64_t fps_launch_count(const fps_lib* lib);
