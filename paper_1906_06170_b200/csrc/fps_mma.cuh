@@ -429,22 +429,27 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     if (lane == 0) {
       // s32 += u8 (library) x s8 (queries, fused-test terms), both K-major
       const u32 idesc = (2u << 4) | (1u << 10) | ((u32)(N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);
-      const u32 sb = smem_u32(sB);
+      // descriptors: built once; a K step / stage only moves the start
+      // address field (bits 0-13, in 16-byte units; shared addresses < 256 KB
+      // never carry out of it), so the issue loop is a few uniform adds per MMA
+      const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
+      const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
+      constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM_A_BYTES / 16;
       for (u64 it = 0; it < ntile; ++it) {
         const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
         if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
         mm_bar_wait(&full_bar[s], (u32)(it / MM_STAGES) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const u32 sa = smem_u32(sA + s * MM_A_BYTES);
+        const u64 das = da0 + (u64)s * DA_S;
         const u32 dt = tmem + (u32)b * N;
 #pragma unroll
         for (int ks = 0; ks < MM_K / 32; ++ks) {
-          const u64 da = mm_desc(sa + ks * 2 * (MM_M / 8 * 128), MM_M / 8 * 128, 128);
-          const u64 db = mm_desc(sb + ks * 2 * (N / 8 * 128), N / 8 * 128, 128);
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(dt),
-              "l"(da), "l"(db), "r"(idesc), "r"((u32)(ks > 0)), "r"(0u));
+          if (ks == 0)
+            asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;" ::"r"(dt), "l"(das), "l"(db0),
+                         "r"(idesc));
+          else
+            asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(dt), "l"(das + ks * DA_K),
+                         "l"(db0 + ks * DB_K), "r"(idesc));
         }
         mm_commit(&empty_bar[s]);
         mm_commit(&tfull[b]);
