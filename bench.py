@@ -1,23 +1,30 @@
 #!/usr/bin/env python
 """bench.py — fingerprint comparisons/s of the B200 scan (and of the reference CPU path).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3] [--impl ours|reference]
 
 A step is one pass of the hot path over one batch of synthetic input: the
-workload's queries against the whole library (sharded contiguously over the
-N ranks, per-rank top-k merged on rank 0 over NCCL when N > 1). The default
-workload is BASELINE.json configs[1] (C2: one query vs 10,000,000 entries,
-k = 100, 1,000 planted near-duplicates) — the single-GPU HBM-bound scan.
-Other configs (c1, c3, c4, c5) are selectable with --workload.
+workload's queries against the whole library. The default workload is
+BASELINE.json configs[2] (C3: one query vs the 95,417,114-entry paper-scale
+library, k = 10) — the north-star single-query HBM-bound scan; c1, c2, c4,
+c5 are selectable with --workload.
+
+Multi-GPU (contiguous shards, libstore.split_sizes): under torchrun each of
+the N ranks holds one shard and per-rank top-k lists are merged on rank 0
+(NCCL gather + the device merge kernel); without torchrun, --gpus N drives N
+GPUs from one process (LibraryGroup: the root's merge kernel reads the other
+shards' results from peer HBM). N must match the ranks and the visible GPUs:
+anything else exits non-zero.
 
 `value` is device-timed (CUDA events on the launching stream, inputs resident
-in HBM, L2 flushed between steps when the per-GPU library is within a few
-L2 sizes); `e2e` is the same metric through the public API with host
-buffers (query H2D + result D2H inside the timed region). `roofline` is for
-the scan kernel, timed live with CUDA events around each of its launches.
-`--impl reference` times the reference algorithm (the numpy restatement of
-fpscan.scan in oracle/, reading FPS1 shard files like the reference) on the
-host cores, rank 0 only.
+in HBM, L2 flushed between steps when the bytes a step reads fit in L2);
+`e2e` is the same metric through the public API with host buffers (query
+H2D + result D2H inside the timed region). `roofline` is for the scan
+kernel, timed live with CUDA events around each of its launches.
+`--impl reference` times the reference CPU path on the host cores, rank 0
+only: the unmodified reference ``fpscan.scan.search`` (installed under
+baseline/_ref by tools/install_reference.sh) over FPS1 shards of the same
+library, else the numpy restatement in oracle/.
 """
 
 from __future__ import annotations
@@ -49,7 +56,7 @@ def parse_args():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--seed", type=int, default=20240808)
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -170,58 +177,139 @@ def traffic_for(workload: str):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of fpscan.scan) — test/baseline infrastructure
+# CPU reference path — baseline infrastructure (never the thing measured on GPU)
 # ---------------------------------------------------------------------------
-def cpu_reference(plan, threads: int, budget_s: float, min_runs: int = 1, max_runs: int = 3,
-                  words: np.ndarray | None = None, queries: np.ndarray | None = None):
-    """Time the reference algorithm on a bounded sample of the workload.
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    The sample library is written as FPS1 shards (shard_count = threads, the
-    reference's unit of parallelism) and scanned by the numpy restatement of
-    scan.search, which reads the shard files block by block like the
-    reference. Returns (comparisons/s, description, runs)."""
+
+def _reference_fpscan():
+    """The unmodified reference package from baseline/_ref (tools/install_reference.sh), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "fpscan" / "scan.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import fpscan.fingerprint as ff
+        import fpscan.libstore as fl
+        import fpscan.scan as fs
+
+        return fs, fl, ff
+    except Exception:  # pragma: no cover - broken install
+        return None
+
+
+def _scratch_dir(nbytes: int) -> str | None:
+    """/dev/shm when it holds the FPS1 files with room to spare (page-cache
+    resident, like the reference's warmed-up runs), else the default temp dir."""
+    import shutil
+
+    for d in ("/dev/shm", None):
+        try:
+            if d is None or shutil.disk_usage(d).free > 1.5 * nbytes + (1 << 30):
+                return d
+        except OSError:
+            continue
+    return None
+
+
+class CpuWorkload:
+    """The workload's library (generated on the host by the C twin of the
+    device generator), planted entries, queries, and FPS1 shards + manifest
+    (shard_count = host threads, the reference's unit of parallelism)."""
+
+    def __init__(self, plan, n: int, q_count: int, threads: int):
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import fps_oracle as orc
+
+        from paper_1906_06170_b200 import synth
+
+        self.orc, self.plan, self.n, self.threads = orc, plan, n, threads
+        t0 = time.perf_counter()
+        words = orc.generate_words_parallel(plan.seed_key, plan.thresholds, 0, n, threads)
+        src = synth.generate_rows(plan.seed_key, plan.thresholds, plan.source_idx)
+        self.queries = plan.queries_from_sources(src)
+        if len(plan.planted_idx):
+            pw = plan.planted_words(self.queries)
+            m = plan.planted_idx < n
+            words[plan.planted_idx[m]] = pw[m]
+        self.words = words
+        self.q_count = q_count
+        self._td = tempfile.TemporaryDirectory(dir=_scratch_dir(n * 32))
+        self.manifest_path = orc.write_fps1_library(Path(self._td.name), words, shard_count=max(1, threads))
+        self.prep_s = time.perf_counter() - t0
+        self.ref = _reference_fpscan()
+        self.kind = "reference" if self.ref is not None else "port"
+        if self.ref is not None:
+            fs, fl, ff = self.ref
+            self.ref_manifest = fl.load_manifest(self.manifest_path.parent)
+            self.ref_queries = [ff.Fingerprint(tuple(int(x) for x in q)) for q in self.queries[:q_count]]
+
+    def describe(self) -> str:
+        if self.plan.radius is not None:
+            how = "range restatement (numpy, oracle/fps_oracle.py; the reference has no range op)"
+        elif self.ref is not None:
+            how = "the unmodified reference fpscan.scan.search (baseline/_ref)"
+        else:
+            how = "numpy restatement of fpscan.scan.search (oracle/fps_oracle.py)"
+        return (f"{self.q_count} quer{'y' if self.q_count == 1 else 'ies'} x {self.n:,} entries of workload "
+                f"{self.plan.name} per step, FPS1 shards={self.threads}, {how}")
+
+    def step(self, parallelism: int):
+        plan = self.plan
+        for qi in range(self.q_count):
+            if plan.radius is not None:
+                self.orc.range_search(self.words, self.queries[qi:qi + 1], plan.radius)
+            elif self.ref is not None:
+                fs, _, _ = self.ref
+                fs.search(self.ref_manifest, self.ref_queries[qi], fs.SearchParams(n=plan.k, parallelism=parallelism))
+            else:
+                self.orc.search_fps1(self.manifest_path, self.queries[qi], plan.k, parallelism=parallelism)
+
+    def close(self):
+        self._td.cleanup()
+
+
+def _cpu_queries(plan) -> int:
+    """Queries per CPU step: the whole batch for single-query configs, a
+    labelled 4-query sample of C4 / C5 (1,024 or 64 full-library passes would
+    take minutes per step on the host)."""
+    return plan.Q if plan.Q == 1 else min(plan.Q, 4)
+
+
+def cpu_baseline(plan, budget_s: float = 20.0) -> dict:
+    """The reference CPU path timed on this host (rank 0, N = 1): a bounded
+    sample of the workload, at P = all host threads and at P = 1."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import fps_oracle as orc
 
-    from paper_1906_06170_b200 import synth
-
-    # bounded sample: at most 16M entries, and at most 4 queries
+    threads = orc.cpu_threads()
     n_s = min(plan.n, 16_000_000)
-    q_s = min(plan.Q, 4)
-    if words is None:
-        words = orc.generate_words_parallel(plan.seed_key, plan.thresholds, 0, n_s, threads)
-        if len(plan.planted_idx):
-            src = synth.generate_rows(plan.seed_key, plan.thresholds, plan.source_idx)
-            queries = plan.queries_from_sources(src)
-            pw = plan.planted_words(queries)
-            m = plan.planted_idx < n_s
-            words[plan.planted_idx[m]] = pw[m]
-        else:
-            src = synth.generate_rows(plan.seed_key, plan.thresholds, plan.source_idx[:q_s])
-            queries = np.zeros((plan.Q, 3), dtype=np.uint64)
-            queries[:q_s] = src
-            for i in range(q_s):
-                queries[i] ^= synth.flip_mask(plan.query_flips[i])
-    words = words[:n_s]
-    with tempfile.TemporaryDirectory(dir="/dev/shm" if Path("/dev/shm").exists() else None) as td:
-        mpath = orc.write_fps1_library(Path(td), words, shard_count=max(1, threads))
+    wl = CpuWorkload(plan, n_s, _cpu_queries(plan), threads)
+    try:
+        wl.step(threads)  # page cache / first-touch warm-up (as test_acceptance.py:179)
         times = []
         t_start = time.perf_counter()
-        for r in range(max_runs):
+        while len(times) < 3 and (not times or time.perf_counter() - t_start < budget_s / 2):
             t0 = time.perf_counter()
-            for qi in range(q_s):
-                if plan.radius is not None:
-                    orc.range_search(words, queries[qi:qi + 1], plan.radius)
-                else:
-                    orc.search_fps1(mpath, queries[qi], plan.k, parallelism=threads)
+            wl.step(threads)
             times.append(time.perf_counter() - t0)
-            if r + 1 >= min_runs and time.perf_counter() - t_start > budget_s:
-                break
-    best = min(times)
-    sample = (f"{q_s} quer{'y' if q_s == 1 else 'ies'} x {n_s:,} entries of workload {plan.name} "
-              f"(FPS1 shards={threads}, {'range restatement' if plan.radius is not None else 'scan.search port'}), "
-              f"best of {len(times)}")
-    return q_s * n_s / best, sample, times
+        value = wl.q_count * n_s / min(times)
+        t0 = time.perf_counter()
+        wl.step(1)
+        p1 = wl.q_count * n_s / (time.perf_counter() - t0)
+        return {"value": value, "unit": UNIT, "cores": threads, "kind": wl.kind,
+                "sample": wl.describe() + f" (bounded sample), best of {len(times)}",
+                "p1": {"value": p1, "cores": 1}, "cpu_model": cpu_model()}
+    finally:
+        wl.close()
 
 
 def run_reference(args, rank: int, world: int):
@@ -234,44 +322,32 @@ def run_reference(args, rank: int, world: int):
 
     plan = synth.make_plan(args.workload, seed=args.seed)
     threads = orc.cpu_threads()
-    # warm-up + timed steps: each step is one bounded-sample search
-    n_s = min(plan.n, 16_000_000)
-    q_s = min(plan.Q, 4)
-    words = orc.generate_words_parallel(plan.seed_key, plan.thresholds, 0, n_s, threads)
-    if len(plan.planted_idx):
-        src = synth.generate_rows(plan.seed_key, plan.thresholds, plan.source_idx)
-        queries = plan.queries_from_sources(src)
-        pw = plan.planted_words(queries)
-        m = plan.planted_idx < n_s
-        words[plan.planted_idx[m]] = pw[m]
-    else:
-        queries = plan.queries_from_sources(synth.generate_rows(plan.seed_key, plan.thresholds, plan.source_idx))
-    with tempfile.TemporaryDirectory(dir="/dev/shm" if Path("/dev/shm").exists() else None) as td:
-        mpath = orc.write_fps1_library(Path(td), words, shard_count=threads)
-
-        def step():
-            for qi in range(q_s):
-                if plan.radius is not None:
-                    orc.range_search(words, queries[qi:qi + 1], plan.radius)
-                else:
-                    orc.search_fps1(mpath, queries[qi], plan.k, parallelism=threads)
-
+    wl = CpuWorkload(plan, plan.n, _cpu_queries(plan), threads)  # the full library
+    try:
         for _ in range(args.warmup):
-            step()
+            wl.step(threads)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            step()
+            wl.step(threads)
         wall = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        wl.step(1)
+        p1 = wl.q_count * plan.n / (time.perf_counter() - t1)
+        sample = wl.describe()
+        kind, prep = wl.kind, wl.prep_s
+    finally:
+        wl.close()
     ms = wall * 1e3 / args.steps
-    value = q_s * n_s * args.steps / wall
+    value = wl.q_count * plan.n * args.steps / wall
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": args.workload, **plan.describe(), "sample_entries": n_s, "sample_queries": q_s},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{q_s} quer{'y' if q_s == 1 else 'ies'} x {n_s:,} entries per step, FPS1 "
-                                   f"shards={threads}, numpy restatement of fpscan.scan (oracle/fps_oracle.py)"},
+        "config": plan.describe(),
+        "sample": sample,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                         "p1": {"value": p1, "cores": 1}, "cpu_model": cpu_model(),
+                         "input_prep_s": prep},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -281,13 +357,31 @@ def run_reference(args, rank: int, world: int):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def fail(msg: str) -> int:
+    print(json.dumps({"error": msg}), flush=True)
+    print(f"bench.py: {msg}", file=sys.stderr, flush=True)
+    return 2
+
+
 def run_ours(args, rank: int, local_rank: int, world: int):
     import torch
     import torch.distributed as dist
 
     from paper_1906_06170_b200 import distributed as D
     from paper_1906_06170_b200 import synth
-    from paper_1906_06170_b200.library import keys_to_hits
+
+    visible = torch.cuda.device_count()
+    group_devs = None  # single process driving args.gpus GPUs
+    if world > 1:
+        if args.gpus != world:
+            return fail(f"--gpus {args.gpus} but torchrun started {world} ranks")
+        if visible < world:
+            return fail(f"{world} ranks but only {visible} visible GPU(s)")
+    elif args.gpus > 1:
+        if visible < args.gpus:
+            return fail(f"--gpus {args.gpus} but only {visible} visible GPU(s)")
+        group_devs = list(range(args.gpus))
+    n_gpus = world if world > 1 else args.gpus
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -300,7 +394,12 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     if args.radius is not None:
         plan.k, plan.radius = None, args.radius
     start, count = D.shard_range(plan.n, world, rank)
-    lib, queries = synth.build_library(plan, device=local_rank, start=start, count=count)
+    t_load = time.perf_counter()
+    lib, queries = synth.build_library(plan, device=local_rank, start=start, count=count, devices=group_devs)
+    torch.cuda.synchronize()
+    load_ms = (time.perf_counter() - t_load) * 1e3
+    shard0 = lib.shards[0] if group_devs else lib
+    shard_n = shard0.n  # entries one scan launch covers (the largest shard)
     Q = plan.Q
     dq = torch.from_numpy(queries.view(np.int64).copy()).to(dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
@@ -311,12 +410,18 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     def flush_l2():
         # write a buffer larger than L2 (evicts the library), then read another
         # one so the dirty lines are written back before the timed region
-        flush_buf.zero_()
-        clean_buf.sum()
+        for d in (group_devs or [local_rank]):
+            with torch.cuda.device(d):
+                flush_buf[d].zero_()
+                clean_buf[d].sum()
 
+    state = {}
     if plan.radius is None:
         k = plan.k
-        lib.topk_prepare(Q, k)
+        t_prep = time.perf_counter()
+        lib.topk_prepare(Q, k)  # scratch + the derived plane copies, before the timed region
+        torch.cuda.synchronize()
+        prep_ms = (time.perf_counter() - t_prep) * 1e3
         keys = torch.empty((Q, k), dtype=torch.int64, device=dev)
         cnt = torch.empty((Q,), dtype=torch.int32, device=dev)
 
@@ -328,22 +433,29 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     else:
         rad = torch.full((Q,), plan.radius, dtype=torch.uint8, device=dev)
         count_t = torch.zeros((1,), dtype=torch.int64, device=dev)
-        cap = 1 << 22
-        out = torch.empty((cap,), dtype=torch.int64, device=dev)
-        lib.range_async(dq, Q, rad, out, cap, count_t, stream)
-        torch.cuda.synchronize()
-        hits = int(count_t.item())
-        if hits > cap:
-            cap = hits + 1024
+        t_prep = time.perf_counter()
+        if group_devs:
+            state["hits"] = lib.range_begin(queries, plan.radius)
+        else:
+            cap = 1 << 22
             out = torch.empty((cap,), dtype=torch.int64, device=dev)
-        state = {"hits": hits}
+            lib.range_async(dq, Q, rad, out, cap, count_t, stream)
+            torch.cuda.synchronize()
+            hits = int(count_t.item())
+            if hits > cap:
+                cap = hits + 1024
+                out = torch.empty((cap,), dtype=torch.int64, device=dev)
+            state.update(hits=hits, cap=cap, out=out)
+        prep_ms = (time.perf_counter() - t_prep) * 1e3
 
         def step():
-            lib.range_async(dq, Q, rad, out, cap, count_t, stream)
-            lib.sort_keys(out, state["hits"], stream)
+            if group_devs:  # per-shard scans + sorts, root merge; hits stay on the root
+                return lib.range_begin(queries, plan.radius)
+            lib.range_async(dq, Q, rad, state["out"], state["cap"], count_t, stream)
+            lib.sort_keys(state["out"], state["hits"], stream)
             if world > 1:
-                return D.gather_range(out[: state["hits"]], D.device_sort)
-            return out[: state["hits"]]
+                return D.gather_range(state["out"][: state["hits"]], D.device_sort)
+            return state["out"][: state["hits"]]
 
     def barrier():
         if world > 1:
@@ -352,23 +464,25 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # Library bytes one step reads: the whole tiled library, or for the
+    # Library bytes one scan launch reads: the whole tiled shard, or for the
     # single-query plane scan only the planes of the query (8 popcount planes +
     # min(|q|, 166 - |q|) key planes, 1 bit per entry each).
     kernel = lib.last_kernel
     compact, bpe = lib.layout()
     if kernel == "single-query plane scan":
-        bytes_per_launch = float(count) * plane_scan_planes(queries[0]) / 8.0
+        bytes_per_launch = float(shard_n) * plane_scan_planes(queries[0]) / 8.0
     else:
-        bytes_per_launch = float(bpe) * count
+        bytes_per_launch = float(bpe) * shard_n
     # Bytes read per step larger than L2 are their own flush: the scans stream
     # with an L2 evict-first policy, so K steps run back to back between one
     # event pair. Smaller ones (C1; C2 on the plane scan) get an explicit flush
     # between steps, outside per-step events.
     flush = (not args.no_flush) and bytes_per_launch <= l2
     if flush:
-        flush_buf = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
-        clean_buf = torch.ones(max(2 * l2, 256 << 20) // 8, dtype=torch.int64, device=dev)
+        flush_buf, clean_buf = {}, {}
+        for d in (group_devs or [local_rank]):
+            flush_buf[d] = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=d)
+            clean_buf[d] = torch.ones(max(2 * l2, 256 << 20) // 8, dtype=torch.int64, device=d)
     launches0 = lib.launches
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -412,6 +526,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     total_ms, scan_avg_ms = float(t[0]), float(t[1])
     comparisons = Q * plan.n
     value = comparisons * args.steps / (total_ms / 1e3)
+    mem = lib.memory()
 
     # e2e through the public API with host buffers
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 20))
@@ -480,17 +595,18 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     else:
         sm = props.multi_processor_count
         mhz = clocks["sm_mhz"] or float(peaks.get("sm_max_mhz", 1965.0))
-        achieved = Q * count / (scan_avg_ms / 1e3) / 1e9
+        achieved = Q * shard_n / (scan_avg_ms / 1e3) / 1e9
         naive = sm * POPC_PER_SM_CLK / POPC_PER_CMP_NAIVE * mhz * 1e6 / 1e9
         model = roofline_model(args.workload)
         if kernel == "tensor-core multi-query scan":
             # int8 GEMM on tcgen05: K = 192 bytes (3 x 64 bits) per pair, 2 ops
-            # per multiply-add. There is no measured int8 peak on this pool:
-            # the denominator is the nominal dense int8/fp8 tensor rate of a
-            # B200 (4.5 POP/s, /opt/skills/guides/B200_PROFILING.md); the
-            # ratio to 2 x the driver-measured dense bf16 rate (int8 issues at
-            # twice the bf16 rate) is reported beside it.
-            ops = 2.0 * 192 * Q * count
+            # per multiply-add. There is no driver-measured int8 peak: the
+            # denominator is the nominal dense int8/fp8 tensor rate of a B200
+            # (4.5 POP/s, /opt/skills/guides/B200_PROFILING.md); the ratio to
+            # 2 x the driver-measured dense bf16 rate (int8 issues at twice
+            # the bf16 rate) is reported beside it. The 6-POPC figure of
+            # SURVEY §8(d) is obsolete for this kernel (it does no POPC).
+            ops = 2.0 * 192 * Q * shard_n
             tops = ops / (scan_avg_ms / 1e3) / 1e12
             bf16 = float(peaks.get("bf16_tflops", 1590.0))
             peak = 4500.0
@@ -519,24 +635,41 @@ def run_ours(args, rank: int, local_rank: int, world: int):
                     "peak_source": f"{sm} SMs x 16 POPC/clk/SM (measured) / {per_cmp:.0f} POPC per comparison x "
                                    f"{mhz:.0f} MHz (median SM clock in the timed region)"}
         roof.update({"naive_6popc_peak": naive, "naive_6popc_frac": achieved / naive,
-                     "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": float(bpe) * count,
+                     "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": float(bpe) * shard_n,
                      "kernel": kernel})
 
+    n_total = float(plan.n)
+    parallel = (f"{n_gpus} GPUs in one process (LibraryGroup, gather {lib.gather})" if group_devs else
+                f"{world} ranks (torchrun), NCCL gather to rank 0" if world > 1 else "1 GPU")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {**plan.describe(), "parallelism": f"shard{world}",
-                   "l2": "flushed between steps outside the timed events (2xL2 write, then 2xL2 read so no dirty "
-                         "lines are left)" if flush else
-                   "library larger than L2 and streamed with an L2 evict-first policy: no flush, the K steps "
-                   "run back to back between one event pair",
-                   "layout": (f"plane-major bit planes (1 bit/entry/plane); the query reads "
-                              f"{plane_scan_planes(queries[0])} of 174 planes = "
-                              f"{plane_scan_planes(queries[0]) / 8:.3f} B/entry"
-                              if kernel == "single-query plane scan" else
-                              f"tiles of 128 entries, SoA inside a tile, {bpe} B/entry "
-                              f"({'compact: word 2 as u32 + u8' if compact else 'full: 3 x u64'})")},
+        "config": plan.describe(),
+        "method": {
+            "parallelism": parallel,
+            "l2": "flushed between steps outside the timed events (2xL2 write, then 2xL2 read so no dirty "
+                  "lines are left)" if flush else
+                  "library larger than L2 and streamed with an L2 evict-first policy: no flush, the K steps "
+                  "run back to back between one event pair",
+            "layout": (f"plane-major bit planes (1 bit/entry/plane); the query reads "
+                       f"{plane_scan_planes(queries[0])} of 174 planes = "
+                       f"{plane_scan_planes(queries[0]) / 8:.3f} B/entry"
+                       if kernel == "single-query plane scan" else
+                       f"tiles of {256 if compact else 128} entries, SoA inside a tile, {bpe} B/entry "
+                       f"({'compact: word 2 as u32 + u8' if compact else 'full: 3 x u64'})"),
+        },
+        "library": {
+            "load_ms": load_ms,
+            "prepare_ms": prep_ms,
+            "derived_build_ms": mem["derived_build_ms"],
+            "hbm_bytes_per_entry": {"library": mem["library_bytes"] / n_total,
+                                    "derived": mem["derived_bytes"] / n_total,
+                                    "scratch": mem["scratch_bytes"] / n_total,
+                                    "total": (mem["library_bytes"] + mem["derived_bytes"] + mem["scratch_bytes"])
+                                    / n_total},
+            "note": "this rank's HBM ÷ this rank's entries" if world > 1 else "all devices of the job ÷ entries",
+        },
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps,
@@ -545,16 +678,14 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sys.path.insert(0, str(ROOT / "oracle"))
-        import fps_oracle as orc
-
-        threads = orc.cpu_threads()
-        cv, sample, _ = cpu_reference(plan, threads, budget_s=10.0)
-        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+    if world > 1:
+        line["library"]["hbm_bytes_per_entry"] = {key: v * n_total / max(count, 1)
+                                                  for key, v in line["library"]["hbm_bytes_per_entry"].items()}
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(plan)
     elif rank == 0:
         line["cpu_baseline"] = None
-    # sanity: results are real (first query's best hit is at a small distance)
+    # sanity: results are real (first query's best hit)
     if rank == 0 and plan.radius is None and world == 1:
         res = lib.search_batch(qhost[:1], plan.k)
         line["check"] = {"q0_best": list(res.hits(0)[:1][0]) if res.count[0] else None}
@@ -569,6 +700,8 @@ def run_ours(args, rank: int, local_rank: int, world: int):
 def main():
     args = parse_args()
     rank, local_rank, world = dist_env()
+    if args.gpus < 1:
+        return fail("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, local_rank, world)

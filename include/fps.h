@@ -97,9 +97,11 @@ int fps_open_generated(uint64_t n, uint64_t start, uint64_t seed_key, const uint
 int fps_close(fps_lib* lib);
 int fps_info(const fps_lib* lib, uint64_t* n, uint64_t* index_base, int* device);
 /* HBM layout: tiles, each a small structure of arrays (w0[] | w1[] | word 2).
- * Default: 128-entry tiles of three u64 sub-planes, 24 B per entry.
- * compact = 1 (opt-in, FPS_LAYOUT=compact, only when no entry sets bits 40.. of
- * word 2): word 2 as u32 (bits 0..31) + u8 (bits 32..39), 21 B per entry. */
+ * compact = 1 (the default whenever no entry sets bits 40.. of word 2, i.e.
+ * every valid fingerprint): 256-entry tiles, word 2 as u32 (bits 0..31) + u8
+ * (bits 32..39), 21 B per entry. compact = 0 (libraries with stray pad bits,
+ * or FPS_LAYOUT=full): 128-entry tiles of three u64 sub-planes, 24 B/entry.
+ * Derived copies built on first use are not counted here (fps_memory). */
 int fps_layout(const fps_lib* lib, int* compact, uint64_t* bytes_per_entry);
 /* Copy entries [start, start + count) back as count x 3 u64 rows (host). */
 int fps_read_entries(fps_lib* lib, uint64_t start, uint64_t count, uint64_t* rows);
@@ -166,11 +168,11 @@ int fps_build_shards(const char* text, uint64_t len, const uint64_t* line_offset
 /* Allocate scratch for (Q, k) so that fps_topk_async does not allocate. */
 int fps_topk_prepare(fps_lib* lib, uint32_t Q, uint32_t k);
 /* d_queries: Q x 3 on the device; out: d_keys Q x k of (distance << 40 |
- * index) keys (UINT64_MAX pads), d_cnt Q. No host synchronisation, except on
- * the tensor-core path (Q >= 192, compact library, stream not capturing):
- * it waits on the stream once per pass to check its candidate lists for
- * overflow (then recomputes with the bit-sliced kernel). Under stream
- * capture the call takes the bit-sliced kernel. */
+ * index) keys (UINT64_MAX pads), d_cnt Q. k <= 1024: no host
+ * synchronisation (graph-capturable; the tensor-core path decides its
+ * overflow fallback on the device). k > 1024: the exact large-k path, which
+ * synchronises (not capturable). The first call on a handle may build a
+ * derived copy of the library (plane-major / bit-plane) synchronously. */
 int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t k, uint64_t* d_keys,
                    uint32_t* d_cnt, void* stream);
 /* Unsorted range hits into d_out (capacity cap), total count (may exceed cap:
@@ -190,6 +192,14 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
  * (reads only the bit planes the query needs), 6 tensor-core multi-query scan
  * (tcgen05 int8 GEMM with the distance test folded in). */
 int fps_last_kernel(const fps_lib* lib);
+/* HBM held by the handle: the tiled library, the derived copies built on
+ * first use (plane-major copy of the single-query plane scan, bit-plane copy
+ * of the multi-query kernels; ~21.75 and ~22.3 B per entry), and per-call
+ * scratch; derived_build_ms = host time spent building derived copies. */
+int fps_memory(const fps_lib* lib, uint64_t* library_bytes, uint64_t* derived_bytes, uint64_t* scratch_bytes,
+               double* derived_build_ms);
+/* Free the derived copies (rebuilt on next use) when HBM is needed elsewhere. */
+int fps_release_derived(fps_lib* lib);
 /* Number of kernels launched by this handle so far (evidence counter). */
 uint64_t fps_launch_count(const fps_lib* lib);
 /* Scan-kernel timing for roofline reporting: when enabled, every scan-kernel
@@ -198,6 +208,55 @@ uint64_t fps_launch_count(const fps_lib* lib);
  * last read, and resets. */
 int fps_timing(fps_lib* lib, int enable);
 int fps_timing_read(fps_lib* lib, double* total_ms, uint64_t* count);
+
+/* ---- one library over several GPUs of one process ---- */
+/* The reference fans a search out over contiguous, balanced shards inside one
+ * process (scan.py:256-287, libstore.split_sizes libstore.py:174-179) and
+ * merges per-shard top-k lists with merge_topk (scan.py:225-236). A group
+ * binds contiguous shards (each an fps_lib on its own device) into one
+ * library: every shard scans concurrently on its own stream, and the root
+ * (shard 0's device) gathers and merges. Results are identical to one
+ * fps_lib over the whole library. */
+typedef struct fps_group fps_group;
+
+enum fps_gather {
+  FPS_GATHER_AUTO = 0, /* P2P when every shard device is peer-accessible from
+                          the root, else COPY; env FPS_GATHER=p2p|nccl|copy    */
+  FPS_GATHER_P2P = 1,  /* the merge kernel reads shard results from peer HBM
+                          over NVLink: gather and merge in one kernel          */
+  FPS_GATHER_NCCL = 2, /* grouped ncclSend/ncclRecv to the root, then merge
+                          (libnccl.so.2 loaded at run time; distinct devices)  */
+  FPS_GATHER_COPY = 3  /* cudaMemcpyPeerAsync to the root, then merge          */
+};
+
+/* Bind n_shards handles into a group. Shard i must start at global index
+ * shards[0].index_base + sum of the earlier shards' sizes (contiguous). On
+ * success the group owns the handles (fps_group_close closes them); on
+ * failure they stay with the caller. At most 32 shards. */
+int fps_group_open(fps_lib* const* shards, uint32_t n_shards, int gather, fps_group** out);
+/* Stream FPS1 shard files into n_devices contiguous slices (split_sizes),
+ * one per devices[i], all devices loading concurrently (fps_open_fps1 per
+ * slice). cids (nullable) receives every record's CID in library order. */
+int fps_group_open_fps1(const char* const* paths, uint32_t n_paths, const int* devices, uint32_t n_devices, int gather,
+                        uint64_t* cids, fps_group** out);
+int fps_group_close(fps_group* g);
+int fps_group_info(const fps_group* g, uint64_t* n, uint32_t* n_shards, int* root_device, int* gather);
+/* Borrowed handle of shard i (inspection: fps_last_kernel, fps_timing ...). */
+int fps_group_shard(const fps_group* g, uint32_t i, fps_lib** shard);
+uint64_t fps_group_launch_count(const fps_group* g);
+/* Same contracts as fps_topk / fps_topk_min / fps_range_begin+fetch. */
+int fps_group_topk(fps_group* g, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx,
+                   uint16_t* out_dist, uint32_t* out_cnt);
+int fps_group_topk_min(fps_group* g, const uint64_t* queries, uint32_t Q, uint32_t k, uint64_t* out_idx,
+                       uint16_t* out_dist, uint32_t* out_cnt);
+int fps_group_range_begin(fps_group* g, const uint64_t* queries, uint32_t Q, const uint8_t* radius, uint64_t* n_out);
+int fps_group_range_fetch(fps_group* g, uint32_t* out_query, uint64_t* out_index, uint16_t* out_dist, uint64_t n);
+/* Stream-ordered: d_queries, d_keys (Q x k) and d_cnt (Q) live on the root
+ * device and `stream` is a root-device stream; the shards start after the
+ * work already queued on it, and the merged keys are ready in stream order. */
+int fps_group_topk_prepare(fps_group* g, uint32_t Q, uint32_t k);
+int fps_group_topk_async(fps_group* g, const uint64_t* d_queries, uint32_t Q, uint32_t k, uint64_t* d_keys,
+                         uint32_t* d_cnt, void* stream);
 
 #ifdef __cplusplus
 }

@@ -202,3 +202,55 @@ uint64_t orc_fnv1a_64(const uint8_t* data, uint64_t len, uint64_t h) {
   for (uint64_t i = 0; i < len; ++i) h = (h ^ data[i]) * 0x100000001B3ull;
   return h;
 }
+
+/* Synthetic library generator — the C twin of generate_words (fps_oracle.py)
+ * and of the device gen_kernel: entry i, key j (1-based) is set iff
+ * u32(i, j) < thr[j-1] (or always when all[j-1]), u32 = half of
+ * splitmix64(seed_key + (i*83 + c + 1) * golden), c = (j-1) >> 1. Input
+ * preparation for the CPU baselines at paper scale (numpy takes minutes). */
+typedef struct {
+  uint64_t seed_key, start, lo, hi;
+  const uint64_t* thr;
+  uint64_t* out;
+} gen_arg_t;
+
+static void* gen_worker(void* arg) {
+  gen_arg_t* a = (gen_arg_t*)arg;
+  for (uint64_t r = a->lo; r < a->hi; ++r) {
+    const uint64_t i = a->start + r;
+    uint64_t w[3] = {0, 0, 0};
+    for (uint64_t c = 0; c < 83; ++c) {
+      uint64_t z = a->seed_key + (i * 83 + c + 1) * 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+      const uint64_t j0 = 2 * c, j1 = 2 * c + 1;
+      if ((z & 0xFFFFFFFFull) < a->thr[j0]) w[j0 >> 6] |= 1ull << (j0 & 63);
+      if ((z >> 32) < a->thr[j1]) w[j1 >> 6] |= 1ull << (j1 & 63);
+    }
+    a->out[3 * r] = w[0];
+    a->out[3 * r + 1] = w[1];
+    a->out[3 * r + 2] = w[2];
+  }
+  return NULL;
+}
+
+/* thr: 166 thresholds in [0, 2^32] (2^32 = always set); out: count x 3 u64. */
+int orc_generate(uint64_t seed_key, const uint64_t* thr, uint64_t start, uint64_t count, int threads,
+                 uint64_t* out) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  gen_arg_t args[256];
+  for (int t = 0; t < threads; ++t) {
+    args[t].seed_key = seed_key;
+    args[t].start = start;
+    args[t].lo = count * (uint64_t)t / (uint64_t)threads;
+    args[t].hi = count * (uint64_t)(t + 1) / (uint64_t)threads;
+    args[t].thr = thr;
+    args[t].out = out;
+    if (pthread_create(&th[t], NULL, gen_worker, &args[t])) return 1;
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}

@@ -353,6 +353,7 @@ def _lib():
         lib.orc_free.argtypes = [vp]
         lib.orc_fnv1a_64.argtypes = [vp, _C.c_uint64, _C.c_uint64]
         lib.orc_fnv1a_64.restype = _C.c_uint64
+        lib.orc_generate.argtypes = [_C.c_uint64, vp, _C.c_uint64, _C.c_uint64, _C.c_int, vp]
         _clib = lib
     return _clib
 
@@ -497,13 +498,13 @@ def search_fps1(manifest_path, qwords, k: int, parallelism: int = 1) -> list[tup
 
 def generate_words_parallel(seed_key: int, thresholds: np.ndarray, start: int, count: int,
                             threads: int | None = None, chunk: int = 1 << 18) -> np.ndarray:
-    """generate_words over chunks on a thread pool (numpy releases the GIL)."""
+    """generate_words for a whole library: the C twin (orc_generate) on all
+    host threads; same words as the numpy generate_words (pinned by tests)."""
     out = np.empty((count, 3), dtype=np.uint64)
-
-    def one(s):
-        m = min(chunk, count - s)
-        out[s:s + m] = generate_words(seed_key, thresholds, start + s, m)
-
-    with ThreadPoolExecutor(max_workers=threads or cpu_threads()) as pool:
-        list(pool.map(one, range(0, count, chunk)))
+    thr = np.ascontiguousarray(np.asarray(thresholds, dtype=np.uint64))
+    if count:
+        rc = _lib().orc_generate(seed_key & _M64, thr.ctypes.data, start, count, threads or cpu_threads(),
+                                 out.ctypes.data)
+        if rc:
+            raise RuntimeError("orc_generate failed")
     return out

@@ -10,7 +10,11 @@ fallback: without libfpsgpu.so and a CUDA device the scan raises.
   ``search``, ``search_batch``, ``range_search`` return (index, distance).
 * ``scan``: drop-in ``search`` / ``batch_search`` / ``scan_shard`` /
   ``merge_topk`` with the reference's types (TopK of (cid, distance)).
-* ``distributed``: contiguous shards, one process per GPU, merge on rank 0.
+* ``LibraryGroup`` (``load_library(..., devices=[...])``): one library over
+  several GPUs of this process, merged on the root device (peer reads over
+  NVLink, NCCL, or peer copies).
+* ``distributed``: contiguous shards, one process per GPU (torchrun), merge
+  on rank 0.
 """
 
 from .errors import (
@@ -23,7 +27,7 @@ from .errors import (
     WrongLength,
 )
 from .fingerprint import NUM_KEYS, Fingerprint, distance_packed, parse_bitstring, to_bitstring
-from .library import Library, RangeResult, TopKResult, load_library
+from .library import Library, LibraryGroup, RangeResult, TopKResult, load_library
 
 __all__ = [
     "NUM_KEYS",
@@ -39,6 +43,7 @@ __all__ = [
     "parse_bitstring",
     "to_bitstring",
     "Library",
+    "LibraryGroup",
     "RangeResult",
     "TopKResult",
     "load_library",

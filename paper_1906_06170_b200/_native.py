@@ -72,7 +72,28 @@ SIGNATURES = {
     "fps_last_kernel": (C.c_int, [_vp]),
     "fps_timing": (C.c_int, [_vp, C.c_int]),
     "fps_timing_read": (C.c_int, [_vp, C.POINTER(C.c_double), _u64p]),
+    "fps_memory": (C.c_int, [_vp, _u64p, _u64p, _u64p, C.POINTER(C.c_double)]),
+    "fps_release_derived": (C.c_int, [_vp]),
+    "fps_group_open": (C.c_int, [C.POINTER(_vp), C.c_uint32, C.c_int, C.POINTER(_vp)]),
+    "fps_group_open_fps1": (C.c_int, [C.POINTER(C.c_char_p), C.c_uint32, C.POINTER(C.c_int), C.c_uint32, C.c_int,
+                                      _vp, C.POINTER(_vp)]),
+    "fps_group_close": (C.c_int, [_vp]),
+    "fps_group_info": (C.c_int, [_vp, _u64p, _u32p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "fps_group_shard": (C.c_int, [_vp, C.c_uint32, C.POINTER(_vp)]),
+    "fps_group_launch_count": (C.c_uint64, [_vp]),
+    "fps_group_topk": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
+    "fps_group_topk_min": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
+    "fps_group_range_begin": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _u64p]),
+    "fps_group_range_fetch": (C.c_int, [_vp, _vp, _vp, _vp, C.c_uint64]),
+    "fps_group_topk_prepare": (C.c_int, [_vp, C.c_uint32, C.c_uint32]),
+    "fps_group_topk_async": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
 }
+
+GATHER_AUTO = 0
+GATHER_P2P = 1
+GATHER_NCCL = 2
+GATHER_COPY = 3
+GATHER_NAMES = {"auto": GATHER_AUTO, "p2p": GATHER_P2P, "nccl": GATHER_NCCL, "copy": GATHER_COPY}
 
 _lib = None
 _lock = threading.Lock()

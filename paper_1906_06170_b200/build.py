@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return OUT
     cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-           "-Xcompiler", "-pthread", "-o", str(OUT) + ".tmp", str(SRC / "fps_capi.cu"), str(SRC / "fps_ingest.cpp")]
+           "-Xcompiler", "-pthread", "-ldl", "-o", str(OUT) + ".tmp", str(SRC / "fps_capi.cu"), str(SRC / "fps_ingest.cpp")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

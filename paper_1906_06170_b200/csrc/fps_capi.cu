@@ -9,11 +9,13 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cerrno>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -59,27 +61,41 @@ int fail(int code, const std::string& msg) {
 constexpr int WPB = 8;  // warps per CTA in the scan kernels
 constexpr u32 KMAX_FUSED = 1024;
 
+// Device / pinned-host buffers own their allocation (move-only RAII): every
+// member of a handle and every local scratch buffer is released when it goes
+// out of scope. Release happens with the owning device current (destroy()
+// and every entry point hold a DeviceGuard).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
   int ensure(size_t want) {
     if (want <= bytes) return FPS_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
+    release();
     size_t b = std::max<size_t>(want, 256);
     cudaError_t e = cudaMalloc(&p, b);
     g_alloc_gen++;
     if (e != cudaSuccess) {
       cudaGetLastError();
+      p = nullptr;
       return fail(FPS_ENOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
     }
     bytes = b;
     return FPS_OK;
   }
   void release() {
-    if (p) cudaFree(p);
-    if (p) g_alloc_gen++;
+    if (p) {
+      cudaFree(p);
+      g_alloc_gen++;
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -90,15 +106,19 @@ struct DevBuf {
 struct HostBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  HostBuf(HostBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  ~HostBuf() { release(); }
   int ensure(size_t want) {
     if (want <= bytes) return FPS_OK;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    bytes = 0;
+    release();
     size_t b = std::max<size_t>(want, 4096);
     cudaError_t e = cudaMallocHost(&p, b);
     if (e != cudaSuccess) {
       cudaGetLastError();
+      p = nullptr;
       return fail(FPS_ENOMEM, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
     }
     bytes = b;
@@ -146,6 +166,7 @@ struct fps_lib {
   DevBuf bs, bsq;
   DevBuf mq;  // min-over-queries merge scratch (fps_topk_min on the batched kernel)
   int bs_state = 0;  // 0 unbuilt, 1 built, -1 ineligible (pad bits set)
+  double derived_ms = 0;  // host time spent building derived copies (plane-major, bit-plane)
   // plane-major copy for the single-query plane scan (built on first use)
   DevBuf pm, pm_perm, pm_meta;
   int pm_state = 0;  // as bs_state
@@ -159,6 +180,7 @@ struct fps_lib {
   u32 done_seq = 0;  // completion sequence of the single-query host path
   // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
   DevBuf mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp, mm_priv;
+  DevBuf mm_ovf;  // candidate-list overflow flag of the tensor-core top-k (gates its fallback pass)
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -183,6 +205,11 @@ struct fps_lib {
   bool timing = false;
   bool timing_suspend = false;  // helper passes (e.g. the bit-slice seed) are not timed
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  cudaEvent_t ev_join = nullptr;  // orders the handle's stream after a caller's stream
+  // shard of a multi-device group (fps_group_*): this shard's per-call result
+  // block on its own device, and the event the root device waits on
+  DevBuf gout;
+  cudaEvent_t ev_done = nullptr;
   size_t ev_used = 0;
   fps::PlanesOut out() const { return fps::PlanesOut{mem, compact ? 1 : 0}; }
   u64 bytes_per_entry() const { return compact ? 21 : 24; }
@@ -203,6 +230,24 @@ struct DeviceGuard {
   }
 };
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context)
+// attribute: remember, per (kernel, device), the largest opt-in set so far,
+// so handles on several devices in one process all launch with it.
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, size_t> g_attr;
+
+cudaError_t smem_optin(const void* func, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  size_t& have = g_attr[{func, dev}];
+  if (have >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) have = smem;
+  return e;
+}
+
 template <int QW, int E, int MODE, bool CMP = false>
 size_t scan_smem() {
   return fps::ScanSmem<QW, E, MODE, CMP>::total(WPB);
@@ -211,10 +256,10 @@ size_t scan_smem() {
 template <int QW, int E, int MODE, bool MINQ = false, bool CMP = false>
 int max_ctas_per_sm() {
   static int cached = 0;
-  if (cached) return cached;
   size_t smem = scan_smem<QW, E, MODE, CMP>();
   auto* k = fps::scan_kernel<QW, E, MODE, MINQ, CMP>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  smem_optin((const void*)k, smem);  // per device: also before a cached return
+  if (cached) return cached;
   int blocks = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, WPB * 32, smem);
   cached = std::max(1, blocks);
@@ -345,7 +390,9 @@ void set_dyn(fps_lib* L, fps::ScanArgs& a) {
 // inside it orders it after the scan's completion (and memory flush).
 cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
                           u32* ghist, u32 gstride, u32 tg_rep, u32 k, u64* out_keys, u32* out_cnt, bool pdl,
-                          u32* dyn_ctr = nullptr, u32* done_flag = nullptr, u32 done_seq = 0) {
+                          u32* dyn_ctr = nullptr, u32* done_flag = nullptr, u32 done_seq = 0,
+                          const u32* gate = nullptr, u32* ovf = nullptr) {
+  smem_optin((const void*)fps::select_kernel, smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(Q);
   cfg.blockDim = dim3(fps::SEL_THREADS);
@@ -357,7 +404,7 @@ cudaError_t launch_select(u32 Q, size_t smem, cudaStream_t s, u64* cand, u32* ca
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, fps::select_kernel, cand, cand_cnt, cand_cap, tg, ghist, gstride, tg_rep, k, out_keys,
-                            out_cnt, 1, dyn_ctr, done_flag, done_seq);
+                            out_cnt, 1, dyn_ctr, done_flag, done_seq, gate, ovf);
 }
 
 // Record an event pair around the next scan-kernel launch when timing is on.
@@ -373,7 +420,7 @@ std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
 
 template <int QW, int E, bool CMP>
 int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
-               u64 n_prefix = 0, const u64* h_qin = nullptr) {
+               u64 n_prefix = 0, const u64* h_qin = nullptr, const u32* gate = nullptr) {
   Config c = make_config<QW, E, fps::MODE_TOPK, false, CMP>(L, Q, k, n_prefix);
   int rc;
   if ((rc = ensure_state(L, Q))) return rc;
@@ -402,6 +449,7 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   a.cand = L->cand.as<u64>();
   a.cand_cnt = L->cand_cnt.as<u32>();
   a.cand_cap = c.cand_cap;
+  a.gate = gate;
   set_dyn<QW, E, fps::MODE_TOPK, CMP>(L, a);
   if (c.warps > 0 && L->n > 0) {
     auto* ev = timing_slot(L);
@@ -441,14 +489,9 @@ int topk_fused(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
   size_t sel_smem = (size_t)(kp + fps::SEL_ECAP) * 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr_set = true;
-  }
   LAUNCH_CHECK("scan_kernel<topk>");
   CUDA_TRY(launch_select(Q, sel_smem, s, a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist, a.gstride, a.tg_rep, k,
-                         d_keys, d_cnt, !(a.flags & 32), a.dyn_ctr));
+                         d_keys, d_cnt, !(a.flags & 32), a.dyn_ctr, nullptr, 0, gate));
   L->launches++;
   LAUNCH_CHECK("select_kernel");
   if (std::getenv("FPS_DEBUG")) {
@@ -493,9 +536,9 @@ size_t bs_smem(u32 qpw) { return qpw == 1 ? bs_smem_t<1>() : qpw == 2 ? bs_smem_
 template <int MODE, int QPW>
 int bs_ctas_per_sm() {
   static int cached = 0;
+  const size_t sm = bs_smem_t<QPW>();
+  smem_optin((const void*)fps::bs_scan_kernel<MODE, QPW>, sm);
   if (!cached) {
-    const size_t sm = bs_smem_t<QPW>();
-    cudaFuncSetAttribute(fps::bs_scan_kernel<MODE, QPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, fps::bs_scan_kernel<MODE, QPW>, fps::BS_WARPS * 32, sm);
     cached = std::max(1, cached);
   }
@@ -520,6 +563,12 @@ cudaError_t bs_launch(u32 qpw, u64 ctas, cudaStream_t s, const fps::BsArgs& b) {
 // Build (once) the bit-plane copy; libraries with pad bits past key 166 stay on the POPC path.
 int bs_ensure(fps_lib* L) {
   if (L->bs_state) return FPS_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Clock {
+    fps_lib* L;
+    std::chrono::steady_clock::time_point t0;
+    ~Clock() { L->derived_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+  } clock{L, t0};
   const u64 tiles = (L->n + fps::BS_TILE_ENTRIES - 1) / fps::BS_TILE_ENTRIES;
   int rc;
   if ((rc = L->bs.ensure((size_t)std::max<u64>(tiles, 1) * fps::BS_TILE_BYTES))) {
@@ -660,6 +709,11 @@ int range_bs(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, u
 // the POPC scan (it counts them, like the reference).
 int pm_ensure(fps_lib* L, bool sorted) {
   if (L->pm_state && (L->pm_state < 0 || L->pm_sorted == sorted)) return FPS_OK;
+  struct Clock {
+    fps_lib* L;
+    std::chrono::steady_clock::time_point t0;
+    ~Clock() { L->derived_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+  } clock{L, std::chrono::steady_clock::now()};
   L->pm.release();
   L->pm_perm.release();
   L->pm_meta.release();
@@ -791,11 +845,7 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
                                          fps::pq_scan_kernel<1, 1, false>, fps::pq_scan_kernel<1, 2, false>,
                                          fps::pq_scan_kernel<1, 1, true>,  fps::pq_scan_kernel<1, 2, true>};
   auto* kern = kerns[kv];
-  static size_t smem_set[6] = {0, 0, 0, 0, 0, 0};
-  if (smem > smem_set[kv]) {  // (the kernel's static shared memory comes on top)
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set[kv] = smem;
-  }
+  CUDA_TRY(smem_optin((const void*)kern, smem));  // (the kernel's static shared memory comes on top)
   if (prepare_only) return FPS_OK;
   fps::PqArgs a{};
   a.pm = L->pm.as<u32>();
@@ -841,11 +891,6 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   LAUNCH_CHECK("pq_scan_kernel");
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
-  static bool sel_attr = false;
-  if (!sel_attr) {
-    cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    sel_attr = true;
-  }
   CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, s, a.cand, a.cand_cnt, cand_cap, a.tg, a.ghist,
                          a.gstride, a.tg_rep, k, d_keys, d_cnt, !(a.flags & 32), nullptr, done_flag, done_seq));
   L->launches++;
@@ -859,39 +904,71 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
 
 
 // ---------------------------------------------------------------------------
-// tensor-core multi-query path (fps_mma.cuh), opt-in: FPS_MMA=1
+// tensor-core multi-query path (fps_mma.cuh)
 // ---------------------------------------------------------------------------
 // Large batches take the tensor cores: one 256-query chunk costs ~4.4 ms on
 // the 95.4 M library against ~4.1 ms for 128 queries on the bit-sliced
 // kernel (tools/mma_time.py, tools/q_sweep.py). FPS_MMA=1 forces it for any
-// batch >= 2, FPS_MMA=0 disables it. Not under stream capture: the call
-// checks the candidate lists on the host before its select.
-bool mma_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
-  const char* e = std::getenv("FPS_MMA");
-  const int mode = e ? std::atoi(e) : -1;
-  // compact libraries only: the fused test uses K slots 168.. (zero there)
-  if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M || !L->compact) return false;
-  if (mode != 1 && Q < 192) return false;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    return false;
+// batch >= 2, FPS_MMA=0 disables it. The call is stream ordered end to end
+// (no host synchronisation, capturable): a candidate list that overflows its
+// capacity raises a device flag, and a gated POPC pass recomputes the batch.
+struct MmaPlan {
+  u64 seed_n = 0, pre_n = 0;  // seed prefix (POPC top-k) and tensor-core prefix pass (0: none)
+  u32 cap[2] = {0, 0};        // per-query candidate capacity of the prefix / full pass
+};
+
+// Passes and candidate capacities for (Q, k). Candidates per query of a pass
+// ~ k x n_scan / bound_n (pairs within the prefix bound); the capacity is 8x
+// that, at least 16,384, and Q x cap x 8 B must fit the scratch budget
+// (FPS_MMA_CAND_MB, default 1,024 MB). Returns false when it cannot: the
+// batch then takes the bit-sliced kernel instead of overflowing.
+bool mma_plan(const fps_lib* L, u32 Q, u32 k, MmaPlan* p) {
+  static const int seed_log2 = [] {
+    const char* e = std::getenv("FPS_MMA_SEED");
+    return e ? std::atoi(e) : 16;  // 2^16 .. 2^18: same bound after the prefix pass, cheaper seed
+  }();
+  static const int pre_log2 = [] {
+    const char* e = std::getenv("FPS_MMA_PREFIX");
+    return e ? std::atoi(e) : 22;
+  }();
+  static const u64 budget = [] {
+    const char* e = std::getenv("FPS_MMA_CAND_MB");
+    return (u64)(e ? std::max(16, std::atoi(e)) : 1024) << 20;
+  }();
+  p->seed_n = std::min<u64>(L->n, 1ull << seed_log2);
+  p->pre_n = (pre_log2 > 0 && L->n >= (8ull << pre_log2)) ? (1ull << pre_log2) : 0;
+  for (int pass = p->pre_n ? 0 : 1; pass < 2; ++pass) {
+    const u64 n_scan = pass == 0 ? p->pre_n : L->n;
+    const u64 bound_n = pass == 0 ? p->seed_n : (p->pre_n ? p->pre_n : p->seed_n);
+    const u64 expect = (u64)k * (n_scan / std::max<u64>(bound_n, 1) + 1);
+    const u64 want = std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
+    const u64 fit = budget / ((u64)Q * 8);
+    if (fit < 2 * expect || fit < 1024) return false;
+    p->cap[pass] = (u32)std::min<u64>(want, fit);
   }
   return true;
 }
 
-// accumulator width by batch: the smallest of 64 / 128 / 256 columns that
-// holds the batch in one chunk (the MMA and epilogue work scale with it)
+bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
+  static const int mode = [] {
+    const char* e = std::getenv("FPS_MMA");
+    return e ? std::atoi(e) : -1;
+  }();
+  // compact libraries only: the fused test uses K slots 168.. (zero there)
+  if (mode == 0 || Q < 2 || k > KMAX_FUSED || L->n < (u64)fps::MM_M || !L->compact) return false;
+  if (mode != 1 && Q < 192) return false;
+  MmaPlan p;
+  if (!mma_plan(L, Q, k, &p)) return false;
+  if (plan) *plan = p;
+  return true;
+}
+
 u32 mma_pick_n(u32 Q) { return Q <= 64 ? 64u : Q <= 128 ? 128u : 256u; }
 
 template <int N>
 int mma_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
-  static bool attr = false;
   const size_t smem = fps::mm_b_bytes(N) + (size_t)fps::MM_STAGES * fps::MM_A_BYTES + (size_t)fps::MM_RAW * fps::MM_RAW_BYTES_MAX;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(fps::mma_scan_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  CUDA_TRY(smem_optin((const void*)fps::mma_scan_kernel<N>, smem));
   auto* ev = timing_slot(L);
   if (ev) cudaEventRecord(ev->first, s);
   fps::mma_scan_kernel<N><<<ctas, fps::MM_THREADS, smem, s>>>(a);
@@ -966,32 +1043,24 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
 }
 
 int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s, bool prepare_only,
-             bool* fallback) {
+             const MmaPlan& plan) {
   int rc;
-  *fallback = false;
+  if ((rc = L->mm_ovf.ensure(256))) return rc;
+  u32* ovf = L->mm_ovf.as<u32>();
+  if (!prepare_only) CUDA_TRY(cudaMemsetAsync(ovf, 0, 4, s));
   // 1. seed bound: exact top-k of a short library prefix (POPC scan)
-  const char* se = std::getenv("FPS_MMA_SEED");
-  const int seed_log2 = se ? std::atoi(se) : 16;  // 2^16 .. 2^18: same bound after the prefix pass, cheaper seed
-  const u64 seed_n = std::min<u64>(L->n, 1ull << seed_log2);
   L->timing_suspend = true;
-  rc = L->compact ? topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n)
-                  : topk_fused<8, 2, false>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, seed_n);
+  rc = topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, plan.seed_n);
   L->timing_suspend = false;
   if (rc) return rc;
   // 2. on long libraries, a tensor-core pass over a longer prefix first: its
   //    top-k bound is tighter, so the full pass collects ~16x fewer pairs
   //    (every pair within a bound is collected: each pass is exact for its range)
-  const char* pe = std::getenv("FPS_MMA_PREFIX");
-  const int pre_log2 = pe ? std::atoi(pe) : 22;
-  const u64 pre_n = (pre_log2 > 0 && L->n >= (8ull << pre_log2)) ? (1ull << pre_log2) : 0;
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
-  for (int pass = pre_n ? 0 : 1; pass < 2; ++pass) {
-    const u64 n_scan = pass == 0 ? pre_n : L->n;
-    const u64 bound_n = pass == 0 ? seed_n : (pre_n ? pre_n : seed_n);
-    // candidates per query: pairs within the bound (~k x n_scan / bound_n expected)
-    const u64 expect = (u64)k * (n_scan / std::max<u64>(bound_n, 1) + 1);
-    const u32 cap = (u32)std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
+  for (int pass = plan.pre_n ? 0 : 1; pass < 2; ++pass) {
+    const u64 n_scan = pass == 0 ? plan.pre_n : L->n;
+    const u32 cap = plan.cap[pass];
     if ((rc = L->mm_tq.ensure((size_t)Q * 4)) || (rc = L->cand.ensure((size_t)Q * cap * 8))) return rc;
     if (!prepare_only) {
       fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
@@ -1009,28 +1078,20 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
                                                   L->cand_cnt.as<u32>(), cap, nullptr, 0);
     L->launches++;
     LAUNCH_CHECK("mm_fix_kernel");
-    // candidate lists must fit their capacity (else: the bit-sliced kernel)
-    std::vector<u32> cc(Q);
-    CUDA_TRY(cudaMemcpyAsync(cc.data(), L->cand_cnt.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    u32 mx = 0;
-    u64 sum = 0;
-    for (u32 v : cc) mx = std::max(mx, v), sum += v;
-    if (std::getenv("FPS_DEBUG"))
-      std::fprintf(stderr, "[fps] mma scan pass %d: Q=%u N=%u n=%llu cap=%u max candidates=%u total=%llu\n", pass, Q,
-                   mma_pick_n(Q), (unsigned long long)n_scan, cap, mx, (unsigned long long)sum);
-    if (mx > cap) {
-      reset_state(L);
-      *fallback = true;
-      return FPS_OK;
-    }
+    // a list past its capacity sets *ovf (its pass's bound, and so the next
+    // pass, may then be wrong: the gated pass below recomputes everything)
     CUDA_TRY(launch_select(Q, (size_t)(kp + fps::SEL_ECAP) * 8, s, L->cand.as<u64>(), L->cand_cnt.as<u32>(), cap,
                            L->tg.as<u32>(), L->ghist.as<u32>(), ghist_stride(Q), tg_replicas(Q), k, d_keys, d_cnt,
-                           false));
+                           false, nullptr, nullptr, 0, nullptr, ovf));
     L->launches++;
     LAUNCH_CHECK("select_kernel (mma)");
   }
-  return FPS_OK;
+  // 3. device-side fallback (adversarial ties): an exact POPC pass over the
+  //    whole library that runs only when a candidate list overflowed
+  L->timing_suspend = true;
+  rc = topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, 0, nullptr, ovf);
+  L->timing_suspend = false;
+  return rc;
 }
 
 // Range search on the tensor cores: the bound is the radius itself (exact,
@@ -1068,11 +1129,10 @@ int range_mma(fps_lib* L, const u64* d_q, u32 Q, const unsigned char* d_radius, 
 
 int topk_dispatch(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
                   bool prepare_only) {
-  if (mma_wanted(L, Q, s)) {
-    bool fb = false;
+  MmaPlan plan;
+  if (mma_wanted(L, Q, k, &plan)) {
     L->last_kernel = 6;
-    const int rc = topk_mma(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, &fb);
-    if (rc || !fb) return rc;
+    return topk_mma(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, plan);
   }
   if (Q == 1 && pq_wanted(L)) return topk_pq(L, d_q, nullptr, k, d_keys, d_cnt, s, prepare_only);
   if (bs_wanted(L, Q)) {
@@ -1249,31 +1309,32 @@ int new_lib(int device, u64 index_base, fps_lib** out) {
   return FPS_OK;
 }
 
+// Release everything the handle owns. The DevBuf / HostBuf members free
+// themselves when the handle is deleted (with its device current); raw
+// allocations, graphs, events and the stream are released here.
 void destroy(fps_lib* L) {
   if (!L) return;
   DeviceGuard g(L->device);
   if (L->stream) cudaStreamSynchronize(L->stream);
   if (L->mem) cudaFree(L->mem);
-  for (DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt, &L->radius,
-                    &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->bs, &L->bsq})
-    b->release();
-  L->h_stage.release();
+  L->mem = nullptr;
   if (L->hmap) cudaFreeHost(L->hmap);
+  L->hmap = nullptr;
   for (auto* gr : L->graphs) {
     if (gr->exec) cudaGraphExecDestroy(gr->exec);
-    gr->hq.release();
-    gr->hout.release();
-    gr->dq.release();
-    gr->dkeys.release();
-    gr->dcnt.release();
     delete gr;
   }
+  L->graphs.clear();
   for (auto& p : L->ev_pool) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
   }
+  L->ev_pool.clear();
+  if (L->ev_join) cudaEventDestroy(L->ev_join);
+  if (L->ev_done) cudaEventDestroy(L->ev_done);
   if (L->stream) cudaStreamDestroy(L->stream);
-  delete L;
+  L->stream = nullptr;
+  delete L;  // member buffers are freed here, device still current
 }
 
 void unpack_topk(const u64* keys, const u32* cnt, u32 Q, u32 k, uint64_t* out_idx, uint16_t* out_dist,
@@ -1333,6 +1394,132 @@ int topk_large(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt
   L->launches++;
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(L->stream));
+  return FPS_OK;
+}
+
+// Sorted range keys on the device -> query / index / distance host columns,
+// through a pinned double buffer: chunk c + 1 copies while chunk c is split
+// (host threads measured slower: spawning them costs more than the split,
+// which is bounded by first-touch faults on the fresh columns).
+cudaError_t fetch_columns(cudaStream_t s, const u64* src, u64 n, HostBuf* hr, uint32_t* out_query,
+                          uint64_t* out_index, uint16_t* out_dist) {
+  constexpr u64 CH = 1 << 17;  // keys per chunk (1 MiB)
+  if (n == 0) return cudaSuccess;
+  if (hr[0].ensure(CH * 8) || hr[1].ensure(CH * 8)) return cudaErrorMemoryAllocation;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  auto issue = [&](u64 c) {
+    const u64 lo = c * CH, m = std::min<u64>(CH, n - lo);
+    cudaMemcpyAsync(hr[c & 1].p, src + lo, m * 8, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(ev[c & 1], s);
+  };
+  const u64 chunks = (n + CH - 1) / CH;
+  issue(0);
+  cudaError_t e = cudaSuccess;
+  for (u64 c = 0; c < chunks && e == cudaSuccess; ++c) {
+    e = cudaEventSynchronize(ev[c & 1]);
+    if (c + 1 < chunks) issue(c + 1);
+    const u64 lo = c * CH, m = std::min<u64>(CH, n - lo);
+    fps_range_unpack(reinterpret_cast<const uint64_t*>(hr[c & 1].p), m, out_query + lo, out_index + lo, out_dist + lo);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  for (auto& x : ev) cudaEventDestroy(x);
+  return e;
+}
+
+// Order the handle's own stream after the work queued so far on s: the
+// large-k path and the range collection run on L->stream and synchronise on
+// it (their sizes are data dependent), so a caller's stream hands over here.
+int join_stream(fps_lib* L, cudaStream_t s) {
+  if (s == L->stream) return FPS_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return fail(FPS_EINVAL, "k > 1024 synchronises on the host and cannot be captured in a graph");
+  }
+  if (!L->ev_join) CUDA_TRY(cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(L->ev_join, s));
+  CUDA_TRY(cudaStreamWaitEvent(L->stream, L->ev_join, 0));
+  return FPS_OK;
+}
+
+// Per-query top-k for any k >= 1 on stream s: the fused kernels for
+// k <= 1024, else the large-k path (which synchronises).
+int topk_any(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s) {
+  if (k <= KMAX_FUSED) return topk_dispatch(L, d_q, Q, k, d_keys, d_cnt, s, false);
+  int rc;
+  if ((rc = join_stream(L, s))) return rc;
+  return topk_large(L, d_q, Q, k, d_keys, d_cnt);
+}
+
+// Min-over-queries top-k (the reference batch_search, scan.py:306-318) on
+// stream s, results left on the device: d_out[k] keys, *d_cnt.
+//  * per-query path (batches on the bit-sliced / tensor-core kernels, and any
+//    k > 1024): per-query top-k lists, then the min merge -- exact, because an
+//    entry's best query ranks it no lower than the global order does, so the
+//    global top-k is inside the union of the per-query lists, and its score
+//    is its smallest listed distance;
+//  * otherwise one POPC pass that scores every entry by its minimum distance.
+int topk_min_dev(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_out, u32* d_cnt, cudaStream_t s) {
+  int rc;
+  if (Q == 0 || k == 0) return fail(FPS_EINVAL, "Q and k must be >= 1");
+  const bool perq = (Q >= 2 && bs_wanted(L, Q)) || k > KMAX_FUSED;
+  if (perq) {
+    const u64 n = (u64)Q * k;
+    if ((rc = L->mq.ensure(n * 8 * 3 + (size_t)Q * 4 + 16))) return rc;
+    u64* pk = L->mq.as<u64>();  // per-query keys
+    u64* tmp = pk + n;
+    u64* out = tmp + n;
+    u32* pc = reinterpret_cast<u32*>(out + n);
+    u32* firsts = pc + Q;
+    if ((rc = topk_any(L, d_q, Q, k, pk, pc, s))) return rc;
+    const int blocks = (int)std::min<u64>((n + 255) / 256, 4096);
+    fps::minq_flip<<<blocks, 256, 0, s>>>(pk, pc, Q, k, tmp);
+    if ((rc = sort_keys(L, tmp, n, s))) return rc;
+    CUDA_TRY(cudaMemsetAsync(firsts, 0, 4, s));
+    fps::minq_first<<<blocks, 256, 0, s>>>(tmp, n, out, firsts);
+    if ((rc = sort_keys(L, out, n, s))) return rc;
+    fps::minq_emit<<<(k + 255) / 256, 256, 0, s>>>(out, firsts, k, d_out, d_cnt);
+    L->launches += 3;
+    LAUNCH_CHECK("minq merge");
+    return FPS_OK;
+  }
+  Config c = L->compact ? make_config<1, 4, fps::MODE_TOPK, true, true>(L, 1, k)
+                        : make_config<1, 4, fps::MODE_TOPK, true, false>(L, 1, k);
+  if ((rc = ensure_state(L, 1))) return rc;
+  if ((rc = L->buf.ensure(c.warps * (size_t)c.cap * 8))) return rc;
+  if ((rc = L->cand.ensure(c.cand_cap * 8))) return rc;
+  fps::ScanArgs a = base_args(L, d_q, 1);
+  a.Qmin = Q;
+  a.k = k;
+  a.cap = c.cap;
+  a.n_qg = 1;
+  a.n_parts = c.n_parts;
+  a.iters = c.iters;
+  a.tg = L->tg.as<u32>();
+  a.ghist = L->ghist.as<u32>();
+  a.gstride = ghist_stride(1);
+  a.tg_rep = tg_replicas(1);
+  a.pub_every = (u32)std::max<u64>(1, c.n_parts / 512);
+  a.buf = L->buf.as<u64>();
+  a.cand = L->cand.as<u64>();
+  a.cand_cnt = L->cand_cnt.as<u32>();
+  a.cand_cap = c.cand_cap;
+  if (L->compact) set_dyn<1, 4, fps::MODE_TOPK, true>(L, a);
+  else set_dyn<1, 4, fps::MODE_TOPK, false>(L, a);
+  L->last_kernel = 1;
+  if (c.warps > 0 && L->n > 0) {
+    if (L->compact) fps::scan_kernel<1, 4, fps::MODE_TOPK, true, true><<<c.grid, WPB * 32, c.smem, s>>>(a);
+    else fps::scan_kernel<1, 4, fps::MODE_TOPK, true, false><<<c.grid, WPB * 32, c.smem, s>>>(a);
+    L->launches++;
+  }
+  LAUNCH_CHECK("scan_kernel<min over queries>");
+  int kp = 1;
+  while (kp < (int)k) kp <<= 1;
+  CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, s, a.cand, a.cand_cnt, c.cand_cap, a.tg, a.ghist,
+                         a.gstride, a.tg_rep, k, d_out, d_cnt, true, a.dyn_ctr));
+  L->launches++;
+  LAUNCH_CHECK("select_kernel (min over queries)");
   return FPS_OK;
 }
 
@@ -1649,6 +1836,9 @@ int fps_open_generated(uint64_t n, uint64_t start, uint64_t seed_key, const uint
 
 int fps_close(fps_lib* lib) {
   if (!lib) return FPS_OK;
+  // wait for a call in flight on another thread; the caller guarantees no new
+  // call starts on a handle it closes (the Python layer reference-counts)
+  { std::lock_guard<std::mutex> lk(lib->mu); }
   destroy(lib);
   return FPS_OK;
 }
@@ -1713,6 +1903,8 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
   lib->bs.release();
   lib->bs_state = 0;
   lib->pm.release();
+  lib->pm_perm.release();
+  lib->pm_meta.release();
   lib->pm_state = 0;
   if (nwide) return fail(FPS_EINVAL, "entry sets bits 40.. of word 2; the library uses the compact layout");
   return FPS_OK;
@@ -1721,7 +1913,7 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
 int fps_topk_prepare(fps_lib* lib, uint32_t Q, uint32_t k) {
   if (int rc = check_lib(lib)) return rc;
   if (Q == 0 || k == 0) return fail(FPS_EINVAL, "Q and k must be >= 1");
-  if (k > KMAX_FUSED) return fail(FPS_EINVAL, "fps_topk_async supports k <= 1024");
+  if (k > KMAX_FUSED) return FPS_OK;  // the large-k path sizes its scratch per call
   std::lock_guard<std::mutex> lk(lib->mu);
   DeviceGuard g(lib->device);
   int rc = topk_dispatch(lib, nullptr, Q, k, nullptr, nullptr, lib->stream, true);
@@ -1733,11 +1925,10 @@ int fps_topk_async(fps_lib* lib, const uint64_t* d_queries, uint32_t Q, uint32_t
                    uint32_t* d_cnt, void* stream) {
   if (int rc = check_lib(lib)) return rc;
   if (Q == 0 || k == 0) return fail(FPS_EINVAL, "Q and k must be >= 1");
-  if (k > KMAX_FUSED) return fail(FPS_EINVAL, "fps_topk_async supports k <= 1024");
   std::lock_guard<std::mutex> lk(lib->mu);
   DeviceGuard g(lib->device);
   cudaStream_t s = (cudaStream_t)stream;  // used as given (0 = legacy default stream)
-  int rc = topk_dispatch(lib, (const u64*)d_queries, Q, k, (u64*)d_keys, d_cnt, s, false);
+  int rc = topk_any(lib, (const u64*)d_queries, Q, k, (u64*)d_keys, d_cnt, s);
   if (rc) reset_state(lib);
   return rc;
 }
@@ -1774,7 +1965,6 @@ int topk_graph(fps_lib* L, const uint64_t* queries, u32 Q, u32 k, fps_lib::TopkG
     if (L->graphs.size() >= 8) {  // bounded cache: drop the oldest
       auto* old = L->graphs.front();
       if (old->exec) cudaGraphExecDestroy(old->exec);
-      old->hq.release(); old->hout.release(); old->dq.release(); old->dkeys.release(); old->dcnt.release();
       delete old;
       L->graphs.erase(L->graphs.begin());
     }
@@ -1898,9 +2088,7 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
       return FPS_OK;
     }
   }
-  // the tensor-core path checks its candidate lists on the host mid-call:
-  // it is not captured (a graph would record the bit-sliced kernel instead)
-  if (k <= KMAX_FUSED && graphs_enabled(lib) && !mma_wanted(lib, Q, lib->stream)) {
+  if (k <= KMAX_FUSED && graphs_enabled(lib)) {
     fps_lib::TopkGraph* gr = nullptr;
     if (topk_graph(lib, queries, Q, k, &gr) == FPS_OK) {
       const u64* hk = gr->hout.as<u64>();
@@ -1963,7 +2151,6 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   if (int rc = check_lib(lib)) return rc;
   if (Q == 0) return fail(FPS_EINVAL, "batch_search requires at least one query");
   if (k == 0) return fail(FPS_EINVAL, "n must be >= 1");
-  if (k > KMAX_FUSED) return fail(FPS_EINVAL, "min-over-queries top-k supports n <= 1024");
   if (!queries || !out_cnt) return fail(FPS_EINVAL, "null argument");
   for (u32 q = 0; q < Q; ++q)
     if (queries[3 * (u64)q + 2] >> 38) return fail(FPS_EPADDING, "padding bits above key 166 must be zero");
@@ -1972,83 +2159,20 @@ int fps_topk_min(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, 
   int rc;
   if ((rc = stage_queries(lib, queries, Q))) return rc;
   if ((rc = lib->keys.ensure((size_t)k * 8)) || (rc = lib->cnt.ensure(4))) return rc;
-  if (Q >= 2 && bs_wanted(lib, Q)) {
-    // Per-query top-k on the batched (bit-sliced) kernel, then the min merge:
-    // the global top-k by min_q distance is contained in the union of the
-    // per-query top-k lists (an entry's best query ranks it no lower than the
-    // global order does), and its score is its smallest listed distance.
-    const u64 n = (u64)Q * k;
-    if ((rc = lib->mq.ensure(n * 8 * 3 + (size_t)Q * 4 + 16))) return rc;
-    u64* pk = lib->mq.as<u64>();  // per-query keys
-    u64* tmp = pk + n;
-    u64* out = tmp + n;
-    u32* pc = reinterpret_cast<u32*>(out + n);
-    u32* firsts = pc + Q;
-    if ((rc = topk_dispatch(lib, lib->queries.as<u64>(), Q, k, pk, pc, lib->stream, false))) {
-      reset_state(lib);
-      return rc;
-    }
-    const int blocks = (int)std::min<u64>((n + 255) / 256, 4096);
-    fps::minq_flip<<<blocks, 256, 0, lib->stream>>>(pk, pc, Q, k, tmp);
-    if ((rc = sort_keys(lib, tmp, n, lib->stream))) return rc;
-    CUDA_TRY(cudaMemsetAsync(firsts, 0, 4, lib->stream));
-    fps::minq_first<<<blocks, 256, 0, lib->stream>>>(tmp, n, out, firsts);
-    if ((rc = sort_keys(lib, out, n, lib->stream))) return rc;
-    lib->launches += 2;
-    if ((rc = lib->h_stage.ensure((size_t)k * 8 + 4))) return rc;
-    u64* hk = lib->h_stage.as<u64>();
-    u32* hc = reinterpret_cast<u32*>(lib->h_stage.as<char>() + (size_t)k * 8);
-    CUDA_TRY(cudaMemcpyAsync(hk, out, (size_t)k * 8, cudaMemcpyDeviceToHost, lib->stream));
-    CUDA_TRY(cudaMemcpyAsync(hc, firsts, 4, cudaMemcpyDeviceToHost, lib->stream));
-    cudaError_t e = cudaStreamSynchronize(lib->stream);
-    if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, std::string("top-k min: ") + cudaGetErrorString(e)); }
-    *hc = std::min<u32>(*hc, k);
-    unpack_topk(hk, hc, 1, k, out_idx, out_dist, out_cnt);
-    return FPS_OK;
+  if ((rc = topk_min_dev(lib, lib->queries.as<u64>(), Q, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), lib->stream))) {
+    reset_state(lib);
+    return rc;
   }
-  Config c = lib->compact ? make_config<1, 4, fps::MODE_TOPK, true, true>(lib, 1, k)
-                          : make_config<1, 4, fps::MODE_TOPK, true, false>(lib, 1, k);
-  if ((rc = ensure_state(lib, 1))) return rc;
-  if ((rc = lib->buf.ensure(c.warps * (size_t)c.cap * 8))) return rc;
-  if ((rc = lib->cand.ensure(c.cand_cap * 8))) return rc;
-  fps::ScanArgs a = base_args(lib, lib->queries.as<u64>(), 1);
-  a.Qmin = Q;
-  a.k = k;
-  a.cap = c.cap;
-  a.n_qg = 1;
-  a.n_parts = c.n_parts;
-  a.iters = c.iters;
-  a.tg = lib->tg.as<u32>();
-  a.ghist = lib->ghist.as<u32>();
-  a.gstride = ghist_stride(1);
-  a.tg_rep = tg_replicas(1);
-  a.pub_every = (u32)std::max<u64>(1, c.n_parts / 512);
-  a.buf = lib->buf.as<u64>();
-  a.cand = lib->cand.as<u64>();
-  a.cand_cnt = lib->cand_cnt.as<u32>();
-  a.cand_cap = c.cand_cap;
-  if (lib->compact) set_dyn<1, 4, fps::MODE_TOPK, true>(lib, a);
-  else set_dyn<1, 4, fps::MODE_TOPK, false>(lib, a);
-  if (c.warps > 0 && lib->n > 0) {
-    if (lib->compact) fps::scan_kernel<1, 4, fps::MODE_TOPK, true, true><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
-    else fps::scan_kernel<1, 4, fps::MODE_TOPK, true, false><<<c.grid, WPB * 32, c.smem, lib->stream>>>(a);
-    lib->launches++;
-  }
-  int kp = 1;
-  while (kp < (int)k) kp <<= 1;
-  cudaFuncSetAttribute(fps::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  CUDA_TRY(launch_select(1, (size_t)(kp + fps::SEL_ECAP) * 8, lib->stream, a.cand, a.cand_cnt, c.cand_cap, a.tg,
-                         a.ghist, a.gstride, a.tg_rep, k, lib->keys.as<u64>(), lib->cnt.as<u32>(), true, a.dyn_ctr));
-  lib->launches++;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, cudaGetErrorString(e)); }
   if ((rc = lib->h_stage.ensure((size_t)k * 8 + 4))) return rc;
   u64* hk = lib->h_stage.as<u64>();
   u32* hc = reinterpret_cast<u32*>(lib->h_stage.as<char>() + (size_t)k * 8);
   CUDA_TRY(cudaMemcpyAsync(hk, lib->keys.p, (size_t)k * 8, cudaMemcpyDeviceToHost, lib->stream));
   CUDA_TRY(cudaMemcpyAsync(hc, lib->cnt.p, 4, cudaMemcpyDeviceToHost, lib->stream));
-  e = cudaStreamSynchronize(lib->stream);
-  if (e != cudaSuccess) { reset_state(lib); return fail(FPS_ECUDA, std::string("top-k min: ") + cudaGetErrorString(e)); }
+  cudaError_t e = cudaStreamSynchronize(lib->stream);
+  if (e != cudaSuccess) {
+    reset_state(lib);
+    return fail(FPS_ECUDA, std::string("top-k min: ") + cudaGetErrorString(e));
+  }
   unpack_topk(hk, hc, 1, k, out_idx, out_dist, out_cnt);
   return FPS_OK;
 }
@@ -2135,32 +2259,7 @@ int fps_range_fetch(fps_lib* lib, uint32_t* out_query, uint64_t* out_index, uint
   DeviceGuard g(lib->device);
   if (n != lib->range_pending) return fail(FPS_EINVAL, "fps_range_fetch: n does not match fps_range_begin");
   if (n && (!out_query || !out_index || !out_dist)) return fail(FPS_EINVAL, "null argument");
-  // pinned double buffer: chunk c + 1 copies while chunk c is split into
-  // columns (host threads measured slower: spawning them costs more than the
-  // split, which is bounded by first-touch faults on the fresh columns)
-  constexpr u64 CH = 1 << 17;  // keys per chunk (1 MiB)
-  int rc;
-  if (n && ((rc = lib->h_range[0].ensure(CH * 8)) || (rc = lib->h_range[1].ensure(CH * 8)))) return rc;
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
-  const u64* src = lib->rkeys.as<u64>();
-  auto issue = [&](u64 c) {
-    const u64 lo = c * CH, m = std::min<u64>(CH, n - lo);
-    cudaMemcpyAsync(lib->h_range[c & 1].p, src + lo, m * 8, cudaMemcpyDeviceToHost, lib->stream);
-    cudaEventRecord(ev[c & 1], lib->stream);
-  };
-  const u64 chunks = (n + CH - 1) / CH;
-  if (chunks) issue(0);
-  cudaError_t e = cudaSuccess;
-  for (u64 c = 0; c < chunks && e == cudaSuccess; ++c) {
-    e = cudaEventSynchronize(ev[c & 1]);
-    if (c + 1 < chunks) issue(c + 1);
-    const u64 lo = c * CH, m = std::min<u64>(CH, n - lo);
-    fps_range_unpack(reinterpret_cast<const uint64_t*>(lib->h_range[c & 1].p), m, out_query + lo, out_index + lo,
-                     out_dist + lo);
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(lib->stream);
-  for (auto& x : ev) cudaEventDestroy(x);
+  const cudaError_t e = fetch_columns(lib->stream, lib->rkeys.as<u64>(), n, lib->h_range, out_query, out_index, out_dist);
   lib->range_pending = 0;
   if (e != cudaSuccess) return fail(FPS_ECUDA, std::string("range fetch: ") + cudaGetErrorString(e));
   return FPS_OK;
@@ -2195,6 +2294,47 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
   return FPS_OK;
 }
 
+int fps_memory(const fps_lib* lib, uint64_t* library_bytes, uint64_t* derived_bytes, uint64_t* scratch_bytes,
+               double* derived_build_ms) {
+  if (int rc = check_lib(lib)) return rc;
+  fps_lib* L = const_cast<fps_lib*>(lib);
+  std::lock_guard<std::mutex> lk(L->mu);
+  const u64 te = fps::tile_entries(L->compact);
+  const u64 lib_b = L->n_alloc / te * fps::tile_bytes(L->compact);
+  const u64 der = L->pm.bytes + L->pm_perm.bytes + L->pm_meta.bytes + L->bs.bytes;
+  u64 scr = 0;
+  for (const DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->dyn, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt,
+                          &L->radius, &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->bsq, &L->mq,
+                          &L->mm_bop, &L->mm_ucol, &L->mm_qpop, &L->mm_tq, &L->mm_qcol, &L->mm_keys, &L->mm_sorted,
+                          &L->mm_tmp, &L->mm_priv, &L->mm_ovf, &L->gout})
+    scr += b->bytes;
+  for (const auto* gr : L->graphs) scr += gr->dq.bytes + gr->dkeys.bytes + gr->dcnt.bytes;
+  if (library_bytes) *library_bytes = lib_b;
+  if (derived_bytes) *derived_bytes = der;
+  if (scratch_bytes) *scratch_bytes = scr;
+  if (derived_build_ms) *derived_build_ms = L->derived_ms;
+  return FPS_OK;
+}
+
+int fps_release_derived(fps_lib* lib) {
+  if (int rc = check_lib(lib)) return rc;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  DeviceGuard g(lib->device);
+  cudaStreamSynchronize(lib->stream);
+  for (auto* gr : lib->graphs) {  // captured graphs may reference the copies
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    delete gr;
+  }
+  lib->graphs.clear();
+  lib->pm.release();
+  lib->pm_perm.release();
+  lib->pm_meta.release();
+  lib->bs.release();
+  if (lib->pm_state > 0) lib->pm_state = 0;
+  if (lib->bs_state > 0) lib->bs_state = 0;
+  return FPS_OK;
+}
+
 uint64_t fps_launch_count(const fps_lib* lib) { return lib ? lib->launches.load() : 0; }
 
 int fps_last_kernel(const fps_lib* lib) { return lib ? lib->last_kernel : 0; }
@@ -2225,3 +2365,5 @@ int fps_timing_read(fps_lib* lib, double* total_ms, uint64_t* count) {
 }
 
 }  // extern "C"
+
+#include "fps_group.cuh"

@@ -203,6 +203,8 @@ struct ScanArgs {
   u64* out_cnt;    // single counter
   u64 out_cap;
   // MODE_HIST output: ghist reused
+  const u32* gate;  // non-null: the grid does nothing unless *gate != 0 (device-side
+                    // fallback of the tensor-core path, decided without the host)
 };
 
 // Global bound maintenance. ghist[q] counts distances of *published*
@@ -335,7 +337,10 @@ __global__ void __launch_bounds__(256, (QW == 1 ? FPS_QW1_MINB : (QW >= 4 ? 2 : 
   // touching that state. The bulk-copy scan first puts its first library
   // tiles in flight -- the library is read-only -- so the HBM ramp overlaps
   // the previous select.
-  if constexpr (!SL::TMA) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if constexpr (!SL::TMA) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.gate && *(volatile const u32*)a.gate == 0) return;  // block-uniform
+  }
   __shared__ u32 s_cta_next;  // bulk-copy scan: next tile of the CTA's run (CTA-dynamic mode)
   if constexpr (SL::TMA) {
     if (threadIdx.x == 0) s_cta_next = 0;
@@ -974,7 +979,8 @@ __device__ __forceinline__ void post_done(u32* done_flag, u32 done_seq) {
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* cand_cnt, u64 cand_cap, u32* tg,
                                                              u32* ghist, u32 gstride, u32 tg_rep, u32 k,
                                                              u64* out_keys, u32* out_cnt, int reset,
-                                                             u32* dyn_ctr, u32* done_flag, u32 done_seq) {
+                                                             u32* dyn_ctr, u32* done_flag, u32 done_seq,
+                                                             const u32* gate, u32* ovf) {
   extern __shared__ u64 ssel[];  // [k_pow2] result + [SEL_ECAP] ties
   __shared__ u32 hist[256];
   __shared__ u32 s_nres, s_ntie, s_T, s_m;
@@ -987,13 +993,20 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
   // launched as a programmatic dependent of the scan: wait for its results
   __shared__ u32 s_wcnt[SEL_THREADS / 32];
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (gate && *(volatile const u32*)gate == 0) return;  // gated off: the scan did nothing either
   SEL_MARK(0);
 #ifdef FPS_SCAN_TRACE
   if (threadIdx.x == 0 && q == 0) g_mark[2] = gtimer();
 #endif
   // speculative first-slot read, independent of the count load
   const u64 my = threadIdx.x < cand_cap ? c[threadIdx.x] : ~0ull;
-  const u32 n = cand_cnt[q];
+  u32 n = cand_cnt[q];
+  if (n > cand_cap) {
+    // a candidate list overflowed its capacity (tensor-core path): flag it for
+    // the device-side fallback and select from what was stored
+    if (ovf && threadIdx.x == 0) atomicOr(ovf, 1u);
+    n = (u32)cand_cap;
+  }
   const u32 bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
 #ifdef FPS_SEL_PROBE
   if (threadIdx.x == 0) g_sel_clock[1] = my + n + bound;  // wait for the loads
@@ -1212,6 +1225,79 @@ __global__ void merge_kernel(const u64* in_keys, const u32* in_cnt, u32 G, u32 Q
 }
 
 // ---------------------------------------------------------------------------
+// Multi-device merges (fps_group_*): the same rank arithmetic as merge_kernel,
+// but each shard's list is reached through its own pointer -- a peer-device
+// pointer read over NVLink (fused gather + merge, no copy) or a slot of a
+// root-side gather buffer filled by NCCL / peer copies.
+// ---------------------------------------------------------------------------
+constexpr int GROUP_MAX = 32;
+struct ShardLists {
+  const u64* keys[GROUP_MAX];  // top-k: [Q][k] sorted keys; range: a sorted run
+  const u32* cnt[GROUP_MAX];   // top-k: [Q] counts (unused for runs)
+  u64 len[GROUP_MAX];          // range: run lengths
+  u64 off[GROUP_MAX];          // range: exclusive prefix of len
+};
+
+// Per-query top-k of G shard lists (merge_topk, scan.py:225-236): keys are
+// unique across shards (disjoint index ranges), so a key's merged rank is its
+// own position plus its lower bound in every other list.
+__global__ void merge_lists_kernel(const ShardLists s, u32 G, u32 Q, u32 k, u64* __restrict__ out_keys,
+                                   u32* __restrict__ out_cnt) {
+  const u64 total = (u64)G * Q * k;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total + Q; t += (u64)gridDim.x * blockDim.x) {
+    if (t >= total) {  // one thread per query: count and padding
+      const u32 q = (u32)(t - total);
+      u32 c = 0;
+      for (u32 g = 0; g < G; ++g) c += s.cnt[g][q];
+      out_cnt[q] = c < k ? c : k;
+      for (u32 i = c; i < k; ++i) out_keys[(u64)q * k + i] = ~0ull;
+      continue;
+    }
+    const u32 g = (u32)(t / ((u64)Q * k));
+    const u32 q = (u32)((t / k) % Q);
+    const u32 i = (u32)(t % k);
+    if (i >= s.cnt[g][q]) continue;
+    const u64 x = s.keys[g][(u64)q * k + i];
+    u64 rank = i;
+    for (u32 h = 0; h < G && rank < k; ++h) {
+      if (h == g) continue;
+      const u64* L = s.keys[h] + (u64)q * k;
+      u32 lo = 0, hi = s.cnt[h][q];
+      while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (L[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      rank += lo;
+    }
+    if (rank < k) out_keys[(u64)q * k + rank] = x;
+  }
+}
+
+// Range hits: G sorted runs of unique (q << 48 | d << 40 | index) keys ->
+// one sorted array (a merge by rank, no re-sort of the union).
+__global__ void merge_runs_kernel(const ShardLists s, u32 G, u64* __restrict__ out) {
+  const u64 total = s.off[G - 1] + s.len[G - 1];
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+    u32 g = 0;
+    while (g + 1 < G && t >= s.off[g + 1]) ++g;
+    const u64 i = t - s.off[g];
+    const u64 x = s.keys[g][i];
+    u64 rank = i;
+    for (u32 h = 0; h < G; ++h) {
+      if (h == g) continue;
+      const u64* L = s.keys[h];
+      u64 lo = 0, hi = s.len[h];
+      while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (L[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      rank += lo;
+    }
+    out[rank] = x;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Library ingestion
 // ---------------------------------------------------------------------------
 // Device view of the tiled library for ingestion / export kernels.
@@ -1368,6 +1454,14 @@ __global__ void minq_first(const u64* __restrict__ sorted, u64 n, u64* __restric
     out[i] = first ? make_key((u32)(x & 0xffu), x >> 8) : ~0ull;
     if (first) atomicAdd(firsts, 1u);
   }
+}
+
+// The first min(*firsts, k) keys of the re-sorted min-merge output -> out[k], *cnt.
+__global__ void minq_emit(const u64* __restrict__ sorted, const u32* __restrict__ firsts, u32 k, u64* __restrict__ out,
+                          u32* __restrict__ cnt) {
+  const u32 m = min(*firsts, k);
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) out[i] = i < m ? sorted[i] : ~0ull;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = m;
 }
 
 // Truncate sorted range output to the first k per query (large-k path).

@@ -78,8 +78,9 @@ class TopKResult:
 class Library:
     """A fingerprint library resident in one GPU's HBM as three u64 planes."""
 
-    def __init__(self, handle: int, cids: np.ndarray | None = None):
+    def __init__(self, handle: int, cids: np.ndarray | None = None, borrowed: bool = False):
         self._h = C.c_void_p(handle)
+        self._borrowed = borrowed  # a shard of a LibraryGroup: closed by the group
         n, base, dev = C.c_uint64(), C.c_uint64(), C.c_int()
         N.check(N.load().fps_info(self._h, C.byref(n), C.byref(base), C.byref(dev)), "fps_info")
         self.n = n.value
@@ -174,7 +175,8 @@ class Library:
 
     def close(self) -> None:
         if self._h and self._h.value:
-            N.load().fps_close(self._h)
+            if not self._borrowed:
+                N.load().fps_close(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):  # pragma: no cover - interpreter shutdown ordering
@@ -215,6 +217,18 @@ class Library:
         if len(idx) != len(w):
             raise ValueError("index and words differ in length")
         N.check(N.load().fps_write_entries(self._h, idx.ctypes.data, w.ctypes.data, len(idx)), "fps_write_entries")
+
+    def memory(self) -> dict:
+        """HBM bytes held (library tiles, derived copies, scratch) and the
+        host time spent building the derived copies."""
+        a, b, c, t = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_double()
+        N.check(N.load().fps_memory(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(t)), "fps_memory")
+        return {"library_bytes": a.value, "derived_bytes": b.value, "scratch_bytes": c.value,
+                "derived_build_ms": t.value}
+
+    def release_derived(self) -> None:
+        """Free the derived plane copies (rebuilt on next use)."""
+        N.check(N.load().fps_release_derived(self._h), "fps_release_derived")
 
     def timing(self, enable: bool) -> None:
         N.check(N.load().fps_timing(self._h, int(enable)), "fps_timing")
@@ -283,6 +297,17 @@ class Library:
                                       cnt.ctypes.data), "fps_topk_min")
         return TopKResult(idx, dist, cnt).hits(0)
 
+    def range_begin(self, queries, radius) -> int:
+        """Scan + device sort of the range hits, left on the device (their
+        count is returned); ``range_search`` also fetches them."""
+        q = as_query_words(queries)
+        rad = np.ascontiguousarray(np.minimum(np.broadcast_to(np.asarray(radius, dtype=np.int64), (len(q),)),
+                                              254).astype(np.uint8))
+        n_out = C.c_uint64()
+        N.check(N.load().fps_range_begin(self._h, q.ctypes.data, len(q), rad.ctypes.data, C.byref(n_out)),
+                "fps_range_begin")
+        return n_out.value
+
     def range_search(self, queries, radius) -> RangeResult:
         """Every (query, index, distance) with distance <= radius (scalar or per query)."""
         q = as_query_words(queries)
@@ -322,6 +347,241 @@ class Library:
         N.check(N.load().fps_sort_keys(self._h, N.ptr(d_keys), n, stream), "fps_sort_keys")
 
 
+class LibraryGroup:
+    """One library over several GPUs of this process (include/fps.h fps_group_*).
+
+    Contiguous shards (``split_sizes``, libstore.py:174-179), shard i on
+    ``devices[i]`` with global indices; every shard scans concurrently on its
+    own device and the root (devices[0]) gathers and merges — the merge kernel
+    reads the shard results straight from peer HBM (``gather="p2p"``), or
+    after an NCCL send/recv (``"nccl"``) or peer copies (``"copy"``). Results
+    equal a single Library over the whole library (merge_topk semantics,
+    scan.py:225-236). Same query methods as Library.
+    """
+
+    GATHERS = {v: k for k, v in N.GATHER_NAMES.items()}
+
+    def __init__(self, handle: int, cids: np.ndarray | None = None):
+        self._h = C.c_void_p(handle)
+        n, ns, root, gather = C.c_uint64(), C.c_uint32(), C.c_int(), C.c_int()
+        N.check(N.load().fps_group_info(self._h, C.byref(n), C.byref(ns), C.byref(root), C.byref(gather)),
+                "fps_group_info")
+        self.n = n.value
+        self.device = root.value
+        self.gather = self.GATHERS.get(gather.value, str(gather.value))
+        self.cids = cids
+        self.shards: list[Library] = []
+        for i in range(ns.value):
+            h = C.c_void_p()
+            N.check(N.load().fps_group_shard(self._h, i, C.byref(h)), "fps_group_shard")
+            self.shards.append(Library(h.value, borrowed=True))
+        self.index_base = self.shards[0].index_base
+        self.devices = [s.device for s in self.shards]
+
+    # ---- construction -------------------------------------------------
+    @staticmethod
+    def _gather(gather) -> int:
+        if isinstance(gather, int):
+            return gather
+        try:
+            return N.GATHER_NAMES[gather]
+        except KeyError:
+            raise ValueError(f"unknown gather mode {gather!r} (auto, p2p, nccl, copy)") from None
+
+    @classmethod
+    def from_shards(cls, shards: Sequence[Library], gather="auto", cids: np.ndarray | None = None) -> "LibraryGroup":
+        """Bind already-open contiguous shard Libraries; the group takes them over."""
+        arr = (C.c_void_p * len(shards))(*[s._h.value for s in shards])
+        h = C.c_void_p()
+        N.check(N.load().fps_group_open(arr, len(shards), cls._gather(gather), C.byref(h)), "fps_group_open")
+        for s in shards:  # now owned by the group
+            s._borrowed = True
+        return cls(h.value, cids)
+
+    @classmethod
+    def from_words(cls, words, devices: Sequence[int], check_padding: bool = True, gather="auto",
+                   cids: np.ndarray | None = None) -> "LibraryGroup":
+        from .libstore import split_sizes
+
+        arr = np.ascontiguousarray(np.asarray(words, dtype=np.uint64).reshape(-1, 3))
+        return cls._split(lambda a, b, dev: Library.from_words(arr[a:b], dev, a, check_padding),
+                          len(arr), devices, gather, cids, split_sizes)
+
+    @classmethod
+    def from_records(cls, records: np.ndarray, devices: Sequence[int], gather="auto") -> "LibraryGroup":
+        from .libstore import split_sizes
+
+        rec = np.ascontiguousarray(np.asarray(records, dtype=np.uint64).reshape(-1, 4))
+        return cls._split(lambda a, b, dev: Library.from_records(rec[a:b], dev, a), len(rec), devices, gather,
+                          rec[:, 0].copy(), split_sizes)
+
+    @classmethod
+    def from_fps1(cls, paths, devices: Sequence[int], gather="auto", with_cids: bool = True) -> "LibraryGroup":
+        """Stream FPS1 shard files into one contiguous slice per device (all
+        devices load concurrently); headers are validated first."""
+        N.require_device()
+        paths = [str(p) for p in paths]
+        arr = (C.c_char_p * max(1, len(paths)))(*[p.encode() for p in paths])
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        cids = np.empty(sum(_fps1_count(p) for p in paths), dtype=np.uint64) if with_cids else None
+        h = C.c_void_p()
+        N.check(N.load().fps_group_open_fps1(arr, len(paths), devs, len(devices), cls._gather(gather),
+                                             cids.ctypes.data if cids is not None else None, C.byref(h)),
+                "fps_group_open_fps1")
+        return cls(h.value, cids)
+
+    @classmethod
+    def generate(cls, n: int, seed_key: int, thresholds: np.ndarray, devices: Sequence[int], start: int = 0,
+                 gather="auto") -> "LibraryGroup":
+        """Synthetic library [start, start + n) generated shard by shard on its device."""
+        from .libstore import split_sizes
+
+        return cls._split(lambda a, b, dev: Library.generate(b - a, seed_key, thresholds, dev, start + a, start + a),
+                          n, devices, gather, None, split_sizes)
+
+    @classmethod
+    def _split(cls, open_one, n: int, devices: Sequence[int], gather, cids, split_sizes) -> "LibraryGroup":
+        N.require_device()
+        if not devices:
+            raise ValueError("at least one device")
+        libs: list[Library] = []
+        a = 0
+        try:
+            for dev, size in zip(devices, split_sizes(n, len(devices))):
+                libs.append(open_one(a, a + size, int(dev)))
+                a += size
+            return cls.from_shards(libs, gather, cids)
+        except BaseException:
+            for lib in libs:
+                lib.close()
+            raise
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            for s in self.shards:
+                s._h = C.c_void_p()
+            N.load().fps_group_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- reporting ------------------------------------------------------
+    @property
+    def last_kernel(self) -> str:
+        return self.shards[0].last_kernel
+
+    @property
+    def launches(self) -> int:
+        return int(N.load().fps_group_launch_count(self._h))
+
+    def layout(self) -> tuple[bool, int]:
+        return self.shards[0].layout()
+
+    def memory(self) -> dict:
+        out: dict = {}
+        for s in self.shards:
+            for key, v in s.memory().items():
+                out[key] = out.get(key, 0) + v
+        return out
+
+    def read_entries(self, start: int = 0, count: int | None = None) -> np.ndarray:
+        count = self.n - start if count is None else count
+        parts = []
+        for s in self.shards:
+            lo, hi = max(start, s.index_base), min(start + count, s.index_base + s.n)
+            if lo < hi:
+                parts.append(s.read_entries(lo - s.index_base, hi - lo))
+        return np.concatenate(parts) if parts else np.zeros((0, 3), np.uint64)
+
+    def words_host(self) -> np.ndarray:
+        return self.read_entries()
+
+    def timing(self, enable: bool) -> None:
+        for s in self.shards:
+            s.timing(enable)
+
+    def timing_read(self) -> tuple[float, int]:
+        """(max over shards of the summed scan-kernel ms, launches of shard 0)."""
+        reads = [s.timing_read() for s in self.shards]
+        return max(r[0] for r in reads), reads[0][1]
+
+    # ---- queries ----------------------------------------------------------
+    def search_batch(self, queries, k: int) -> TopKResult:
+        q = as_query_words(queries)
+        if k < 1:
+            raise ValueError("n must be >= 1")
+        Q = len(q)
+        idx = np.empty((Q, k), np.uint64)
+        dist = np.empty((Q, k), np.uint16)
+        cnt = np.zeros((Q,), np.uint32)
+        if Q:
+            N.check(N.load().fps_group_topk(self._h, q.ctypes.data, Q, k, idx.ctypes.data, dist.ctypes.data,
+                                            cnt.ctypes.data), "fps_group_topk")
+        return TopKResult(idx, dist, cnt)
+
+    def search(self, query, k: int) -> list[tuple[int, int]]:
+        return self.search_batch(query, k).hits(0)
+
+    def search_min(self, queries, k: int) -> list[tuple[int, int]]:
+        q = as_query_words(queries)
+        if len(q) == 0:
+            raise ValueError("batch_search requires at least one query")
+        idx = np.empty((1, k), dtype=np.uint64)
+        dist = np.empty((1, k), dtype=np.uint16)
+        cnt = np.zeros(1, dtype=np.uint32)
+        N.check(N.load().fps_group_topk_min(self._h, q.ctypes.data, len(q), k, idx.ctypes.data, dist.ctypes.data,
+                                            cnt.ctypes.data), "fps_group_topk_min")
+        return TopKResult(idx, dist, cnt).hits(0)
+
+    def range_begin(self, queries, radius) -> int:
+        """Per-shard scans + the root merge of the range hits, left on the root
+        device (their count is returned); ``range_search`` also fetches them."""
+        q = as_query_words(queries)
+        rad = np.ascontiguousarray(np.minimum(np.broadcast_to(np.asarray(radius, dtype=np.int64), (len(q),)),
+                                              254).astype(np.uint8))
+        n_out = C.c_uint64()
+        N.check(N.load().fps_group_range_begin(self._h, q.ctypes.data, len(q), rad.ctypes.data, C.byref(n_out)),
+                "fps_group_range_begin")
+        return n_out.value
+
+    def range_search(self, queries, radius) -> RangeResult:
+        q = as_query_words(queries)
+        Q = len(q)
+        r = np.broadcast_to(np.asarray(radius, dtype=np.int64), (Q,))
+        if np.any(r < 0):
+            raise ValueError("radius must be >= 0")
+        if Q == 0:
+            return RangeResult.from_keys(np.zeros(0, np.uint64))
+        rad = np.ascontiguousarray(np.minimum(r, 254).astype(np.uint8))
+        n_out = C.c_uint64()
+        lib = N.load()
+        N.check(lib.fps_group_range_begin(self._h, q.ctypes.data, Q, rad.ctypes.data, C.byref(n_out)),
+                "fps_group_range_begin")
+        m = n_out.value
+        query, index, distance = np.empty(m, np.uint32), np.empty(m, np.uint64), np.empty(m, np.uint16)
+        N.check(lib.fps_group_range_fetch(self._h, query.ctypes.data, index.ctypes.data, distance.ctypes.data, m),
+                "fps_group_range_fetch")
+        return RangeResult(query=query, index=index, distance=distance)
+
+    # ---- stream-ordered device API (root device) ---------------------------
+    def topk_prepare(self, Q: int, k: int) -> None:
+        N.check(N.load().fps_group_topk_prepare(self._h, Q, k), "fps_group_topk_prepare")
+
+    def topk_async(self, d_queries, Q: int, k: int, d_keys, d_cnt, stream: int) -> None:
+        N.check(N.load().fps_group_topk_async(self._h, N.ptr(d_queries), Q, k, N.ptr(d_keys), N.ptr(d_cnt), stream),
+                "fps_group_topk_async")
+
+
 def merge_async(d_in_keys, d_in_cnt, G: int, Q: int, k: int, d_out_keys, d_out_cnt, stream: int) -> None:
     """Device merge of G per-shard sorted top-k lists (merge_topk semantics)."""
     N.check(N.load().fps_merge_async(N.ptr(d_in_keys), N.ptr(d_in_cnt), G, Q, k, N.ptr(d_out_keys),
@@ -348,11 +608,27 @@ def _fps1_count(path) -> int:
     return int.from_bytes(head[8:16], "little")
 
 
-def load_library(source, device: int | None = None, index_base: int = 0) -> Library:
+def load_library(source, device: int | None = None, index_base: int = 0, devices: Sequence[int] | None = None,
+                 gather: str = "auto"):
     """Upload a library once: an (n, 3) word array, an (n, 4) FPS1 record
-    array, a ShardManifest / library directory (FPS1 shards), or a Library."""
-    if isinstance(source, Library):
+    array, a ShardManifest / library directory (FPS1 shards), or a Library.
+
+    ``devices=[d0, d1, ...]`` (two or more) shards it contiguously over those
+    GPUs and returns a LibraryGroup (same query methods); a device may repeat
+    (several shards on one GPU)."""
+    if isinstance(source, (Library, LibraryGroup)):
         return source
+    if devices is not None and len(devices) > 1:
+        if isinstance(source, np.ndarray):
+            if source.ndim == 2 and source.shape[1] == 4:
+                return LibraryGroup.from_records(source, devices, gather)
+            return LibraryGroup.from_words(source, devices, gather=gather)
+        from . import libstore
+
+        manifest = source if hasattr(source, "shards") else libstore.load_manifest(Path(source))
+        return LibraryGroup.from_fps1([s.path for s in manifest.shards], devices, gather)
+    if devices is not None and len(devices) == 1:
+        device = devices[0]
     if isinstance(source, np.ndarray):
         if source.ndim == 2 and source.shape[1] == 4:
             return Library.from_records(source, device, index_base)

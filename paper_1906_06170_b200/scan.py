@@ -20,6 +20,7 @@ Differences, by design:
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass
 from pathlib import Path
@@ -29,7 +30,7 @@ import numpy as np
 
 from .errors import DuplicateCid, LibstoreError, ScanCancelled, ScanError
 from .fingerprint import as_query_words
-from .library import Library
+from .library import Library, LibraryGroup
 
 ShardProgressFn = Callable[[int], None]
 SearchProgressFn = Callable[[str, int, int], None]
@@ -95,19 +96,22 @@ def merge_topk(parts: Sequence[TopK], n: int) -> TopK:
 
 
 # --------------------------------------------------------------------------
-# resident libraries, one per (manifest contents, device)
+# resident libraries, one per (manifest contents, devices)
 # --------------------------------------------------------------------------
 @dataclass
 class _Resident:
-    lib: Library
+    lib: "Library | LibraryGroup"
     cids: np.ndarray
     cid_monotone: bool
     offsets: list[int]
+    users: int = 0        # searches in flight (guarded by _cache_lock)
+    evicted: bool = False  # out of the cache: closed when the last user leaves
 
 
 _cache: dict[tuple, _Resident] = {}
 _CACHE_MAX = 8
 _cache_lock = threading.Lock()
+RECORDS_PER_DEVICE = 8_000_000  # below this a library stays on one GPU (launch cost > scan)
 
 
 def _manifest_key(manifest) -> tuple:
@@ -122,41 +126,77 @@ def _manifest_key(manifest) -> tuple:
     return tuple(parts)
 
 
-def _resident(manifest, device: int | None) -> _Resident:
+def search_devices(total_records: int) -> tuple[int, ...] | None:
+    """GPUs a resident library is sharded over (the reference's shard fan-out,
+    scan.py:256-287, is per process too): ``FPS_DEVICES=0,1,...`` if set,
+    else every visible GPU, one per RECORDS_PER_DEVICE records (None: the
+    current device only)."""
+    env = os.environ.get("FPS_DEVICES")
+    if env:
+        devs = tuple(int(x) for x in env.replace(" ", "").split(",") if x)
+        return devs or None
+    from . import _native as N
+
+    n = N.device_count()
+    use = min(n, max(1, total_records // RECORDS_PER_DEVICE))
+    return tuple(range(use)) if use > 1 else None
+
+
+def _close(res: _Resident) -> None:
+    res.lib.close()
+
+
+def _acquire(manifest, devices: tuple[int, ...] | None) -> _Resident:
+    """The resident library for this manifest, with a use reference taken:
+    eviction never closes a library another thread is searching."""
     from . import libstore
 
-    key = (_manifest_key(manifest), device)
+    key = (_manifest_key(manifest), devices)
     with _cache_lock:
         hit = _cache.get(key)
         if hit is not None:
+            hit.users += 1
             return hit
         # header pre-check in shard order, so the first bad shard is the one reported
+        offsets = [0]
         for shard in manifest.shards:
             try:
                 with open(shard.path, "rb") as f:
-                    libstore.read_shard_header(f, shard.path)
+                    offsets.append(offsets[-1] + libstore.read_shard_header(f, shard.path))
             except (OSError, LibstoreError) as exc:
                 raise ScanError(f"shard {shard.path}: {exc}") from exc
-        lib = Library.from_fps1([s.path for s in manifest.shards], device=device)
-        offsets = [0]
-        for shard in manifest.shards:
-            with open(shard.path, "rb") as f:
-                offsets.append(offsets[-1] + libstore.read_shard_header(f, shard.path))
+        paths = [s.path for s in manifest.shards]
+        if devices is not None and len(devices) > 1:
+            lib = LibraryGroup.from_fps1(paths, devices)
+        else:
+            lib = Library.from_fps1(paths, device=devices[0] if devices else None)
         cids = lib.cids
         monotone = bool(np.all(cids[1:] > cids[:-1])) if len(cids) > 1 else True
-        res = _Resident(lib=lib, cids=cids, cid_monotone=monotone, offsets=offsets)
+        res = _Resident(lib=lib, cids=cids, cid_monotone=monotone, offsets=offsets, users=1)
         _cache[key] = res
         while len(_cache) > _CACHE_MAX:  # bounded HBM use: evict the oldest library
-            old = next(iter(_cache))
-            _cache.pop(old).lib.close()
+            old = _cache.pop(next(iter(_cache)))
+            old.evicted = True
+            if old.users == 0:
+                _close(old)
         return res
 
 
+def _release(res: _Resident) -> None:
+    with _cache_lock:
+        res.users -= 1
+        if res.evicted and res.users == 0:
+            _close(res)
+
+
 def clear_cache() -> None:
-    """Release every resident library (frees HBM)."""
+    """Release every resident library (frees HBM); libraries still being
+    searched are closed when their last search returns."""
     with _cache_lock:
         for r in _cache.values():
-            r.lib.close()
+            r.evicted = True
+            if r.users == 0:
+                _close(r)
         _cache.clear()
 
 
@@ -205,11 +245,18 @@ def _search_multi(manifest, queries: np.ndarray, params: SearchParams, progress:
         return TopK(capacity=params.n, hits=())
     if cancel is not None and cancel():
         raise ScanCancelled(str(shards[0].path))
-    res = _resident(manifest, device)
-    if res.lib.n == 0:
-        top = TopK(capacity=params.n, hits=())
+    if device is not None:
+        devices = (device,)
     else:
-        top = _topk_one(res, queries, params.n, minq)
+        devices = search_devices(sum(int(s.record_count) for s in shards))
+    res = _acquire(manifest, devices)
+    try:
+        if res.lib.n == 0:
+            top = TopK(capacity=params.n, hits=())
+        else:
+            top = _topk_one(res, queries, params.n, minq)
+    finally:
+        _release(res)
     if progress is not None:
         for shard, a, b in zip(shards, res.offsets, res.offsets[1:]):
             progress(shard.dataset_label, b - a, shard.record_count)

@@ -142,24 +142,34 @@ def make_plan(name: str, seed: int = 20240808, n: int | None = None, planted_per
 
 
 def build_library(plan: Plan, device: int | None = None, index_base: int = 0, start: int = 0,
-                  count: int | None = None):
+                  count: int | None = None, devices=None):
     """Generate the plan's library on the GPU (this rank's contiguous slice
-    [start, start + count)), apply planted entries, and return (Library, queries).
+    [start, start + count)), apply planted entries, and return (library, queries).
 
-    Queries need the source entries' words; they are regenerated on the host
-    from the same counter-based stream (cheap: Q entries)."""
-    from .library import Library
+    ``devices=[d0, d1, ...]`` generates the slice as a LibraryGroup sharded
+    over those GPUs (one process). Queries need the source entries' words;
+    they are regenerated on the host from the same counter-based stream
+    (cheap: Q entries)."""
+    from .library import Library, LibraryGroup
 
     count = plan.n - start if count is None else count
-    lib = Library.generate(count, plan.seed_key, plan.thresholds, device=device, start=start,
-                           index_base=start if index_base == 0 else index_base)
+    if devices is not None and len(devices) > 1:
+        lib = LibraryGroup.generate(count, plan.seed_key, plan.thresholds, devices, start=start)
+        shards = lib.shards
+    else:
+        dev = devices[0] if devices else device
+        lib = Library.generate(count, plan.seed_key, plan.thresholds, device=dev, start=start,
+                               index_base=start if index_base == 0 else index_base)
+        shards = [lib]
     src_words = generate_rows(plan.seed_key, plan.thresholds, plan.source_idx)
     queries = plan.queries_from_sources(src_words)
     if len(plan.planted_idx):
         words = plan.planted_words(queries)
-        mine = (plan.planted_idx >= start) & (plan.planted_idx < start + count)
-        if np.any(mine):
-            lib.write_entries(plan.planted_idx[mine] - start, words[mine])
+        for sh in shards:  # global index of a shard's entry 0 is its index_base (== start for one shard)
+            lo = sh.index_base if len(shards) > 1 else start
+            mine = (plan.planted_idx >= lo) & (plan.planted_idx < lo + sh.n)
+            if np.any(mine):
+                sh.write_entries(plan.planted_idx[mine] - lo, words[mine])
     return lib, queries
 
 

@@ -203,3 +203,33 @@ def test_key_decoding():
     assert res.hits(0) == [(17, 3), (2, 5)]
     rr = RangeResult.from_keys(np.array([(7 << 48) | (4 << 40) | 123], dtype=np.uint64))
     assert rr.rows().tolist() == [[7, 123, 4]]
+
+
+def test_c_generator_matches_numpy_twin():
+    """orc_generate (C, threads) == generate_words (numpy) == the device gen_kernel's definition."""
+    import fps_oracle as orc
+
+    from paper_1906_06170_b200 import synth
+
+    plan = synth.make_plan("c2", seed=99, n=5000)
+    a = orc.generate_words(plan.seed_key, plan.thresholds, 123_456, 3001)
+    b = orc.generate_words_parallel(plan.seed_key, plan.thresholds, 123_456, 3001, threads=3)
+    assert np.array_equal(a, b)
+
+
+def test_bench_rejects_more_gpus_than_visible():
+    """bench.py --gpus N fails loudly (non-zero) when N GPUs are not there,
+    instead of silently measuring fewer."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("two GPUs visible")
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "visible GPU" in r.stdout + r.stderr
