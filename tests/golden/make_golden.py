@@ -163,6 +163,38 @@ def main() -> None:
                                 "sha256": words_sha(w), "queries": [[int(x) for x in r] for r in q],
                                 "rows": rows})
 
+        # --- tensor-core shapes: >= 192 queries (the default kernel for large
+        #     batches, tcgen05 int8 GEMM) -- per-query top-k and range --------
+        plan = synth.make_plan("c4", seed=20240813, n=40_000, Q=256)
+        w = orc.generate_words(plan.seed_key, plan.thresholds, 0, plan.n)
+        q = synth.planted_after_sources(plan, w)
+        m = ref_manifest(td / "c4tc", w, 2)
+        golden["per_query_tc"] = {
+            "case": "c4", "seed": 20240813, "n": plan.n, "Q": plan.Q, "k": 10, "sha256": words_sha(w),
+            "queries": [[int(x) for x in r] for r in q],
+            "hits": [hits(scan.search(m, Fingerprint(tuple(int(x) for x in r)), scan.SearchParams(n=10)))
+                     for r in q],
+        }
+        # reference batch_search for n > 1024 (any n >= 1 is valid: scan.py:82-84)
+        golden["batch_min_large"] = []
+        for k in (1025, 4000):
+            bq = q[:3]
+            top = scan.batch_search(m, [Fingerprint(tuple(int(x) for x in r)) for r in bq], scan.SearchParams(n=k))
+            golden["batch_min_large"].append({"seed": 20240813, "n": plan.n, "k": k,
+                                              "queries": [[int(x) for x in r] for r in bq], "hits": hits(top)})
+        plan = synth.make_plan("c5", seed=20240814, n=40_000, Q=200, planted_per_query=10)
+        w = orc.generate_words(plan.seed_key, plan.thresholds, 0, plan.n)
+        q = synth.planted_after_sources(plan, w)
+        rows = []
+        for qi, qq in enumerate(q):
+            d = scan._distances_packed(w, np.asarray([qq], dtype=np.uint64))
+            hit = np.flatnonzero(d <= 5)
+            for i in sorted(hit, key=lambda i: (int(d[i]), int(i))):
+                rows.append([qi, int(i), int(d[i])])
+        golden["range_tc"] = {"case": "c5", "seed": 20240814, "n": plan.n, "Q": plan.Q, "radius": 5,
+                              "planted_per_query": 10, "sha256": words_sha(w),
+                              "queries": [[int(x) for x in r] for r in q], "rows": rows}
+
         # --- random-CID library with distance ties (test_scan.py:28-40 pattern) ---
         rng = random.Random(9)
         cids = rng.sample(range(1, 2**40), 3000)

@@ -122,6 +122,40 @@ def test_range_matches_reference_golden(golden):
     assert np.array_equal(r.rows(), np.array(case["rows"], dtype=np.int64).reshape(-1, 3))
 
 
+def test_tensor_core_per_query_matches_reference_golden(golden):
+    """256 queries take the tcgen05 int8 kernel by default; pinned directly to
+    the reference's own search() outputs (make_golden.py per_query_tc)."""
+    case = golden["per_query_tc"]
+    plan = synth.make_plan("c4", seed=case["seed"], n=case["n"], Q=case["Q"])
+    lib, q = synth.build_library(plan)
+    assert words_sha(lib.words_host()) == case["sha256"]
+    assert q.tolist() == case["queries"]
+    res = lib.search_batch(q, case["k"])
+    assert lib.last_kernel == "tensor-core multi-query scan"
+    for qi, hits in enumerate(case["hits"]):
+        assert res.hits(qi) == [(c - 1, d) for c, d in hits], qi
+
+
+def test_tensor_core_range_matches_reference_golden(golden):
+    case = golden["range_tc"]
+    plan = synth.make_plan("c5", seed=case["seed"], n=case["n"], Q=case["Q"],
+                           planted_per_query=case["planted_per_query"])
+    lib, q = synth.build_library(plan)
+    assert words_sha(lib.words_host()) == case["sha256"]
+    r = lib.range_search(q, case["radius"])
+    assert lib.last_kernel == "tensor-core multi-query scan"
+    assert np.array_equal(r.rows(), np.array(case["rows"], dtype=np.int64).reshape(-1, 3))
+
+
+def test_batch_min_large_n_matches_reference_golden(golden):
+    """batch_search with n > 1024 (the reference accepts any n >= 1)."""
+    plan = synth.make_plan("c4", seed=20240813, n=40_000, Q=256)
+    lib, _ = synth.build_library(plan)
+    for case in golden["batch_min_large"]:
+        got = lib.search_min(np.array(case["queries"], dtype=np.uint64), case["k"])
+        assert got == [(c - 1, d) for c, d in case["hits"]], case["k"]
+
+
 def test_random_cid_library_matches_reference_golden(golden, tmp_path):
     rec = np.load(GOLDEN_DIR / "cid_library.npy")
     mpath = orc.write_fps1_library(tmp_path / "cids", rec[:, 1:], 3, cids=rec[:, 0])

@@ -137,6 +137,27 @@ def test_range_case(golden):
         assert len(hit) == 1 and hit[0, 2] == len(f)
 
 
+def test_tensor_core_shaped_cases(golden):
+    """The >= 192-query goldens (the GPU's tensor-core path) pin the oracles too."""
+    case = golden["per_query_tc"]
+    plan = synth.make_plan("c4", seed=case["seed"], n=case["n"], Q=case["Q"])
+    w = orc.generate_words(plan.seed_key, plan.thresholds, 0, plan.n)
+    q = synth.planted_after_sources(plan, w)
+    assert words_sha(w) == case["sha256"] and q.tolist() == case["queries"]
+    idx, dist, cnt = orc.c_topk(w, q, case["k"])
+    for qi, hits in enumerate(case["hits"]):
+        assert list(zip(idx[qi, :cnt[qi]].tolist(), dist[qi, :cnt[qi]].tolist())) == [(c - 1, d) for c, d in hits]
+    for bm in golden["batch_min_large"]:
+        assert orc.batch_min_topk(w, np.array(bm["queries"], dtype=np.uint64), bm["k"]) == \
+            [(c - 1, d) for c, d in bm["hits"]]
+    rc = golden["range_tc"]
+    plan = synth.make_plan("c5", seed=rc["seed"], n=rc["n"], Q=rc["Q"], planted_per_query=rc["planted_per_query"])
+    w = orc.generate_words(plan.seed_key, plan.thresholds, 0, plan.n)
+    q = synth.planted_after_sources(plan, w)
+    assert words_sha(w) == rc["sha256"]
+    assert np.array_equal(orc.c_range(w, q, rc["radius"]), np.array(rc["rows"], dtype=np.int64).reshape(-1, 3))
+
+
 def test_cid_library_search(golden):
     from pathlib import Path
 
