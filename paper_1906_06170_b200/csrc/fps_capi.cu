@@ -923,18 +923,13 @@ struct MmaPlan {
 // (FPS_MMA_CAND_MB, default 1,024 MB). Returns false when it cannot: the
 // batch then takes the bit-sliced kernel instead of overflowing.
 bool mma_plan(const fps_lib* L, u32 Q, u32 k, MmaPlan* p) {
-  static const int seed_log2 = [] {
-    const char* e = std::getenv("FPS_MMA_SEED");
-    return e ? std::atoi(e) : 16;  // 2^16 .. 2^18: same bound after the prefix pass, cheaper seed
-  }();
-  static const int pre_log2 = [] {
-    const char* e = std::getenv("FPS_MMA_PREFIX");
-    return e ? std::atoi(e) : 22;
-  }();
-  static const u64 budget = [] {
-    const char* e = std::getenv("FPS_MMA_CAND_MB");
-    return (u64)(e ? std::max(16, std::atoi(e)) : 1024) << 20;
-  }();
+  // (knobs read per call: batched calls are not latency bound, and tests set them at run time)
+  const char* es = std::getenv("FPS_MMA_SEED");
+  const int seed_log2 = es ? std::atoi(es) : 16;  // 2^16 .. 2^18: same bound after the prefix pass, cheaper seed
+  const char* ep = std::getenv("FPS_MMA_PREFIX");
+  const int pre_log2 = ep ? std::atoi(ep) : 22;
+  const char* eb = std::getenv("FPS_MMA_CAND_MB");
+  const u64 budget = (u64)(eb ? std::max(16, std::atoi(eb)) : 1024) << 20;
   p->seed_n = std::min<u64>(L->n, 1ull << seed_log2);
   p->pre_n = (pre_log2 > 0 && L->n >= (8ull << pre_log2)) ? (1ull << pre_log2) : 0;
   for (int pass = p->pre_n ? 0 : 1; pass < 2; ++pass) {
@@ -950,10 +945,8 @@ bool mma_plan(const fps_lib* L, u32 Q, u32 k, MmaPlan* p) {
 }
 
 bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
-  static const int mode = [] {
-    const char* e = std::getenv("FPS_MMA");
-    return e ? std::atoi(e) : -1;
-  }();
+  const char* e = std::getenv("FPS_MMA");
+  const int mode = e ? std::atoi(e) : -1;
   // compact libraries only: the fused test uses K slots 168.. (zero there)
   if (mode == 0 || Q < 2 || k > KMAX_FUSED || L->n < (u64)fps::MM_M || !L->compact) return false;
   if (mode != 1 && Q < 192) return false;
