@@ -137,7 +137,8 @@ __global__ void mm_fix_kernel(PlanesOut lib, u64 index_base, const u64* __restri
     return;
   }
   const u32 qi = blockIdx.y;
-  const u32 n = min(cnt[qi], cap);
+  if (cnt[qi] > cap) return;  // overflowed list (unwritten slots): the gated fallback pass recomputes the batch
+  const u32 n = cnt[qi];
   const u64 q0 = q[3 * (u64)qi], q1 = q[3 * (u64)qi + 1], q2 = q[3 * (u64)qi + 2];
   u64* kq = keys + (u64)qi * cap;
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
