@@ -991,6 +991,15 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   size_t tb = 0;
   CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
   if ((rc = L->mm_tmp.ensure(tb))) return rc;
+  const u32 ctas = nchunks * parts;
+  u64 pcap = 0;
+  if (mode == 0) {
+    // private per-(CTA, column) candidate lists: ~cap / parts expected per list
+    pcap = std::max<u64>(256, 4 * (u64)cap / 8 / parts + 64);
+    pcap = (pcap + 63) / 64 * 64;
+    while (pcap > 256 && (u64)ctas * NN * pcap * 8 > (1ull << 30)) pcap /= 2;
+    if ((rc = L->mm_priv.ensure((size_t)ctas * NN * pcap * 8))) return rc;  // before a graph capture
+  }
   if (prepare_only) return FPS_OK;
 
   fps::mm_ukeys_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_q, Q, L->mm_tq.as<u32>(), L->mm_keys.as<u64>());
@@ -1020,13 +1029,7 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   a.out_cnt = out_cnt;
   a.out_cap = out_cap;
   a.flags = scan_flags();
-  const u32 ctas = nchunks * parts;
   if (mode == 0) {
-    // private per-(CTA, column) candidate lists: ~cap / parts expected per list
-    u64 pcap = std::max<u64>(256, 4 * (u64)cap / 8 / parts + 64);
-    pcap = (pcap + 63) / 64 * 64;
-    while (pcap > 256 && (u64)ctas * NN * pcap * 8 > (1ull << 30)) pcap /= 2;
-    if ((rc = L->mm_priv.ensure((size_t)ctas * NN * pcap * 8))) return rc;
     a.priv = L->mm_priv.as<u64>();
     a.pcap = (u32)pcap;
   }

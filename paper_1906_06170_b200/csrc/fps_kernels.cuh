@@ -1000,12 +1000,22 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(u64* cand, u32* can
 #endif
   // speculative first-slot read, independent of the count load
   const u64 my = threadIdx.x < cand_cap ? c[threadIdx.x] : ~0ull;
-  u32 n = cand_cnt[q];
+  const u32 n = cand_cnt[q];
   if (n > cand_cap) {
-    // a candidate list overflowed its capacity (tensor-core path): flag it for
-    // the device-side fallback and select from what was stored
+    // a candidate list overflowed its capacity (tensor-core path; its slots
+    // are not all written): flag it for the device-side fallback pass, which
+    // recomputes the batch, and leave an empty, clean result
     if (ovf && threadIdx.x == 0) atomicOr(ovf, 1u);
-    n = (u32)cand_cap;
+    for (u32 i = threadIdx.x; i < k; i += blockDim.x) out_keys[(u64)q * k + i] = ~0ull;
+    if (threadIdx.x == 0) out_cnt[q] = 0;
+    if (reset) {
+      for (int i = threadIdx.x; i < HB; i += blockDim.x) ghist[((u64)q * HB + i) * gstride] = 0;
+      for (u32 r = threadIdx.x; r < tg_rep; r += blockDim.x) tg[((u64)q * tg_rep + r) * gstride] = T_OPEN;
+      if (threadIdx.x == 0) cand_cnt[q] = 0;
+      if (dyn_ctr && q == 0 && threadIdx.x == 0) *dyn_ctr = 0;
+    }
+    post_done(done_flag, done_seq);
+    return;
   }
   const u32 bound = tg[(u64)q * tg_rep * gstride];  // every replica holds the same bound
 #ifdef FPS_SEL_PROBE
