@@ -197,6 +197,8 @@ struct fps_lib {
   struct TopkGraph {
     u32 Q = 0, k = 0;
     u64 gen = 0;
+    bool mma = false;  // captured on the tensor-core path (re-captured when the choice changes)
+    int kernel = 0;    // last_kernel of the captured path
     cudaGraphExec_t exec = nullptr;
     HostBuf hq, hout;
     DevBuf dq, dkeys, dcnt;
@@ -1973,7 +1975,8 @@ int topk_graph(fps_lib* L, const uint64_t* queries, u32 Q, u32 k, fps_lib::TopkG
         (rc = gr->dcnt.ensure((size_t)Q * 4)))
       return rc;
   }
-  if (!gr->exec || gr->gen != g_alloc_gen.load()) {
+  const bool mma_now = mma_wanted(L, Q, k);
+  if (!gr->exec || gr->gen != g_alloc_gen.load() || gr->mma != mma_now) {
     if (gr->exec) cudaGraphExecDestroy(gr->exec);
     gr->exec = nullptr;
     // every scratch buffer must exist before capture (no allocation inside it)
@@ -2002,7 +2005,10 @@ int topk_graph(fps_lib* L, const uint64_t* queries, u32 Q, u32 k, fps_lib::TopkG
       return fail(FPS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
     gr->gen = gen;
+    gr->mma = mma_now;
+    gr->kernel = L->last_kernel;
   }
+  L->last_kernel = gr->kernel;
   std::memcpy(gr->hq.p, queries, (size_t)Q * 24);
   CUDA_TRY(cudaGraphLaunch(gr->exec, L->stream));
   cudaError_t e = wait_stream(L->stream);
