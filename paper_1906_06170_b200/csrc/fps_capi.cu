@@ -26,6 +26,7 @@
 #include "fps_kernels.cuh"
 #include "fps_planeq.cuh"
 #include "fps_mma.cuh"
+#include "fps_mma4.cuh"
 
 using fps::u32;
 using fps::u64;
@@ -958,7 +959,30 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   return true;
 }
 
-u32 mma_pick_n(u32 Q) { return Q <= 64 ? 64u : Q <= 128 ? 128u : 256u; }
+// Operand kind of the tensor-core scan: block-scaled fp4 (kind::mxf4, twice
+// the int8 MMA rate; default) or int8 (kind::i8; FPS_MMA_KIND=i8).
+bool mma_fp4() {
+  const char* e = std::getenv("FPS_MMA_KIND");
+  return !(e && std::string(e) == "i8");
+}
+
+// Accumulator width (queries per chunk). int8: 64 / 128 / 256. fp4: two
+// accumulators + the scale factors fit 512 TMEM columns up to N = 240; the
+// width minimises chunks x per-tile time, with a per-tile floor of ~304 clk
+// for N <= 128 (3 MMAs) and ~1.5 clk per column above (umma_peak.cu), e.g.
+// 1,024 queries -> 5 chunks of 208.
+u32 mma_pick_n(u32 Q, bool fp4) {
+  if (!fp4) return Q <= 64 ? 64u : Q <= 128 ? 128u : 256u;
+  if (Q <= 64) return 64u;
+  if (Q <= 128) return 128u;
+  u32 best = 240;
+  double best_cost = 1e30;
+  for (u32 n : {128u, 160u, 208u, 240u}) {
+    const double cost = (double)((Q + n - 1) / n) * std::max(304.0, 1.5 * n);
+    if (cost < best_cost - 1e-9) best_cost = cost, best = n;
+  }
+  return best;
+}
 
 template <int N>
 int mma_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
@@ -973,6 +997,19 @@ int mma_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   return FPS_OK;
 }
 
+template <int N>
+int mma4_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
+  const size_t smem = fps::mm4_smem(N);
+  CUDA_TRY(smem_optin((const void*)fps::mma4_scan_kernel<N>, smem));
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::mma4_scan_kernel<N><<<ctas, fps::MM_THREADS, smem, s>>>(a);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  LAUNCH_CHECK("mma4_scan_kernel");
+  return FPS_OK;
+}
+
 // Shared part of the tensor-core calls: per-query operands from the bound
 // mm_tq[q] (top-k: the seed's k-th distance; range: the radius), columns
 // ordered by u = T - |q|, then the scan. mode 0 appends candidate keys to the
@@ -980,12 +1017,13 @@ int mma_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
 int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
             cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull) {
   int rc;
-  const u32 NN = mma_pick_n(Q);
+  const bool fp4 = mma_fp4();
+  const u32 NN = mma_pick_n(Q, fp4);
   const u32 nchunks = (Q + NN - 1) / NN;
   n_scan = std::min<u64>(n_scan, L->n);  // entries [0, n_scan) (a prefix pass of the top-k path)
   const u64 n_tiles = (n_scan + fps::MM_M - 1) / fps::MM_M;
   const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles));
-  if ((rc = L->mm_bop.ensure((size_t)nchunks * fps::mm_b_bytes((int)NN))) ||
+  if ((rc = L->mm_bop.ensure((size_t)nchunks * (fp4 ? fps::mm4_b_bytes((int)NN) : fps::mm_b_bytes((int)NN)))) ||
       (rc = L->mm_ucol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_qpop.ensure((size_t)nchunks * NN * 4)) ||
       (rc = L->mm_qcol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_keys.ensure((size_t)Q * 8)) ||
       (rc = L->mm_sorted.ensure((size_t)Q * 8)))
@@ -1006,9 +1044,14 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
 
   fps::mm_ukeys_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_q, Q, L->mm_tq.as<u32>(), L->mm_keys.as<u64>());
   CUDA_TRY(cub::DeviceRadixSort::SortKeys(L->mm_tmp.p, tb, L->mm_keys.as<u64>(), L->mm_sorted.as<u64>(), (int)Q, 0, 64, s));
-  fps::mm_prep_kernel<<<(nchunks * NN + 127) / 128, 128, 0, s>>>(
-      d_q, Q, L->mm_tq.as<u32>(), L->mm_bop.as<unsigned char>(), L->mm_ucol.as<int>(), L->mm_qpop.as<u32>(), nchunks,
-      L->mm_sorted.as<u64>(), L->mm_qcol.as<u32>(), NN);
+  if (fp4)
+    fps::mm4_prep_kernel<<<(nchunks * NN + 127) / 128, 128, 0, s>>>(
+        d_q, Q, L->mm_tq.as<u32>(), L->mm_bop.as<unsigned char>(), L->mm_ucol.as<int>(), L->mm_qpop.as<u32>(), nchunks,
+        L->mm_sorted.as<u64>(), L->mm_qcol.as<u32>(), NN);
+  else
+    fps::mm_prep_kernel<<<(nchunks * NN + 127) / 128, 128, 0, s>>>(
+        d_q, Q, L->mm_tq.as<u32>(), L->mm_bop.as<unsigned char>(), L->mm_ucol.as<int>(), L->mm_qpop.as<u32>(), nchunks,
+        L->mm_sorted.as<u64>(), L->mm_qcol.as<u32>(), NN);
   L->launches += 3;
   LAUNCH_CHECK("mm_prep");
   fps::MmArgs a{};
@@ -1034,6 +1077,13 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   if (mode == 0) {
     a.priv = L->mm_priv.as<u64>();
     a.pcap = (u32)pcap;
+  }
+  if (fp4) {
+    if (NN == 64) return mma4_launch_n<64>(L, ctas, s, a);
+    if (NN == 128) return mma4_launch_n<128>(L, ctas, s, a);
+    if (NN == 160) return mma4_launch_n<160>(L, ctas, s, a);
+    if (NN == 208) return mma4_launch_n<208>(L, ctas, s, a);
+    return mma4_launch_n<240>(L, ctas, s, a);
   }
   if (NN == 64) return mma_launch_n<64>(L, ctas, s, a);
   if (NN == 128) return mma_launch_n<128>(L, ctas, s, a);

@@ -1,0 +1,375 @@
+// fps_mma4.cuh — the multi-query scan on the block-scaled fp4 tensor-core
+// path (tcgen05.mma kind::mxf4, e2m1 operands, f32 accumulators in TMEM):
+// twice the MMA rate of kind::i8 on B200 (measured: 8.84 vs 4.56 dense POP/s,
+// tools/microbench/umma_peak.cu, profiles/r02_umma_peak.txt).
+//
+// Same algebra as fps_mma.cuh (for 0/1 vectors the AND-popcount is a dot
+// product; the reference distance popcount(a XOR q) over the three words,
+// scan.py:137-143, is d = |a| + |q| - 2c), with the operands as e2m1 values
+// and every block scale factor 1.0 (ue8m0 127):
+//   A (library row)  : element k = 1.0 if bit k is set (k < 168), then test digits
+//   B (query column) : element k = 2.0 if query bit k is set, then test digits
+// K slots 168..191 are zero bits in a compact library (the 21 B/entry layout
+// keeps 168 bits), so they carry the test terms (e2m1 values are 0, .5, 1,
+// 1.5, 2, 3, 4, 6 and negatives):
+//   168..172  A = digits of P = |a| / 6      B = -6
+//   173..174  A = digits of R = |a| % 6      B = -1
+//   175..182  A = 6                          B = digits of X = trunc(v / 6), v = T - |q| + 0.5
+//   183..184  A = 1                          B = digits of Y = v - 6X
+// so the accumulator is D = 2c - |a| + v = T - d + 0.5: never zero, and the
+// pair passes (d <= T) iff the f32 sign bit is clear. All terms are small
+// integers or halves: the f32 sums are exact (checked bit-exactly on random
+// and extreme rows / columns by the microbenchmark, and end to end by the
+// parity tests against the reference goldens and the C oracle).
+//
+// Pipeline as in fps_mma.cuh (one CTA per SM): a loader warp streams library
+// tiles (bulk copies), 4 producer warps expand a 128-entry tile to the
+// canonical K-major fp4 layout (a byte -> 8 nibbles table lookup, 96 B per
+// row instead of 192), one lane issues 3 x K=64 MMAs per tile into one of two
+// TMEM accumulators, 16 epilogue warps test the sign bits. TMEM: two N-column
+// accumulators (N <= 240) and the scale factors in columns 480..511.
+#pragma once
+#include "fps_mma.cuh"
+
+namespace fps {
+
+constexpr int MM4_KB = 96;                       // bytes per operand row (192 e2m1 elements)
+constexpr u32 MM4_A_BYTES = MM_M * MM4_KB;       // 12 KB per stage
+constexpr int MM4_STAGES = 6;
+constexpr u32 MM4_SF_COL = 480;                  // scale factors (all 1.0): SFA at 480, SFB at 496
+__host__ __device__ constexpr u32 mm4_b_bytes(int n) { return (u32)n * MM4_KB; }
+__host__ __device__ constexpr size_t mm4_smem(int n) {
+  return mm4_b_bytes(n) + (size_t)MM4_STAGES * MM4_A_BYTES + (size_t)MM_RAW * MM_RAW_BYTES_MAX;
+}
+
+// e2m1 code of a value in {0, .5, 1, 1.5, 2, 3, 4, 6} (and negatives)
+__host__ __device__ __forceinline__ u32 e2m1(int twice) {  // argument: 2 x value
+  const u32 s = twice < 0 ? 8u : 0u;
+  const int a = twice < 0 ? -twice : twice;
+  const u32 c = a == 0 ? 0u : a == 1 ? 1u : a == 2 ? 2u : a == 3 ? 3u : a == 4 ? 4u : a == 6 ? 5u : a == 8 ? 6u : 7u;
+  return c ? (s | c) : 0u;
+}
+// greedy e2m1 digits of x/2 (x = 2 x the value, a multiple of 1) into `slots`
+// nibbles of `out` starting at nibble `pos` (values 6, 4, 3, 2, 1.5, 1, .5)
+__host__ __device__ inline u64 e2m1_digits(int x, int slots) {
+  const int sg = x < 0 ? -1 : 1;
+  int a = x * sg;
+  u64 out = 0;
+  for (int i = 0; i < slots; ++i) {
+    const int v = a >= 12 ? 12 : a >= 8 ? 8 : a >= 6 ? 6 : a >= 4 ? 4 : a;  // 2 x {6, 4, 3, 2, <=1.5}
+    a -= v;
+    out |= (u64)e2m1(sg * v) << (4 * i);
+  }
+  return out;
+}
+
+// B of the fp4 fused test: columns ordered by u = T - |q| (as mm_prep_kernel),
+// padding columns (past Q) get v = -0.5 (D < 0 for every entry).
+__global__ void mm4_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __restrict__ tq,
+                                unsigned char* __restrict__ bop, int* __restrict__ tcol, u32* __restrict__ qpop,
+                                u32 nchunks, const u64* __restrict__ order, u32* __restrict__ qcol, u32 NN) {
+  const u32 col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= nchunks * NN) return;
+  const u32 chunk = col / NN, j = col % NN;
+  u64 w[3] = {0, 0, 0};
+  const bool ok = col < Q;
+  const u32 qi = ok ? (u32)(order[col] & 0xffffffffu) : 0u;
+  if (ok) { w[0] = q[3 * (u64)qi]; w[1] = q[3 * (u64)qi + 1]; w[2] = q[3 * (u64)qi + 2]; }
+  qcol[col] = qi;
+  const u32 pop = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
+  qpop[col] = pop;
+  tcol[col] = ok ? (int)tq[qi] : 0;
+  // v = T - |q| + 0.5 in halves: 2v = 2(T - |q|) + 1
+  const int v2 = ok ? 2 * ((int)tq[qi] - (int)pop) + 1 : -1;
+  const int X = v2 / 12;                  // trunc(v / 6)
+  const int Y2 = v2 - 12 * X;             // 2 x (v - 6X)
+  u64 nib[3] = {0, 0, 0};                 // elements 168..191 (24 nibbles)
+  nib[0] = e2m1_digits(-12, 1) * 0x11111ull;                       // 168..172: -6
+  nib[0] |= (u64)e2m1(-2) << 20 | (u64)e2m1(-2) << 24;             // 173..174: -1
+  const u64 dx = e2m1_digits(2 * X, 8);                            // 175..182
+  const u64 dy = e2m1_digits(Y2, 2);                               // 183..184
+  const u64 tail = dx | dy << 32;                                  // nibbles of 175..184
+  unsigned char* b = bop + (u64)chunk * mm4_b_bytes((int)NN);
+  for (u32 kb = 0; kb < (u32)MM4_KB; ++kb) {
+    u32 byte = 0;
+    for (u32 h = 0; h < 2; ++h) {
+      const u32 k = 2 * kb + h;
+      u32 code;
+      if (k < 168) code = ((w[k >> 6] >> (k & 63)) & 1) ? 4u : 0u;  // 2.0
+      else if (k < 175) code = (u32)(nib[0] >> (4 * (k - 168))) & 15u;
+      else if (k < 185) code = (u32)(tail >> (4 * (k - 175))) & 15u;
+      else code = 0;
+      byte |= code << (4 * h);
+    }
+    b[mm_canon(j, kb, NN)] = (unsigned char)byte;
+  }
+}
+
+__device__ __forceinline__ void mm4_mma(u32 d, u64 a, u64 b, u32 idesc, u32 acc, u32 sfa, u32 sfb) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+
+template <int NREG>
+__device__ __forceinline__ void mm4_ld(u32 taddr, u32 (&r)[NREG]);
+template <>
+__device__ __forceinline__ void mm4_ld<32>(u32 taddr, u32 (&r)[32]) { mm_ld32(taddr, r); }
+template <>
+__device__ __forceinline__ void mm4_ld<16>(u32 taddr, u32 (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void mm4_ld<8>(u32 taddr, u32 (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// One epilogue round: NREG columns starting at TMEM column offset `col`
+// (relative to the accumulator), global column index cb0 of the first.
+template <int NREG, int N>
+__device__ __forceinline__ void mm4_round(const MmArgs& a, u32 taddr, int cb0, u64 e, u32* s_pcnt, const u32* s_qcol) {
+  u32 r[NREG];
+  mm4_ld<NREG>(taddr, r);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  if (a.flags & 4096) return;
+  u32 t = r[0];
+#pragma unroll
+  for (int i = 1; i < NREG; ++i) t &= r[i];
+  const bool any = (t & 0x80000000u) == 0 && e < a.n;
+  if (!__any_sync(0xffffffffu, any) || !any) return;
+  u64 hm = 0;
+#pragma unroll
+  for (int i = 0; i < NREG; ++i) hm |= (u64)((~r[i]) >> 31) << i;
+  const u64 idx = a.index_base + e;
+  while (hm) {
+    const int c = cb0 + __ffsll((long long)hm) - 1;
+    hm &= hm - 1;
+    if (a.mode == 0) {
+      const u32 pos = atomicAdd(s_pcnt + c, 1u);
+      if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
+    } else {
+      const u64 pos = atomicAdd(a.out_cnt, 1ull);
+      if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a) {
+  static_assert(N % 16 == 0 && N >= 64 && N <= 240, "accumulator width (two accumulators + scale factors in 512 columns)");
+  constexpr u32 B_BYTES = mm4_b_bytes(N);
+  constexpr u32 TMEM_COLS = 512;
+  extern __shared__ __align__(1024) unsigned char msm[];
+  unsigned char* sB = msm;
+  unsigned char* sA = msm + B_BYTES;  // [MM4_STAGES][12 KB]
+  char* raw = reinterpret_cast<char*>(msm + B_BYTES + MM4_STAGES * MM4_A_BYTES);  // [MM_RAW][library tile]
+  __shared__ __align__(8) u64 full_bar[MM4_STAGES], empty_bar[MM4_STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) u64 raw_full[MM_RAW], raw_empty[MM_RAW];
+  __shared__ u32 tmem_base;
+  __shared__ u32 lut8[256];   // byte -> 8 e2m1 nibbles (bit -> 1.0)
+  __shared__ u32 luta[176];   // |a| -> nibbles of elements 168..175 (digits of -|a|, then A = 6)
+  __shared__ u32 s_qcol[N], s_pcnt[N];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const u32 chunk = blockIdx.x % a.nchunks;
+  const u64 part = blockIdx.x / a.nchunks;
+  const u32 SUB = a.lib.compact ? TILE_CMP / MM_M : TILE_FULL / MM_M;
+  const u32 RAW_BYTES = (u32)tile_bytes(a.lib.compact);
+  const u64 n_raw = (a.n + tile_entries(a.lib.compact) - 1) / tile_entries(a.lib.compact);
+  const u64 r0 = part * n_raw / a.parts, r1 = (part + 1) * n_raw / a.parts;
+  const u64 nraw = r1 > r0 ? r1 - r0 : 0;
+  const u64 t0 = r0 * SUB;
+
+  // ---- setup: B chunk, tables, barriers, TMEM (+ scale factors)
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.bop + (u64)chunk * B_BYTES);
+    uint4* dst = reinterpret_cast<uint4*>(sB);
+    for (u32 i = tid; i < B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+  }
+  for (int i = tid; i < N; i += blockDim.x) {
+    s_qcol[i] = a.qcol[chunk * N + i];
+    s_pcnt[i] = 0;
+  }
+  for (int i = tid; i < 256; i += blockDim.x) {
+    u32 v = 0;
+    for (int b = 0; b < 8; ++b) v |= ((u32)(i >> b) & 1u) * 2u << (4 * b);  // 1.0 = 0b0010
+    lut8[i] = v;
+  }
+  for (int i = tid; i < 176; i += blockDim.x) {
+    // elements 168..172: digits of |a| / 6; 173..174: digits of |a| % 6; 175: A = 6
+    const u64 p = e2m1_digits(2 * (i / 6), 5), r = e2m1_digits(2 * (i % 6), 2);
+    luta[i] = (u32)(p | r << 20 | (u64)e2m1(12) << 28);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < MM4_STAGES; ++s) {
+      mm_bar_init(&full_bar[s], 128);
+      mm_bar_init(&empty_bar[s], 1);
+    }
+    for (int r = 0; r < MM_RAW; ++r) {
+      mm_bar_init(&raw_full[r], 1);
+      mm_bar_init(&raw_empty[r], 128);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mm_bar_init(&tfull[b], 1);
+      mm_bar_init(&tempty[b], MM_EPI / 2 * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4 + MM_EPI) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const u32 tmem = tmem_base;
+  if (warp < 4) {  // scale factors: every byte of columns 480..511 = ue8m0 127 (1.0)
+    for (u32 c = MM4_SF_COL; c < TMEM_COLS; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       tmem + ((u32)(32 * warp) << 16) + c),
+                   "r"(0x7f7f7f7fu));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const u64 ntile = nraw * SUB;
+
+  if (warp < 4) {
+    // ===== producers: thread = entry row; 6 x 16 B of e2m1 nibbles per row
+    const u32 row = (u32)tid;
+    for (u64 it = 0; it < ntile; ++it) {
+      const int s = (int)(it % MM4_STAGES);
+      const u64 r = it / SUB;
+      const u32 sub = (u32)(it % SUB);
+      const int rs = (int)(r % MM_RAW);
+      if (sub == 0) mm_bar_wait(&raw_full[rs], (u32)(r / MM_RAW) & 1u);
+      u64 w[3];
+      {
+        const char* tb = raw + (u64)rs * RAW_BYTES;
+        const u32 e = sub * MM_M + row;
+        if (a.lib.compact) {
+          w[0] = reinterpret_cast<const u64*>(tb)[e];
+          w[1] = reinterpret_cast<const u64*>(tb + 8 * TILE_CMP)[e];
+          w[2] = (u64)reinterpret_cast<const u32*>(tb + 16 * TILE_CMP)[e] |
+                 ((u64)reinterpret_cast<const unsigned char*>(tb + 20 * TILE_CMP)[e] << 32);
+        } else {
+          w[0] = reinterpret_cast<const u64*>(tb)[e];
+          w[1] = reinterpret_cast<const u64*>(tb + 8 * TILE_FULL)[e];
+          w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
+        }
+      }
+      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
+      const u32 pa = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
+      if (it >= MM4_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM4_STAGES) - 1) & 1u);
+      unsigned char* A = sA + s * MM4_A_BYTES;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {  // 16 B = 32 elements = 4 bytes of the 192-bit string
+        uint4 v;
+        const u64 word = w[c >> 1];
+        const u32 sh = 32 * (c & 1);
+        v.x = lut8[(word >> sh) & 0xff];
+        v.y = lut8[(word >> (sh + 8)) & 0xff];
+        if (c < 5) {
+          v.z = lut8[(word >> (sh + 16)) & 0xff];
+          v.w = lut8[(word >> (sh + 24)) & 0xff];
+        } else {  // elements 168..191: the test terms
+          v.y = luta[pa < 176 ? pa : 175];
+          v.z = e2m1(12) * 0x1111111u | e2m1(2) << 28;  // 176..182: A = 6, 183: A = 1
+          v.w = e2m1(2);                                // 184: A = 1
+        }
+        *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mm_bar_arrive(&full_bar[s]);
+    }
+  } else if (warp == 5 + MM_EPI) {
+    // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
+    if (lane == 0) {
+      const u64 pol = l2_evict_first_policy();
+      for (u64 r = 0; r < nraw; ++r) {
+        const int rs = (int)(r % MM_RAW);
+        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
+        mbar_expect_tx(&raw_full[rs], RAW_BYTES);
+        bulk_g2s_stream(raw + (u64)rs * RAW_BYTES, a.lib.base + (r0 + r) * RAW_BYTES, RAW_BYTES, &raw_full[rs], pol);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4 + MM_EPI) {
+    // ===== epilogue: two groups of 8 warps on alternate tiles; warp (quad,
+    // half) reads lane quadrant quad, columns [half * N / 2, (half + 1) * N / 2)
+    const u32 grp = (u32)(warp - 4) / 8;
+    const u32 wq = (u32)(warp - 4) % 8;
+    const u32 quad = wq % 4, half = wq / 4;
+    const u32 row = quad * 32 + lane;
+    constexpr int NC = N / 2;                  // columns per warp (multiple of 8)
+    constexpr int NR32 = NC / 32, T16 = (NC % 32) / 16, T8 = (NC % 16) / 8;
+    for (u64 it = grp; it < ntile; it += 2) {
+      const int b = (int)grp;
+      const u64 e = (t0 + it) * MM_M + row;
+      mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
+      const int cb = (int)(half * NC);
+#pragma unroll 1
+      for (int rnd = 0; rnd < NR32; ++rnd) mm4_round<32, N>(a, taddr + 32 * rnd, cb + 32 * rnd, e, s_pcnt, s_qcol);
+      if constexpr (T16) mm4_round<16, N>(a, taddr + 32 * NR32, cb + 32 * NR32, e, s_pcnt, s_qcol);
+      if constexpr (T8) mm4_round<8, N>(a, taddr + 32 * NR32 + 16 * T16, cb + 32 * NR32 + 16 * T16, e, s_pcnt, s_qcol);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mm_bar_arrive(&tempty[b]);
+    }
+  } else {
+    // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
+    if (lane == 0) {
+      const u32 idesc = (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | (1u << 23) | ((u32)(MM_M >> 4) << 24);
+      const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
+      const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
+      // K = 64 elements = 32 bytes = two core matrices per MMA
+      constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4_A_BYTES / 16;
+      const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
+      for (u64 it = 0; it < ntile; ++it) {
+        const int s = (int)(it % MM4_STAGES), b = (int)(it & 1);
+        if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+        mm_bar_wait(&full_bar[s], (u32)(it / MM4_STAGES) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const u64 das = da0 + (u64)s * DA_S;
+        const u32 dt = tmem + (u32)b * N;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) mm4_mma(dt, das + ks * DA_K, db0 + ks * DB_K, idesc, ks > 0, sfa, sfb);
+        mm_commit(&empty_bar[s]);
+        mm_commit(&tfull[b]);
+      }
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (a.mode == 0) {
+    // publish the private lists: one global atomic per (column, CTA); a list
+    // past its capacity poisons its query's count (> cap: the device fallback)
+    for (int c = warp; c < N; c += MM_THREADS / 32) {
+      const u32 cnt = s_pcnt[c];
+      if (cnt == 0) continue;
+      const u32 qi = s_qcol[c];
+      if (qi >= a.Q || chunk * N + c >= a.Q) continue;
+      u32 base = 0;
+      if (lane == 0) base = atomicAdd(a.cand_cnt + qi, cnt > a.pcap ? a.cap + 1 : cnt);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (cnt > a.pcap) continue;
+      const u64* src = a.priv + ((u64)blockIdx.x * N + c) * a.pcap;
+      for (u32 i = lane; i < cnt; i += 32)
+        if (base + i < a.cap) a.cand[(u64)qi * a.cap + base + i] = src[i];
+    }
+  }
+  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+}  // namespace fps
