@@ -9,13 +9,20 @@
 // and every block scale factor 1.0 (ue8m0 127):
 //   A (library row)  : element k = 1.0 if bit k is set (k < 168), then test digits
 //   B (query column) : element k = 2.0 if query bit k is set, then test digits
-// K slots 168..191 are zero bits in a compact library (the 21 B/entry layout
-// keeps 168 bits), so they carry the test terms (e2m1 values are 0, .5, 1,
-// 1.5, 2, 3, 4, 6 and negatives):
-//   168..172  A = digits of P = |a| / 6      B = -6
-//   173..174  A = digits of R = |a| % 6      B = -1
-//   175..182  A = 6                          B = digits of X = trunc(v / 6), v = T - |q| + 0.5
-//   183..184  A = 1                          B = digits of Y = v - 6X
+// Element order (any permutation of K applied to both operands leaves the
+// dot product unchanged): in each 32-element block c, u32 word t (elements
+// 8t..8t+7), nibble j holds bit 32c + 4j + t, so a producer builds a word as
+// ((x >> t) << 1) & 0x22222222 from the block's 32 bits x -- two ALU ops, no
+// table. Bits 168..191 are zero in a compact library (the 21 B/entry layout
+// keeps 168 bits), so in block 5 only nibbles 0-1 of each word carry bits
+// (160..167) and nibbles 2-7 of words 0-2 carry the test terms (e2m1 values
+// are 0, .5, 1, 1.5, 2, 3, 4, 6 and negatives):
+//   word 0 nibbles 2-6   A = digits of P = |a| / 6      B = -6
+//   word 0 nibble 7,
+//   word 1 nibble 2      A = digits of R = |a| % 6      B = -1
+//   word 1 nibbles 3-7,
+//   word 2 nibbles 2-4   A = 6                          B = digits of X = trunc(v / 6), v = T - |q| + 0.5
+//   word 2 nibbles 5-6   A = 1                          B = digits of Y = v - 6X
 // so the accumulator is D = 2c - |a| + v = T - d + 0.5: never zero, and the
 // pair passes (d <= T) iff the f32 sign bit is clear. All terms are small
 // integers or halves: the f32 sums are exact (checked bit-exactly on random
@@ -24,8 +31,8 @@
 //
 // Pipeline as in fps_mma.cuh (one CTA per SM): a loader warp streams library
 // tiles (bulk copies), 4 producer warps expand a 128-entry tile to the
-// canonical K-major fp4 layout (a byte -> 8 nibbles table lookup, 96 B per
-// row instead of 192), one lane issues 3 x K=64 MMAs per tile into one of two
+// canonical K-major fp4 layout (two ALU ops per 8 elements, 96 B per row
+// instead of 192), one lane issues 3 x K=64 MMAs per tile into one of two
 // TMEM accumulators, 16 epilogue warps test the sign bits. TMEM: two N-column
 // accumulators (N <= 240) and the scale factors in columns 480..511.
 #pragma once
@@ -63,6 +70,22 @@ __host__ __device__ inline u64 e2m1_digits(int x, int slots) {
   return out;
 }
 
+// Block-5 test slots, as (word, nibble) -> a flat nibble index 8 * word + nibble.
+constexpr int MM4_P0 = 2;    // P digits: word 0 nibbles 2..6
+constexpr int MM4_R0 = 7;    // R digits: word 0 nibble 7, word 1 nibble 2 (flat 7 and 10)
+constexpr int MM4_X0 = 11;   // X digits: word 1 nibbles 3..7 (flat 11..15), word 2 nibbles 2..4 (flat 18..20)
+constexpr int MM4_Y0 = 21;   // Y digits: word 2 nibbles 5..6 (flat 21..22)
+
+// The four u32 words of a 32-element block from its 32 bits x (element order above).
+__host__ __device__ __forceinline__ void mm4_words(u32 x, u32 code, u32 (&o)[4]) {
+  // code = e2m1 code of the operand's "1" value (1.0 = 2 for A, 2.0 = 4 for B), placed by a multiply
+  const u32 m = 0x11111111u;
+  o[0] = (x & m) * code;
+  o[1] = ((x >> 1) & m) * code;
+  o[2] = ((x >> 2) & m) * code;
+  o[3] = ((x >> 3) & m) * code;
+}
+
 // B of the fp4 fused test: columns ordered by u = T - |q| (as mm_prep_kernel),
 // padding columns (past Q) get v = -0.5 (D < 0 for every entry).
 __global__ void mm4_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __restrict__ tq,
@@ -83,25 +106,23 @@ __global__ void mm4_prep_kernel(const u64* __restrict__ q, u32 Q, const u32* __r
   const int v2 = ok ? 2 * ((int)tq[qi] - (int)pop) + 1 : -1;
   const int X = v2 / 12;                  // trunc(v / 6)
   const int Y2 = v2 - 12 * X;             // 2 x (v - 6X)
-  u64 nib[3] = {0, 0, 0};                 // elements 168..191 (24 nibbles)
-  nib[0] = e2m1_digits(-12, 1) * 0x11111ull;                       // 168..172: -6
-  nib[0] |= (u64)e2m1(-2) << 20 | (u64)e2m1(-2) << 24;             // 173..174: -1
-  const u64 dx = e2m1_digits(2 * X, 8);                            // 175..182
-  const u64 dy = e2m1_digits(Y2, 2);                               // 183..184
-  const u64 tail = dx | dy << 32;                                  // nibbles of 175..184
+  const u64 dx = e2m1_digits(2 * X, 8), dy = e2m1_digits(Y2, 2);
+  u32 t5[4] = {0, 0, 0, 0};               // block 5 test nibbles (flat index 8 * word + nibble)
+  auto setn = [&](int flat, u32 code) { t5[flat >> 3] |= code << (4 * (flat & 7)); };
+  for (int i = 0; i < 5; ++i) setn(MM4_P0 + i, e2m1(-12));            // -6
+  setn(MM4_R0, e2m1(-2));                                              // -1
+  setn(MM4_R0 + 3, e2m1(-2));
+  for (int i = 0; i < 8; ++i) setn(i < 5 ? MM4_X0 + i : 18 + (i - 5), (u32)(dx >> (4 * i)) & 15u);
+  for (int i = 0; i < 2; ++i) setn(MM4_Y0 + i, (u32)(dy >> (4 * i)) & 15u);
   unsigned char* b = bop + (u64)chunk * mm4_b_bytes((int)NN);
-  for (u32 kb = 0; kb < (u32)MM4_KB; ++kb) {
-    u32 byte = 0;
-    for (u32 h = 0; h < 2; ++h) {
-      const u32 k = 2 * kb + h;
-      u32 code;
-      if (k < 168) code = ((w[k >> 6] >> (k & 63)) & 1) ? 4u : 0u;  // 2.0
-      else if (k < 175) code = (u32)(nib[0] >> (4 * (k - 168))) & 15u;
-      else if (k < 185) code = (u32)(tail >> (4 * (k - 175))) & 15u;
-      else code = 0;
-      byte |= code << (4 * h);
-    }
-    b[mm_canon(j, kb, NN)] = (unsigned char)byte;
+  for (int c = 0; c < 6; ++c) {
+    const u32 x = (u32)(w[c >> 1] >> (32 * (c & 1)));
+    u32 o[4];
+    mm4_words(x, 4u, o);  // 2.0 per set query bit
+    if (c == 5)
+      for (int t = 0; t < 4; ++t) o[t] = (o[t] & 0xffu) | t5[t];
+    for (int t = 0; t < 4; ++t)
+      for (int by = 0; by < 4; ++by) b[mm_canon(j, 16 * c + 4 * t + by, NN)] = (unsigned char)(o[t] >> (8 * by));
   }
 }
 
@@ -173,8 +194,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
   __shared__ __align__(8) u64 full_bar[MM4_STAGES], empty_bar[MM4_STAGES], tfull[2], tempty[2];
   __shared__ __align__(8) u64 raw_full[MM_RAW], raw_empty[MM_RAW];
   __shared__ u32 tmem_base;
-  __shared__ u32 lut8[256];   // byte -> 8 e2m1 nibbles (bit -> 1.0)
-  __shared__ u32 luta[176];   // |a| -> nibbles of elements 168..175 (digits of -|a|, then A = 6)
+  __shared__ uint2 luta[176];  // |a| -> block-5 test nibbles of words 0 and 1 (digits of -|a|, A = 6)
   __shared__ u32 s_qcol[N], s_pcnt[N];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
@@ -196,15 +216,15 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
     s_qcol[i] = a.qcol[chunk * N + i];
     s_pcnt[i] = 0;
   }
-  for (int i = tid; i < 256; i += blockDim.x) {
-    u32 v = 0;
-    for (int b = 0; b < 8; ++b) v |= ((u32)(i >> b) & 1u) * 2u << (4 * b);  // 1.0 = 0b0010
-    lut8[i] = v;
-  }
   for (int i = tid; i < 176; i += blockDim.x) {
-    // elements 168..172: digits of |a| / 6; 173..174: digits of |a| % 6; 175: A = 6
     const u64 p = e2m1_digits(2 * (i / 6), 5), r = e2m1_digits(2 * (i % 6), 2);
-    luta[i] = (u32)(p | r << 20 | (u64)e2m1(12) << 28);
+    u32 t5[2] = {0, 0};
+    auto setn = [&](int flat, u32 code) { t5[flat >> 3] |= code << (4 * (flat & 7)); };
+    for (int d = 0; d < 5; ++d) setn(MM4_P0 + d, (u32)(p >> (4 * d)) & 15u);
+    setn(MM4_R0, (u32)r & 15u);
+    setn(MM4_R0 + 3, (u32)(r >> 4) & 15u);
+    for (int d = 0; d < 5; ++d) setn(MM4_X0 + d, e2m1(12));  // A = 6 (word 1 nibbles 3..7)
+    luta[i] = make_uint2(t5[0], t5[1]);
   }
   if (tid == 0) {
     for (int s = 0; s < MM4_STAGES; ++s) {
@@ -271,22 +291,18 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       const u32 pa = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
       if (it >= MM4_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM4_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM4_A_BYTES;
+      const uint2 ta = luta[pa < 176 ? pa : 175];
 #pragma unroll
-      for (int c = 0; c < 6; ++c) {  // 16 B = 32 elements = 4 bytes of the 192-bit string
-        uint4 v;
-        const u64 word = w[c >> 1];
-        const u32 sh = 32 * (c & 1);
-        v.x = lut8[(word >> sh) & 0xff];
-        v.y = lut8[(word >> (sh + 8)) & 0xff];
-        if (c < 5) {
-          v.z = lut8[(word >> (sh + 16)) & 0xff];
-          v.w = lut8[(word >> (sh + 24)) & 0xff];
-        } else {  // elements 168..191: the test terms
-          v.y = luta[pa < 176 ? pa : 175];
-          v.z = e2m1(12) * 0x1111111u | e2m1(2) << 28;  // 176..182: A = 6, 183: A = 1
-          v.w = e2m1(2);                                // 184: A = 1
+      for (int c = 0; c < 6; ++c) {  // 16 B = one 32-element block
+        u32 o[4];
+        mm4_words((u32)(w[c >> 1] >> (32 * (c & 1))), 2u, o);  // 1.0 per set bit
+        if (c == 5) {  // block 5: bits 160..167 in nibbles 0-1, test terms in 2-7
+          o[0] = (o[0] & 0xffu) | ta.x;
+          o[1] = (o[1] & 0xffu) | ta.y;
+          o[2] = (o[2] & 0xffu) | e2m1(12) * 0x111u << 8 | e2m1(2) * 0x11u << 20;  // A = 6 (nibbles 2-4), 1 (5-6)
+          o[3] = o[3] & 0xffu;
         }
-        *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = v;
+        *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = make_uint4(o[0], o[1], o[2], o[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mm_bar_arrive(&full_bar[s]);
