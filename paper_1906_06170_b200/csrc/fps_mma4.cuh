@@ -33,7 +33,8 @@
 // tiles (bulk copies), 4 producer warps expand a 128-entry tile to the
 // canonical K-major fp4 layout (two ALU ops per 8 elements, 96 B per row
 // instead of 192), one lane issues 3 x K=64 MMAs per tile into one of two
-// TMEM accumulators, 16 epilogue warps test the sign bits. TMEM: two N-column
+// TMEM accumulators, 16 epilogue warps (4 lane quadrants x 4 column
+// quarters, every tile) test the sign bits. TMEM: two N-column
 // accumulators (N <= 240) and the scale factors in columns 480..511.
 #pragma once
 #include "fps_mma.cuh"
@@ -152,27 +153,43 @@ __device__ __forceinline__ void mm4_ld<8>(u32 taddr, u32 (&r)[8]) {
                : "r"(taddr));
 }
 
-// One epilogue round: NREG columns starting at TMEM column offset `col`
-// (relative to the accumulator), global column index cb0 of the first.
-template <int NREG, int N>
-__device__ __forceinline__ void mm4_round(const MmArgs& a, u32 taddr, int cb0, u64 e, u32* s_pcnt, const u32* s_qcol) {
-  u32 r[NREG];
-  mm4_ld<NREG>(taddr, r);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  if (a.flags & 4096) return;
+// Issue the TMEM loads of CNT consecutive columns (CNT a multiple of 8, <= 64)
+// into r[0, CNT): x32 / x16 / x8 pieces, one wait for all of them afterwards.
+template <int CNT>
+__device__ __forceinline__ void mm4_issue(u32 taddr, u32* r) {
+  if constexpr (CNT >= 32) {
+    mm4_ld<32>(taddr, *reinterpret_cast<u32(*)[32]>(r));
+    mm4_issue<CNT - 32>(taddr + 32, r + 32);
+  } else if constexpr (CNT >= 16) {
+    mm4_ld<16>(taddr, *reinterpret_cast<u32(*)[16]>(r));
+    mm4_issue<CNT - 16>(taddr + 16, r + 16);
+  } else if constexpr (CNT >= 8) {
+    mm4_ld<8>(taddr, *reinterpret_cast<u32(*)[8]>(r));
+    mm4_issue<CNT - 8>(taddr + 8, r + 8);
+  }
+}
+
+// Test CNT loaded columns (f32 D = T - d + 0.5: a pair passes iff the sign
+// bit is clear): the AND of the sign bits first, the per-column extraction
+// only for lanes that hold a passing pair. cb0 = the first column's index.
+template <int CNT, int N>
+__device__ __forceinline__ void mm4_test(const MmArgs& a, const u32* r, int cb0, u64 e, u32* s_pcnt,
+                                         const u32* s_qcol) {
   u32 t = r[0];
 #pragma unroll
-  for (int i = 1; i < NREG; ++i) t &= r[i];
+  for (int i = 1; i < CNT; ++i) t &= r[i];
   const bool any = (t & 0x80000000u) == 0 && e < a.n;
   if (!__any_sync(0xffffffffu, any) || !any) return;
   u64 hm = 0;
 #pragma unroll
-  for (int i = 0; i < NREG; ++i) hm |= (u64)((~r[i]) >> 31) << i;
+  for (int i = 0; i < CNT; ++i) hm |= (u64)((~r[i]) >> 31) << i;
   const u64 idx = a.index_base + e;
   while (hm) {
     const int c = cb0 + __ffsll((long long)hm) - 1;
     hm &= hm - 1;
     if (a.mode == 0) {
+      // the CTA's private list of this column: a shared-memory counter and a
+      // store nothing waits on; published at the end
       const u32 pos = atomicAdd(s_pcnt + c, 1u);
       if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
     } else {
@@ -180,6 +197,30 @@ __device__ __forceinline__ void mm4_round(const MmArgs& a, u32 taddr, int cb0, u
       if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
     }
   }
+}
+
+// Epilogue columns of a warp: the N accumulator columns in 4 quarters of
+// multiples of 8 (e.g. N = 208: 56, 56, 48, 48).
+template <int N>
+struct Mm4Quarters {
+  static constexpr int U = N / 8;                       // 8-column units
+  static constexpr int W_HI = 8 * ((U + 3) / 4), W_LO = 8 * (U / 4);
+  static constexpr int N_HI = U % 4 ? U % 4 : 4;        // quarters of width W_HI
+  __device__ static constexpr int off(int q) { return q < N_HI ? q * W_HI : N_HI * W_HI + (q - N_HI) * W_LO; }
+};
+
+// One tile of one epilogue warp: load the quarter (one wait), release the
+// accumulator, test.
+template <int CNT, int N>
+__device__ __forceinline__ void mm4_tile(const MmArgs& a, u32 taddr, int cb0, u64 e, u64* tempty_bar, u32* s_pcnt,
+                                         const u32* s_qcol) {
+  u32 r[CNT];
+  mm4_issue<CNT>(taddr, r);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  mm_bar_arrive(tempty_bar);
+  if (a.flags & 4096) return;
+  mm4_test<CNT, N>(a, r, cb0, e, s_pcnt, s_qcol);
 }
 
 template <int N>
@@ -237,7 +278,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], MM_EPI / 2 * 32);
+      mm_bar_init(&tempty[b], MM_EPI * 32);  // every epilogue warp reads every tile
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -292,6 +333,11 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       if (it >= MM4_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM4_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM4_A_BYTES;
       const uint2 ta = luta[pa < 176 ? pa : 175];
+      if (a.flags & 65536) {  // experiment: no expansion (stage left as is)
+        if (!(a.flags & 32768)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mm_bar_arrive(&full_bar[s]);
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 6; ++c) {  // 16 B = one 32-element block
         u32 o[4];
@@ -304,12 +350,18 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
         }
         *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = make_uint4(o[0], o[1], o[2], o[3]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!(a.flags & 32768)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mm_bar_arrive(&full_bar[s]);
     }
   } else if (warp == 5 + MM_EPI) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
-    if (lane == 0) {
+    if (lane == 0 && (a.flags & 8192)) {  // experiment: no library loads
+      for (u64 r = 0; r < nraw; ++r) {
+        const int rs = (int)(r % MM_RAW);
+        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
+        mm_bar_arrive(&raw_full[rs]);
+      }
+    } else if (lane == 0) {
       const u64 pol = l2_evict_first_policy();
       for (u64 r = 0; r < nraw; ++r) {
         const int rs = (int)(r % MM_RAW);
@@ -320,27 +372,22 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
     }
     __syncwarp();
   } else if (warp < 4 + MM_EPI) {
-    // ===== epilogue: two groups of 8 warps on alternate tiles; warp (quad,
-    // half) reads lane quadrant quad, columns [half * N / 2, (half + 1) * N / 2)
-    const u32 grp = (u32)(warp - 4) / 8;
-    const u32 wq = (u32)(warp - 4) % 8;
-    const u32 quad = wq % 4, half = wq / 4;
+    // ===== epilogue: 16 warps, every tile; warp e reads TMEM lane quadrant
+    // e % 4 (its warp id mod 4) and column quarter e / 4 -- one load wait
+    // per tile per warp, then the accumulator is released and tested
+    const u32 ew = (u32)(warp - 4);
+    const u32 quad = ew % 4, qt = ew / 4;
     const u32 row = quad * 32 + lane;
-    constexpr int NC = N / 2;                  // columns per warp (multiple of 8)
-    constexpr int NR32 = NC / 32, T16 = (NC % 32) / 16, T8 = (NC % 16) / 8;
-    for (u64 it = grp; it < ntile; it += 2) {
-      const int b = (int)grp;
+    using QS = Mm4Quarters<N>;
+    const int c0 = QS::off((int)qt);
+    for (u64 it = 0; it < ntile; ++it) {
+      const int b = (int)(it & 1);
       const u64 e = (t0 + it) * MM_M + row;
       mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
-      const int cb = (int)(half * NC);
-#pragma unroll 1
-      for (int rnd = 0; rnd < NR32; ++rnd) mm4_round<32, N>(a, taddr + 32 * rnd, cb + 32 * rnd, e, s_pcnt, s_qcol);
-      if constexpr (T16) mm4_round<16, N>(a, taddr + 32 * NR32, cb + 32 * NR32, e, s_pcnt, s_qcol);
-      if constexpr (T8) mm4_round<8, N>(a, taddr + 32 * NR32 + 16 * T16, cb + 32 * NR32 + 16 * T16, e, s_pcnt, s_qcol);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mm_bar_arrive(&tempty[b]);
+      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + (u32)c0;
+      if ((int)qt < QS::N_HI) mm4_tile<QS::W_HI, N>(a, taddr, c0, e, &tempty[b], s_pcnt, s_qcol);
+      else mm4_tile<QS::W_LO, N>(a, taddr, c0, e, &tempty[b], s_pcnt, s_qcol);
     }
   } else {
     // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
