@@ -1074,6 +1074,10 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   a.out_cnt = out_cnt;
   a.out_cap = out_cap;
   a.flags = scan_flags();
+  {
+    const char* e = std::getenv("FPS_MM_SUSPEND_NS");
+    a.suspend_ns = e ? (u32)std::atoi(e) : 20000u;
+  }
   if (mode == 0) {
     a.priv = L->mm_priv.as<u64>();
     a.pcap = (u32)pcap;
@@ -2172,6 +2176,13 @@ int fps_topk(fps_lib* lib, const uint64_t* queries, uint32_t Q, uint32_t k, uint
   }
   unpack_topk(hk, hc, Q, k, out_idx, out_dist, out_cnt);
   return FPS_OK;
+}
+
+// debug (not part of include/fps.h): per-tile timestamps of the fp4 scan
+// (scan flag 1 << 20; tools/dbg/mm4_trace.py)
+extern "C" int fps_dbg_mm4_trace(uint64_t* out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, fps::g_mm4_trace, sizeof(fps::g_mm4_trace));
 }
 
 #ifdef FPS_SCAN_TRACE

@@ -168,6 +168,7 @@ struct MmArgs {
   u32 flags;                // experiments: 4096 = epilogue without tests, 8192 = producer without library loads
   u64* priv;                // top-k: [CTA][N columns][pcap] private candidate lists (no global atomics on the scan path)
   u32 pcap;
+  u32 suspend_ns;           // fp4 kernel: try_wait suspend hint on the MMA / epilogue barriers (0: spin)
 };
 
 __device__ __forceinline__ void mm_bar_init(u64* bar, u32 count) {
@@ -175,6 +176,20 @@ __device__ __forceinline__ void mm_bar_init(u64* bar, u32 count) {
 }
 __device__ __forceinline__ void mm_bar_arrive(u64* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mm_bar_wait_ns(u64* bar, u32 parity, u32 ns) {
+  asm volatile(
+      "{\n .reg .pred p;\n MMWN: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra MMWN;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+__device__ __forceinline__ void mm_bar_wait_spin(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n MMWS: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra MMWS;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void mm_bar_wait(u64* bar, u32 parity) {
   asm volatile(

@@ -41,6 +41,13 @@
 
 namespace fps {
 
+__device__ unsigned long long g_mm4_trace[64 * 8];  // debug (scan flag 1 << 20): CTA 0, tiles 2000..2063
+#define MM4_TRACE(slot)                                                                      \
+  do {                                                                                       \
+    if ((a.flags & (1u << 20)) && blockIdx.x == 0 && it >= 2000 && it < 2064)                \
+      g_mm4_trace[(it - 2000) * 8 + (slot)] = clock64();                                     \
+  } while (0)
+
 constexpr int MM4_KB = 96;                       // bytes per operand row (192 e2m1 elements)
 constexpr u32 MM4_A_BYTES = MM_M * MM4_KB;       // 12 KB per stage
 constexpr int MM4_STAGES = 6;
@@ -313,6 +320,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       const u32 sub = (u32)(it % SUB);
       const int rs = (int)(r % MM_RAW);
       if (sub == 0) mm_bar_wait(&raw_full[rs], (u32)(r / MM_RAW) & 1u);
+      if (tid == 0) MM4_TRACE(3);
       u64 w[3];
       {
         const char* tb = raw + (u64)rs * RAW_BYTES;
@@ -331,6 +339,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
       const u32 pa = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
       if (it >= MM4_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM4_STAGES) - 1) & 1u);
+      if (tid == 0) MM4_TRACE(4);
       unsigned char* A = sA + s * MM4_A_BYTES;
       const uint2 ta = luta[pa < 176 ? pa : 175];
       if (a.flags & 65536) {  // experiment: no expansion (stage left as is)
@@ -352,6 +361,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       }
       if (!(a.flags & 32768)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mm_bar_arrive(&full_bar[s]);
+      if (tid == 0) MM4_TRACE(5);
     }
   } else if (warp == 5 + MM_EPI) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
@@ -383,11 +393,14 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
     for (u64 it = 0; it < ntile; ++it) {
       const int b = (int)(it & 1);
       const u64 e = (t0 + it) * MM_M + row;
-      mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
+      if (a.suspend_ns) mm_bar_wait_ns(&tfull[b], (u32)(it >> 1) & 1u, a.suspend_ns);
+      else mm_bar_wait_spin(&tfull[b], (u32)(it >> 1) & 1u);
+      if (ew == 0 && lane == 0) MM4_TRACE(6);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + (u32)c0;
       if ((int)qt < QS::N_HI) mm4_tile<QS::W_HI, N>(a, taddr, c0, e, &tempty[b], s_pcnt, s_qcol);
       else mm4_tile<QS::W_LO, N>(a, taddr, c0, e, &tempty[b], s_pcnt, s_qcol);
+      if (ew == 0 && lane == 0) MM4_TRACE(7);
     }
   } else {
     // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
@@ -400,8 +413,15 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
       for (u64 it = 0; it < ntile; ++it) {
         const int s = (int)(it % MM4_STAGES), b = (int)(it & 1);
-        if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
-        mm_bar_wait(&full_bar[s], (u32)(it / MM4_STAGES) & 1u);
+        if (a.suspend_ns) {
+          if (it >= 2) mm_bar_wait_ns(&tempty[b], (u32)((it >> 1) - 1) & 1u, a.suspend_ns);
+          mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4_STAGES) & 1u, a.suspend_ns);
+        } else {
+          if (it >= 2) mm_bar_wait_spin(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+          MM4_TRACE(0);
+          mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4_STAGES) & 1u);
+        }
+        MM4_TRACE(1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u64 das = da0 + (u64)s * DA_S;
         const u32 dt = tmem + (u32)b * N;
@@ -409,6 +429,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
         for (int ks = 0; ks < 3; ++ks) mm4_mma(dt, das + ks * DA_K, db0 + ks * DB_K, idesc, ks > 0, sfa, sfb);
         mm_commit(&empty_bar[s]);
         mm_commit(&tfull[b]);
+        MM4_TRACE(2);
       }
     }
     __syncwarp();

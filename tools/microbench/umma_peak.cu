@@ -334,6 +334,113 @@ static void peak(int sms) {
   cudaFree(dclk);
 }
 
+
+// ------------------------------------------------------------------ 3. pipeline round trip
+// As k_peak, plus 16 epilogue warps that, per tile, wait for the accumulator
+// (tcgen05.commit -> mbarrier), load their quarter of it from TMEM, and
+// release it (mbarrier arrive) before the issuer may reuse it: the
+// MMA -> epilogue -> MMA round trip with NACC accumulator buffers.
+template <int N, int NACC>
+__global__ void __launch_bounds__(32 * 18, 1) k_pipe(int tiles, unsigned long long* clk, int spin) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sa = sm;
+  uint8_t* sb = sm + M * KB;
+  __shared__ uint64_t tfull[NACC], tempty[NACC];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (M * KB + N * KB) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int b = 0; b < NACC; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&tfull[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 512;" ::"r"(su32(&tempty[b])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tmem_base;
+  tmem_fill(tm, 480, 32, 0x7f7f7f7fu);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp >= 2) {  // 16 epilogue warps: quadrant warp % 4, quarter (warp - 2) / 4
+    const int ew = warp - 2, quad = warp % 4, qt = ew / 4;
+    constexpr int W = (N / 4) / 8 * 8;
+    for (int t = 0; t < tiles; ++t) {
+      const int b = t % NACC;
+      bar_wait(&tfull[b], (uint32_t)(t / NACC) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t ta = tm + ((uint32_t)(32 * quad) << 16) + (uint32_t)(b * N + qt * W);
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+            "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+            "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(ta));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+      if (r[0] == 0x12345678u && r[31] == 7u) clk[0] = 1;  // keep the loads
+    }
+  } else if (tid == 0) {
+    const unsigned long long t0 = clock64();
+    const uint64_t da0 = desc(su32(sa), M / 8 * 128, 128);
+    const uint64_t db0 = desc(su32(sb), N / 8 * 128, 128);
+    constexpr uint64_t DA = 2 * (M / 8 * 128) / 16, DB = 2 * (N / 8 * 128) / 16;
+    for (int t = 0; t < tiles; ++t) {
+      const int b = t % NACC;
+      if (t >= NACC) {
+        if (spin) bar_wait(&tempty[b], (uint32_t)((t / NACC) - 1) & 1u);
+        else
+          asm volatile(
+              "{\n .reg .pred p;\n WS: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 20000;\n @!p bra WS;\n}\n" ::"r"(
+                  su32(&tempty[b])),
+              "r"((uint32_t)((t / NACC) - 1) & 1u)
+              : "memory");
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tm + (uint32_t)b * N;
+#pragma unroll
+      for (int ks = 0; ks < 3; ++ks)
+        mma_mxf4(dt, da0 + ks * DA, db0 + ks * DB, idesc_mxf4(N), ks > 0, tm + 480, tm + 496);
+      commit(&tfull[b]);
+    }
+    clk[blockIdx.x + 1] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+template <int N, int NACC>
+static void pipe(int sms, int spin) {
+  const int tiles = 20000;
+  const int smem = M * KB + N * KB;
+  CK(cudaFuncSetAttribute(k_pipe<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  unsigned long long* dclk;
+  CK(cudaMalloc(&dclk, (sms + 1) * 8));
+  k_pipe<N, NACC><<<sms, 32 * 18, smem>>>(100, dclk, spin);
+  CK(cudaDeviceSynchronize());
+  k_pipe<N, NACC><<<sms, 32 * 18, smem>>>(tiles, dclk, spin);
+  CK(cudaDeviceSynchronize());
+  std::vector<unsigned long long> clk(sms + 1);
+  CK(cudaMemcpy(clk.data(), dclk, (sms + 1) * 8, cudaMemcpyDeviceToHost));
+  unsigned long long mx = 0;
+  for (int i = 1; i <= sms; ++i) mx = clk[i] > mx ? clk[i] : mx;
+  printf("pipe mxf4 N=%3d, %d accumulators, %s: %.1f clk per tile (MMA + epilogue round trip)\n", N, NACC,
+         spin ? "spin waits" : "suspend-hint waits", (double)mx / tiles);
+  cudaFree(dclk);
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -346,5 +453,10 @@ int main() {
   peak<1, 208>(sms);
   peak<1, 128>(sms);
   peak<1, 64>(sms);
+  pipe<208, 2>(sms, 1);
+  pipe<208, 2>(sms, 0);
+  pipe<160, 3>(sms, 1);
+  pipe<112, 4>(sms, 1);
+  pipe<128, 2>(sms, 1);
   return bad != 0;
 }
