@@ -1003,7 +1003,7 @@ int mma4_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   CUDA_TRY(smem_optin((const void*)fps::mma4_scan_kernel<N>, smem));
   auto* ev = timing_slot(L);
   if (ev) cudaEventRecord(ev->first, s);
-  fps::mma4_scan_kernel<N><<<ctas, fps::MM4_THREADS, smem, s>>>(a);
+  fps::mma4_scan_kernel<N><<<ctas, fps::MM_THREADS, smem, s>>>(a);
   if (ev) cudaEventRecord(ev->second, s);
   L->launches++;
   LAUNCH_CHECK("mma4_scan_kernel");

@@ -51,9 +51,6 @@ __device__ unsigned long long g_mm4_trace[64 * 8];  // debug (scan flag 1 << 20)
 constexpr int MM4_KB = 96;                       // bytes per operand row (192 e2m1 elements)
 constexpr u32 MM4_A_BYTES = MM_M * MM4_KB;       // 12 KB per stage
 constexpr int MM4_STAGES = 6;
-constexpr int MM4_PG = 2;                        // producer groups (4 warps each) on alternate tiles
-constexpr int MM4_PW = 4 * MM4_PG;               // producer warps
-constexpr int MM4_THREADS = (MM4_PW + MM_EPI + 2) * 32;  // producers, epilogue, MMA issuer, loader
 constexpr u32 MM4_SF_COL = 480;                  // scale factors (all 1.0): SFA at 480, SFB at 496
 __host__ __device__ constexpr u32 mm4_b_bytes(int n) { return (u32)n * MM4_KB; }
 __host__ __device__ constexpr size_t mm4_smem(int n) {
@@ -234,7 +231,7 @@ __device__ __forceinline__ void mm4_tile(const MmArgs& a, u32 taddr, int cb0, u6
 }
 
 template <int N>
-__global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs a) {
+__global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a) {
   static_assert(N % 16 == 0 && N >= 64 && N <= 240, "accumulator width (two accumulators + scale factors in 512 columns)");
   constexpr u32 B_BYTES = mm4_b_bytes(N);
   constexpr u32 TMEM_COLS = 512;
@@ -284,7 +281,7 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
     }
     for (int r = 0; r < MM_RAW; ++r) {
       mm_bar_init(&raw_full[r], 1);
-      mm_bar_init(&raw_empty[r], 128 * SUB);  // every entry row of the raw tile, read once
+      mm_bar_init(&raw_empty[r], 128);
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
@@ -292,7 +289,7 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MM4_PW + MM_EPI) {
+  if (warp == 4 + MM_EPI) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -314,11 +311,10 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const u64 ntile = nraw * SUB;
 
-  if (warp < MM4_PW) {
-    // ===== producers: group g (4 warps) takes tiles g, g + 2, ...; thread =
-    // entry row; 6 x 16 B of e2m1 nibbles per row
-    const u32 row = (u32)tid % 128;
-    for (u64 it = (u32)tid / 128; it < ntile; it += MM4_PG) {
+  if (warp < 4) {
+    // ===== producers: thread = entry row; 6 x 16 B of e2m1 nibbles per row
+    const u32 row = (u32)tid;
+    for (u64 it = 0; it < ntile; ++it) {
       const int s = (int)(it % MM4_STAGES);
       const u64 r = it / SUB;
       const u32 sub = (u32)(it % SUB);
@@ -340,7 +336,7 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
           w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
         }
       }
-      mm_bar_arrive(&raw_empty[rs]);
+      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
       const u32 pa = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
       if (it >= MM4_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM4_STAGES) - 1) & 1u);
       if (tid == 0) MM4_TRACE(4);
@@ -367,7 +363,7 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
       mm_bar_arrive(&full_bar[s]);
       if (tid == 0) MM4_TRACE(5);
     }
-  } else if (warp == MM4_PW + MM_EPI + 1) {
+  } else if (warp == 5 + MM_EPI) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
     if (lane == 0 && (a.flags & 8192)) {  // experiment: no library loads
       for (u64 r = 0; r < nraw; ++r) {
@@ -385,11 +381,11 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
       }
     }
     __syncwarp();
-  } else if (warp < MM4_PW + MM_EPI) {
+  } else if (warp < 4 + MM_EPI) {
     // ===== epilogue: 16 warps, every tile; warp e reads TMEM lane quadrant
     // e % 4 (its warp id mod 4) and column quarter e / 4 -- one load wait
     // per tile per warp, then the accumulator is released and tested
-    const u32 ew = (u32)(warp - MM4_PW);
+    const u32 ew = (u32)(warp - 4);
     const u32 quad = ew % 4, qt = ew / 4;
     const u32 row = quad * 32 + lane;
     using QS = Mm4Quarters<N>;
@@ -443,7 +439,7 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
   if (a.mode == 0) {
     // publish the private lists: one global atomic per (column, CTA); a list
     // past its capacity poisons its query's count (> cap: the device fallback)
-    for (int c = warp; c < N; c += MM4_THREADS / 32) {
+    for (int c = warp; c < N; c += MM_THREADS / 32) {
       const u32 cnt = s_pcnt[c];
       if (cnt == 0) continue;
       const u32 qi = s_qcol[c];
@@ -457,7 +453,7 @@ __global__ void __launch_bounds__(MM4_THREADS, 1) mma4_scan_kernel(const MmArgs 
         if (base + i < a.cap) a.cand[(u64)qi * a.cap + base + i] = src[i];
     }
   }
-  if (warp == MM4_PW + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  if (warp == 4 + MM_EPI) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 }  // namespace fps
