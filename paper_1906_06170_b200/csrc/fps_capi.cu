@@ -959,11 +959,15 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   return true;
 }
 
-// Operand kind of the tensor-core scan: block-scaled fp4 (kind::mxf4, twice
-// the int8 MMA rate; default) or int8 (kind::i8; FPS_MMA_KIND=i8).
+// Operand kind of the tensor-core scan: int8 (kind::i8, default) or
+// block-scaled fp4 (kind::mxf4, FPS_MMA_KIND=fp4). fp4 has twice the MMA
+// rate, but its f32 accumulators cost 4 B of TMEM read per (entry, query)
+// pair against 2 B for the int8 kernel's packed 16-bit reads, and the TMEM
+// read bandwidth -- not the MMA -- bounds the large-batch scan
+// (profiles/r02_summary.md), so int8 is faster end to end.
 bool mma_fp4() {
   const char* e = std::getenv("FPS_MMA_KIND");
-  return !(e && std::string(e) == "i8");
+  return e && std::string(e) == "fp4";
 }
 
 // Accumulator width (queries per chunk). int8: 64 / 128 / 256. fp4: two
