@@ -165,6 +165,15 @@ def roofline_model(workload: str) -> dict:
     return {}
 
 
+def tensor_peaks() -> dict:
+    """Measured tcgen05 dense rates per operand kind and accumulator width."""
+    p = ROOT / "profiles" / "tensor_peaks.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {"nominal": {"i8": 4500.0, "mxf4": 9000.0}}
+
+
 def traffic_for(workload: str):
     """dram bytes per scan-kernel launch from the committed ncu --set full capture."""
     p = ROOT / "profiles" / "traffic.json"
@@ -454,7 +463,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
             lib.range_async(dq, Q, rad, state["out"], state["cap"], count_t, stream)
             lib.sort_keys(state["out"], state["hits"], stream)
             if world > 1:
-                return D.gather_range(state["out"][: state["hits"]], D.device_sort)
+                return D.gather_range(state["out"][: state["hits"]], D.device_merge_runs)
             return state["out"][: state["hits"]]
 
     def barrier():
@@ -599,22 +608,27 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         naive = sm * POPC_PER_SM_CLK / POPC_PER_CMP_NAIVE * mhz * 1e6 / 1e9
         model = roofline_model(args.workload)
         if kernel == "tensor-core multi-query scan":
-            # int8 GEMM on tcgen05: K = 192 bytes (3 x 64 bits) per pair, 2 ops
-            # per multiply-add. There is no driver-measured int8 peak: the
-            # denominator is the nominal dense int8/fp8 tensor rate of a B200
-            # (4.5 POP/s, /opt/skills/guides/B200_PROFILING.md); the ratio to
-            # 2 x the driver-measured dense bf16 rate (int8 issues at twice
-            # the bf16 rate) is reported beside it. The 6-POPC figure of
-            # SURVEY §8(d) is obsolete for this kernel (it does no POPC).
+            # tcgen05 GEMM: K = 192 elements (3 x 64 bits) per (query, entry)
+            # pair, 2 ops per multiply-add. Denominator: the MEASURED dense
+            # issue rate of the operand kind the scan ran with, at its
+            # accumulator width (tools/microbench/umma_peak.cu,
+            # profiles/tensor_peaks.json); nominal rates beside it. The
+            # 6-POPC figure of SURVEY §8(d) is obsolete for this kernel.
+            mk = lib.last_mma_kind or "i8"
+            fam = "i8" if mk == "i8" else "mxf4"
+            width = (256 if Q > 128 else 128 if Q > 64 else 64) if fam == "i8" else (
+                64 if Q <= 64 else 128 if Q <= 128 else 208)
+            tp = tensor_peaks()
+            peak = float(tp.get(fam, {}).get(str(width), tp.get("nominal", {}).get(fam, 4500.0)))
             ops = 2.0 * 192 * Q * shard_n
             tops = ops / (scan_avg_ms / 1e3) / 1e12
-            bf16 = float(peaks.get("bf16_tflops", 1590.0))
-            peak = 4500.0
-            roof = {"bound": "tensor", "achieved": tops, "peak": peak, "unit": "TOP/s (int8)", "frac": tops / peak,
-                    "traffic": traffic_for(args.workload),
-                    "peak_source": "nominal dense int8 tensor rate of a B200 (4.5 POP/s, no measured int8 peak); "
-                                   f"vs 2 x measured dense bf16 {2 * bf16:.0f} TOP/s ({peaks['_source']}): "
-                                   f"{tops / (2 * bf16):.3f}",
+            roof = {"bound": "tensor", "achieved": tops, "peak": peak,
+                    "unit": f"TOP/s ({'int8' if fam == 'i8' else 'fp4 e2m1, block-scaled'})", "frac": tops / peak,
+                    "traffic": traffic_for(args.workload), "operand_kind": mk, "accumulator_columns": width,
+                    "peak_source": f"measured dense tcgen05 kind::{'i8' if fam == 'i8' else 'mxf4'} rate at N = {width} "
+                                   "(profiles/tensor_peaks.json, tools/microbench/umma_peak.cu); nominal "
+                                   f"{tp.get('nominal', {}).get(fam, 0):.0f} TOP/s: "
+                                   f"{tops / max(tp.get('nominal', {}).get(fam, 1.0), 1.0):.3f}",
                     "algorithmic_ops_per_launch": ops, "comparisons_per_s": achieved * 1e9}
         elif kernel == "bit-sliced multi-query scan" and model.get("alu_warp_instr_per_cmp"):
             # ALU-pipe bound: 2 warp-instructions/clk/SM issue on the ALU pipe;

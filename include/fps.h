@@ -186,12 +186,25 @@ int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream);
  * d_in_keys G x Q x k (each row sorted, UINT64_MAX pads), d_in_cnt G x Q. */
 int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_t G, uint32_t Q, uint32_t k,
                     uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream);
+/* Rank-0 merge of G <= 32 sorted runs of unique range keys (one per shard,
+ * the torchrun gather of bench.py / distributed.gather_range): run g is
+ * d_runs[g][0 .. run_len[g]) on the device, run_len is a host array; the
+ * union lands sorted in d_out by a merge by rank (no re-sort). Replaces the
+ * reference's in-process union of shard results (merge_topk, scan.py:225-236)
+ * for the range output, which the reference does not have. */
+int fps_merge_runs_async(const uint64_t* const* d_runs, const uint64_t* run_len, uint32_t G, uint64_t* d_out,
+                         void* stream);
 /* Kernel family of the last scan on this handle (reporting / tests):
  * 1 single-query HBM scan, 2 multi-query POPC scan, 3 bit-sliced multi-query
  * scan, 4 large-k (histogram + range + sort) path, 5 single-query plane scan
  * (reads only the bit planes the query needs), 6 tensor-core multi-query scan
  * (tcgen05 int8 GEMM with the distance test folded in). */
 int fps_last_kernel(const fps_lib* lib);
+/* Operand kind of the last tensor-core scan on this handle (reporting / tests):
+ * 0 none yet, 1 int8 (kind::i8, tiles expanded in the kernel), 2 block-scaled
+ * fp4 expanded in the kernel (kind::mxf4), 3 block-scaled fp4 from the
+ * library's fp4 operand copy (the default; FPS_MMA_KIND=i8|fp4|fp4x). */
+int fps_last_mma_kind(const fps_lib* lib);
 /* HBM held by the handle: the tiled library, the derived copies built on
  * first use (plane-major copy of the single-query plane scan, bit-plane copy
  * of the multi-query kernels; ~21.75 and ~22.3 B per entry), and per-call

@@ -68,8 +68,10 @@ SIGNATURES = {
     "fps_range_async": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _vp, C.c_uint64, _vp, _vp]),
     "fps_sort_keys": (C.c_int, [_vp, _vp, C.c_uint64, _vp]),
     "fps_merge_async": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
+    "fps_merge_runs_async": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _vp]),
     "fps_launch_count": (C.c_uint64, [_vp]),
     "fps_last_kernel": (C.c_int, [_vp]),
+    "fps_last_mma_kind": (C.c_int, [_vp]),
     "fps_timing": (C.c_int, [_vp, C.c_int]),
     "fps_timing_read": (C.c_int, [_vp, C.POINTER(C.c_double), _u64p]),
     "fps_memory": (C.c_int, [_vp, _u64p, _u64p, _u64p, C.POINTER(C.c_double)]),

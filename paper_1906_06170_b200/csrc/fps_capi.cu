@@ -7,6 +7,7 @@
 // the per-search shard streaming of scan.py:158-170 (the library is uploaded
 // once instead of being re-read per search).
 #include <cub/device/device_radix_sort.cuh>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -27,6 +28,7 @@
 #include "fps_planeq.cuh"
 #include "fps_mma.cuh"
 #include "fps_mma4.cuh"
+#include "fps_mma4x.cuh"
 
 using fps::u32;
 using fps::u64;
@@ -182,6 +184,10 @@ struct fps_lib {
   // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
   DevBuf mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp, mm_priv;
   DevBuf mm_ovf;  // candidate-list overflow flag of the tensor-core top-k (gates its fallback pass)
+  // fp4 operand copy of the library for the tensor-core scan (fps_mma4x.cuh, built on first use)
+  DevBuf mq4x;
+  int mq4x_state = 0;  // as bs_state (-1: not compact, or no memory for it)
+  alignas(64) CUtensorMap mq4x_map;  // the copy as rows of 256 B for TMA tensor loads
   u64 pm_stride = 0;  // u32 words per plane
   HostBuf h_stage;
   HostBuf h_range[2];     // pinned staging of range results (fps_range_fetch)
@@ -193,6 +199,7 @@ struct fps_lib {
   size_t hmap_bytes = 0;
   // optional per-launch timing of the scan kernel (bench roofline evidence)
   int last_kernel = 0;  // fps_last_kernel
+  int last_mma_kind = 0;  // fps_last_mma_kind: operand kind of the last tensor-core scan (1 + MmaKind)
   // host-API top-k calls replayed as one CUDA graph per (Q, k):
   // H2D queries -> scan -> select -> D2H, captured once
   struct TopkGraph {
@@ -959,15 +966,71 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   return true;
 }
 
-// Operand kind of the tensor-core scan: int8 (kind::i8, default) or
-// block-scaled fp4 (kind::mxf4, FPS_MMA_KIND=fp4). fp4 has twice the MMA
-// rate, but its f32 accumulators cost 4 B of TMEM read per (entry, query)
-// pair against 2 B for the int8 kernel's packed 16-bit reads, and the TMEM
-// read bandwidth -- not the MMA -- bounds the large-batch scan
-// (profiles/r02_summary.md), so int8 is faster end to end.
-bool mma_fp4() {
+// Operand kind of the tensor-core scan (FPS_MMA_KIND): "fp4x" (default) is
+// the block-scaled fp4 kernel fed from the library's fp4 operand copy
+// (fps_mma4x.cuh: no per-tile expansion, twice the MMA rate of int8);
+// "fp4" expands tiles on the fly (fps_mma4.cuh), "i8" is the int8 kernel
+// (fps_mma.cuh) -- also the fallback when the operand copy (96 B per entry)
+// does not fit in HBM.
+enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
+MmaKind mma_kind_env() {
   const char* e = std::getenv("FPS_MMA_KIND");
-  return e && std::string(e) == "fp4";
+  if (!e) return MMA_FP4X;
+  const std::string v(e);
+  return v == "fp4" ? MMA_FP4 : v == "i8" ? MMA_I8 : MMA_FP4X;
+}
+bool mma_fp4() { return mma_kind_env() != MMA_I8; }
+
+// Build (once) the fp4 operand copy; on failure (no memory) the scan uses int8.
+int mq4x_ensure(fps_lib* L) {
+  if (L->mq4x_state) return FPS_OK;
+  if (!L->compact) {
+    L->mq4x_state = -1;
+    return FPS_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const u64 tiles = (L->n + fps::MM_M - 1) / fps::MM_M;
+  if (L->mq4x.ensure((size_t)std::max<u64>(tiles, 1) * fps::MM4X_TILE)) {
+    cudaGetLastError();
+    L->mq4x_state = -1;
+    return FPS_OK;
+  }
+  const int grid = (int)std::min<u64>((tiles * 6 * fps::MM_M + 255) / 256, (u64)L->sms * 32);
+  fps::mm4x_build_kernel<<<std::max(grid, 1), 256, 0, L->stream>>>(L->out(), L->n, tiles, L->mq4x.as<unsigned char>());
+  L->launches++;
+  CUDA_TRY(cudaGetLastError());
+  // tensor map over the copy: [tiles * 48 rows][256 B] u8, one 48-row box per tile
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      cudaGetLastError();
+      return fail(FPS_ECUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t gdim[2] = {fps::MM4X_ROW, (cuuint64_t)tiles * fps::MM4X_BOX_ROWS};
+  const cuuint64_t gstride[1] = {fps::MM4X_ROW};
+  const cuuint32_t box[2] = {fps::MM4X_ROW, fps::MM4X_BOX_ROWS};
+  const cuuint32_t estride[2] = {1, 1};
+  const CUresult cr = encode(&L->mq4x_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, L->mq4x.p, gdim, gstride, box, estride,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(FPS_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)cr) + ")");
+  CUDA_TRY(cudaStreamSynchronize(L->stream));
+  L->mq4x_state = 1;
+  L->derived_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return FPS_OK;
+}
+
+// The kind a call runs: fp4x only once its operand copy exists.
+MmaKind mma_kind(fps_lib* L) {
+  MmaKind k = mma_kind_env();
+  if (k == MMA_FP4X) {
+    if (mq4x_ensure(L) != FPS_OK || L->mq4x_state != 1) k = MMA_I8;
+  }
+  return k;
 }
 
 // Accumulator width (queries per chunk). int8: 64 / 128 / 256. fp4: two
@@ -1014,6 +1077,28 @@ int mma4_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   return FPS_OK;
 }
 
+template <int N, int EPI>
+int mma4x_launch_ne(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
+  const size_t smem = fps::mm4x_smem(N);
+  CUDA_TRY(smem_optin((const void*)fps::mma4x_scan_kernel<N, EPI>, smem));
+  auto* ev = timing_slot(L);
+  if (ev) cudaEventRecord(ev->first, s);
+  fps::mma4x_scan_kernel<N, EPI><<<ctas, fps::mm4x_threads(EPI), smem, s>>>(a, L->mq4x.as<unsigned char>(),
+                                                                               L->mq4x_map);
+  if (ev) cudaEventRecord(ev->second, s);
+  L->launches++;
+  LAUNCH_CHECK("mma4x_scan_kernel");
+  return FPS_OK;
+}
+// Epilogue warps of the fp4 operand-copy kernel (FPS_MM4X_EPI: 8 or 16).
+template <int N>
+int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
+  const char* e = std::getenv("FPS_MM4X_EPI");
+  const int epi = e ? std::atoi(e) : 8;
+  if (epi == 16) return mma4x_launch_ne<N, 16>(L, ctas, s, a);
+  return mma4x_launch_ne<N, 8>(L, ctas, s, a);
+}
+
 // Shared part of the tensor-core calls: per-query operands from the bound
 // mm_tq[q] (top-k: the seed's k-th distance; range: the radius), columns
 // ordered by u = T - |q|, then the scan. mode 0 appends candidate keys to the
@@ -1021,7 +1106,9 @@ int mma4_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
 int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
             cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull) {
   int rc;
-  const bool fp4 = mma_fp4();
+  const MmaKind kind = mma_kind(L);
+  const bool fp4 = kind != MMA_I8;
+  L->last_mma_kind = 1 + (int)kind;
   const u32 NN = mma_pick_n(Q, fp4);
   const u32 nchunks = (Q + NN - 1) / NN;
   n_scan = std::min<u64>(n_scan, L->n);  // entries [0, n_scan) (a prefix pass of the top-k path)
@@ -1085,6 +1172,13 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   if (mode == 0) {
     a.priv = L->mm_priv.as<u64>();
     a.pcap = (u32)pcap;
+  }
+  if (kind == MMA_FP4X) {
+    if (NN == 64) return mma4x_launch_n<64>(L, ctas, s, a);
+    if (NN == 128) return mma4x_launch_n<128>(L, ctas, s, a);
+    if (NN == 160) return mma4x_launch_n<160>(L, ctas, s, a);
+    if (NN == 208) return mma4x_launch_n<208>(L, ctas, s, a);
+    return mma4x_launch_n<240>(L, ctas, s, a);
   }
   if (fp4) {
     if (NN == 64) return mma4_launch_n<64>(L, ctas, s, a);
@@ -1958,6 +2052,8 @@ int fps_write_entries(fps_lib* lib, const uint64_t* idx, const uint64_t* words, 
   // the bit-plane copies are derived from the entries: rebuild on next use
   lib->bs.release();
   lib->bs_state = 0;
+  lib->mq4x.release();
+  lib->mq4x_state = 0;
   lib->pm.release();
   lib->pm_perm.release();
   lib->pm_meta.release();
@@ -2361,6 +2457,29 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
   return FPS_OK;
 }
 
+int fps_merge_runs_async(const uint64_t* const* d_runs, const uint64_t* run_len, uint32_t G, uint64_t* d_out,
+                         void* stream) {
+  if (G == 0 || G > (uint32_t)fps::GROUP_MAX || !d_runs || !run_len)
+    return fail(FPS_EINVAL, "1 <= G <= 32 runs and their lengths are required");
+  fps::ShardLists lists{};
+  u64 off = 0;
+  for (u32 g = 0; g < G; ++g) {
+    lists.keys[g] = (const u64*)d_runs[g];
+    lists.len[g] = run_len[g];
+    lists.off[g] = off;
+    off += run_len[g];
+  }
+  if (off == 0) return FPS_OK;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = (int)std::min<u64>((off + 255) / 256, (u64)sms * 8);
+  fps::merge_runs_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(lists, G, (u64*)d_out);
+  CUDA_TRY(cudaGetLastError());
+  return FPS_OK;
+}
+
 int fps_memory(const fps_lib* lib, uint64_t* library_bytes, uint64_t* derived_bytes, uint64_t* scratch_bytes,
                double* derived_build_ms) {
   if (int rc = check_lib(lib)) return rc;
@@ -2368,7 +2487,7 @@ int fps_memory(const fps_lib* lib, uint64_t* library_bytes, uint64_t* derived_by
   std::lock_guard<std::mutex> lk(L->mu);
   const u64 te = fps::tile_entries(L->compact);
   const u64 lib_b = L->n_alloc / te * fps::tile_bytes(L->compact);
-  const u64 der = L->pm.bytes + L->pm_perm.bytes + L->pm_meta.bytes + L->bs.bytes;
+  const u64 der = L->pm.bytes + L->pm_perm.bytes + L->pm_meta.bytes + L->bs.bytes + L->mq4x.bytes;
   u64 scr = 0;
   for (const DevBuf* b : {&L->tg, &L->ghist, &L->cand_cnt, &L->dyn, &L->buf, &L->cand, &L->queries, &L->keys, &L->cnt,
                           &L->radius, &L->rkeys, &L->rcount, &L->sort_tmp, &L->sort_out, &L->seg, &L->bsq, &L->mq,
@@ -2397,14 +2516,17 @@ int fps_release_derived(fps_lib* lib) {
   lib->pm_perm.release();
   lib->pm_meta.release();
   lib->bs.release();
+  lib->mq4x.release();
   if (lib->pm_state > 0) lib->pm_state = 0;
   if (lib->bs_state > 0) lib->bs_state = 0;
+  if (lib->mq4x_state > 0) lib->mq4x_state = 0;
   return FPS_OK;
 }
 
 uint64_t fps_launch_count(const fps_lib* lib) { return lib ? lib->launches.load() : 0; }
 
 int fps_last_kernel(const fps_lib* lib) { return lib ? lib->last_kernel : 0; }
+int fps_last_mma_kind(const fps_lib* lib) { return lib ? lib->last_mma_kind : 0; }
 
 int fps_timing(fps_lib* lib, int enable) {
   if (int rc = check_lib(lib)) return rc;

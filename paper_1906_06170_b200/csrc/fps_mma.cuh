@@ -177,6 +177,13 @@ __device__ __forceinline__ void mm_bar_init(u64* bar, u32 count) {
 __device__ __forceinline__ void mm_bar_arrive(u64* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// One arrival per warp (after every lane's prior accesses): per-thread
+// arrivals on one mbarrier serialise (512 epilogue arrivals per tile cost
+// more than the MMA of a small tile).
+__device__ __forceinline__ void mm_bar_arrive_warp(u64* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mm_bar_arrive(bar);
+}
 __device__ __forceinline__ void mm_bar_wait_ns(u64* bar, u32 parity, u32 ns) {
   asm volatile(
       "{\n .reg .pred p;\n MMWN: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra MMWN;\n}\n" ::"r"(
@@ -278,16 +285,16 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   if (tid < 16) lut[tid] = (tid & 1) | ((tid >> 1) & 1) << 8 | ((tid >> 2) & 1) << 16 | ((tid >> 3) & 1) << 24;
   if (tid == 0) {
     for (int s = 0; s < MM_STAGES; ++s) {
-      mm_bar_init(&full_bar[s], 128);
+      mm_bar_init(&full_bar[s], 4);  // one arrival per producer warp
       mm_bar_init(&empty_bar[s], 1);
     }
     for (int r = 0; r < MM_RAW; ++r) {
       mm_bar_init(&raw_full[r], 1);
-      mm_bar_init(&raw_empty[r], 128);
+      mm_bar_init(&raw_empty[r], 4);
     }
     for (int b = 0; b < NACC; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], MM_EPI * 32);  // every epilogue warp reads every tile
+      mm_bar_init(&tempty[b], MM_EPI);  // every epilogue warp reads every tile (one arrival each)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
           w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
         }
       }
-      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
+      if (sub == SUB - 1) mm_bar_arrive_warp(&raw_empty[rs]);
       if (it >= MM_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM_A_BYTES;
 #pragma unroll
@@ -348,7 +355,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mm_bar_arrive(&full_bar[s]);
+      mm_bar_arrive_warp(&full_bar[s]);
     }
   } else if (warp == 5 + MM_EPI) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mm_bar_arrive(&tempty[b]);
+      mm_bar_arrive_warp(&tempty[b]);
       if (a.flags & 4096) continue;
       u32 t = r[0];
 #pragma unroll

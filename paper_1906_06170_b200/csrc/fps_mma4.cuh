@@ -187,21 +187,24 @@ __device__ __forceinline__ void mm4_test(const MmArgs& a, const u32* r, int cb0,
   for (int i = 1; i < CNT; ++i) t &= r[i];
   const bool any = (t & 0x80000000u) == 0 && e < a.n;
   if (!__any_sync(0xffffffffu, any) || !any) return;
-  u64 hm = 0;
-#pragma unroll
-  for (int i = 0; i < CNT; ++i) hm |= (u64)((~r[i]) >> 31) << i;
   const u64 idx = a.index_base + e;
-  while (hm) {
-    const int c = cb0 + __ffsll((long long)hm) - 1;
-    hm &= hm - 1;
-    if (a.mode == 0) {
-      // the CTA's private list of this column: a shared-memory counter and a
-      // store nothing waits on; published at the end
-      const u32 pos = atomicAdd(s_pcnt + c, 1u);
-      if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
-    } else {
-      const u64 pos = atomicAdd(a.out_cnt, 1ull);
-      if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
+#pragma unroll
+  for (int g0 = 0; g0 < CNT; g0 += 64) {  // passing columns as 64-bit masks
+    u64 hm = 0;
+#pragma unroll
+    for (int i = g0; i < (g0 + 64 < CNT ? g0 + 64 : CNT); ++i) hm |= (u64)((~r[i]) >> 31) << (i - g0);
+    while (hm) {
+      const int c = cb0 + g0 + __ffsll((long long)hm) - 1;
+      hm &= hm - 1;
+      if (a.mode == 0) {
+        // the CTA's private list of this column: a shared-memory counter and a
+        // store nothing waits on; published at the end
+        const u32 pos = atomicAdd(s_pcnt + c, 1u);
+        if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
+      } else {
+        const u64 pos = atomicAdd(a.out_cnt, 1ull);
+        if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
+      }
     }
   }
 }
@@ -225,7 +228,7 @@ __device__ __forceinline__ void mm4_tile(const MmArgs& a, u32 taddr, int cb0, u6
   mm4_issue<CNT>(taddr, r);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  mm_bar_arrive(tempty_bar);
+  mm_bar_arrive_warp(tempty_bar);
   if (a.flags & 4096) return;
   mm4_test<CNT, N>(a, r, cb0, e, s_pcnt, s_qcol);
 }
@@ -276,16 +279,16 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
   }
   if (tid == 0) {
     for (int s = 0; s < MM4_STAGES; ++s) {
-      mm_bar_init(&full_bar[s], 128);
+      mm_bar_init(&full_bar[s], 4);  // one arrival per producer warp
       mm_bar_init(&empty_bar[s], 1);
     }
     for (int r = 0; r < MM_RAW; ++r) {
       mm_bar_init(&raw_full[r], 1);
-      mm_bar_init(&raw_empty[r], 128);
+      mm_bar_init(&raw_empty[r], 4);
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], MM_EPI * 32);  // every epilogue warp reads every tile
+      mm_bar_init(&tempty[b], MM_EPI);  // every epilogue warp reads every tile (one arrival each)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
           w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
         }
       }
-      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
+      if (sub == SUB - 1) mm_bar_arrive_warp(&raw_empty[rs]);
       const u32 pa = (u32)(__popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]));
       if (it >= MM4_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM4_STAGES) - 1) & 1u);
       if (tid == 0) MM4_TRACE(4);
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       const uint2 ta = luta[pa < 176 ? pa : 175];
       if (a.flags & 65536) {  // experiment: no expansion (stage left as is)
         if (!(a.flags & 32768)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mm_bar_arrive(&full_bar[s]);
+        mm_bar_arrive_warp(&full_bar[s]);
         continue;
       }
 #pragma unroll
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
         *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = make_uint4(o[0], o[1], o[2], o[3]);
       }
       if (!(a.flags & 32768)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mm_bar_arrive(&full_bar[s]);
+      mm_bar_arrive_warp(&full_bar[s]);
       if (tid == 0) MM4_TRACE(5);
     }
   } else if (warp == 5 + MM_EPI) {

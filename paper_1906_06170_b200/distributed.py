@@ -10,7 +10,8 @@ NCCL (NVLink on a B200 box) and merged there by the device merge kernel.
 The top-k of a union equals the top-k of per-shard top-ks under a total
 order, and shards are disjoint, so the merge is exact and associative.
 Range hits are variable-sized: counts are all-gathered first, then padded
-buffers gathered and the union re-sorted on rank 0.
+buffers gathered and the per-rank sorted runs merged by rank on rank 0
+(``fps_merge_runs_async``; no re-sort of the union).
 
 The collective plumbing is backend-agnostic (NCCL on GPUs, gloo in the CPU
 tests); the merge / sort step is injected so the CPU tests can check the
@@ -27,7 +28,7 @@ import torch.distributed as dist
 from .libstore import split_sizes
 
 MergeFn = Callable[[torch.Tensor, torch.Tensor, int], tuple[torch.Tensor, torch.Tensor]]
-SortFn = Callable[[torch.Tensor], torch.Tensor]
+MergeRunsFn = Callable[[list[torch.Tensor]], torch.Tensor]
 
 
 def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
@@ -60,9 +61,9 @@ def gather_topk(keys: torch.Tensor, cnt: torch.Tensor, k: int, merge: MergeFn, g
     return None
 
 
-def gather_range(keys: torch.Tensor, sort: SortFn, group=None, dst: int = 0) -> torch.Tensor | None:
-    """Gather variable-length sorted range-key vectors to ``dst``, re-sort the
-    union there ((q, d, idx) order). Returns the merged keys on dst."""
+def gather_range(keys: torch.Tensor, merge_runs: MergeRunsFn, group=None, dst: int = 0) -> torch.Tensor | None:
+    """Gather every rank's sorted range-key run ((q, d, idx) order) to
+    ``dst`` and merge the runs there. Returns the merged keys on dst."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     keys = keys.contiguous()
@@ -78,8 +79,7 @@ def gather_range(keys: torch.Tensor, sort: SortFn, group=None, dst: int = 0) -> 
     if rank == dst:
         bufs = [torch.empty_like(padded) for _ in range(world)]
         dist.gather(padded, bufs, dst=dst, group=group)
-        parts = [b[:s] for b, s in zip(bufs, sizes)]
-        return sort(torch.cat(parts))
+        return merge_runs([b[:s] for b, s in zip(bufs, sizes)])
     dist.gather(padded, None, dst=dst, group=group)
     return None
 
@@ -95,13 +95,21 @@ def device_merge(in_keys: torch.Tensor, in_cnt: torch.Tensor, k: int) -> tuple[t
     return out_keys, out_cnt
 
 
-def device_sort(keys: torch.Tensor) -> torch.Tensor:
-    """Radix sort of range keys on the device (libfpsgpu, CUB)."""
+def device_merge_runs(runs: list[torch.Tensor]) -> torch.Tensor:
+    """Merge sorted runs of unique range keys by rank on the device (rank 0)."""
+    import ctypes as C
+
     from . import _native as N
 
-    out = keys.clone()
-    N.check(N.load().fps_sort_keys(None, out.data_ptr(), out.numel(),
-                                   torch.cuda.current_stream(keys.device).cuda_stream), "fps_sort_keys")
+    dev = runs[0].device
+    total = sum(r.numel() for r in runs)
+    out = torch.empty((total,), dtype=torch.int64, device=dev)
+    if total == 0:
+        return out
+    ptrs = (C.c_void_p * len(runs))(*[r.data_ptr() for r in runs])
+    lens = (C.c_uint64 * len(runs))(*[r.numel() for r in runs])
+    N.check(N.load().fps_merge_runs_async(ptrs, lens, len(runs), out.data_ptr(),
+                                          torch.cuda.current_stream(dev).cuda_stream), "fps_merge_runs_async")
     return out
 
 

@@ -247,6 +247,13 @@ class Library:
     def last_kernel(self) -> str:
         return self.KERNELS.get(int(N.load().fps_last_kernel(self._h)), "unknown")
 
+    MMA_KINDS = {0: None, 1: "i8", 2: "fp4", 3: "fp4x"}
+
+    @property
+    def last_mma_kind(self) -> str | None:
+        """Operand kind of the last tensor-core scan: "i8", "fp4" or "fp4x"."""
+        return self.MMA_KINDS.get(int(N.load().fps_last_mma_kind(self._h)))
+
     @property
     def launches(self) -> int:
         return int(N.load().fps_launch_count(self._h))
@@ -479,6 +486,10 @@ class LibraryGroup:
     @property
     def last_kernel(self) -> str:
         return self.shards[0].last_kernel
+
+    @property
+    def last_mma_kind(self) -> str | None:
+        return self.shards[0].last_mma_kind
 
     @property
     def launches(self) -> int:

@@ -56,6 +56,13 @@ def _host_merge(in_keys, in_cnt, k):
     return out, outc
 
 
+def _host_merge_runs(runs):
+    """Host stand-in for fps_merge_runs_async: every run arrives sorted."""
+    for r in runs:
+        assert bool(torch.all(r[1:] > r[:-1])) if r.numel() > 1 else True
+    return torch.sort(torch.cat(runs)).values
+
+
 def _worker(rank, world, port, n, k, result_path):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -79,7 +86,7 @@ def _worker(rank, world, port, n, k, result_path):
 
         rr = orc.c_range(w[start:start + count], q, 25, threads=2)
         rkeys = torch.from_numpy(((rr[:, 0] << 48) | (rr[:, 2] << 40) | (rr[:, 1] + start)).astype(np.int64))
-        rmerged = D.gather_range(rkeys, lambda t: torch.sort(t).values)
+        rmerged = D.gather_range(rkeys, _host_merge_runs)
         if rank == 0:
             ei, ed, ec = orc.c_topk(w, q, k, threads=2)
             ek, ecn = _encode(ei, ed, ec, k)

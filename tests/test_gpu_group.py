@@ -319,3 +319,23 @@ def test_memory_report_and_release(mid):
     assert lib.memory()["derived_bytes"] == 0
     assert lib.search(q[0], 10) == oracle_lists(w, q[:1], 10)[0]  # rebuilt on demand
     lib.close()
+
+
+def test_merge_runs_async_equals_sorted_union():
+    """fps_merge_runs_async (the torchrun range gather's rank-0 merge):
+    G sorted runs of unique keys, some empty, merged by rank on the device."""
+    import torch
+
+    from paper_1906_06170_b200 import distributed as D
+
+    rng = np.random.default_rng(11)
+    for G in (1, 2, 3, 8, 32):
+        pool = rng.choice(1 << 50, size=G * 700, replace=False).astype(np.int64)
+        cuts = np.sort(rng.integers(0, len(pool), G - 1))
+        runs_h = [np.sort(p) for p in np.split(pool, cuts)]
+        if G > 2:
+            runs_h[1] = runs_h[1][:0]  # an empty run
+        runs = [torch.from_numpy(r.copy()).cuda() for r in runs_h]
+        got = D.device_merge_runs(runs)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), np.sort(np.concatenate(runs_h)))

@@ -122,9 +122,13 @@ def test_range_matches_reference_golden(golden):
     assert np.array_equal(r.rows(), np.array(case["rows"], dtype=np.int64).reshape(-1, 3))
 
 
-def test_tensor_core_per_query_matches_reference_golden(golden):
-    """256 queries take the tcgen05 int8 kernel by default; pinned directly to
-    the reference's own search() outputs (make_golden.py per_query_tc)."""
+@pytest.mark.parametrize("kind", [None, "i8", "fp4"])
+def test_tensor_core_per_query_matches_reference_golden(golden, kind, monkeypatch):
+    """256 queries take the tcgen05 kernel by default (fp4 operand copy; also
+    the int8 and in-kernel fp4 kinds); pinned directly to the reference's own
+    search() outputs (make_golden.py per_query_tc)."""
+    if kind:
+        monkeypatch.setenv("FPS_MMA_KIND", kind)
     case = golden["per_query_tc"]
     plan = synth.make_plan("c4", seed=case["seed"], n=case["n"], Q=case["Q"])
     lib, q = synth.build_library(plan)
@@ -132,11 +136,15 @@ def test_tensor_core_per_query_matches_reference_golden(golden):
     assert q.tolist() == case["queries"]
     res = lib.search_batch(q, case["k"])
     assert lib.last_kernel == "tensor-core multi-query scan"
+    assert lib.last_mma_kind == (kind or "fp4x")
     for qi, hits in enumerate(case["hits"]):
         assert res.hits(qi) == [(c - 1, d) for c, d in hits], qi
 
 
-def test_tensor_core_range_matches_reference_golden(golden):
+@pytest.mark.parametrize("kind", [None, "i8"])
+def test_tensor_core_range_matches_reference_golden(golden, kind, monkeypatch):
+    if kind:
+        monkeypatch.setenv("FPS_MMA_KIND", kind)
     case = golden["range_tc"]
     plan = synth.make_plan("c5", seed=case["seed"], n=case["n"], Q=case["Q"],
                            planted_per_query=case["planted_per_query"])
@@ -659,12 +667,18 @@ def test_sorted_plane_scan_config_shapes(monkeypatch):
 
 
 # ---------------------------------------------------------------- tensor-core multi-query path
+MMA_KINDS = ["fp4x", "i8", "fp4"]
+
+
+@pytest.mark.parametrize("kind", MMA_KINDS)
 @pytest.mark.parametrize("n", [1, 127, 128, 129, 70_001, 300_007])
-def test_mma_multi_query_vs_oracle(n, monkeypatch):
-    """tcgen05 int8 MMA path (FPS_MMA=1): every pair within the seeded bound
-    collected, select keeps the k smallest (distance, index); chunks of 256
-    queries, columns ordered by bound, tails of 128-entry tiles."""
+def test_mma_multi_query_vs_oracle(n, kind, monkeypatch):
+    """tcgen05 MMA path (FPS_MMA=1), every operand kind (fp4 from the operand
+    copy, int8 and fp4 expanded in the kernel): every pair within the seeded
+    bound collected, select keeps the k smallest (distance, index); several
+    query chunks, columns ordered by bound, tails of 128-entry tiles."""
     monkeypatch.setenv("FPS_MMA", "1")
+    monkeypatch.setenv("FPS_MMA_KIND", kind)
     seed = 600 + n
     w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
     lib = Library.from_words(w)
@@ -678,6 +692,8 @@ def test_mma_multi_query_vs_oracle(n, monkeypatch):
             exp = oracle_topk(w, q, k)
             for i in range(Q):
                 assert res.hits(i) == exp[i], (n, Q, k, i)
+            if n >= 128:
+                assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == kind
 
 
 def test_mma_candidate_overflow_falls_back(monkeypatch):
@@ -715,12 +731,14 @@ def test_mma_pad_bits_counted():
         assert res.hits(i) == exp[i]
 
 
+@pytest.mark.parametrize("kind", MMA_KINDS)
 @pytest.mark.parametrize("n", [127, 129, 70_001, 300_007])
-def test_mma_range_vs_oracle(n, monkeypatch):
+def test_mma_range_vs_oracle(n, kind, monkeypatch):
     """Range search on the tensor cores (FPS_MMA=1): the radius is the bound,
     every pair with d <= r is emitted; 64 / 128 / 256-column accumulators,
-    several chunks, tails of library tiles, a dense query."""
+    several chunks, tails of library tiles, a dense query; every operand kind."""
     monkeypatch.setenv("FPS_MMA", "1")
+    monkeypatch.setenv("FPS_MMA_KIND", kind)
     seed = 700 + n
     w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
     lib = Library.from_words(w)
