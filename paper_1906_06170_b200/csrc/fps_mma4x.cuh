@@ -290,8 +290,13 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
       for (u64 it = 0; it < ntile; ++it) {
         const int s = (int)(it % MM4X_STAGES), b = (int)(it & 1);
         MM4_TRACE(0);
-        if (it >= 2) mm_bar_wait_spin(&tempty[b], (u32)((it >> 1) - 1) & 1u);
-        mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u);
+        if (a.flags & (1u << 27)) {  // experiment: suspend-hint waits on the MMA lane
+          if (it >= 2) mm_bar_wait_ns(&tempty[b], (u32)((it >> 1) - 1) & 1u, 20000u);
+          mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u, 20000u);
+        } else {
+          if (it >= 2) mm_bar_wait_spin(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+          mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u);
+        }
         MM4_TRACE(1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u64 das = da0 + (u64)s * DA_S;
