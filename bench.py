@@ -678,8 +678,12 @@ def run_ours(args, rank: int, local_rank: int, world: int):
                     "traffic": traffic_for(args.workload),
                     "peak_source": f"{sm} SMs x 16 POPC/clk/SM (measured) / {per_cmp:.0f} POPC per comparison x "
                                    f"{mhz:.0f} MHz (median SM clock in the timed region)"}
+        # bytes the scan streams from HBM per launch: the fp4 operand copy
+        # (96 B/entry, read once per pass; the query chunks share it in L2),
+        # else the tiled library / bit-plane copy
+        src_bpe = 96.0 if (kernel == "tensor-core multi-query scan" and lib.last_mma_kind == "fp4x") else float(bpe)
         roof.update({"naive_6popc_peak": naive, "naive_6popc_frac": achieved / naive,
-                     "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": float(bpe) * shard_n,
+                     "scan_kernel_ms": scan_avg_ms, "hbm_bytes_per_launch": src_bpe * shard_n,
                      "kernel": kernel})
 
     n_total = float(plan.n)
