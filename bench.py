@@ -381,11 +381,18 @@ def run_ours(args, rank: int, local_rank: int, world: int):
 
     visible = torch.cuda.device_count()
     group_devs = None  # single process driving args.gpus GPUs
+    # test-only plumbing check (tests/test_gpu_torchrun.py): several ranks may
+    # share the visible GPUs, with the gloo backend (no cross-rank GPU waits)
+    share = os.environ.get("FPS_BENCH_SHARE_GPU") == "1"
+    backend = os.environ.get("FPS_BENCH_DIST_BACKEND", "nccl")
     if world > 1:
         if args.gpus != world:
             return fail(f"--gpus {args.gpus} but torchrun started {world} ranks")
-        if visible < world:
+        if visible < world and not share:
             return fail(f"{world} ranks but only {visible} visible GPU(s)")
+        if share and backend == "nccl":
+            return fail("FPS_BENCH_SHARE_GPU needs a non-NCCL backend (NCCL rejects ranks sharing a GPU)")
+        local_rank = local_rank % max(visible, 1)
     elif args.gpus > 1:
         if visible < args.gpus:
             return fail(f"--gpus {args.gpus} but only {visible} visible GPU(s)")
@@ -396,7 +403,10 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_stream(torch.cuda.Stream(dev))  # a real stream: kernels, events and copies share it
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     plan = synth.make_plan(args.workload, seed=args.seed)
     if args.k is not None:
         plan.k, plan.radius = args.k, None
@@ -495,7 +505,10 @@ def run_ours(args, rank: int, local_rank: int, world: int):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local_rank])
+            else:
+                dist.barrier()
 
     for _ in range(args.warmup):
         step()
@@ -535,7 +548,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     else:
         ev0 = ev0[:1]
         ev1 = ev1[:1]
-        pipelined = world > 1 and plan.radius is None
+        pipelined = world > 1 and plan.radius is None  # (this branch: shards larger than L2, no flush)
         ev0[0].record()
         for i in range(args.steps):
             step(pipelined) if pipelined else step()
@@ -688,7 +701,8 @@ def run_ours(args, rank: int, local_rank: int, world: int):
 
     n_total = float(plan.n)
     parallel = (f"{n_gpus} GPUs in one process (LibraryGroup, gather {lib.gather})" if group_devs else
-                f"{world} ranks (torchrun), NCCL gather to rank 0" if world > 1 else "1 GPU")
+                f"{world} ranks (torchrun), {backend} gather to rank 0"
+            + (" (test mode: ranks share the visible GPUs)" if share else "") if world > 1 else "1 GPU")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -696,9 +710,9 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         "config": plan.describe(),
         "method": {
             "parallelism": parallel,
-            "pipelining": ("torchrun: step i's NCCL gather + rank-0 merge overlap step i+1's scan (second stream, "
-                           "double-buffered results); all K steps' scans, gathers and merges are inside the timed "
-                           "region" if (world > 1 and plan.radius is None) else None),
+            "pipelining": (f"pipelined: step i's {backend} gather + rank-0 merge overlap step i+1's scan (second "
+                           "stream, double-buffered results); all K steps' scans, gathers and merges are inside the "
+                           "timed region" if (world > 1 and plan.radius is None and not flush) else None),
             "l2": "flushed between steps outside the timed events (2xL2 write, then 2xL2 read so no dirty "
                   "lines are left)" if flush else
                   "library larger than L2 and streamed with an L2 evict-first policy: no flush, the K steps "
@@ -736,10 +750,24 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         line["cpu_baseline"] = cpu_baseline(plan)
     elif rank == 0:
         line["cpu_baseline"] = None
-    # sanity: results are real (first query's best hit)
+    # sanity: results are real (first query's best hit; under torchrun the
+    # rank-0 merge of every rank's shard)
     if rank == 0 and plan.radius is None and world == 1:
         res = lib.search_batch(qhost[:1], plan.k)
         line["check"] = {"q0_best": list(res.hits(0)[:1][0]) if res.count[0] else None}
+    if world > 1 and plan.radius is None:
+        r = step()
+        if rank == 0:
+            kk, cc = r
+            kk, cc = kk.cpu().numpy().view(np.uint64), cc.cpu().numpy()
+            line["check"] = {"q0_best": [int(kk[0, 0] & np.uint64((1 << 40) - 1)), int(kk[0, 0] >> np.uint64(40))]
+                             if cc[0] else None}
+    elif world > 1:
+        r = step()
+        if rank == 0:
+            h = r.cpu().numpy().view(np.uint64)
+            line["check"] = {"range_hits": int(len(h)),
+                             "sorted": bool(np.all(h[1:] > h[:-1])) if len(h) > 1 else True}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -37,6 +37,12 @@ def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
     return sum(sizes[:rank]), sizes[rank]
 
 
+def _host_collective(t: torch.Tensor, group) -> bool:
+    """gloo gathers CPU tensors only: device tensors take a host round trip
+    (the CPU tests and the shared-GPU plumbing test; NCCL gathers in HBM)."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
 def gather_topk(keys: torch.Tensor, cnt: torch.Tensor, k: int, merge: MergeFn, group=None,
                 dst: int = 0) -> tuple[torch.Tensor, torch.Tensor] | None:
     """Gather every rank's (Q, k) sorted key lists and (Q,) counts to ``dst``
@@ -50,10 +56,13 @@ def gather_topk(keys: torch.Tensor, cnt: torch.Tensor, k: int, merge: MergeFn, g
     # one collective per call: keys and counts travel in a single int64 buffer
     Q = cnt.numel()
     packed = torch.cat([keys.reshape(-1).view(torch.int64), cnt.to(torch.int64)])
+    dev = packed.device
+    if _host_collective(packed, group):
+        packed = packed.cpu()
     if rank == dst:
         bufs = [torch.empty_like(packed) for _ in range(world)]
         dist.gather(packed, bufs, dst=dst, group=group)
-        allp = torch.stack(bufs)  # (G, Q*k + Q)
+        allp = torch.stack(bufs).to(dev)  # (G, Q*k + Q)
         kk = allp[:, :Q * k].reshape(world, *keys.shape).view(keys.dtype)
         cc = allp[:, Q * k:].to(cnt.dtype)
         return merge(kk.contiguous(), cc.contiguous(), k)
@@ -69,17 +78,20 @@ def gather_range(keys: torch.Tensor, merge_runs: MergeRunsFn, group=None, dst: i
     keys = keys.contiguous()
     if world == 1:
         return keys
-    n = torch.tensor([keys.numel()], dtype=torch.int64, device=keys.device)
+    dev = keys.device
+    host = _host_collective(keys, group)
+    cdev = torch.device("cpu") if host else dev
+    n = torch.tensor([keys.numel()], dtype=torch.int64, device=cdev)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
     sizes = [int(s.item()) for s in sizes]
     m = max(sizes)
-    padded = torch.full((max(m, 1),), -1, dtype=keys.dtype, device=keys.device)
-    padded[: keys.numel()] = keys
+    padded = torch.full((max(m, 1),), -1, dtype=keys.dtype, device=cdev)
+    padded[: keys.numel()] = keys.to(cdev)
     if rank == dst:
         bufs = [torch.empty_like(padded) for _ in range(world)]
         dist.gather(padded, bufs, dst=dst, group=group)
-        return merge_runs([b[:s] for b, s in zip(bufs, sizes)])
+        return merge_runs([b[:s].to(dev) for b, s in zip(bufs, sizes)])
     dist.gather(padded, None, dst=dst, group=group)
     return None
 
