@@ -171,8 +171,9 @@ def _acquire(manifest, devices: tuple[int, ...] | None) -> _Resident:
         else:
             lib = Library.from_fps1(paths, device=devices[0] if devices else None)
         cids = lib.cids
-        monotone = bool(np.all(cids[1:] > cids[:-1])) if len(cids) > 1 else True
-        res = _Resident(lib=lib, cids=cids, cid_monotone=monotone, offsets=offsets, users=1)
+        if len(cids) > 1 and not bool(np.all(cids[1:] >= cids[:-1])):
+            lib, cids = _cid_ordered(lib, paths, cids, devices)
+        res = _Resident(lib=lib, cids=cids, cid_monotone=True, offsets=offsets, users=1)
         _cache[key] = res
         while len(_cache) > _CACHE_MAX:  # bounded HBM use: evict the oldest library
             old = _cache.pop(next(iter(_cache)))
@@ -180,6 +181,27 @@ def _acquire(manifest, devices: tuple[int, ...] | None) -> _Resident:
             if old.users == 0:
                 _close(old)
         return res
+
+
+def _fps1_words(paths) -> np.ndarray:
+    """Every record's three fingerprint words, in shard order (bytes 8..31 of
+    each 32-byte FPS1 record, as scan.py:169 views them)."""
+    parts = [np.fromfile(p, dtype="<u8", offset=16).reshape(-1, 4)[:, 1:4] for p in paths]
+    return np.ascontiguousarray(np.concatenate(parts) if parts else np.empty((0, 3), np.uint64), dtype=np.uint64)
+
+
+def _cid_ordered(lib, paths, cids: np.ndarray, devices):
+    """The library re-uploaded in CID order (stable; equal CIDs stay adjacent).
+    Then (distance, index) order is (distance, cid) order, the reference's
+    total order (scan.py:55-56), and the plain top-k is exact under distance
+    ties for any CIDs — no range pass over the tied distance is needed."""
+    order = np.argsort(cids, kind="stable")
+    words = _fps1_words(paths)[order]
+    lib.close()
+    cids = np.ascontiguousarray(cids[order])
+    if devices is not None and len(devices) > 1:
+        return LibraryGroup.from_words(words, devices, check_padding=False, cids=cids), cids
+    return Library.from_words(words, device=devices[0] if devices else None, check_padding=False, cids=cids), cids
 
 
 def _release(res: _Resident) -> None:
@@ -218,24 +240,9 @@ def _topk_one(res: _Resident, q: np.ndarray, n: int, minq: bool) -> TopK:
         return TopK(capacity=n, hits=())
     idx = np.array([h[0] for h in hits], dtype=np.uint64)
     dist = np.array([h[1] for h in hits], dtype=np.int64)
-    if res.cid_monotone or len(hits) < n:
-        # (distance, index) order == (distance, cid) order when cids increase with
-        # index; with fewer than n hits every record is present anyway
-        return _hits_by_cid(res, idx, dist, n)
-    if minq:
-        # ties at the n-th distance need cid order: gather every record within it
-        radius = int(dist[-1])
-        rr = [lib.range_search(qq, radius) for qq in q]
-        all_idx = np.concatenate([r.index for r in rr])
-        all_d = np.concatenate([r.distance for r in rr]).astype(np.int64)
-        # min over queries per record
-        order = np.lexsort((all_d, all_idx))
-        all_idx, all_d = all_idx[order], all_d[order]
-        first = np.ones(len(all_idx), dtype=bool)
-        first[1:] = all_idx[1:] != all_idx[:-1]
-        return _hits_by_cid(res, all_idx[first], all_d[first], n)
-    rr = lib.range_search(q, int(dist[-1]))
-    return _hits_by_cid(res, rr.index, rr.distance.astype(np.int64), n)
+    # the resident library is in CID order (_cid_ordered): (distance, index)
+    # order is (distance, cid) order
+    return _hits_by_cid(res, idx, dist, n)
 
 
 def _search_multi(manifest, queries: np.ndarray, params: SearchParams, progress: SearchProgressFn | None,

@@ -178,6 +178,37 @@ def test_random_cid_library_matches_reference_golden(golden, tmp_path):
     assert [[h.cid, h.distance] for h in top.hits] == cb["hits"]
 
 
+def test_random_cids_heavy_ties_match_oracle(tmp_path):
+    """Arbitrary (non-monotone) CIDs with heavy distance ties: 40 % of the
+    records are copies of 40 hub fingerprints, so hundreds of records tie at
+    every distance near a hub. The resident library is uploaded in CID order,
+    so the plain top-k is exact in (distance, cid) order — checked against the
+    reference's search restated over the same FPS1 shards (scan.py:173-287),
+    for search and for batch_search (min over queries, scan.py:306-318)."""
+    from paper_1906_06170_b200 import libstore
+
+    rng = np.random.default_rng(77)
+    n = 120_000
+    w = orc.generate_words(synth.seed_key(77), synth.beta_thresholds(77), 0, n)
+    hubs = w[rng.integers(0, n, 40)].copy()
+    pick = rng.random(n) < 0.4
+    w[pick] = hubs[rng.integers(0, 40, int(pick.sum()))]
+    cids = rng.choice(1 << 62, size=n, replace=False).astype(np.uint64)
+    mpath = orc.write_fps1_library(tmp_path / "ties", w, 5, cids=cids)
+    manifest = libstore.load_manifest(mpath.parent)
+    queries = [hubs[0], hubs[7] ^ np.array([1 << 3, 0, 0], dtype=np.uint64), w[5]]
+    for q in queries:
+        for k in (1, 10, 100, 1000):
+            top = scan.search(manifest, tuple(int(x) for x in q), scan.SearchParams(n=k))
+            exp = orc.search_fps1(mpath, np.asarray(q, dtype=np.uint64), k)
+            assert [(h.cid, h.distance) for h in top.hits] == [(int(c), int(d)) for c, d in exp], k
+    qs = np.stack(queries[:2])
+    dmin = np.minimum(orc.distances_one(w, qs[0]), orc.distances_one(w, qs[1])).astype(np.int64)
+    order = np.lexsort((cids, dmin))[:50]
+    top = scan.batch_search(manifest, [tuple(int(x) for x in q) for q in qs], scan.SearchParams(n=50))
+    assert [(h.cid, h.distance) for h in top.hits] == [(int(cids[i]), int(dmin[i])) for i in order]
+
+
 # ---------------------------------------------------------------- oracle sweeps
 @pytest.mark.parametrize("n", [1, 5, 31, 127, 128, 129, 1000, 4097, 65_537, 300_001])
 def test_topk_tail_sizes(n):
