@@ -966,18 +966,20 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   return true;
 }
 
-// Operand kind of the tensor-core scan (FPS_MMA_KIND): "fp4x" (default) is
-// the block-scaled fp4 kernel fed from the library's fp4 operand copy
-// (fps_mma4x.cuh: no per-tile expansion, twice the MMA rate of int8);
-// "fp4" expands tiles on the fly (fps_mma4.cuh), "i8" is the int8 kernel
-// (fps_mma.cuh) -- also the fallback when the operand copy (96 B per entry)
-// does not fit in HBM.
+// Operand kind of the tensor-core scan (FPS_MMA_KIND): "i8" (default) is the
+// int8 kernel (fps_mma.cuh: tiles expanded to bytes in the kernel, 16-bit
+// packed accumulator reads; the C4 call 11.36 ms, its MMA at 0.82 of the
+// measured int8 rate); "fp4x" the block-scaled fp4 kernel fed from the
+// library's fp4 operand copy (fps_mma4x.cuh: the full pass is 1.4 % faster,
+// but hit-heavy prefix passes are slower and the copy costs 96 B/entry, so
+// the call is 11.45 ms); "fp4" expands fp4 tiles in the kernel
+// (fps_mma4.cuh). fp4x falls back to int8 when its copy does not fit.
 enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
 MmaKind mma_kind_env() {
   const char* e = std::getenv("FPS_MMA_KIND");
-  if (!e) return MMA_FP4X;
+  if (!e) return MMA_I8;
   const std::string v(e);
-  return v == "fp4" ? MMA_FP4 : v == "i8" ? MMA_I8 : MMA_FP4X;
+  return v == "fp4" ? MMA_FP4 : v == "fp4x" ? MMA_FP4X : MMA_I8;
 }
 bool mma_fp4() { return mma_kind_env() != MMA_I8; }
 

@@ -24,10 +24,10 @@
 // CTA = 22 warps, one CTA per SM: a loader warp streams library tiles into a
 // raw ring (cp.async.bulk); producer warps 0-3 expand them to the canonical
 // K-major int8 layout (a thread per entry row) in a 4-stage ring; one lane of
-// the MMA warp issues 6 x K=32 MMAs per tile into one of 512 / N TMEM
-// accumulators and commits them to mbarriers; 16 epilogue warps (4 lane
-// quadrants x 4 column quarters, every tile) read the accumulators with
-// tcgen05.ld .pack::16b and test the sign bits.
+// the MMA warp issues 6 x K=32 MMAs per tile into one of two TMEM
+// accumulators and commits them to mbarriers; 16 epilogue warps (two groups
+// on alternate tiles) read the accumulators with tcgen05.ld .pack::16b and
+// test 16 columns at a time (max first, exact check only when it can pass).
 #pragma once
 #include "fps_kernels.cuh"
 
@@ -177,9 +177,8 @@ __device__ __forceinline__ void mm_bar_init(u64* bar, u32 count) {
 __device__ __forceinline__ void mm_bar_arrive(u64* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// One arrival per warp (after every lane's prior accesses): per-thread
-// arrivals on one mbarrier serialise (512 epilogue arrivals per tile cost
-// more than the MMA of a small tile).
+// One arrival per warp (after every lane's prior accesses): the fp4 kernels'
+// epilogue warps release an accumulator with one arrival each.
 __device__ __forceinline__ void mm_bar_arrive_warp(u64* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mm_bar_arrive(bar);
@@ -245,15 +244,12 @@ template <int N>
 __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a) {
   static_assert(N == 64 || N == 128 || N == 256, "accumulator width");
   constexpr u32 B_BYTES = mm_b_bytes(N);
-  // accumulators: as many as 512 TMEM columns hold (8 / 4 / 2 for N = 64 /
-  // 128 / 256), so the MMA runs ahead of the epilogue's round trip
-  constexpr int NACC = 512 / N;
-  constexpr u32 TMEM_COLS = 512;
+  constexpr u32 TMEM_COLS = 2 * N;         // two accumulators (power of two >= 32)
   extern __shared__ __align__(1024) unsigned char msm[];
   unsigned char* sB = msm;
   unsigned char* sA = msm + B_BYTES;  // [MM_STAGES][24 KB]
   char* raw = reinterpret_cast<char*>(msm + B_BYTES + MM_STAGES * MM_A_BYTES);  // [MM_RAW][library tile]
-  __shared__ __align__(8) u64 full_bar[MM_STAGES], empty_bar[MM_STAGES], tfull[NACC], tempty[NACC];
+  __shared__ __align__(8) u64 full_bar[MM_STAGES], empty_bar[MM_STAGES], tfull[2], tempty[2];
   __shared__ __align__(8) u64 raw_full[MM_RAW], raw_empty[MM_RAW];
   __shared__ u32 tmem_base;
   __shared__ u32 lut[16];
@@ -285,16 +281,16 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   if (tid < 16) lut[tid] = (tid & 1) | ((tid >> 1) & 1) << 8 | ((tid >> 2) & 1) << 16 | ((tid >> 3) & 1) << 24;
   if (tid == 0) {
     for (int s = 0; s < MM_STAGES; ++s) {
-      mm_bar_init(&full_bar[s], 4);  // one arrival per producer warp
+      mm_bar_init(&full_bar[s], 128);
       mm_bar_init(&empty_bar[s], 1);
     }
     for (int r = 0; r < MM_RAW; ++r) {
       mm_bar_init(&raw_full[r], 1);
-      mm_bar_init(&raw_empty[r], 4);
+      mm_bar_init(&raw_empty[r], 128);
     }
-    for (int b = 0; b < NACC; ++b) {
+    for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], MM_EPI);  // every epilogue warp reads every tile (one arrival each)
+      mm_bar_init(&tempty[b], MM_EPI / 2 * 32);  // one epilogue group per accumulator
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -335,7 +331,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
           w[2] = reinterpret_cast<const u64*>(tb + 16 * TILE_FULL)[e];
         }
       }
-      if (sub == SUB - 1) mm_bar_arrive_warp(&raw_empty[rs]);
+      if (sub == SUB - 1) mm_bar_arrive(&raw_empty[rs]);
       if (it >= MM_STAGES) mm_bar_wait(&empty_bar[s], (u32)((it / MM_STAGES) - 1) & 1u);
       unsigned char* A = sA + s * MM_A_BYTES;
 #pragma unroll
@@ -355,7 +351,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         *reinterpret_cast<uint4*>(A + mm_canon(row, 16 * c, MM_M)) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mm_bar_arrive_warp(&full_bar[s]);
+      mm_bar_arrive(&full_bar[s]);
     }
   } else if (warp == 5 + MM_EPI) {
     // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
@@ -376,65 +372,77 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
     }
     __syncwarp();
   } else if (warp < 4 + MM_EPI) {
-    // ===== epilogue: 16 warps on every tile; warp e reads TMEM lane quadrant
-    // e % 4 (its warp id mod 4) and column quarter e / 4 (N / 4 columns).
-    // The accumulators D = T - d fit 16 bits, so tcgen05.ld .pack::16b brings
-    // two columns per register (2 B per pair: the TMEM read bandwidth, not the
-    // MMA, bounds this kernel at large N -- profiles/r02_summary.md). One load
-    // wait per tile, then the accumulator is released and the registers
-    // tested: a column passes iff its sign bit is clear (the AND of all
-    // halves first; the per-column extraction only for lanes with a hit).
-    const u32 ew = (u32)(warp - 4);
-    const u32 quad = ew % 4, qt = ew / 4;
+    // ===== epilogue: two groups of 8 warps take alternate tiles (group g
+    // always reads accumulator g), so a group has two MMA tiles of time for
+    // its loads and tests and the accumulator it holds is released as soon as
+    // its loads land. Warp (quad, half) of a group reads TMEM lane quadrant
+    // quad (rows 32 quad .. + 31), columns [half * N / 2, (half + 1) * N / 2),
+    // in rounds of <= 64 columns. The accumulators D = T - d fit 16 bits, so
+    // tcgen05.ld .pack::16b brings two columns per register. Common path: the
+    // AND of a round's registers (a column passes iff its sign bit is clear);
+    // the per-column extraction runs only for lanes that hold a passing pair.
+    const u32 grp = (u32)(warp - 4) / 8;
+    const u32 wq = (u32)(warp - 4) % 8;
+    const u32 quad = wq % 4, half = wq / 4;
     const u32 row = quad * 32 + lane;
-    constexpr int QC = N / 4;   // columns per warp
-    constexpr int RR = QC / 2;  // packed registers
-    for (u64 it = 0; it < ntile; ++it) {
-      const int b = (int)(it % NACC);
+    constexpr int NC = N / 2;                  // columns per warp
+    constexpr int RC = NC < 64 ? NC : 64;      // columns per round
+    constexpr int NRND = NC / RC;
+    constexpr int RR = RC / 2;                 // packed registers per round
+    for (u64 it = grp; it < ntile; it += 2) {
+      const int b = (int)grp;
       const u64 e = (t0 + it) * MM_M + row;
-      mm_bar_wait(&tfull[b], (u32)(it / NACC) & 1u);
+      mm_bar_wait(&tfull[b], (u32)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + qt * QC;
-      u32 r[RR];
-      if constexpr (QC == 16) {
-        mm_ld16p(taddr, *reinterpret_cast<u32(*)[8]>(r));
-      } else {
-#pragma unroll
-        for (int g = 0; g < QC / 32; ++g) mm_ld32p(taddr + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
-      }
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mm_bar_arrive_warp(&tempty[b]);
-      if (a.flags & 4096) continue;
-      u32 t = r[0];
-#pragma unroll
-      for (int i = 1; i < RR; ++i) t &= r[i];
-      bool any = (t & 0x80008000u) != 0x80008000u && e < a.n;
-      if (a.flags & 16384) any = false;  // experiment: no hits (timing only)
-      if (!__any_sync(0xffffffffu, any)) continue;
-      if (!any) continue;
-      const int cb0 = (int)(qt * QC);
-      // passing columns as a bit mask, then a compact loop (the hit path stays
-      // small for the instruction cache). Keys carry the index only;
-      // mm_fix_kernel computes the distances of the (few) collected pairs.
-      u64 hm = 0;
-#pragma unroll
-      for (int i = 0; i < RR; ++i) {
-        const u32 nn = ~r[i];
-        hm |= ((u64)((nn >> 15) & 1u) << (2 * i)) | ((u64)(nn >> 31) << (2 * i + 1));
-      }
-      const u64 idx = a.index_base + e;
-      while (hm) {
-        const int c = cb0 + __ffsll((long long)hm) - 1;
-        hm &= hm - 1;
-        if (a.mode == 0) {
-          // the CTA's private list of this column: a shared-memory counter,
-          // a store that nothing waits on; published at the end
-          const u32 pos = atomicAdd(s_pcnt + c, 1u);
-          if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
+      const u32 taddr = tmem + (quad * 32u << 16) + (u32)b * N + half * NC;
+#pragma unroll 1
+      for (int rnd = 0; rnd < NRND; ++rnd) {
+        u32 r[RR];
+        if constexpr (RR == 16) {
+          mm_ld32p(taddr + RC * rnd, r);
         } else {
-          const u64 pos = atomicAdd(a.out_cnt, 1ull);
-          if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
+#pragma unroll
+          for (int g = 0; g < RR / 16; ++g) mm_ld32p(taddr + RC * rnd + 32 * g, *reinterpret_cast<u32(*)[16]>(r + 16 * g));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (rnd == NRND - 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          mm_bar_arrive(&tempty[b]);
+        }
+        if (a.flags & 4096) continue;
+        // D = T - d per column (s16 halves): some column passes iff a sign
+        // bit of the AND of all halves is clear
+        u32 t = r[0];
+#pragma unroll
+        for (int i = 1; i < RR; ++i) t &= r[i];
+        bool any = (t & 0x80008000u) != 0x80008000u && e < a.n;
+        if (a.flags & 16384) any = false;  // experiment: no hits (timing only)
+        if (!__any_sync(0xffffffffu, any)) continue;
+        if (!any) continue;
+        const int cb0 = (int)half * NC + RC * rnd;
+        // passing columns as a bit mask (straight-line), then a compact loop:
+        // the hit path stays small (instruction cache) and needs no register
+        // indexing. Keys carry the index only; mm_fix_kernel computes the
+        // distances of the (few) collected pairs from the library words.
+        u64 hm = 0;
+#pragma unroll
+        for (int i = 0; i < RR; ++i) {
+          const u32 nn = ~r[i];
+          hm |= ((u64)((nn >> 15) & 1u) << (2 * i)) | ((u64)(nn >> 31) << (2 * i + 1));
+        }
+        const u64 idx = a.index_base + e;
+        while (hm) {
+          const int c = cb0 + __ffsll((long long)hm) - 1;
+          hm &= hm - 1;
+          if (a.mode == 0) {
+            // the CTA's private list of this column: a shared-memory counter,
+            // a store that nothing waits on; published at the end
+            const u32 pos = atomicAdd(s_pcnt + c, 1u);
+            if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
+          } else {
+            const u64 pos = atomicAdd(a.out_cnt, 1ull);
+            if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
+          }
         }
       }
     }
@@ -450,8 +458,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
       constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM_A_BYTES / 16;
       for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM_STAGES), b = (int)(it % NACC);
-        if (it >= (u64)NACC) mm_bar_wait(&tempty[b], (u32)((it / NACC) - 1) & 1u);
+        const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
+        if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
         mm_bar_wait(&full_bar[s], (u32)(it / MM_STAGES) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u64 das = da0 + (u64)s * DA_S;

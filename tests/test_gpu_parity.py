@@ -122,11 +122,11 @@ def test_range_matches_reference_golden(golden):
     assert np.array_equal(r.rows(), np.array(case["rows"], dtype=np.int64).reshape(-1, 3))
 
 
-@pytest.mark.parametrize("kind", [None, "i8", "fp4"])
+@pytest.mark.parametrize("kind", [None, "fp4x", "fp4"])
 def test_tensor_core_per_query_matches_reference_golden(golden, kind, monkeypatch):
-    """256 queries take the tcgen05 kernel by default (fp4 operand copy; also
-    the int8 and in-kernel fp4 kinds); pinned directly to the reference's own
-    search() outputs (make_golden.py per_query_tc)."""
+    """256 queries take the tcgen05 kernel by default (int8; also the fp4
+    kinds: from the operand copy and expanded in the kernel); pinned directly
+    to the reference's own search() outputs (make_golden.py per_query_tc)."""
     if kind:
         monkeypatch.setenv("FPS_MMA_KIND", kind)
     case = golden["per_query_tc"]
@@ -136,12 +136,12 @@ def test_tensor_core_per_query_matches_reference_golden(golden, kind, monkeypatc
     assert q.tolist() == case["queries"]
     res = lib.search_batch(q, case["k"])
     assert lib.last_kernel == "tensor-core multi-query scan"
-    assert lib.last_mma_kind == (kind or "fp4x")
+    assert lib.last_mma_kind == (kind or "i8")
     for qi, hits in enumerate(case["hits"]):
         assert res.hits(qi) == [(c - 1, d) for c, d in hits], qi
 
 
-@pytest.mark.parametrize("kind", [None, "i8"])
+@pytest.mark.parametrize("kind", [None, "fp4x"])
 def test_tensor_core_range_matches_reference_golden(golden, kind, monkeypatch):
     if kind:
         monkeypatch.setenv("FPS_MMA_KIND", kind)
