@@ -5,7 +5,7 @@
 // fps_mma4.cuh expands every library tile to e2m1 operands on the fly: four
 // producer warps spend ~260 issue slots per 128-entry tile, once per query
 // chunk, and the SM runs out of issue slots before the MMA does (ncu:
-// profiles/r02_ncu_c4_details.csv). Here the expansion happens once per
+// profiles/r02_ncu_c4_i8_16warp_variant_details.csv). Here the expansion happens once per
 // library: `mm4x_build_kernel` writes every 128-entry tile as the MMA's A
 // operand, already in the canonical K-major layout (12 KB per tile, 96 B per
 // entry: the 166 key bits as e2m1 1.0, then the |a|-dependent test digits of
