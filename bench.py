@@ -444,14 +444,16 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         keys = torch.empty((Q, k), dtype=torch.int64, device=dev)
         cnt = torch.empty((Q,), dtype=torch.int32, device=dev)
         if world > 1:
-            # consecutive steps pipeline as in a serving loop: step i's gather
-            # + rank-0 merge (NCCL, on a second stream) overlap step i + 1's
-            # scan; double-buffered per-rank results (a scan waits until the
-            # gather that last read its buffer is done). Every step's scan,
-            # gather and merge run inside the timed region.
+            # per-rank results land in packed blocks (keys, then counts) that
+            # go to the collective as they are; rank 0 gathers them into one
+            # (world, block) buffer and merges with one kernel. Consecutive
+            # steps pipeline as in a serving loop: step i's gather + merge (on
+            # a second stream) overlap step i + 1's scan, double-buffered (a
+            # scan waits until the gather that last read its block is done).
+            # Every step's scan, gather and merge run inside the timed region.
             comm = torch.cuda.Stream(dev)
-            pkeys = [keys, torch.empty_like(keys)]
-            pcnt = [cnt, torch.empty_like(cnt)]
+            blocks = [D.packed_block(Q, k, dev) for _ in range(2)]
+            gbufs = [None, None]
             gdone = [None, None]
             state["i"] = 0
 
@@ -459,20 +461,24 @@ def run_ours(args, rank: int, local_rank: int, world: int):
             if world == 1:
                 lib.topk_async(dq, Q, k, keys, cnt, stream)
                 return keys, cnt
+            blk, bk, bc = blocks[0]
             if not pipelined:
-                lib.topk_async(dq, Q, k, keys, cnt, stream)
-                return D.gather_topk(keys, cnt, k, D.device_merge)
+                lib.topk_async(dq, Q, k, bk, bc, stream)
+                return D.gather_topk_packed(blk, Q, k)
             j = state["i"] % 2
             state["i"] += 1
+            blk, bk, bc = blocks[j]
             cur = torch.cuda.current_stream(dev)
             if gdone[j] is not None:
                 cur.wait_event(gdone[j])
-            lib.topk_async(dq, Q, k, pkeys[j], pcnt[j], stream)
+            lib.topk_async(dq, Q, k, bk, bc, stream)
             scanned = torch.cuda.Event()
             scanned.record(cur)
             with torch.cuda.stream(comm):
                 comm.wait_event(scanned)
-                r = D.gather_topk(pkeys[j], pcnt[j], k, D.device_merge)
+                if gbufs[j] is None and rank == 0:
+                    gbufs[j] = torch.empty((world, blk.numel()), dtype=torch.int64, device=dev)
+                r = D.gather_topk_packed(blk, Q, k, gbuf=gbufs[j])
                 gdone[j] = torch.cuda.Event()
                 gdone[j].record(comm)
             return r

@@ -186,6 +186,14 @@ int fps_sort_keys(fps_lib* lib, uint64_t* d_keys, uint64_t n, void* stream);
  * d_in_keys G x Q x k (each row sorted, UINT64_MAX pads), d_in_cnt G x Q. */
 int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_t G, uint32_t Q, uint32_t k,
                     uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream);
+/* Rank-0 merge of G <= 32 per-rank top-k blocks gathered into one buffer
+ * (the torchrun gather of bench.py / distributed.gather_topk): block g starts
+ * at d_packed + g * row_bytes and holds Q x k sorted u64 keys followed by Q
+ * u32 counts -- the layout fps_topk_async writes when its key and count
+ * pointers are taken from one such block -- so no repacking precedes the
+ * merge (merge_topk, scan.py:225-236). */
+int fps_merge_packed_async(const void* d_packed, uint64_t row_bytes, uint32_t G, uint32_t Q, uint32_t k,
+                           uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream);
 /* Rank-0 merge of G <= 32 sorted runs of unique range keys (one per shard,
  * the torchrun gather of bench.py / distributed.gather_range): run g is
  * d_runs[g][0 .. run_len[g]) on the device, run_len is a host array; the

@@ -69,6 +69,7 @@ SIGNATURES = {
     "fps_sort_keys": (C.c_int, [_vp, _vp, C.c_uint64, _vp]),
     "fps_merge_async": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "fps_merge_runs_async": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _vp]),
+    "fps_merge_packed_async": (C.c_int, [_vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "fps_launch_count": (C.c_uint64, [_vp]),
     "fps_last_kernel": (C.c_int, [_vp]),
     "fps_last_mma_kind": (C.c_int, [_vp]),

@@ -2459,6 +2459,25 @@ int fps_merge_async(const uint64_t* d_in_keys, const uint32_t* d_in_cnt, uint32_
   return FPS_OK;
 }
 
+int fps_merge_packed_async(const void* d_packed, uint64_t row_bytes, uint32_t G, uint32_t Q, uint32_t k,
+                           uint64_t* d_out_keys, uint32_t* d_out_cnt, void* stream) {
+  if (G == 0 || G > (uint32_t)fps::GROUP_MAX || Q == 0 || k == 0 || !d_packed)
+    return fail(FPS_EINVAL, "1 <= G <= 32 blocks, Q, k >= 1 and a buffer are required");
+  if (row_bytes < (u64)Q * k * 8 + (u64)Q * 4 || row_bytes % 8)
+    return fail(FPS_EINVAL, "row_bytes must hold Q x k keys and Q counts (8-byte aligned)");
+  fps::ShardLists lists{};
+  for (u32 g = 0; g < G; ++g) {
+    const char* row = (const char*)d_packed + (u64)g * row_bytes;
+    lists.keys[g] = (const u64*)row;
+    lists.cnt[g] = (const u32*)(row + (u64)Q * k * 8);
+  }
+  const u64 total = (u64)G * Q * k + Q;
+  const int blocks = (int)std::min<u64>((total + 255) / 256, 4096);
+  fps::merge_lists_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(lists, G, Q, k, (u64*)d_out_keys, d_out_cnt);
+  CUDA_TRY(cudaGetLastError());
+  return FPS_OK;
+}
+
 int fps_merge_runs_async(const uint64_t* const* d_runs, const uint64_t* run_len, uint32_t G, uint64_t* d_out,
                          void* stream) {
   if (G == 0 || G > (uint32_t)fps::GROUP_MAX || !d_runs || !run_len)

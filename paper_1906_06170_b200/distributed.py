@@ -70,6 +70,44 @@ def gather_topk(keys: torch.Tensor, cnt: torch.Tensor, k: int, merge: MergeFn, g
     return None
 
 
+def packed_block(Q: int, k: int, device) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """One rank's result block for gather_topk_packed: Q x k keys then Q u32
+    counts in one int64 buffer; returns (block, keys view, counts view) --
+    the views are what fps_topk_async writes, so the block goes to the
+    collective as is (no repacking)."""
+    blk = torch.empty((Q * k + Q,), dtype=torch.int64, device=device)
+    return blk, blk[: Q * k].view(Q, k), blk[Q * k:].view(torch.int32)[:Q]
+
+
+def gather_topk_packed(block: torch.Tensor, Q: int, k: int, group=None, dst: int = 0,
+                       gbuf: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor] | None:
+    """Gather every rank's packed result block (packed_block) into one
+    (world, Q*k + Q) buffer on ``dst`` and merge it there with one kernel
+    (fps_merge_packed_async). Returns the merged (keys, counts) on dst."""
+    from . import _native as N
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = block.device
+    L = block.numel()
+    host = _host_collective(block, group)
+    src = block.cpu() if host else block
+    if rank != dst:
+        dist.gather(src, None, dst=dst, group=group)
+        return None
+    if gbuf is None or gbuf.shape != (world, L) or gbuf.device != src.device:
+        gbuf = torch.empty((world, L), dtype=torch.int64, device=src.device)
+    dist.gather(src, list(gbuf.unbind(0)), dst=dst, group=group)
+    if host:
+        gbuf = gbuf.to(dev)
+    out_keys = torch.empty((Q, k), dtype=torch.int64, device=dev)
+    out_cnt = torch.empty((Q,), dtype=torch.int32, device=dev)
+    N.check(N.load().fps_merge_packed_async(gbuf.data_ptr(), L * 8, world, Q, k, out_keys.data_ptr(),
+                                            out_cnt.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+            "fps_merge_packed_async")
+    return out_keys, out_cnt
+
+
 def gather_range(keys: torch.Tensor, merge_runs: MergeRunsFn, group=None, dst: int = 0) -> torch.Tensor | None:
     """Gather every rank's sorted range-key run ((q, d, idx) order) to
     ``dst`` and merge the runs there. Returns the merged keys on dst."""
@@ -137,8 +175,7 @@ class ShardedLibrary:
         """Local top-k on this GPU, gathered and merged on rank 0 (device tensors)."""
         Q = d_queries.shape[0]
         dev = d_queries.device
-        keys = torch.empty((Q, k), dtype=torch.int64, device=dev)
-        cnt = torch.empty((Q,), dtype=torch.int32, device=dev)
+        blk, keys, cnt = packed_block(Q, k, dev)
         s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
         self.local.topk_async(d_queries, Q, k, keys, cnt, s)
-        return gather_topk(keys, cnt, k, device_merge, self.group)
+        return gather_topk_packed(blk, Q, k, self.group)

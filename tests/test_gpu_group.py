@@ -339,3 +339,40 @@ def test_merge_runs_async_equals_sorted_union():
         got = D.device_merge_runs(runs)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), np.sort(np.concatenate(runs_h)))
+
+
+def test_merge_packed_async_equals_merge_topk():
+    """fps_merge_packed_async (the torchrun top-k gather's rank-0 merge): G
+    per-rank blocks of Q x k sorted keys + Q u32 counts in one buffer, merged
+    with one kernel; equals merge_topk over the rank lists (scan.py:225-236)."""
+    import torch
+
+    from paper_1906_06170_b200 import _native as N
+    from paper_1906_06170_b200 import distributed as D
+
+    rng = np.random.default_rng(5)
+    for G, Q, k in ((2, 1, 10), (3, 7, 100), (8, 33, 17), (32, 2, 5)):
+        pool = rng.choice(1 << 48, size=G * Q * k, replace=False).astype(np.int64).reshape(G, Q, k)
+        cnts = rng.integers(0, k + 1, size=(G, Q))
+        L = Q * k + Q
+        buf = np.zeros((G, L), dtype=np.int64)
+        for g in range(G):
+            keys = np.full((Q, k), -1, dtype=np.int64)
+            for q in range(Q):
+                keys[q, :cnts[g, q]] = np.sort(pool[g, q, :cnts[g, q]])
+            buf[g, :Q * k] = keys.reshape(-1)
+            buf[g, Q * k:].view(np.int32)[:Q] = cnts[g]
+        dbuf = torch.from_numpy(buf).cuda()
+        out_k = torch.empty((Q, k), dtype=torch.int64, device="cuda")
+        out_c = torch.empty((Q,), dtype=torch.int32, device="cuda")
+        N.check(N.load().fps_merge_packed_async(dbuf.data_ptr(), L * 8, G, Q, k, out_k.data_ptr(), out_c.data_ptr(),
+                                                torch.cuda.current_stream().cuda_stream), "fps_merge_packed_async")
+        torch.cuda.synchronize()
+        gk, gc = out_k.cpu().numpy(), out_c.cpu().numpy()
+        for q in range(Q):
+            allk = np.sort(np.concatenate([pool[g, q, :cnts[g, q]] for g in range(G)]))[:k]
+            assert gc[q] == len(allk)
+            assert np.array_equal(gk[q, :len(allk)], allk)
+    # the packed block helper writes the same layout
+    blk, kv, cv = D.packed_block(3, 4, "cuda")
+    assert kv.data_ptr() == blk.data_ptr() and cv.data_ptr() == blk.data_ptr() + 3 * 4 * 8
