@@ -154,6 +154,22 @@ def plane_scan_planes(q) -> int:
     return 8 + (166 - pop166 if pop > 83 else pop166)
 
 
+L2_BYTES = 126 << 20  # B200 L2 (cudaDeviceProp.l2CacheSize); both arms' configs state the same L2 policy
+
+
+def l2_policy(plan, queries, world: int) -> str:
+    """The timing rule's L2 choice for this workload, per GPU: the bytes one
+    scan launch reads (the query's bit planes for a single query, the 21
+    B/entry tiles otherwise) against L2 -- larger is its own flush, smaller is
+    flushed between steps. Stated in both arms' config dicts."""
+    shard = -(-plan.n // max(world, 1))
+    if plan.Q == 1 and plan.radius is None:
+        nbytes = shard * plane_scan_planes(queries[0]) / 8.0
+    else:
+        nbytes = shard * 21.0
+    return "flushed between steps" if nbytes <= L2_BYTES else "inputs larger than L2 (no flush)"
+
+
 def roofline_model(workload: str) -> dict:
     """Per-kernel instruction-mix constants measured once with ncu (profiles/roofline_model.json)."""
     p = ROOT / "profiles" / "roofline_model.json"
@@ -344,6 +360,7 @@ def run_reference(args, rank: int, world: int):
         p1 = wl.q_count * plan.n / (time.perf_counter() - t1)
         sample = wl.describe()
         kind, prep = wl.kind, wl.prep_s
+        l2_queries_policy = l2_policy(plan, wl.queries, world)
     finally:
         wl.close()
     ms = wall * 1e3 / args.steps
@@ -352,7 +369,7 @@ def run_reference(args, rank: int, world: int):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": plan.describe(),
+        "config": dict(plan.describe(), l2=l2_queries_policy),
         "sample": sample,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
                          "p1": {"value": p1, "cores": 1}, "cpu_model": cpu_model(),
@@ -532,7 +549,8 @@ def run_ours(args, rank: int, local_rank: int, world: int):
     # with an L2 evict-first policy, so K steps run back to back between one
     # event pair. Smaller ones (C1; C2 on the plane scan) get an explicit flush
     # between steps, outside per-step events.
-    flush = (not args.no_flush) and bytes_per_launch <= l2
+    policy = l2_policy(plan, queries, world if world > 1 else max(1, len(group_devs or [0])))
+    flush = (not args.no_flush) and policy.startswith("flushed")
     if flush:
         flush_buf, clean_buf = {}, {}
         for d in (group_devs or [local_rank]):
@@ -713,7 +731,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": plan.describe(),
+        "config": dict(plan.describe(), l2=policy if not args.no_flush else "no flush (--no-flush)"),
         "method": {
             "parallelism": parallel,
             "pipelining": (f"pipelined: step i's {backend} gather + rank-0 merge overlap step i+1's scan (second "
