@@ -966,22 +966,24 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   return true;
 }
 
-// Operand kind of the tensor-core scan (FPS_MMA_KIND): "i8" (default) is the
-// int8 kernel (fps_mma.cuh: tiles expanded to bytes in the kernel, 16-bit
-// packed accumulator reads; the C4 call 11.36 ms, its MMA at 0.82 of the
-// measured int8 rate); "fp4x" the block-scaled fp4 kernel fed from the
-// library's fp4 operand copy (fps_mma4x.cuh: the full pass is 1.4 % faster,
-// but hit-heavy prefix passes are slower and the copy costs 96 B/entry, so
-// the call is 11.45 ms); "fp4" expands fp4 tiles in the kernel
-// (fps_mma4.cuh). fp4x falls back to int8 when its copy does not fit.
+// Operand kind of the tensor-core scan (FPS_MMA_KIND overrides). Default by
+// accumulator width: batches of <= 128 queries (N <= 128: range search on
+// 64 queries, C5) take "fp4x", the block-scaled fp4 kernel fed from the
+// library's fp4 operand copy (fps_mma4x.cuh, two epilogue groups of 8 warps on
+// alternate tiles: C5 1.87 ms against 2.21 ms bit-sliced and 2.29 ms int8);
+// wider batches (N = 256: top-k of >= 192 queries, C4) take "i8", the int8
+// kernel (fps_mma.cuh: tiles expanded to bytes in the kernel, 16-bit packed
+// accumulator reads; the C4 call 11.36 ms, its MMA at 0.82 of the measured
+// int8 rate; fp4x's 208-column accumulators drain too slowly: 11.45 ms).
+// "fp4" expands fp4 tiles in the kernel (fps_mma4.cuh). fp4x falls back to
+// int8 when its copy (96 B/entry) does not fit.
 enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
-MmaKind mma_kind_env() {
+MmaKind mma_kind_env(u32 Q) {
   const char* e = std::getenv("FPS_MMA_KIND");
-  if (!e) return MMA_I8;
+  if (!e) return Q <= 128 ? MMA_FP4X : MMA_I8;
   const std::string v(e);
   return v == "fp4" ? MMA_FP4 : v == "fp4x" ? MMA_FP4X : MMA_I8;
 }
-bool mma_fp4() { return mma_kind_env() != MMA_I8; }
 
 // Build (once) the fp4 operand copy; on failure (no memory) the scan uses int8.
 int mq4x_ensure(fps_lib* L) {
@@ -1027,8 +1029,8 @@ int mq4x_ensure(fps_lib* L) {
 }
 
 // The kind a call runs: fp4x only once its operand copy exists.
-MmaKind mma_kind(fps_lib* L) {
-  MmaKind k = mma_kind_env();
+MmaKind mma_kind(fps_lib* L, u32 Q) {
+  MmaKind k = mma_kind_env(Q);
   if (k == MMA_FP4X) {
     if (mq4x_ensure(L) != FPS_OK || L->mq4x_state != 1) k = MMA_I8;
   }
@@ -1095,8 +1097,11 @@ int mma4x_launch_ne(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) 
 // Epilogue warps of the fp4 operand-copy kernel (FPS_MM4X_EPI: 8 or 16).
 template <int N>
 int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
+  // two groups of 8 warps on alternate tiles where a warp's share of the
+  // accumulator fits its registers (N <= 128: <= 64 columns), else 8 warps on
+  // every tile (FPS_MM4X_EPI=8|16 overrides)
   const char* e = std::getenv("FPS_MM4X_EPI");
-  const int epi = e ? std::atoi(e) : 8;
+  const int epi = e ? std::atoi(e) : (N <= 128 ? 16 : 8);
   if (epi == 16) return mma4x_launch_ne<N, 16>(L, ctas, s, a);
   return mma4x_launch_ne<N, 8>(L, ctas, s, a);
 }
@@ -1108,7 +1113,7 @@ int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
 int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
             cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull) {
   int rc;
-  const MmaKind kind = mma_kind(L);
+  const MmaKind kind = mma_kind(L, Q);
   const bool fp4 = kind != MMA_I8;
   L->last_mma_kind = 1 + (int)kind;
   const u32 NN = mma_pick_n(Q, fp4);
@@ -1249,14 +1254,14 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
 // Range search on the tensor cores: the bound is the radius itself (exact,
 // no seed); hits go straight to the range output. FPS_MMA=0 disables it,
 // FPS_MMA=1 forces it for any batch >= 2; by default it serves batches of
-// >= FPS_MMA_RANGE_MIN_Q (default 192) queries (C5, 64 queries: the
-// bit-sliced kernel is faster, 2.2 vs 3.6 ms).
+// >= FPS_MMA_RANGE_MIN_Q (default 64) queries (C5, 64 queries: the fp4
+// operand-copy kernel 1.87 ms against the bit-sliced kernel's 2.21 ms).
 bool mma_range_wanted(fps_lib* L, u32 Q, cudaStream_t s) {
   const char* e = std::getenv("FPS_MMA");
   const int mode = e ? std::atoi(e) : -1;
   if (mode == 0 || Q < 2 || L->n < (u64)fps::MM_M || !L->compact) return false;
   const char* m = std::getenv("FPS_MMA_RANGE_MIN_Q");
-  if (mode != 1 && Q < (u32)(m ? std::atoi(m) : 192)) return false;
+  if (mode != 1 && Q < (u32)(m ? std::atoi(m) : 64)) return false;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();

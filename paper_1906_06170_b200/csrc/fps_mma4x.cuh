@@ -125,11 +125,11 @@ __device__ __noinline__ void mm4x_hits(const MmArgs& a, u64 hm0, u64 hm1, int cb
 // tfull[0..1] / tempty[0..1] at bf / be (8 bytes apart).
 template <int W, int N>
 __device__ __forceinline__ void mm4x_epilogue(const MmArgs& a, u32 ntile, u64 e0, u32 bf, u32 be, u32 ta0, int cb0,
-                                              bool tests, u32* s_pcnt, const u32* s_qcol) {
+                                              bool tests, u32* s_pcnt, const u32* s_qcol, u32 it0, u32 istep) {
   static_assert(W % 8 == 0 && W <= 128, "columns per warp");
   const u32 lane = threadIdx.x & 31;
 #pragma unroll 1
-  for (u32 it = 0; it < ntile; ++it) {
+  for (u32 it = it0; it < ntile; it += istep) {
     const u32 b = it & 1u;
     mm4x_wait(bf + 8 * b, (it >> 1) & 1u);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -168,6 +168,9 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
   static_assert(N % 16 == 0 && N >= 64 && N <= 240, "accumulator width (two accumulators + scale factors in 512 columns)");
   static_assert(EPI == 8 || EPI == 16, "epilogue warps: whole lane quadrants, <= 128 columns each");
   constexpr int MM4X_EPI = EPI;
+  // 16 epilogue warps: two groups of 8 on alternate tiles (group g always
+  // drains accumulator g, so it has two MMA tiles of time); 8: every tile
+  constexpr int GROUPS = EPI == 16 ? 2 : 1, GW = EPI / GROUPS;
   constexpr int MM4X_THREADS = mm4x_threads(EPI);
   constexpr u32 B_BYTES = mm4_b_bytes(N);
   constexpr u32 TMEM_COLS = 512;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
     }
     for (int b = 0; b < 2; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], (u32)MM4X_EPI);  // one arrival per epilogue warp
+      mm_bar_init(&tempty[b], (u32)(MM4X_EPI / GROUPS));  // one arrival per warp of the accumulator's group
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -266,18 +269,19 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
     // tested (addresses, parities and the row index are carried in
     // registers: the loop is the loads, the AND chain and a vote).
     const u32 ew = (u32)warp;
-    const u32 quad = ew % 4, qt = ew / 4;
-    using QS = Mm4Split<N, EPI / 4>;
+    const u32 grp = ew / GW, wg = ew % GW;
+    const u32 quad = wg % 4, qt = wg / 4;
+    using QS = Mm4Split<N, GW / 4>;
     const int c0 = QS::off((int)qt);
     const u32 ta0 = tmem + (quad * 32u << 16) + (u32)c0;
     const u64 e0 = t0 * MM_M + quad * 32 + lane;
     const bool tests = !(a.flags & 4096);
     if ((int)qt < QS::N_HI)
       mm4x_epilogue<QS::W_HI, N>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
-                                 s_pcnt, s_qcol);
+                                 s_pcnt, s_qcol, grp, (u32)GROUPS);
     else
       mm4x_epilogue<QS::W_LO, N>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
-                                 s_pcnt, s_qcol);
+                                 s_pcnt, s_qcol, grp, (u32)GROUPS);
   } else {
     // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
     if (lane == 0) {

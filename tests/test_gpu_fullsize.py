@@ -71,6 +71,7 @@ def test_config4_full_size(monkeypatch):
 def test_config5_full_size():
     plan, lib, q, w = full("c5")
     r = lib.range_search(q, plan.radius)
+    assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == "fp4x"
     rows = r.rows()
     assert np.array_equal(rows, orc.c_range(w, q, plan.radius))
     # every planted near-duplicate (0-6 flips) is present at its flip count
@@ -78,15 +79,20 @@ def test_config5_full_size():
     for i, qi, f in zip(plan.planted_idx, plan.planted_query, plan.planted_flips):
         assert (int(qi), int(i), len(f)) in got
     assert len(rows) >= 640_064
-    # the tensor-core range path (FPS_MMA=1) gives the same triples
+    # the bit-sliced kernel (FPS_MMA=0) and the int8 tensor-core kernel give
+    # the same triples
     import os
-    os.environ["FPS_MMA"] = "1"
-    try:
-        r2 = lib.range_search(q, plan.radius)
-        assert lib.last_kernel == "tensor-core multi-query scan"
-    finally:
-        del os.environ["FPS_MMA"]
-    assert np.array_equal(r2.rows(), rows)
+    for env, kernel in ((("FPS_MMA", "0"),), "bit-sliced multi-query scan"), \
+                       ((("FPS_MMA", "1"), ("FPS_MMA_KIND", "i8")), "tensor-core multi-query scan"):
+        for key, v in env:
+            os.environ[key] = v
+        try:
+            r2 = lib.range_search(q, plan.radius)
+            assert lib.last_kernel == kernel
+        finally:
+            for key, _ in env:
+                del os.environ[key]
+        assert np.array_equal(r2.rows(), rows)
 
 
 def test_config3_sharded_merge_full_size():

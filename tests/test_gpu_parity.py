@@ -800,17 +800,21 @@ def test_mma_range_per_query_radius_and_overflow_retry(monkeypatch):
 
 
 def test_mma_range_default_dispatch_config_shape():
-    """C5-shaped calls (radius 6, planted near-duplicates): 64 queries take
-    the bit-sliced kernel, 256 the tensor-core range path; both match the oracle."""
+    """C5-shaped calls (radius 6, planted near-duplicates): 40 queries take
+    the bit-sliced kernel, 64 the fp4 operand-copy tensor-core kernel (two
+    epilogue groups), 256 the int8 tensor-core kernel; all match the oracle."""
     plan = synth.make_plan("c5", n=1_000_000, planted_per_query=300)
     lib, q = synth.build_library(plan)
     w = lib.words_host()
-    r = lib.range_search(q, plan.radius)
+    r = lib.range_search(q[:40], plan.radius)
     assert lib.last_kernel == "bit-sliced multi-query scan"
+    assert np.array_equal(r.rows(), orc.c_range(w, q[:40], plan.radius))
+    r = lib.range_search(q, plan.radius)
+    assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == "fp4x"
     assert np.array_equal(r.rows(), orc.c_range(w, q, plan.radius))
     q4 = np.concatenate([q, q ^ np.uint64(1), q ^ np.uint64(2), q ^ np.uint64(4)])
     r = lib.range_search(q4, plan.radius)
-    assert lib.last_kernel == "tensor-core multi-query scan"
+    assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == "i8"
     assert np.array_equal(r.rows(), orc.c_range(w, q4, plan.radius))
 
 
