@@ -1081,29 +1081,36 @@ int mma4_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   return FPS_OK;
 }
 
-template <int N, int EPI>
+template <int N, int EPI, int NACC>
 int mma4x_launch_ne(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   const size_t smem = fps::mm4x_smem(N);
-  CUDA_TRY(smem_optin((const void*)fps::mma4x_scan_kernel<N, EPI>, smem));
+  CUDA_TRY(smem_optin((const void*)fps::mma4x_scan_kernel<N, EPI, NACC>, smem));
   auto* ev = timing_slot(L);
   if (ev) cudaEventRecord(ev->first, s);
-  fps::mma4x_scan_kernel<N, EPI><<<ctas, fps::mm4x_threads(EPI), smem, s>>>(a, L->mq4x.as<unsigned char>(),
+  fps::mma4x_scan_kernel<N, EPI, NACC><<<ctas, fps::mm4x_threads(EPI), smem, s>>>(a, L->mq4x.as<unsigned char>(),
                                                                                L->mq4x_map);
   if (ev) cudaEventRecord(ev->second, s);
   L->launches++;
   LAUNCH_CHECK("mma4x_scan_kernel");
   return FPS_OK;
 }
-// Epilogue warps of the fp4 operand-copy kernel (FPS_MM4X_EPI: 8 or 16).
+// Epilogue warps and accumulators of the fp4 operand-copy kernel.
 template <int N>
 int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
-  // two groups of 8 warps on alternate tiles where a warp's share of the
-  // accumulator fits its registers (N <= 128: <= 64 columns), else 8 warps on
-  // every tile (FPS_MM4X_EPI=8|16 overrides)
+  // epilogue shape by width (FPS_MM4X_EPI=8 forces 8 warps on every tile):
+  // N = 64: 4 accumulators, 4 groups of 4 warps (64 columns each; C5 scan
+  // 1.87 -> 1.71 ms against 2 groups of 8); N = 128: 2 accumulators, 2 groups
+  // of 8 warps (3 accumulators in 3 groups of 4 warps of 128 columns spill:
+  // 13.7 -> 18.3 ms on C4 at N = 128); wider: 2 accumulators, 8 warps on
+  // every tile (a group's warps would spill)
   const char* e = std::getenv("FPS_MM4X_EPI");
-  const int epi = e ? std::atoi(e) : (N <= 128 ? 16 : 8);
-  if (epi == 16) return mma4x_launch_ne<N, 16>(L, ctas, s, a);
-  return mma4x_launch_ne<N, 8>(L, ctas, s, a);
+  const int epi = e ? std::atoi(e) : 0;
+  if constexpr (N <= 64) {
+    if (epi != 8) return mma4x_launch_ne<N, 16, 4>(L, ctas, s, a);
+  } else if constexpr (N <= 128) {
+    if (epi != 8) return mma4x_launch_ne<N, 16, 2>(L, ctas, s, a);
+  }
+  return mma4x_launch_ne<N, 8, 2>(L, ctas, s, a);
 }
 
 // Shared part of the tensor-core calls: per-query operands from the bound
@@ -1116,7 +1123,9 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   const MmaKind kind = mma_kind(L, Q);
   const bool fp4 = kind != MMA_I8;
   L->last_mma_kind = 1 + (int)kind;
-  const u32 NN = mma_pick_n(Q, fp4);
+  u32 NN = mma_pick_n(Q, fp4);
+  if (const char* en = std::getenv("FPS_MMA_N"))  // experiments: accumulator width (fp4: 64/128/160/208/240)
+    if (fp4) NN = (u32)std::atoi(en);
   const u32 nchunks = (Q + NN - 1) / NN;
   n_scan = std::min<u64>(n_scan, L->n);  // entries [0, n_scan) (a prefix pass of the top-k path)
   const u64 n_tiles = (n_scan + fps::MM_M - 1) / fps::MM_M;

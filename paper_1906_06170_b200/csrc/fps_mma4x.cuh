@@ -123,15 +123,15 @@ __device__ __noinline__ void mm4x_hits(const MmArgs& a, u64 hm0, u64 hm1, int cb
 // The epilogue loop of one warp: W accumulator columns starting at TMEM
 // address ta0 (accumulator 0; accumulator 1 is N columns on), barriers
 // tfull[0..1] / tempty[0..1] at bf / be (8 bytes apart).
-template <int W, int N>
+template <int W, int N, int NACC>
 __device__ __forceinline__ void mm4x_epilogue(const MmArgs& a, u32 ntile, u64 e0, u32 bf, u32 be, u32 ta0, int cb0,
                                               bool tests, u32* s_pcnt, const u32* s_qcol, u32 it0, u32 istep) {
   static_assert(W % 8 == 0 && W <= 128, "columns per warp");
   const u32 lane = threadIdx.x & 31;
 #pragma unroll 1
   for (u32 it = it0; it < ntile; it += istep) {
-    const u32 b = it & 1u;
-    mm4x_wait(bf + 8 * b, (it >> 1) & 1u);
+    const u32 b = it % NACC;
+    mm4x_wait(bf + 8 * b, (it / NACC) & 1u);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     u32 r[W];
     mm4_issue<W>(ta0 + b * N, r);
@@ -162,22 +162,29 @@ __device__ __forceinline__ void mm4x_epilogue(const MmArgs& a, u32 ntile, u64 e0
 // 128-entry tile = 48 rows (one box).
 constexpr u32 MM4X_ROW = 256, MM4X_BOX_ROWS = MM4X_TILE / MM4X_ROW;
 
-template <int N, int EPI>
+// NACC accumulators in flight; EPI epilogue warps, in NACC groups of
+// EPI / NACC (>= 4, whole lane quadrants) when EPI > 8 -- group g drains
+// accumulator g of every NACC tiles, so it has NACC MMA tiles of time -- or
+// 8 warps on every tile (EPI = 8).
+template <int N, int EPI, int NACC = 2>
 __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
     mma4x_scan_kernel(const MmArgs a, const unsigned char* __restrict__ op, const __grid_constant__ CUtensorMap tmap) {
   static_assert(N % 16 == 0 && N >= 64 && N <= 240, "accumulator width (two accumulators + scale factors in 512 columns)");
-  static_assert(EPI == 8 || EPI == 16, "epilogue warps: whole lane quadrants, <= 128 columns each");
+  static_assert(EPI % 4 == 0 && EPI >= 8 && EPI <= 28, "epilogue warps: whole lane quadrants");
+  static_assert(NACC >= 2 && NACC * N + 32 <= 512, "accumulators + scale factors fit 512 TMEM columns");
+  static_assert(EPI == 8 || (EPI % NACC == 0 && (EPI / NACC) % 4 == 0), "whole groups of lane quadrants");
   constexpr int MM4X_EPI = EPI;
   // 16 epilogue warps: two groups of 8 on alternate tiles (group g always
   // drains accumulator g, so it has two MMA tiles of time); 8: every tile
-  constexpr int GROUPS = EPI == 16 ? 2 : 1, GW = EPI / GROUPS;
+  constexpr int GROUPS = EPI == 8 ? 1 : NACC, GW = EPI / GROUPS;
+  static_assert(N / (GW / 4) <= 128, "a warp's columns fit its registers");
   constexpr int MM4X_THREADS = mm4x_threads(EPI);
   constexpr u32 B_BYTES = mm4_b_bytes(N);
   constexpr u32 TMEM_COLS = 512;
   extern __shared__ __align__(1024) unsigned char msm[];
   unsigned char* sB = msm;
   unsigned char* sA = msm + B_BYTES;  // [MM4X_STAGES][12 KB]
-  __shared__ __align__(8) u64 full_bar[MM4X_STAGES], empty_bar[MM4X_STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) u64 full_bar[MM4X_STAGES], empty_bar[MM4X_STAGES], tfull[NACC], tempty[NACC];
   __shared__ u32 tmem_base;
   __shared__ u32 s_qcol[N], s_pcnt[N];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
       mm_bar_init(&full_bar[s], 1);
       mm_bar_init(&empty_bar[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mm_bar_init(&tfull[b], 1);
       mm_bar_init(&tempty[b], (u32)(MM4X_EPI / GROUPS));  // one arrival per warp of the accumulator's group
     }
@@ -277,10 +284,10 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
     const u64 e0 = t0 * MM_M + quad * 32 + lane;
     const bool tests = !(a.flags & 4096);
     if ((int)qt < QS::N_HI)
-      mm4x_epilogue<QS::W_HI, N>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
+      mm4x_epilogue<QS::W_HI, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
                                  s_pcnt, s_qcol, grp, (u32)GROUPS);
     else
-      mm4x_epilogue<QS::W_LO, N>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
+      mm4x_epilogue<QS::W_LO, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
                                  s_pcnt, s_qcol, grp, (u32)GROUPS);
   } else {
     // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
@@ -292,13 +299,13 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
       constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4X_TILE / 16;
       const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
       for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM4X_STAGES), b = (int)(it & 1);
+        const int s = (int)(it % MM4X_STAGES), b = (int)(it % NACC);
         MM4_TRACE(0);
         if (a.flags & (1u << 27)) {  // experiment: suspend-hint waits on the MMA lane
-          if (it >= 2) mm_bar_wait_ns(&tempty[b], (u32)((it >> 1) - 1) & 1u, 20000u);
+          if (it >= NACC) mm_bar_wait_ns(&tempty[b], (u32)((it / NACC) - 1) & 1u, 20000u);
           mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u, 20000u);
         } else {
-          if (it >= 2) mm_bar_wait_spin(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+          if (it >= NACC) mm_bar_wait_spin(&tempty[b], (u32)((it / NACC) - 1) & 1u);
           mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u);
         }
         MM4_TRACE(1);

@@ -39,14 +39,14 @@ void run(u64 n_tiles, u32 nchunks, u32 parts, unsigned flags, unsigned char* op,
   a.mode = 0;
   a.flags = flags;
   const size_t smem = mm4x_smem(N);
-  CK(cudaFuncSetAttribute(mma4x_scan_kernel<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  mma4x_scan_kernel<N, EPI><<<nchunks * parts, mm4x_threads(EPI), smem>>>(a, op, tmap);
+  CK(cudaFuncSetAttribute(mma4x_scan_kernel<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  mma4x_scan_kernel<N, EPI, 2><<<nchunks * parts, mm4x_threads(EPI), smem>>>(a, op, tmap);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma4x_scan_kernel<N, EPI><<<nchunks * parts, mm4x_threads(EPI), smem>>>(a, op, tmap);
+  mma4x_scan_kernel<N, EPI, 2><<<nchunks * parts, mm4x_threads(EPI), smem>>>(a, op, tmap);
   cudaEventRecord(e1);
   CK(cudaDeviceSynchronize());
   float ms = 0;
