@@ -63,6 +63,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-flush", action="store_true")
     p.add_argument("--k", type=int, default=None, help="override the workload's k (experiments)")
+    p.add_argument("--queries", type=int, default=None, help="override the workload's batch size (experiments)")
     p.add_argument("--radius", type=int, default=None, help="run a range search at this radius instead")
     return p.parse_args()
 
@@ -424,7 +425,7 @@ def run_ours(args, rank: int, local_rank: int, world: int):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    plan = synth.make_plan(args.workload, seed=args.seed)
+    plan = synth.make_plan(args.workload, seed=args.seed, Q=args.queries)
     if args.k is not None:
         plan.k, plan.radius = args.k, None
     if args.radius is not None:

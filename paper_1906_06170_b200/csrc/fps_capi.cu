@@ -916,10 +916,10 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
 // ---------------------------------------------------------------------------
 // tensor-core multi-query path (fps_mma.cuh)
 // ---------------------------------------------------------------------------
-// Large batches take the tensor cores: one 256-query chunk costs ~4.4 ms on
-// the 95.4 M library against ~4.1 ms for 128 queries on the bit-sliced
-// kernel (tools/mma_time.py, tools/q_sweep.py). FPS_MMA=1 forces it for any
-// batch >= 2, FPS_MMA=0 disables it. The call is stream ordered end to end
+// Batches of >= 64 queries take the tensor cores (95.4 M entries, top-k: 64
+// queries 1.91 vs 2.12 ms bit-sliced, 128: 2.01 vs 4.08, 192: 2.41 vs 6.06;
+// tools/dbg/mm4x_bench.sh with bench.py --queries). FPS_MMA=1 forces it for
+// any batch >= 2, FPS_MMA=0 disables it. The call is stream ordered end to end
 // (no host synchronisation, capturable): a candidate list that overflows its
 // capacity raises a device flag, and a gated POPC pass recomputes the batch.
 struct MmaPlan {
@@ -959,7 +959,7 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   const int mode = e ? std::atoi(e) : -1;
   // compact libraries only: the fused test uses K slots 168.. (zero there)
   if (mode == 0 || Q < 2 || k > KMAX_FUSED || L->n < (u64)fps::MM_M || !L->compact) return false;
-  if (mode != 1 && Q < 192) return false;
+  if (mode != 1 && Q < 64) return false;  // (64-query top-k: 1.91 ms tensor vs 2.12 bit-sliced)
   MmaPlan p;
   if (!mma_plan(L, Q, k, &p)) return false;
   if (plan) *plan = p;
@@ -967,20 +967,19 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
 }
 
 // Operand kind of the tensor-core scan (FPS_MMA_KIND overrides). Default by
-// accumulator width: batches of <= 128 queries (N <= 128: range search on
-// 64 queries, C5) take "fp4x", the block-scaled fp4 kernel fed from the
-// library's fp4 operand copy (fps_mma4x.cuh, two epilogue groups of 8 warps on
-// alternate tiles: C5 1.87 ms against 2.21 ms bit-sliced and 2.29 ms int8);
-// wider batches (N = 256: top-k of >= 192 queries, C4) take "i8", the int8
-// kernel (fps_mma.cuh: tiles expanded to bytes in the kernel, 16-bit packed
-// accumulator reads; the C4 call 11.36 ms, its MMA at 0.82 of the measured
-// int8 rate; fp4x's 208-column accumulators drain too slowly: 11.45 ms).
-// "fp4" expands fp4 tiles in the kernel (fps_mma4.cuh). fp4x falls back to
-// int8 when its copy (96 B/entry) does not fit.
+// batch: "fp4x", the block-scaled fp4 kernel fed from the library's fp4
+// operand copy (fps_mma4x.cuh), while the batch fits one fp4 accumulator
+// chunk (top-k: Q <= 240; range, whose hit path is heavier: Q <= 128) --
+// C5 (64-query range) 1.95 ms vs 2.29 int8 vs 2.36 bit-sliced; 192-query
+// top-k 2.41 vs 2.95 ms int8 -- else "i8", the int8 kernel (fps_mma.cuh: 256
+// queries per chunk, 16-bit packed accumulator reads; the C4 call 11.36 ms,
+// its MMA at 0.82 of the measured int8 rate; fp4x 11.45 ms). "fp4" expands
+// fp4 tiles in the kernel (fps_mma4.cuh). fp4x falls back to int8 when its
+// copy (96 B/entry) does not fit.
 enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
-MmaKind mma_kind_env(u32 Q) {
+MmaKind mma_kind_env(u32 Q, u32 mode) {
   const char* e = std::getenv("FPS_MMA_KIND");
-  if (!e) return Q <= 128 ? MMA_FP4X : MMA_I8;
+  if (!e) return Q <= (mode == 0 ? 240u : 128u) ? MMA_FP4X : MMA_I8;
   const std::string v(e);
   return v == "fp4" ? MMA_FP4 : v == "fp4x" ? MMA_FP4X : MMA_I8;
 }
@@ -1029,8 +1028,8 @@ int mq4x_ensure(fps_lib* L) {
 }
 
 // The kind a call runs: fp4x only once its operand copy exists.
-MmaKind mma_kind(fps_lib* L, u32 Q) {
-  MmaKind k = mma_kind_env(Q);
+MmaKind mma_kind(fps_lib* L, u32 Q, u32 mode) {
+  MmaKind k = mma_kind_env(Q, mode);
   if (k == MMA_FP4X) {
     if (mq4x_ensure(L) != FPS_OK || L->mq4x_state != 1) k = MMA_I8;
   }
@@ -1120,7 +1119,7 @@ int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
 int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
             cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull) {
   int rc;
-  const MmaKind kind = mma_kind(L, Q);
+  const MmaKind kind = mma_kind(L, Q, mode);
   const bool fp4 = kind != MMA_I8;
   L->last_mma_kind = 1 + (int)kind;
   u32 NN = mma_pick_n(Q, fp4);

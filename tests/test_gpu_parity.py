@@ -474,12 +474,13 @@ def test_fps1_streaming_loader(tmp_path):
 
 
 @pytest.mark.parametrize("n", [2048, 2049, 2080, 2081, 4095, 70_001, 132_127])
-def test_bitslice_tails_and_query_groups(n):
+def test_bitslice_tails_and_query_groups(n, monkeypatch):
     """Q >= 32 runs the bit-sliced kernel: 2,048-entry tiles, two 32-entry
     blocks per lane. Library sizes around the tile / block / lane-pair
     boundaries, two query groups (Q = 70 > 64 per CTA), sparse and dense
     queries (|q| > 83 counts the zero keys), top-k and range: all equal the
-    oracle."""
+    oracle (FPS_MMA=0: batches of >= 64 queries default to the tensor cores)."""
+    monkeypatch.setenv("FPS_MMA", "0")
     seed = 9000 + n
     thr = synth.beta_thresholds(seed)
     w = orc.generate_words(synth.seed_key(seed), thr, 0, n)
