@@ -139,6 +139,12 @@ def test_tensor_core_per_query_matches_reference_golden(golden, kind, monkeypatc
     assert lib.last_mma_kind == (kind or "i8")
     for qi, hits in enumerate(case["hits"]):
         assert res.hits(qi) == [(c - 1, d) for c, d in hits], qi
+    if kind is None:
+        # 100 of the queries: one fp4 chunk, the default fp4 operand-copy kernel
+        res = lib.search_batch(q[:100], case["k"])
+        assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == "fp4x"
+        for qi, hits in enumerate(case["hits"][:100]):
+            assert res.hits(qi) == [(c - 1, d) for c, d in hits], qi
 
 
 @pytest.mark.parametrize("kind", [None, "fp4x"])
