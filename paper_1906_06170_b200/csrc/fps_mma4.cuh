@@ -233,6 +233,75 @@ __device__ __forceinline__ void mm4_tile(const MmArgs& a, u32 taddr, int cb0, u6
   mm4_test<CNT, N>(a, r, cb0, e, s_pcnt, s_qcol);
 }
 
+__device__ __forceinline__ void mm4x_wait(u32 bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n M4XW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra M4XW;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Record the passing columns of one row (rare): W <= 128 columns as two
+// 64-bit masks, then one private-list append (top-k) or range-output append
+// per passing pair. Out of line: inlined, the epilogue loop outgrows the
+// instruction cache (C4 scan 9.8 -> 12.7 ms).
+template <int W, int N>
+__device__ __noinline__ void mm4x_hits(const MmArgs& a, u64 hm0, u64 hm1, int cb0, u64 idx, u32* s_pcnt,
+                                       const u32* s_qcol) {
+#pragma unroll 1
+  for (int g = 0; g < 2; ++g) {
+    u64 hm = g ? hm1 : hm0;
+    while (hm) {
+      const int c = cb0 + 64 * g + __ffsll((long long)hm) - 1;
+      hm &= hm - 1;
+      if (a.mode == 0) {
+        const u32 pos = atomicAdd(s_pcnt + c, 1u);
+        if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
+      } else {
+        const u64 pos = atomicAdd(a.out_cnt, 1ull);
+        if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
+      }
+    }
+  }
+}
+
+// The epilogue loop of one warp: W accumulator columns starting at TMEM
+// address ta0 (accumulator 0; accumulator 1 is N columns on), barriers
+// tfull[0..1] / tempty[0..1] at bf / be (8 bytes apart).
+template <int W, int N, int NACC>
+__device__ __forceinline__ void mm4x_epilogue(const MmArgs& a, u32 ntile, u64 e0, u32 bf, u32 be, u32 ta0, int cb0,
+                                              bool tests, u32* s_pcnt, const u32* s_qcol, u32 it0, u32 istep) {
+  static_assert(W % 8 == 0 && W <= 128, "columns per warp");
+  const u32 lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (u32 it = it0; it < ntile; it += istep) {
+    const u32 b = it % NACC;
+    mm4x_wait(bf + 8 * b, (it / NACC) & 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    u32 r[W];
+    mm4_issue<W>(ta0 + b * N, r);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(be + 8 * b) : "memory");
+    if (!tests) continue;
+    u32 t = r[0];
+#pragma unroll
+    for (int i = 1; i < W; ++i) t &= r[i];
+    const bool any = (int)t >= 0;  // some column's sign bit is clear: D > 0, the pair passes
+    if (!__any_sync(0xffffffffu, any) || !any) continue;
+    const u64 e = e0 + (u64)it * MM_M;
+    if (e >= a.n) continue;  // padding rows of the last tile (zero operands: D > 0)
+    u64 hm0 = 0, hm1 = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const u64 bit = (u64)((~r[i]) >> 31);
+      if (i < 64) hm0 |= bit << i;
+      else hm1 |= bit << (i - 64);
+    }
+    mm4x_hits<W, N>(a, hm0, hm1, cb0, a.index_base + e, s_pcnt, s_qcol);
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a) {
   static_assert(N % 16 == 0 && N >= 64 && N <= 240, "accumulator width (two accumulators + scale factors in 512 columns)");
@@ -242,7 +311,12 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
   unsigned char* sB = msm;
   unsigned char* sA = msm + B_BYTES;  // [MM4_STAGES][12 KB]
   char* raw = reinterpret_cast<char*>(msm + B_BYTES + MM4_STAGES * MM4_A_BYTES);  // [MM_RAW][library tile]
-  __shared__ __align__(8) u64 full_bar[MM4_STAGES], empty_bar[MM4_STAGES], tfull[2], tempty[2];
+  // N = 64: 4 accumulators and 4 epilogue groups of 4 warps (group g drains
+  // accumulator g of every four tiles); wider: 2 accumulators, all 16
+  // epilogue warps on every tile
+  constexpr int NACC = N <= 64 ? 4 : 2;
+  constexpr bool GROUPED = N <= 64;
+  __shared__ __align__(8) u64 full_bar[MM4_STAGES], empty_bar[MM4_STAGES], tfull[NACC], tempty[NACC];
   __shared__ __align__(8) u64 raw_full[MM_RAW], raw_empty[MM_RAW];
   __shared__ u32 tmem_base;
   __shared__ uint2 luta[176];  // |a| -> block-5 test nibbles of words 0 and 1 (digits of -|a|, A = 6)
@@ -286,9 +360,9 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       mm_bar_init(&raw_full[r], 1);
       mm_bar_init(&raw_empty[r], 4);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mm_bar_init(&tfull[b], 1);
-      mm_bar_init(&tempty[b], MM_EPI);  // every epilogue warp reads every tile (one arrival each)
+      mm_bar_init(&tempty[b], GROUPED ? MM_EPI / NACC : MM_EPI);  // one arrival per warp that drains it
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -385,6 +459,15 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
     }
     __syncwarp();
   } else if (warp < 4 + MM_EPI) {
+   if constexpr (GROUPED) {
+    // ===== epilogue, N = 64: 4 groups of 4 warps (one per lane quadrant, all
+    // 64 columns), group g drains accumulator g of every four tiles
+    const u32 ew = (u32)(warp - 4);
+    const u32 quad = (u32)warp % 4, grp = ew / 4;
+    mm4x_epilogue<(N <= 128 ? N : 128), N, NACC>(a, (u32)ntile, t0 * MM_M + quad * 32 + lane, smem_u32(&tfull[0]),
+                                               smem_u32(&tempty[0]), tmem + (quad * 32u << 16), 0,
+                                               !(a.flags & 4096), s_pcnt, s_qcol, grp, (u32)NACC);
+   } else {
     // ===== epilogue: 16 warps, every tile; warp e reads TMEM lane quadrant
     // e % 4 (its warp id mod 4) and column quarter e / 4 -- one load wait
     // per tile per warp, then the accumulator is released and tested
@@ -405,6 +488,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       else mm4_tile<QS::W_LO, N>(a, taddr, c0, e, &tempty[b], s_pcnt, s_qcol);
       if (ew == 0 && lane == 0) MM4_TRACE(7);
     }
+   }
   } else {
     // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
     if (lane == 0) {
@@ -415,12 +499,12 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4_A_BYTES / 16;
       const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
       for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM4_STAGES), b = (int)(it & 1);
+        const int s = (int)(it % MM4_STAGES), b = (int)(it % NACC);
         if (a.suspend_ns) {
-          if (it >= 2) mm_bar_wait_ns(&tempty[b], (u32)((it >> 1) - 1) & 1u, a.suspend_ns);
+          if (it >= NACC) mm_bar_wait_ns(&tempty[b], (u32)((it / NACC) - 1) & 1u, a.suspend_ns);
           mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4_STAGES) & 1u, a.suspend_ns);
         } else {
-          if (it >= 2) mm_bar_wait_spin(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+          if (it >= NACC) mm_bar_wait_spin(&tempty[b], (u32)((it / NACC) - 1) & 1u);
           MM4_TRACE(0);
           mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4_STAGES) & 1u);
         }

@@ -89,75 +89,6 @@ __global__ void mm4x_build_kernel(PlanesOut lib, u64 n, u64 n_tiles, unsigned ch
   }
 }
 
-__device__ __forceinline__ void mm4x_wait(u32 bar, u32 parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n M4XW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra M4XW;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-// Record the passing columns of one row (rare): W <= 128 columns as two
-// 64-bit masks, then one private-list append (top-k) or range-output append
-// per passing pair. Out of line: inlined, the epilogue loop outgrows the
-// instruction cache (C4 scan 9.8 -> 12.7 ms).
-template <int W, int N>
-__device__ __noinline__ void mm4x_hits(const MmArgs& a, u64 hm0, u64 hm1, int cb0, u64 idx, u32* s_pcnt,
-                                       const u32* s_qcol) {
-#pragma unroll 1
-  for (int g = 0; g < 2; ++g) {
-    u64 hm = g ? hm1 : hm0;
-    while (hm) {
-      const int c = cb0 + 64 * g + __ffsll((long long)hm) - 1;
-      hm &= hm - 1;
-      if (a.mode == 0) {
-        const u32 pos = atomicAdd(s_pcnt + c, 1u);
-        if (pos < a.pcap) a.priv[((u64)blockIdx.x * N + c) * a.pcap + pos] = idx;
-      } else {
-        const u64 pos = atomicAdd(a.out_cnt, 1ull);
-        if (pos < a.out_cap) a.out[pos] = ((u64)s_qcol[c] << 48) | idx;
-      }
-    }
-  }
-}
-
-// The epilogue loop of one warp: W accumulator columns starting at TMEM
-// address ta0 (accumulator 0; accumulator 1 is N columns on), barriers
-// tfull[0..1] / tempty[0..1] at bf / be (8 bytes apart).
-template <int W, int N, int NACC>
-__device__ __forceinline__ void mm4x_epilogue(const MmArgs& a, u32 ntile, u64 e0, u32 bf, u32 be, u32 ta0, int cb0,
-                                              bool tests, u32* s_pcnt, const u32* s_qcol, u32 it0, u32 istep) {
-  static_assert(W % 8 == 0 && W <= 128, "columns per warp");
-  const u32 lane = threadIdx.x & 31;
-#pragma unroll 1
-  for (u32 it = it0; it < ntile; it += istep) {
-    const u32 b = it % NACC;
-    mm4x_wait(bf + 8 * b, (it / NACC) & 1u);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    u32 r[W];
-    mm4_issue<W>(ta0 + b * N, r);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(be + 8 * b) : "memory");
-    if (!tests) continue;
-    u32 t = r[0];
-#pragma unroll
-    for (int i = 1; i < W; ++i) t &= r[i];
-    const bool any = (int)t >= 0;  // some column's sign bit is clear: D > 0, the pair passes
-    if (!__any_sync(0xffffffffu, any) || !any) continue;
-    const u64 e = e0 + (u64)it * MM_M;
-    if (e >= a.n) continue;  // padding rows of the last tile (zero operands: D > 0)
-    u64 hm0 = 0, hm1 = 0;
-#pragma unroll
-    for (int i = 0; i < W; ++i) {
-      const u64 bit = (u64)((~r[i]) >> 31);
-      if (i < 64) hm0 |= bit << i;
-      else hm1 |= bit << (i - 64);
-    }
-    mm4x_hits<W, N>(a, hm0, hm1, cb0, a.index_base + e, s_pcnt, s_qcol);
-  }
-}
-
 // The operand copy as a 2-D tensor for the TMA engine: rows of 256 B, a
 // 128-entry tile = 48 rows (one box).
 constexpr u32 MM4X_ROW = 256, MM4X_BOX_ROWS = MM4X_TILE / MM4X_ROW;
