@@ -863,3 +863,38 @@ def test_mma_two_pass_prefix_bound(prefix_log2, monkeypatch):
         exp = oracle_topk(w, q, k)
         for i in range(300):
             assert res.hits(i) == exp[i], (prefix_log2, k, i)
+
+
+def test_fp4_operand_copy_rebuilt_after_writes_and_released():
+    """The fp4 operand copy (96 B/entry, built by the first fp4x call) follows
+    entry writes (invalidated, rebuilt on the next call) and fps_release_derived;
+    the 64-query range and top-k results always equal the oracle's."""
+    seed = 4711
+    n = 200_003
+    w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
+    lib = Library.from_words(w)
+    rng = np.random.default_rng(seed)
+    q = w[rng.integers(0, n, 64)].copy()
+    q[:, 1] ^= np.uint64(0b101)
+    r = lib.range_search(q, 10)
+    assert lib.last_mma_kind == "fp4x"
+    assert np.array_equal(r.rows(), orc.c_range(w, q, 10))
+    before = lib.memory()["derived_bytes"]
+    assert before >= (n + 127) // 128 * 12288
+    # rewrite 1,000 entries as exact copies of queries: new distance-0 hits
+    idx = rng.choice(n, 1000, replace=False).astype(np.uint64)
+    w2 = w.copy()
+    w2[idx.astype(np.int64)] = q[rng.integers(0, 64, 1000)]
+    lib.write_entries(idx, w2[idx.astype(np.int64)])
+    r = lib.range_search(q, 10)
+    assert lib.last_mma_kind == "fp4x"
+    assert np.array_equal(r.rows(), orc.c_range(w2, q, 10))
+    res = lib.search_batch(q, 10)
+    exp = oracle_topk(w2, q, 10)
+    for i in range(64):
+        assert res.hits(i) == exp[i], i
+    lib.release_derived()
+    assert lib.memory()["derived_bytes"] == 0
+    r = lib.range_search(q, 10)
+    assert np.array_equal(r.rows(), orc.c_range(w2, q, 10))
+    lib.close()

@@ -3,7 +3,7 @@ import sys, time, ctypes as C
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_1906_06170_b200 import synth, _native as N
-plan = synth.make_plan("c2")
+plan = synth.make_plan(sys.argv[1] if len(sys.argv) > 1 else "c2")
 lib, q = synth.build_library(plan)
 L = N.load()
 k = plan.k
