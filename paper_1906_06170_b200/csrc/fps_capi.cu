@@ -978,8 +978,15 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
 // copy (96 B/entry) does not fit.
 enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
 MmaKind mma_kind_env(u32 Q, u32 mode) {
+  (void)mode;
   const char* e = std::getenv("FPS_MMA_KIND");
-  if (!e) return Q <= (mode == 0 ? 240u : 128u) ? MMA_FP4X : MMA_I8;
+  if (!e) {
+    // per library tile: an fp4x chunk (<= 208 queries) costs ~358 ns, an int8
+    // chunk (256 queries) ~500 ns (95.4 M entries: 9.21 vs 10.07 ms at 5 / 4
+    // chunks); the fewer-chunk-ns kind wins, ties to int8 (no operand copy)
+    const u32 c4 = (Q + 207) / 208, c8 = (Q + 255) / 256;
+    return c4 * 358u < c8 * 500u ? MMA_FP4X : MMA_I8;
+  }
   const std::string v(e);
   return v == "fp4" ? MMA_FP4 : v == "fp4x" ? MMA_FP4X : MMA_I8;
 }
@@ -1037,21 +1044,15 @@ MmaKind mma_kind(fps_lib* L, u32 Q, u32 mode) {
 }
 
 // Accumulator width (queries per chunk). int8: 64 / 128 / 256. fp4: two
-// accumulators + the scale factors fit 512 TMEM columns up to N = 240; the
-// width minimises chunks x per-tile time, with a per-tile floor of ~304 clk
-// for N <= 128 (3 MMAs) and ~1.5 clk per column above (umma_peak.cu), e.g.
-// 1,024 queries -> 5 chunks of 208.
+// accumulators + the scale factors fit 512 TMEM columns up to N = 240 (four
+// at N = 64); e.g. 1,024 queries -> 5 chunks of 208.
 u32 mma_pick_n(u32 Q, bool fp4) {
   if (!fp4) return Q <= 64 ? 64u : Q <= 128 ? 128u : 256u;
   if (Q <= 64) return 64u;
   if (Q <= 128) return 128u;
-  u32 best = 240;
-  double best_cost = 1e30;
-  for (u32 n : {128u, 160u, 208u, 240u}) {
-    const double cost = (double)((Q + n - 1) / n) * std::max(304.0, 1.5 * n);
-    if (cost < best_cost - 1e-9) best_cost = cost, best = n;
-  }
-  return best;
+  // a tile costs about the same at any width (drain- and barrier-bound), so
+  // the fewest chunks win; 208 over 240 on ties (measured: 9.21 ms for C4)
+  return (Q + 239) / 240 < (Q + 207) / 208 ? 240u : 208u;
 }
 
 template <int N>
@@ -1100,13 +1101,17 @@ int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
   // N = 64: 4 accumulators, 4 groups of 4 warps (64 columns each; C5 scan
   // 1.87 -> 1.71 ms against 2 groups of 8); N = 128: 2 accumulators, 2 groups
   // of 8 warps (3 accumulators in 3 groups of 4 warps of 128 columns spill:
-  // 13.7 -> 18.3 ms on C4 at N = 128); wider: 2 accumulators, 8 warps on
-  // every tile (a group's warps would spill)
+  // 13.7 -> 18.3 ms on C4 at N = 128)
   const char* e = std::getenv("FPS_MM4X_EPI");
   const int epi = e ? std::atoi(e) : 0;
   if constexpr (N <= 64) {
     if (epi != 8) return mma4x_launch_ne<N, 16, 4>(L, ctas, s, a);
   } else if constexpr (N <= 128) {
+    if (epi != 8) return mma4x_launch_ne<N, 16, 2>(L, ctas, s, a);
+  } else {
+    // wider: 2 groups of 8 warps on alternate tiles, each warp draining its
+    // <= 120 columns in two rounds (C4 scan 9.93 -> 9.21 ms against 8 warps
+    // on every tile)
     if (epi != 8) return mma4x_launch_ne<N, 16, 2>(L, ctas, s, a);
   }
   return mma4x_launch_ne<N, 8, 2>(L, ctas, s, a);

@@ -302,6 +302,59 @@ __device__ __forceinline__ void mm4x_epilogue(const MmArgs& a, u32 ntile, u64 e0
   }
 }
 
+// The same loop for a warp owning W = 2 H columns (H <= 64) of a wide
+// accumulator in a group that drains every other tile: two rounds of H
+// loaded columns (half the registers), each tested as it lands; the
+// accumulator is released after the second round's loads.
+template <int W, int N, int NACC>
+__device__ __forceinline__ void mm4x_epilogue2(const MmArgs& a, u32 ntile, u64 e0, u32 bf, u32 be, u32 ta0, int cb0,
+                                               bool tests, u32* s_pcnt, const u32* s_qcol, u32 it0, u32 istep) {
+  constexpr int H0 = 8 * ((W / 8 + 1) / 2), H1 = W - H0;  // e.g. 104 = 56 + 48
+  static_assert(W % 8 == 0 && H0 <= 64 && H1 > 0, "two rounds of at most 64 columns");
+  const u32 lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (u32 it = it0; it < ntile; it += istep) {
+    const u32 b = it % NACC;
+    mm4x_wait(bf + 8 * b, (it / NACC) & 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    u32 r[H0];
+    mm4_issue<H0>(ta0 + b * N, r);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    u64 m0 = 0, m1 = 0;
+    bool any = false;
+    if (tests) {
+      u32 t = r[0];
+#pragma unroll
+      for (int i = 1; i < H0; ++i) t &= r[i];
+      if ((int)t >= 0) {
+        any = true;
+#pragma unroll
+        for (int i = 0; i < H0; ++i) m0 |= (u64)((~r[i]) >> 31) << i;
+      }
+    }
+    mm4_issue<H1>(ta0 + b * N + H0, r);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(be + 8 * b) : "memory");
+    if (!tests) continue;
+    u32 t = r[0];
+#pragma unroll
+    for (int i = 1; i < H1; ++i) t &= r[i];
+    if ((int)t >= 0) {
+      any = true;
+#pragma unroll
+      for (int i = 0; i < H1; ++i) m1 |= (u64)((~r[i]) >> 31) << i;
+    }
+    if (!__any_sync(0xffffffffu, any) || !any) continue;
+    const u64 e = e0 + (u64)it * MM_M;
+    if (e >= a.n) continue;  // padding rows of the last tile
+    // columns [0, H0) in m0, [H0, W) in m1 -> 64-bit halves of the W columns
+    const u64 hm0 = m0 | (m1 << H0), hm1 = m1 >> (64 - H0);
+    mm4x_hits<W, N>(a, hm0, hm1, cb0, a.index_base + e, s_pcnt, s_qcol);
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a) {
   static_assert(N % 16 == 0 && N >= 64 && N <= 240, "accumulator width (two accumulators + scale factors in 512 columns)");

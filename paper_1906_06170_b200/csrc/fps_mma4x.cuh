@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
   // 16 epilogue warps: two groups of 8 on alternate tiles (group g always
   // drains accumulator g, so it has two MMA tiles of time); 8: every tile
   constexpr int GROUPS = EPI == 8 ? 1 : NACC, GW = EPI / GROUPS;
-  static_assert(N / (GW / 4) <= 128, "a warp's columns fit its registers");
+  static_assert(N / (GW / 4) <= 128, "a warp's columns fit its registers (in two rounds when grouped)");
   constexpr int MM4X_THREADS = mm4x_threads(EPI);
   constexpr u32 B_BYTES = mm4_b_bytes(N);
   constexpr u32 TMEM_COLS = 512;
@@ -214,12 +214,21 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
     const u32 ta0 = tmem + (quad * 32u << 16) + (u32)c0;
     const u64 e0 = t0 * MM_M + quad * 32 + lane;
     const bool tests = !(a.flags & 4096);
-    if ((int)qt < QS::N_HI)
-      mm4x_epilogue<QS::W_HI, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
-                                 s_pcnt, s_qcol, grp, (u32)GROUPS);
-    else
-      mm4x_epilogue<QS::W_LO, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0, tests,
-                                 s_pcnt, s_qcol, grp, (u32)GROUPS);
+    if constexpr (GROUPS > 1 && QS::W_HI > 64) {  // wide columns in groups: two rounds per tile
+      if ((int)qt < QS::N_HI)
+        mm4x_epilogue2<QS::W_HI, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0,
+                                          tests, s_pcnt, s_qcol, grp, (u32)GROUPS);
+      else
+        mm4x_epilogue2<QS::W_LO, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0,
+                                          tests, s_pcnt, s_qcol, grp, (u32)GROUPS);
+    } else {
+      if ((int)qt < QS::N_HI)
+        mm4x_epilogue<QS::W_HI, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0,
+                                         tests, s_pcnt, s_qcol, grp, (u32)GROUPS);
+      else
+        mm4x_epilogue<QS::W_LO, N, NACC>(a, (u32)ntile, e0, smem_u32(&tfull[0]), smem_u32(&tempty[0]), ta0, c0,
+                                         tests, s_pcnt, s_qcol, grp, (u32)GROUPS);
+    }
   } else {
     // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
     if (lane == 0) {
