@@ -213,6 +213,10 @@ int fps_last_kernel(const fps_lib* lib);
  * fp4 expanded in the kernel (kind::mxf4), 3 block-scaled fp4 from the
  * library's fp4 operand copy (the default; FPS_MMA_KIND=i8|fp4|fp4x). */
 int fps_last_mma_kind(const fps_lib* lib);
+/* Diagnostic (synchronises the device): 1 if the last tensor-core top-k had a
+ * candidate list overflow its capacity, so its exact POPC fallback pass ran
+ * (expected only for adversarial ties; the answer is exact either way). */
+int fps_mma_overflowed(fps_lib* lib, int* flag);
 /* HBM held by the handle: the tiled library, the derived copies built on
  * first use (plane-major copy of the single-query plane scan, bit-plane copy
  * of the multi-query kernels; ~21.75 and ~22.3 B per entry), and per-call

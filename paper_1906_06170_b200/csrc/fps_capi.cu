@@ -966,25 +966,23 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
   return true;
 }
 
-// Operand kind of the tensor-core scan (FPS_MMA_KIND overrides). Default by
-// batch: "fp4x", the block-scaled fp4 kernel fed from the library's fp4
-// operand copy (fps_mma4x.cuh), while the batch fits one fp4 accumulator
-// chunk (top-k: Q <= 240; range, whose hit path is heavier: Q <= 128) --
-// C5 (64-query range) 1.95 ms vs 2.29 int8 vs 2.36 bit-sliced; 192-query
-// top-k 2.41 vs 2.95 ms int8 -- else "i8", the int8 kernel (fps_mma.cuh: 256
-// queries per chunk, 16-bit packed accumulator reads; the C4 call 11.36 ms,
-// its MMA at 0.82 of the measured int8 rate; fp4x 11.45 ms). "fp4" expands
-// fp4 tiles in the kernel (fps_mma4.cuh). fp4x falls back to int8 when its
-// copy (96 B/entry) does not fit.
+// Operand kind of the tensor-core scan (FPS_MMA_KIND overrides). Default: the
+// kind whose query chunks cost fewer ns per library tile -- "fp4x", the
+// block-scaled fp4 kernel fed from the library's fp4 operand copy
+// (fps_mma4x.cuh, chunks of <= 208 / 240 queries, ~358 ns per tile), or "i8",
+// the int8 kernel (fps_mma.cuh, chunks of 256 queries, 16-bit packed
+// accumulator reads, ~500 ns per tile). Measured on 95.4 M entries: C4 (1,024
+// queries) 10.44 ms fp4x vs 11.36 i8; 240 queries 2.37 vs 2.99; 480 4.49 vs
+// 5.80; 2,048 19.7 vs 23.1; int8 wins at 241-256 and 481-512 queries. "fp4"
+// expands fp4 tiles in the kernel (fps_mma4.cuh). fp4x falls back to int8
+// when its copy (96 B/entry) does not fit.
 enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
 MmaKind mma_kind_env(u32 Q, u32 mode) {
   (void)mode;
   const char* e = std::getenv("FPS_MMA_KIND");
   if (!e) {
-    // per library tile: an fp4x chunk (<= 208 queries) costs ~358 ns, an int8
-    // chunk (256 queries) ~500 ns (95.4 M entries: 9.21 vs 10.07 ms at 5 / 4
-    // chunks); the fewer-chunk-ns kind wins, ties to int8 (no operand copy)
-    const u32 c4 = (Q + 207) / 208, c8 = (Q + 255) / 256;
+    // ties go to int8 (no operand copy)
+    const u32 c4 = std::min((Q + 207) / 208, (Q + 239) / 240), c8 = (Q + 255) / 256;  // (mma_pick_n's chunks)
     return c4 * 358u < c8 * 500u ? MMA_FP4X : MMA_I8;
   }
   const std::string v(e);
@@ -2566,6 +2564,20 @@ uint64_t fps_launch_count(const fps_lib* lib) { return lib ? lib->launches.load(
 
 int fps_last_kernel(const fps_lib* lib) { return lib ? lib->last_kernel : 0; }
 int fps_last_mma_kind(const fps_lib* lib) { return lib ? lib->last_mma_kind : 0; }
+
+int fps_mma_overflowed(fps_lib* lib, int* flag) {
+  if (int rc = check_lib(lib)) return rc;
+  if (!flag) return FPS_EINVAL;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  *flag = 0;
+  if (!lib->mm_ovf.p) return FPS_OK;
+  DeviceGuard g(lib->device);
+  u32 v = 0;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(&v, lib->mm_ovf.p, 4, cudaMemcpyDeviceToHost));
+  *flag = v != 0;
+  return FPS_OK;
+}
 
 int fps_timing(fps_lib* lib, int enable) {
   if (int rc = check_lib(lib)) return rc;

@@ -350,7 +350,8 @@ __device__ __forceinline__ void mm4x_epilogue2(const MmArgs& a, u32 ntile, u64 e
     const u64 e = e0 + (u64)it * MM_M;
     if (e >= a.n) continue;  // padding rows of the last tile
     // columns [0, H0) in m0, [H0, W) in m1 -> 64-bit halves of the W columns
-    const u64 hm0 = m0 | (m1 << H0), hm1 = m1 >> (64 - H0);
+    u64 hm0 = m0, hm1 = m1;  // (H0 == 64: already the halves)
+    if constexpr (H0 < 64) hm0 |= m1 << H0, hm1 = m1 >> (64 - H0);
     mm4x_hits<W, N>(a, hm0, hm1, cb0, a.index_base + e, s_pcnt, s_qcol);
   }
 }

@@ -255,6 +255,14 @@ class Library:
         return self.MMA_KINDS.get(int(N.load().fps_last_mma_kind(self._h)))
 
     @property
+    def mma_overflowed(self) -> bool:
+        """True if the last tensor-core top-k overflowed a candidate list and ran
+        its exact fallback pass (diagnostic; synchronises the device)."""
+        f = C.c_int(0)
+        N.check(N.load().fps_mma_overflowed(self._h, C.byref(f)), "fps_mma_overflowed")
+        return bool(f.value)
+
+    @property
     def launches(self) -> int:
         return int(N.load().fps_launch_count(self._h))
 

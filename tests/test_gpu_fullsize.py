@@ -54,12 +54,18 @@ def test_single_query_full_size(name):
 def test_config4_full_size(monkeypatch):
     plan, lib, q, w = full("c4")
     res = lib.search_batch(q, plan.k)
-    assert lib.last_kernel == "tensor-core multi-query scan"
+    assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == "fp4x"
+    assert not lib.mma_overflowed
     exp = oracle_lists(w, q, plan.k)
     for i in range(plan.Q):
         assert res.hits(i) == exp[i], i
         # the query's source entry is within its flip count
         assert res.hits(i)[0][1] <= len(plan.query_flips[i])
+    # 240 queries: one 240-column fp4 chunk
+    res240 = lib.search_batch(q[:240], plan.k)
+    assert not lib.mma_overflowed
+    for i in range(240):
+        assert res240.hits(i) == exp[i], i
     # the bit-sliced kernel (FPS_MMA=0) gives the same lists
     monkeypatch.setenv("FPS_MMA", "0")
     res2 = lib.search_batch(q, plan.k)

@@ -721,7 +721,9 @@ def test_mma_multi_query_vs_oracle(n, kind, monkeypatch):
     w = orc.generate_words(synth.seed_key(seed), synth.beta_thresholds(seed), 0, n)
     lib = Library.from_words(w)
     rng = np.random.default_rng(n)
-    for Q in (2, 100, 257, 600):  # accumulators of 64 / 128 / 256 columns, 1-3 chunks
+    # accumulators of 64 / 128 / 208-256 columns, 1-3 chunks (fp4: 230 and 470
+    # queries run 240-column chunks, 257 and 600 208-column ones)
+    for Q in (2, 100, 230, 257, 470, 600):
         q = w[rng.integers(0, n, Q)].copy()
         q[:, 0] ^= rng.integers(0, 2**24, Q).astype(np.uint64) << np.uint64(1)
         q[Q // 2] = _query_with_pop(rng, 120)  # a dense query
@@ -732,6 +734,9 @@ def test_mma_multi_query_vs_oracle(n, kind, monkeypatch):
                 assert res.hits(i) == exp[i], (n, Q, k, i)
             if n >= 128:
                 assert lib.last_kernel == "tensor-core multi-query scan" and lib.last_mma_kind == kind
+                # no candidate list overflowed (the exact fallback pass would hide
+                # a kernel that reports spurious hits)
+                assert not lib.mma_overflowed, (n, Q, k)
 
 
 def test_mma_candidate_overflow_falls_back(monkeypatch):
@@ -744,6 +749,7 @@ def test_mma_candidate_overflow_falls_back(monkeypatch):
     res = lib.search_batch(q, 10)
     for i in range(300):
         assert res.hits(i) == [(j, 1) for j in range(10)]
+    assert lib.mma_overflowed
 
 
 def test_mma_pad_bits_counted():
