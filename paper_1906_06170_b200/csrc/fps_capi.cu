@@ -969,13 +969,12 @@ bool mma_wanted(fps_lib* L, u32 Q, u32 k, MmaPlan* plan = nullptr) {
 // Operand kind of the tensor-core scan (FPS_MMA_KIND overrides). Default: the
 // kind whose query chunks cost fewer ns per library tile -- "fp4x", the
 // block-scaled fp4 kernel fed from the library's fp4 operand copy
-// (fps_mma4x.cuh, chunks of <= 208 / 240 queries, ~358 ns per tile), or "i8",
+// (fps_mma4x.cuh, chunks of <= 208 / 240 queries, ~303 ns per tile), or "i8",
 // the int8 kernel (fps_mma.cuh, chunks of 256 queries, 16-bit packed
-// accumulator reads, ~500 ns per tile). Measured on 95.4 M entries: C4 (1,024
-// queries) 10.44 ms fp4x vs 11.36 i8; 240 queries 2.37 vs 2.99; 480 4.49 vs
-// 5.80; 2,048 19.7 vs 23.1; int8 wins at 241-256 and 481-512 queries. "fp4"
-// expands fp4 tiles in the kernel (fps_mma4.cuh). fp4x falls back to int8
-// when its copy (96 B/entry) does not fit.
+// accumulator reads, ~482 ns per tile). Measured on 95.4 M entries (scan
+// kernel): 1,024 queries 7.63 ms fp4x vs 9.58 i8; 256 queries 2.43 ms i8 vs
+// 2 fp4x chunks. "fp4" expands fp4 tiles in the kernel (fps_mma4.cuh). fp4x
+// falls back to int8 when its copy (96 B/entry) does not fit.
 enum MmaKind { MMA_I8 = 0, MMA_FP4 = 1, MMA_FP4X = 2 };
 MmaKind mma_kind_env(u32 Q, u32 mode) {
   (void)mode;
@@ -983,7 +982,7 @@ MmaKind mma_kind_env(u32 Q, u32 mode) {
   if (!e) {
     // ties go to int8 (no operand copy)
     const u32 c4 = std::min((Q + 207) / 208, (Q + 239) / 240), c8 = (Q + 255) / 256;  // (mma_pick_n's chunks)
-    return c4 * 358u < c8 * 500u ? MMA_FP4X : MMA_I8;
+    return c4 * 310u < c8 * 482u ? MMA_FP4X : MMA_I8;
   }
   const std::string v(e);
   return v == "fp4" ? MMA_FP4 : v == "fp4x" ? MMA_FP4X : MMA_I8;

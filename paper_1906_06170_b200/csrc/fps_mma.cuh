@@ -204,6 +204,19 @@ __device__ __forceinline__ void mm_bar_wait(u64* bar, u32 parity) {
       "r"(parity), "r"(MM_SUSPEND_NS)
       : "memory");
 }
+// One elected lane of a converged warp. The single-thread roles (MMA issuer,
+// TMA loader) run their loops with the whole warp and issue under this: in a
+// lane-0-only branch every tcgen05 / TMA instruction's operands live in vector
+// registers and ptxas wraps each in a per-lane loop (R2UR, ELECT, BRA.U.ANY),
+// which costs ~775 clk per tile of 3 MMAs + 2 commits + 2 waits against 312 clk
+// warp-uniform (tools/microbench/mma_lane.cu, profiles/r02_mma_lane.txt).
+__device__ __forceinline__ bool mm_elect_one() {
+  u32 pred = 0;
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
+// A warp index / shared value the compiler can treat as warp-uniform.
+__device__ __forceinline__ int mm_warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
 __device__ __forceinline__ void mm_commit(u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   __shared__ u32 lut[16];
   __shared__ int s_t[N];
   __shared__ u32 s_qcol[N], s_qpop[N], s_pcnt[N];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = mm_warp_uniform(tid >> 5), lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
   const u64 part = blockIdx.x / a.nchunks;
   // CTA work: a contiguous run of library tiles (SUB MMA tiles of 128 entries each)
@@ -303,7 +316,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const u32 tmem = tmem_base;
+  const u32 tmem = (u32)mm_warp_uniform((int)tmem_base);
   const u64 ntile = nraw * SUB;
 
   if (warp < 4) {
@@ -354,23 +367,22 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       mm_bar_arrive(&full_bar[s]);
     }
   } else if (warp == 5 + MM_EPI) {
-    // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
-    if (lane == 0 && !(a.flags & 8192)) {
-      const u64 pol = l2_evict_first_policy();
-      for (u64 r = 0; r < nraw; ++r) {
-        const int rs = (int)(r % MM_RAW);
-        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
-        mbar_expect_tx(&raw_full[rs], RAW_BYTES);
-        bulk_g2s_stream(raw + (u64)rs * RAW_BYTES, a.lib.base + (r0 + r) * RAW_BYTES, RAW_BYTES, &raw_full[rs], pol);
+    // ===== loader (the whole warp waits, one elected lane issues): library
+    // tiles -> raw ring, cp.async.bulk
+    const u64 pol = l2_evict_first_policy();
+    for (u64 r = 0; r < nraw; ++r) {
+      const int rs = (int)(r % MM_RAW);
+      if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
+      if (mm_elect_one()) {
+        if (a.flags & 8192) {  // experiment: no library loads
+          mm_bar_arrive(&raw_full[rs]);
+        } else {
+          mbar_expect_tx(&raw_full[rs], RAW_BYTES);
+          bulk_g2s_stream(raw + (u64)rs * RAW_BYTES, a.lib.base + (r0 + r) * RAW_BYTES, RAW_BYTES, &raw_full[rs], pol);
+        }
       }
-    } else if (lane == 0) {
-      for (u64 r = 0; r < nraw; ++r) {
-        const int rs = (int)(r % MM_RAW);
-        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
-        mm_bar_arrive(&raw_full[rs]);
-      }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp < 4 + MM_EPI) {
     // ===== epilogue: two groups of 8 warps take alternate tiles (group g
     // always reads accumulator g), so a group has two MMA tiles of time for
@@ -447,21 +459,21 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
       }
     }
   } else {
-    // ===== MMA issuer (one lane)
-    if (lane == 0) {
-      // s32 += u8 (library) x s8 (queries, fused-test terms), both K-major
-      const u32 idesc = (2u << 4) | (1u << 10) | ((u32)(N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);
-      // descriptors: built once; a K step / stage only moves the start
-      // address field (bits 0-13, in 16-byte units; shared addresses < 256 KB
-      // never carry out of it), so the issue loop is a few uniform adds per MMA
-      const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
-      const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
-      constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM_A_BYTES / 16;
-      for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
-        if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
-        mm_bar_wait(&full_bar[s], (u32)(it / MM_STAGES) & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ===== MMA issuer (the whole warp waits, one elected lane issues)
+    // s32 += u8 (library) x s8 (queries, fused-test terms), both K-major
+    const u32 idesc = (2u << 4) | (1u << 10) | ((u32)(N >> 3) << 17) | ((u32)(MM_M >> 4) << 24);
+    // descriptors: built once; a K step / stage only moves the start
+    // address field (bits 0-13, in 16-byte units; shared addresses < 256 KB
+    // never carry out of it), so the issue loop is a few uniform adds per MMA
+    const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
+    const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
+    constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM_A_BYTES / 16;
+    for (u64 it = 0; it < ntile; ++it) {
+      const int s = (int)(it % MM_STAGES), b = (int)(it & 1);
+      if (it >= 2) mm_bar_wait(&tempty[b], (u32)((it >> 1) - 1) & 1u);
+      mm_bar_wait(&full_bar[s], (u32)(it / MM_STAGES) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (mm_elect_one()) {
         const u64 das = da0 + (u64)s * DA_S;
         const u32 dt = tmem + (u32)b * N;
 #pragma unroll
@@ -476,8 +488,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
         mm_commit(&empty_bar[s]);
         mm_commit(&tfull[b]);
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

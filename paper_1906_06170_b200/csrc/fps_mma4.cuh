@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
   __shared__ u32 tmem_base;
   __shared__ uint2 luta[176];  // |a| -> block-5 test nibbles of words 0 and 1 (digits of -|a|, A = 6)
   __shared__ u32 s_qcol[N], s_pcnt[N];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = mm_warp_uniform(tid >> 5), lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
   const u64 part = blockIdx.x / a.nchunks;
   const u32 SUB = a.lib.compact ? TILE_CMP / MM_M : TILE_FULL / MM_M;
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const u32 tmem = tmem_base;
+  const u32 tmem = (u32)mm_warp_uniform((int)tmem_base);
   if (warp < 4) {  // scale factors: every byte of columns 480..511 = ue8m0 127 (1.0)
     for (u32 c = MM4_SF_COL; c < TMEM_COLS; c += 8)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
@@ -495,23 +495,22 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
       if (tid == 0) MM4_TRACE(5);
     }
   } else if (warp == 5 + MM_EPI) {
-    // ===== loader (one lane): library tiles -> raw ring, cp.async.bulk
-    if (lane == 0 && (a.flags & 8192)) {  // experiment: no library loads
-      for (u64 r = 0; r < nraw; ++r) {
-        const int rs = (int)(r % MM_RAW);
-        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
-        mm_bar_arrive(&raw_full[rs]);
+    // ===== loader (the whole warp waits, one elected lane issues): library
+    // tiles -> raw ring, cp.async.bulk
+    const u64 pol = l2_evict_first_policy();
+    for (u64 r = 0; r < nraw; ++r) {
+      const int rs = (int)(r % MM_RAW);
+      if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
+      if (mm_elect_one()) {
+        if (a.flags & 8192) {  // experiment: no library loads
+          mm_bar_arrive(&raw_full[rs]);
+        } else {
+          mbar_expect_tx(&raw_full[rs], RAW_BYTES);
+          bulk_g2s_stream(raw + (u64)rs * RAW_BYTES, a.lib.base + (r0 + r) * RAW_BYTES, RAW_BYTES, &raw_full[rs], pol);
+        }
       }
-    } else if (lane == 0) {
-      const u64 pol = l2_evict_first_policy();
-      for (u64 r = 0; r < nraw; ++r) {
-        const int rs = (int)(r % MM_RAW);
-        if (r >= MM_RAW) mm_bar_wait(&raw_empty[rs], (u32)((r / MM_RAW) - 1) & 1u);
-        mbar_expect_tx(&raw_full[rs], RAW_BYTES);
-        bulk_g2s_stream(raw + (u64)rs * RAW_BYTES, a.lib.base + (r0 + r) * RAW_BYTES, RAW_BYTES, &raw_full[rs], pol);
-      }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp < 4 + MM_EPI) {
    if constexpr (GROUPED) {
     // ===== epilogue, N = 64: 4 groups of 4 warps (one per lane quadrant, all
@@ -544,36 +543,37 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
     }
    }
   } else {
-    // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
-    if (lane == 0) {
-      const u32 idesc = (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | (1u << 23) | ((u32)(MM_M >> 4) << 24);
-      const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
-      const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
-      // K = 64 elements = 32 bytes = two core matrices per MMA
-      constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4_A_BYTES / 16;
-      const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
-      for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM4_STAGES), b = (int)(it % NACC);
-        if (a.suspend_ns) {
-          if (it >= NACC) mm_bar_wait_ns(&tempty[b], (u32)((it / NACC) - 1) & 1u, a.suspend_ns);
-          mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4_STAGES) & 1u, a.suspend_ns);
-        } else {
-          if (it >= NACC) mm_bar_wait_spin(&tempty[b], (u32)((it / NACC) - 1) & 1u);
-          MM4_TRACE(0);
-          mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4_STAGES) & 1u);
-        }
-        MM4_TRACE(1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ===== MMA issuer (the whole warp waits, one elected lane issues):
+    // f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
+    const u32 idesc = (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | (1u << 23) | ((u32)(MM_M >> 4) << 24);
+    const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
+    const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
+    // K = 64 elements = 32 bytes = two core matrices per MMA
+    constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4_A_BYTES / 16;
+    const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
+    for (u64 it = 0; it < ntile; ++it) {
+      const int s = (int)(it % MM4_STAGES), b = (int)(it % NACC);
+      if (a.suspend_ns) {
+        if (it >= NACC) mm_bar_wait_ns(&tempty[b], (u32)((it / NACC) - 1) & 1u, a.suspend_ns);
+        mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4_STAGES) & 1u, a.suspend_ns);
+      } else {
+        if (it >= NACC) mm_bar_wait_spin(&tempty[b], (u32)((it / NACC) - 1) & 1u);
+        MM4_TRACE(0);
+        mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4_STAGES) & 1u);
+      }
+      MM4_TRACE(1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (mm_elect_one()) {
         const u64 das = da0 + (u64)s * DA_S;
         const u32 dt = tmem + (u32)b * N;
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks) mm4_mma(dt, das + ks * DA_K, db0 + ks * DB_K, idesc, ks > 0, sfa, sfb);
         mm_commit(&empty_bar[s]);
         mm_commit(&tfull[b]);
-        MM4_TRACE(2);
       }
+      __syncwarp();
+      MM4_TRACE(2);
     }
-    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
   __shared__ __align__(8) u64 full_bar[MM4X_STAGES], empty_bar[MM4X_STAGES], tfull[NACC], tempty[NACC];
   __shared__ u32 tmem_base;
   __shared__ u32 s_qcol[N], s_pcnt[N];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = mm_warp_uniform(tid >> 5), lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
   const u64 part = blockIdx.x / a.nchunks;
   const u64 t0 = part * a.n_tiles / a.parts, t1 = (part + 1) * a.n_tiles / a.parts;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const u32 tmem = tmem_base;
+  const u32 tmem = (u32)mm_warp_uniform((int)tmem_base);
   if (warp < 4) {  // scale factors: every byte of columns 480..511 = ue8m0 127 (1.0)
     for (u32 c = MM4_SF_COL; c < TMEM_COLS; c += 8)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
@@ -167,39 +167,40 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   if (warp == MM4X_EPI + 1) {
-    // ===== loader (one lane): A tiles of the operand copy -> stage ring
-    if (lane == 0) {
-      const bool first = (a.flags & (1u << 22)) != 0;  // experiment: L2 evict-first on the operand tiles
-      const u64 pol = l2_evict_first_policy();
-      for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM4X_STAGES);
-        if (it >= (u64)MM4X_STAGES) mm_bar_wait_spin(&empty_bar[s], (u32)((it / MM4X_STAGES) - 1) & 1u);
-        MM4_TRACE(3);
+    // ===== loader (the whole warp waits, one elected lane issues): A tiles
+    // of the operand copy -> stage ring
+    const bool first = (a.flags & (1u << 22)) != 0;  // experiment: L2 evict-first on the operand tiles
+    const u64 pol = l2_evict_first_policy();
+    for (u64 it = 0; it < ntile; ++it) {
+      const int s = (int)(it % MM4X_STAGES);
+      if (it >= (u64)MM4X_STAGES) mm_bar_wait_spin(&empty_bar[s], (u32)((it / MM4X_STAGES) - 1) & 1u);
+      MM4_TRACE(3);
+      if (mm_elect_one()) {
         if (a.flags & 8192) {  // experiment: no operand loads (timing only)
           mm_bar_arrive(&full_bar[s]);
-          continue;
-        }
-        mbar_expect_tx(&full_bar[s], MM4X_TILE);
-        const unsigned char* src = op + (t0 + it) * MM4X_TILE;
-        if (!(a.flags & (1u << 24))) {  // default: one TMA tensor box (flag 1 << 24: a 1-D bulk copy)
-          asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-              "[%4];" ::"r"(smem_u32(sA + (u64)s * MM4X_TILE)),
-              "l"(reinterpret_cast<u64>(&tmap)), "r"(0), "r"((u32)((t0 + it) * MM4X_BOX_ROWS)),
-              "r"(smem_u32(&full_bar[s]))
-              : "memory");
-        } else if (first) {
-          bulk_g2s_stream(sA + (u64)s * MM4X_TILE, src, MM4X_TILE, &full_bar[s], pol);
         } else {
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(sA + (u64)s * MM4X_TILE)),
-              "l"(src), "r"(MM4X_TILE), "r"(smem_u32(&full_bar[s]))
-              : "memory");
+          mbar_expect_tx(&full_bar[s], MM4X_TILE);
+          const unsigned char* src = op + (t0 + it) * MM4X_TILE;
+          if (!(a.flags & (1u << 24))) {  // default: one TMA tensor box (flag 1 << 24: a 1-D bulk copy)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3}], [%4];" ::"r"(smem_u32(sA + (u64)s * MM4X_TILE)),
+                "l"(reinterpret_cast<u64>(&tmap)), "r"(0), "r"((u32)((t0 + it) * MM4X_BOX_ROWS)),
+                "r"(smem_u32(&full_bar[s]))
+                : "memory");
+          } else if (first) {
+            bulk_g2s_stream(sA + (u64)s * MM4X_TILE, src, MM4X_TILE, &full_bar[s], pol);
+          } else {
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sA + (u64)s * MM4X_TILE)),
+                "l"(src), "r"(MM4X_TILE), "r"(smem_u32(&full_bar[s]))
+                : "memory");
+          }
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp < MM4X_EPI) {
     // ===== epilogue: EPI warps, every tile; warp e reads TMEM lane quadrant
     // e % 4 and column part e / 4 -- one load wait per tile per warp, one
@@ -230,26 +231,22 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
                                          tests, s_pcnt, s_qcol, grp, (u32)GROUPS);
     }
   } else {
-    // ===== MMA issuer (one lane): f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
-    if (lane == 0) {
-      const u32 idesc = (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | (1u << 23) | ((u32)(MM_M >> 4) << 24);
-      const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
-      const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
-      // K = 64 elements = 32 bytes = two core matrices per MMA
-      constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4X_TILE / 16;
-      const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
-      for (u64 it = 0; it < ntile; ++it) {
-        const int s = (int)(it % MM4X_STAGES), b = (int)(it % NACC);
-        MM4_TRACE(0);
-        if (a.flags & (1u << 27)) {  // experiment: suspend-hint waits on the MMA lane
-          if (it >= NACC) mm_bar_wait_ns(&tempty[b], (u32)((it / NACC) - 1) & 1u, 20000u);
-          mm_bar_wait_ns(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u, 20000u);
-        } else {
-          if (it >= NACC) mm_bar_wait_spin(&tempty[b], (u32)((it / NACC) - 1) & 1u);
-          mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u);
-        }
-        MM4_TRACE(1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ===== MMA issuer (the whole warp waits, one elected lane issues):
+    // f32 += e2m1 (library) x e2m1 (queries, test terms), K-major
+    const u32 idesc = (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | (1u << 23) | ((u32)(MM_M >> 4) << 24);
+    const u64 db0 = mm_desc(smem_u32(sB), N / 8 * 128, 128);
+    const u64 da0 = mm_desc(smem_u32(sA), MM_M / 8 * 128, 128);
+    // K = 64 elements = 32 bytes = two core matrices per MMA
+    constexpr u64 DA_K = 2 * (MM_M / 8 * 128) / 16, DB_K = 2 * (N / 8 * 128) / 16, DA_S = MM4X_TILE / 16;
+    const u32 sfa = tmem + MM4_SF_COL, sfb = tmem + MM4_SF_COL + 16;
+    for (u64 it = 0; it < ntile; ++it) {
+      const int s = (int)(it % MM4X_STAGES), b = (int)(it % NACC);
+      MM4_TRACE(0);
+      if (it >= NACC) mm_bar_wait_spin(&tempty[b], (u32)((it / NACC) - 1) & 1u);
+      mm_bar_wait_spin(&full_bar[s], (u32)(it / MM4X_STAGES) & 1u);
+      MM4_TRACE(1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (mm_elect_one()) {
         const u64 das = da0 + (u64)s * DA_S;
         const u32 dt = tmem + (u32)b * N;
         if (!(a.flags & (1u << 23))) {  // (experiment: no MMAs, timing only)
@@ -258,10 +255,10 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
         }
         mm_commit(&empty_bar[s]);
         mm_commit(&tfull[b]);
-        MM4_TRACE(2);
       }
+      __syncwarp();
+      MM4_TRACE(2);
     }
-    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
