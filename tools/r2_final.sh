@@ -10,5 +10,5 @@ timeout 900 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.er
 timeout 900 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref_c3.json 2> gpurun_out/bench_ref_c3.err
 for w in c1 c2 c4 c5; do timeout 900 python bench.py --workload $w --steps 20 --warmup 3 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
 CMD="python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu-baseline"
-$CMD > gpurun_out/plain_c4.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:mma -s 3 -c 1 -o gpurun_out/prof_c4 $CMD > gpurun_out/ncu_c4.log 2>&1
+$CMD > gpurun_out/plain_c4.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:mma4x_scan -s 3 -c 1 -o gpurun_out/prof_c4 $CMD > gpurun_out/ncu_c4.log 2>&1
 echo "ncu rc=$?"
