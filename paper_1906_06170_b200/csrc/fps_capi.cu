@@ -178,7 +178,7 @@ struct fps_lib {
   // getenv is a linear scan of the environment, and this is the per-call path
   struct PqKnobs {
     bool init = false, sorted = false;
-    int bpl = 0, warps = 8, stages = 2, smem_kb = 210, copy = 1, refresh = 0;
+    int bpl = 0, warps = 8, stages = 2, smem_kb = 210, copy = 1, refresh = 0, wave_pct = 50, wave_ns = 8000;
   } pqk;
   u32 done_seq = 0;  // completion sequence of the single-query host path
   // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
@@ -795,6 +795,10 @@ bool pq_wanted(fps_lib* L) {
     L->pqk.smem_kb = ev("FPS_PQ_SMEM_KB", 210);
     L->pqk.copy = ev("FPS_PQ_COPY", 1) == 1 ? 1 : 0;
     L->pqk.refresh = ev("FPS_PQ_REFRESH", 0);
+    // first wave: before its second step a warp waits (at most wave_ns) until
+    // wave_pct % of the warps have posted their first step's witnesses
+    L->pqk.wave_pct = std::max(0, std::min(100, ev("FPS_PQ_WAVE_PCT", 50)));
+    L->pqk.wave_ns = std::max(0, ev("FPS_PQ_WAVE_NS", 8000));
     L->pqk.init = true;
   }
   if (pm_ensure(L, L->pqk.sorted) != FPS_OK) {
@@ -873,6 +877,14 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   a.meta = srt ? reinterpret_cast<const unsigned short*>(L->pm_meta.p) : nullptr;
   a.meta_cap = meta_cap;
   a.pub_every = (u32)std::max<u64>(1, warps / 512);
+  {
+    // warps whose first step is a full one post k witnesses each
+    const u64 tw = std::min<u64>(L->n / step_entries, warps);
+    const u64 need = tw * (u64)L->pqk.wave_pct / 100;
+    // (libraries with fewer than two steps per warp have no second step to speed up)
+    a.wave_target = (k <= step_entries && need > 0 && steps >= 2 * warps) ? (u32)std::min<u64>(need * k, 0x7fffffffu) : 0u;
+    a.wave_wait_ns = (u32)L->pqk.wave_ns;
+  }
   a.flags = scan_flags();
   a.tg = L->tg.as<u32>();
   a.ghist = L->ghist.as<u32>();
@@ -2317,11 +2329,25 @@ extern "C" int fps_trace_phases(uint64_t* ph) {
   cudaDeviceSynchronize();
   return (int)cudaMemcpyFromSymbol(ph, fps::g_pq_phase, sizeof(fps::g_pq_phase));
 }
+extern "C" int fps_trace_prologue(uint64_t* pro) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(pro, fps::g_pq_pro, sizeof(fps::g_pq_pro));
+}
+extern "C" int fps_trace_s1(uint64_t* st) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(st, fps::g_pq_s1, sizeof(fps::g_pq_s1));
+}
+extern "C" int fps_trace_steps(uint64_t* st) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(st, fps::g_pq_steps, sizeof(fps::g_pq_steps));
+}
 extern "C" int fps_trace_clear() {
   static u64 zeros[16384 * 8];
   cudaDeviceSynchronize();
   cudaMemcpyToSymbol(fps::g_mark, zeros, 8 * sizeof(u64));
   cudaMemcpyToSymbol(fps::g_pq_phase, zeros, sizeof(fps::g_pq_phase));
+  cudaMemcpyToSymbol(fps::g_pq_steps, zeros, sizeof(fps::g_pq_steps));
+  cudaMemcpyToSymbol(fps::g_pq_s1, zeros, sizeof(fps::g_pq_s1));
   return (int)cudaMemcpyToSymbol(fps::g_scan_trace, zeros, sizeof(fps::g_scan_trace));
 }
 #endif

@@ -125,6 +125,8 @@ struct PqArgs {
   u32 pub_every;        // warps with g % pub_every == 0 publish witnesses
   u32 flags;            // FPS_SCAN_FLAGS: 1 = no publishing, 2 = no tg refresh
   u32 refresh;          // steps between reads of the global bound (1 = every step)
+  u32 wave_target;      // witnesses of the first wave a warp waits for before its second step (0: no wait)
+  u32 wave_wait_ns;     // ... for at most this long
   u32* tg;
   u32* ghist;
   u32 gstride, tg_rep;
@@ -151,6 +153,9 @@ __host__ __device__ inline size_t pq_smem(int nwb, u32 ring_bytes, u32 meta_cap 
 // (LDGSTS) per lane, two planes per warp instruction, completion through
 // cp.async.mbarrier.arrive.noinc on the same stage barriers.
 #ifdef FPS_SCAN_TRACE
+__device__ u64 g_pq_pro[16384 * 4];    // per warp, prologue: list built, ring initialised, requests issued, dependency wait over
+__device__ u64 g_pq_s1[16384 * 4];     // per warp, second step: bound taken, held-back entries inserted, CSA done
+__device__ u64 g_pq_steps[16384 * 8];  // per warp: tile-ready time of its first 8 steps
 __device__ u64 g_pq_phase[16384 * 8];  // per warp, first step: CSA done, refill issued, bound, mask, inserted, published
 #endif
 // SORTED: the plane copy is ordered by popcount |a| (then index). A step whose
@@ -159,6 +164,11 @@ __device__ u64 g_pq_phase[16384 * 8];  // per warp, first step: CSA done, refill
 // (d >= ||a| - |q||) are not read at all, and since a warp no longer meets
 // entries in index order, ties at its own k-th distance are kept and resolved
 // by index (full (d, index) key order) when the buffer is compacted.
+__device__ __forceinline__ u64 pq_now_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 template <int COPY, int BPL, bool SORTED>
 __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   static_assert(!SORTED || COPY == 1, "the sorted copy is read with cp.async");
@@ -173,9 +183,11 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
 #ifdef FPS_SCAN_TRACE
   u64 tr_start = gtimer(), tr_first = 0, tr_step1 = 0;
   bool ph_done = false;
+  u32 tr_iter = ~0u;  // steps taken so far - 1
 #endif
   __shared__ u32 s_list[PQ_NPMAX];  // source plane of each stage position (BS_ZERO: zero padding)
   __shared__ u32 s_np, s_nc, s_pop, s_dense, s_next;
+  __shared__ u32 s_wave_poll, s_wave_T;  // first wave: poller election, the bound it found (| 1 << 31)
   __shared__ const u32* s_base[PQ_NPMAX];  // plane base of each copied position (COPY 1)
 
   // ---- the query's plane list (read-only inputs: safe before the dependency wait)
@@ -207,6 +219,8 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       s_pop = pop;
       s_dense = dense;
       s_next = 0;
+      s_wave_poll = 0;
+      s_wave_T = 0;
     }
   }
   __syncthreads();
@@ -236,6 +250,9 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     }
   }
   __syncthreads();  // the last block-level barrier
+#ifdef FPS_SCAN_TRACE
+  const u64 tr_p0 = gtimer();
+#endif
   const u32 np = s_np, nc = s_nc, pop = s_pop;
   const bool dense = s_dense != 0;
   const u32 stage_bytes = np * PQ_CHUNK;
@@ -258,27 +275,23 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
                                                 2 * nwb * PQ_SMAX) + nwb * HB) + wib;
   const u64 g = (u64)blockIdx.x * nact + wib;  // global warp id (buffers, publishing)
 
-  // zero padding positions of every slot (never written by the copies)
-  for (u32 st = 0; st < S; ++st) {
-    u32* sp = reinterpret_cast<u32*>(ring + st * stage_bytes);
-    for (u32 i = nc * PQ_WORDS + lane; i < np * PQ_WORDS; i += 32) sp[i] = 0;
-  }
+  // the stage barriers first: the requests go out as early as possible, the
+  // rest of the per-warp state is set up while they fly
   const u32* src[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const u32 pos = lane + 32 * r;
     src[r] = pos < nc ? a.pm + (u64)s_list[pos] * a.pstride : nullptr;
   }
-  for (int i = lane; i < HB; i += 32) hist[i] = 0;
   if (lane == 0) {
-    ws->town[0] = T_OPEN;
-    ws->pubd[0] = 0;
-    ws->cnt[0] = 0;
     for (u32 st = 0; st < S; ++st) mbar_init(&bars[st], COPY == 1 ? 32u : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
 
+#ifdef FPS_SCAN_TRACE
+  const u64 tr_p1 = gtimer();
+#endif
   const u64 pol = l2_evict_first_policy();
   const u32 half = (u32)lane / LPP;  // position within a cp.async group
   u32 T = T_OPEN;  // accept d < T
@@ -344,8 +357,31 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     }
   };
   for (u32 st = 0; st < S; ++st) issue(st);
+  // zero padding positions of every slot (never written by the copies)
+  for (u32 st = 0; st < S; ++st) {
+    u32* sp = reinterpret_cast<u32*>(ring + st * stage_bytes);
+    for (u32 i = nc * PQ_WORDS + lane; i < np * PQ_WORDS; i += 32) sp[i] = 0;
+  }
+  for (int i = lane; i < HB; i += 32) hist[i] = 0;
+  if (lane == 0) {
+    ws->town[0] = T_OPEN;
+    ws->pubd[0] = 0;
+    ws->cnt[0] = 0;
+  }
+  __syncwarp();
+#ifdef FPS_SCAN_TRACE
+  const u64 tr_p2 = gtimer();
+#endif
   // ---- everything below touches the per-call state the previous select resets
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef FPS_SCAN_TRACE
+  if (lane == 0 && g < 16384) {
+    g_pq_pro[g * 4 + 0] = tr_p0;
+    g_pq_pro[g * 4 + 1] = tr_p1;
+    g_pq_pro[g * 4 + 2] = tr_p2;
+    g_pq_pro[g * 4 + 3] = gtimer();
+  }
+#endif
 
   u64* wbuf = a.buf + g * (u64)a.cap;
   u64* tie_scratch = reinterpret_cast<u64*>(pqs + pq_smem(nwb, a.ring_bytes) - (size_t)nwb * 32 * 8) + wib * 32;
@@ -357,7 +393,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   bool tpend = false;
   // smallest T with >= k published witnesses d <= T -> every replica of tg;
   // returns the new filter limit (accept d < limit)
-  auto finish_tighten = [&]() -> u32 {
+  auto finish_tighten = [&](bool post = true) -> u32 {
     tpend = false;
     u32 sum = 0;
 #pragma unroll
@@ -376,9 +412,12 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       }
     }
     tt = __shfl_sync(FULL, tt, src);
-    for (u32 r = lane; r < a.tg_rep; r += 32) atomicMin(tgrep(a, 0, r), tt);
+    if (post)
+      for (u32 r = lane; r < a.tg_rep; r += 32) atomicMin(tgrep(a, 0, r), tt);
     return (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
   };
+  bool first = true;  // the warp's first tile: the bound is read afresh
+  bool wave = false;  // first-step witnesses posted: the second step waits for the first wave's
 
   // Compaction to the k best by (d, index): every entry with d < tt (the
   // k-th distance), then m = k - count(d < tt) of the ties. In index order
@@ -581,13 +620,54 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     if (t == PQ_NONE) break;
 #ifdef FPS_SCAN_TRACE
     if (!tr_first) tr_first = gtimer();
+    ++tr_iter;
+    if (lane == 0 && g < 16384 && tr_iter < 8) g_pq_steps[g * 8 + tr_iter] = gtimer();  // start of every step (a store: no stall)
 #endif
+    // first tile: the bound other warps may have set meanwhile (the load
+    // flies under the carry-save count)
+    u32 tfresh = T_OPEN;
+    if (first && !(a.flags & 2)) tfresh = *tgw;
     if (a.flags & 512) {  // experiment: stream only (no compute; results are not valid)
       __syncwarp();
       issue(st);
       continue;
     }
-    if (tpend) {
+    if (wave) {
+      // Second step: every warp posted its first step's witnesses at about
+      // the same time. Wait (bounded) until wave_target of them are visible,
+      // then take the bound from the histogram: this step, the held-back
+      // first-step entries and everything after run under a bound drawn from
+      // hundreds of thousands of entries instead of the warp's own 2,048 --
+      // inserts become rare and the scan streams.
+      wave = false;
+      // one warp per CTA polls the global histogram (every warp polling its
+      // 224 lines costs ~4 us of L2 hot-line traffic); the others take the
+      // bound from shared memory
+      u32 r = 0;
+      if (lane == 0) r = atomicAdd(&s_wave_poll, 1u);
+      r = __shfl_sync(FULL, r, 0);
+      const u64 t0 = pq_now_ns();
+      u32 lim = T_OPEN;
+      if (r == 0) {
+        for (;;) {
+#pragma unroll
+          for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
+          u32 sum = 0;
+#pragma unroll
+          for (int i = 0; i < 7; ++i) sum += hv[i];
+          sum = __reduce_add_sync(FULL, sum);
+          if (sum >= a.wave_target || pq_now_ns() - t0 > a.wave_wait_ns) break;
+        }
+        lim = finish_tighten(true);
+        if (lane == 0) *(volatile u32*)&s_wave_T = lim | 0x80000000u;
+      } else {
+        u32 v;
+        while (!(v = *(volatile const u32*)&s_wave_T) && pq_now_ns() - t0 < (u64)a.wave_wait_ns + 2000) __nanosleep(40);
+        if (v) lim = v & 0xffffu;
+      }
+      T = lim < T ? lim : T;
+      tlim = lim < tlim ? lim : tlim;
+    } else if (tpend) {
       const u32 lim = finish_tighten();
       T = lim < T ? lim : T;
       tlim = lim < tlim ? lim : tlim;
@@ -598,7 +678,13 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       T = tl < T ? tl : T;
       tlim = tl < tlim ? tl : tlim;
     }
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && tr_iter == 1) g_pq_s1[g * 4 + 0] = gtimer();
+#endif
     if (pending) flush_pending(false);  // the previous step's held-back entries first (index order)
+#ifdef FPS_SCAN_TRACE
+    if (lane == 0 && g < 16384 && tr_iter == 1) g_pq_s1[g * 4 + 1] = gtimer();
+#endif
     const char* stage = ring + st * stage_bytes;
     const char* lb = stage + 4 * BPL * lane;  // this lane's BPL words of every position
     // one shared load fetches a plane word of all BPL blocks of the lane
@@ -705,14 +791,15 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
 #undef CSA
 
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 0]) g_pq_phase[g * 8 + 0] = gtimer();
+    if (lane == 0 && g < 16384 && tr_iter == 0) g_pq_phase[g * 8 + 0] = gtimer();
+    if (lane == 0 && g < 16384 && tr_iter == 1) g_pq_s1[g * 4 + 2] = gtimer();
 #endif
     // every lane is done reading this slot: refill it with the step S ahead
     __syncwarp();
     if (COPY == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 1]) g_pq_phase[g * 8 + 1] = gtimer();
+    if (lane == 0 && g < 16384 && tr_iter == 0) g_pq_phase[g * 8 + 1] = gtimer();
 #endif
     issue(st);
     if (!(a.flags & 2) && ++since_refresh >= a.refresh) {  // applied at the next step
@@ -739,9 +826,15 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       return bs_sign_after_add(X[h], (pop - Tq) & 0x3ffu) & valid[h];
     };
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 2]) g_pq_phase[g * 8 + 2] = gtimer();
+    if (lane == 0 && g < 16384 && tr_iter == 0) g_pq_phase[g * 8 + 2] = gtimer();
 #endif
 
+    if (first) {
+      first = false;
+      const u32 tl = (tfresh < T_OPEN ? tfresh : T_OPEN - 1) + 1;
+      T = tl < T ? tl : T;
+      tlim = tl < tlim ? tl : tlim;
+    }
     if (T >= T_OPEN && !pending) {
       // ---- the warp's first step, no bound known yet. Distances of the
       // whole step bit-sliced (D = X + |q|), the k-th smallest by radix
@@ -807,9 +900,12 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       Tsv = 256;  // fewer than k entries: every one is a candidate
       if (nv >= a.k) {
         u32 town1 = 0;
-        if (publisher) {
+        const bool wv = a.wave_target != 0 && !(a.flags & 1);
+        if (publisher || wv) {
           // witnesses: 1 at the smallest distance, 1 at the 2nd, 2 at the 4th,
-          // k - 4 at the k-th (ranks capped at k)
+          // k - 4 at the k-th (ranks capped at k). With many more warps than
+          // k the bound is set by the warps' smallest distances: higher ranks
+          // (8th ... 64th) bought nothing.
           const u32 rs[4] = {1u, min(2u, a.k), min(4u, a.k), a.k};
           u32 ts[4];
           rsel(rs, ts);
@@ -820,10 +916,16 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
             if (rl > prev) atomicAdd(gbin(a, 0, tl), rl - prev);
           }
           town1 = ts[3];
-          if (lane == 0) ws->pubd[0] = 1;
+          if (publisher && lane == 0) ws->pubd[0] = 1;
+          if (wv) {
+            // first wave: every warp posts; the second step takes the bound
+            // from all of them (below)
+            wave = true;
+          } else {
 #pragma unroll
-          for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
-          tpend = true;
+            for (int i = 0; i < 7; ++i) hv[i] = *(volatile const u32*)gbin(a, 0, lane * 7 + i);
+            tpend = true;
+          }
         } else {
           const u32 rs[1] = {a.k};
           u32 ts[1];
@@ -846,7 +948,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     }
 
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 3]) g_pq_phase[g * 8 + 3] = gtimer();
+    if (lane == 0 && g < 16384 && tr_iter == 1) g_pq_phase[g * 8 + 3] = gtimer();
 #endif
     u32 em[BPL];
 #pragma unroll
@@ -864,7 +966,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       return dense ? pop - av + 2 * cv : av + pop - 2 * cv;
     }, true);
 #ifdef FPS_SCAN_TRACE
-    if (lane == 0 && g < 16384 && !g_pq_phase[g * 8 + 5]) g_pq_phase[g * 8 + 5] = gtimer();
+    if (lane == 0 && g < 16384 && tr_iter == 1) g_pq_phase[g * 8 + 5] = gtimer();
     ph_done = true;
 #endif
     __syncwarp();

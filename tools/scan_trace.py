@@ -20,8 +20,9 @@ for wl in sys.argv[1:] or ["c2"]:
     marks = np.zeros(8, np.uint64)
     warps = np.zeros(16384 * 4, np.uint64)
     for r in range(3):
-        flush.fill_(r + 1)
-        flush.sum()
+        if not os.environ.get("NOFLUSH"):
+            flush.fill_(r + 1)
+            flush.sum()
         torch.cuda.synchronize()
         L.fps_trace_clear()
         L.fps_trace_mark(lib._h, 0)
@@ -49,5 +50,43 @@ for wl in sys.argv[1:] or ["c2"]:
                 v = v[v > 0] - m0
                 if len(v):
                     print(f"  1st step {name:14s}", pct(v))
+        if hasattr(L, "fps_trace_phases") and len(t) % 8 == 0:
+            allw = warps.reshape(-1, 4).astype(np.int64)[: len(t)]
+            seed = np.arange(len(t)) % 8 == 0
+            f3 = allw[:, 3] - m0
+            print("  first tile, seed warps ", pct(f3[seed & (allw[:, 3] > 0)]))
+            print("  first tile, other warps", pct(f3[~seed & (allw[:, 3] > 0)]))
+            p4 = ph[: len(t), 4]
+            opened = (p4 < 0).sum()
+            p4 = (p4 & ((1 << 62) - 1))
+            if (p4 > 0).any():
+                print("  seed tightened          ", pct(p4[p4 > 0] - m0), " still open:", opened)
+            took = ph[: len(t), 6] > 0
+            print("  warps on the bound-less first step: seed %d / %d, others %d / %d" % (
+                (took & seed).sum(), seed.sum(), (took & ~seed).sum(), (~seed).sum()))
+        if hasattr(L, "fps_trace_prologue"):
+            pro = np.zeros(16384 * 4, np.uint64)
+            L.fps_trace_prologue(pro.ctypes.data)
+            pro = pro.reshape(-1, 4).astype(np.int64)[: len(t)]
+            for i, name in enumerate(["list built (sync 2)", "ring initialised", "requests issued", "dependency wait over"]):
+                print(f"  prologue {name:22s}", pct(pro[:, i] - m0))
+        if hasattr(L, "fps_trace_steps"):
+            stp = np.zeros(16384 * 8, np.uint64)
+            L.fps_trace_steps(stp.ctypes.data)
+            stp = stp.reshape(-1, 8).astype(np.int64)[: len(t)]
+            for i in range(8):
+                v = stp[:, i]
+                v = v[v > 0] - m0
+                if len(v):
+                    print(f"  step {i} tile ready ({len(v):4d} warps)", pct(v))
+        if hasattr(L, "fps_trace_s1"):
+            s1 = np.zeros(16384 * 4, np.uint64)
+            L.fps_trace_s1(s1.ctypes.data)
+            s1 = s1.reshape(-1, 4).astype(np.int64)[: len(t)]
+            for i, name in enumerate(["bound taken", "held-back inserted", "csa done"]):
+                v = s1[:, i]
+                v = v[v > 0] - m0
+                if len(v):
+                    print(f"  2nd step {name:20s}", pct(v))
         print("  select start %.1f  end %.1f" % ((int(marks[2]) - m0) / 1e3, (int(marks[3]) - m0) / 1e3))
     lib.close()
