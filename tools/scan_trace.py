@@ -89,4 +89,6 @@ for wl in sys.argv[1:] or ["c2"]:
                 if len(v):
                     print(f"  2nd step {name:20s}", pct(v))
         print("  select start %.1f  end %.1f" % ((int(marks[2]) - m0) / 1e3, (int(marks[3]) - m0) / 1e3))
+        if int(marks[4]):
+            print("  last warp found %.1f  its selection done %.1f" % ((int(marks[4]) - m0) / 1e3, (int(marks[5]) - m0) / 1e3 if int(marks[5]) else -1))
     lib.close()
