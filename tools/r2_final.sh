@@ -12,3 +12,9 @@ for w in c1 c2 c4 c5; do timeout 900 python bench.py --workload $w --steps 20 --
 CMD="python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain_c4.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:mma4x_scan -s 3 -c 1 -o gpurun_out/prof_c4 $CMD > gpurun_out/ncu_c4.log 2>&1
 echo "ncu rc=$?"
+# plane scan captures (C3: the headline kernel; C2: the short, latency-bound scan)
+for w in c3 c2; do
+  CMD="python bench.py --workload $w --steps 2 --warmup 3 --no-cpu-baseline"
+  $CMD > gpurun_out/plain_$w.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$w.csv $CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:pq_scan -s 3 -c 1 -o gpurun_out/prof_$w $CMD > gpurun_out/ncu_$w.log 2>&1
+  echo "ncu $w rc=$?"
+done
