@@ -214,6 +214,8 @@ struct fps_lib {
   std::vector<TopkGraph*> graphs;
   bool timing = false;
   bool timing_suspend = false;  // helper passes (e.g. the bit-slice seed) are not timed
+  bool timing_continue = false; // the next timed launch belongs to the previous one's scan (one count)
+  size_t ev_groups = 0;         // timed scans (a scan may be several launches)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   cudaEvent_t ev_join = nullptr;  // orders the handle's stream after a caller's stream
   // shard of a multi-device group (fps_group_*): this shard's per-call result
@@ -425,6 +427,7 @@ std::pair<cudaEvent_t, cudaEvent_t>* timing_slot(fps_lib* L) {
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
     L->ev_pool.emplace_back(a, b);
   }
+  if (!L->timing_continue || L->ev_groups == 0) L->ev_groups++;
   return &L->ev_pool[L->ev_used++];
 }
 
@@ -934,30 +937,53 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
 // any batch >= 2, FPS_MMA=0 disables it. The call is stream ordered end to end
 // (no host synchronisation, capturable): a candidate list that overflows its
 // capacity raises a device flag, and a gated POPC pass recomputes the batch.
+constexpr int MMA_MAX_PASS = 6;
 struct MmaPlan {
-  u64 seed_n = 0, pre_n = 0;  // seed prefix (POPC top-k) and tensor-core prefix pass (0: none)
-  u32 cap[2] = {0, 0};        // per-query candidate capacity of the prefix / full pass
+  u64 seed_n = 0;               // seed prefix [0, seed_n): POPC top-k
+  int npass = 0;                // tensor-core passes over [n_scan[i-1], n_scan[i]) (the first from seed_n)
+  u64 n_scan[MMA_MAX_PASS] = {};  // (the last: the library)
+  u32 cap[MMA_MAX_PASS] = {};   // per-query candidate capacity of each pass
 };
 
-// Passes and candidate capacities for (Q, k). Candidates per query of a pass
-// ~ k x n_scan / bound_n (pairs within the prefix bound); the capacity is 8x
-// that, at least 16,384, and Q x cap x 8 B must fit the scratch budget
-// (FPS_MMA_CAND_MB, default 1,024 MB). Returns false when it cannot: the
-// batch then takes the bit-sliced kernel instead of overflowing.
+// Passes and candidate capacities for (Q, k). The library is scanned ONCE, in
+// growing ranges: a POPC top-k of the first 2^14 entries, then tensor-core
+// passes over [2^14, 2^18), [2^18, 2^21), [2^21, 2^24) and the rest (ranges
+// up to 1/2 of the library; FPS_MMA_PREFIX="18,21,24", FPS_MMA_SEED=14). Each
+// pass starts from the exact top-k of everything before it (carried into its
+// candidate lists), collects every pair within that bound, and its select is
+// the exact top-k so far: the bound tightens 8-16x per pass while no entry is
+// read twice. Candidates per query of a pass ~ k x n_scan / bound_n; the
+// capacity is 8x that (+ the k carried), at least 16,384, and Q x cap x 8 B
+// must fit the scratch budget (FPS_MMA_CAND_MB, default 1,024 MB). Returns
+// false when it cannot: the batch then takes the bit-sliced kernel instead of
+// overflowing. (C4: 8.81 ms per call with a 2^16 seed and a 2^22 prefix pass
+// that the full pass scanned again; prefixes re-scanned by the full pass cost
+// more than their tighter bound saves beyond 2^22.)
 bool mma_plan(const fps_lib* L, u32 Q, u32 k, MmaPlan* p) {
   // (knobs read per call: batched calls are not latency bound, and tests set them at run time)
   const char* es = std::getenv("FPS_MMA_SEED");
-  const int seed_log2 = es ? std::atoi(es) : 16;  // 2^16 .. 2^18: same bound after the prefix pass, cheaper seed
+  const int seed_log2 = es ? std::atoi(es) : 14;
   const char* ep = std::getenv("FPS_MMA_PREFIX");
-  const int pre_log2 = ep ? std::atoi(ep) : 22;
+  const std::string levels = ep ? ep : "18,21,24";
   const char* eb = std::getenv("FPS_MMA_CAND_MB");
   const u64 budget = (u64)(eb ? std::max(16, std::atoi(eb)) : 1024) << 20;
-  p->seed_n = std::min<u64>(L->n, 1ull << seed_log2);
-  p->pre_n = (pre_log2 > 0 && L->n >= (8ull << pre_log2)) ? (1ull << pre_log2) : 0;
-  for (int pass = p->pre_n ? 0 : 1; pass < 2; ++pass) {
-    const u64 n_scan = pass == 0 ? p->pre_n : L->n;
-    const u64 bound_n = pass == 0 ? p->seed_n : (p->pre_n ? p->pre_n : p->seed_n);
-    const u64 expect = (u64)k * (n_scan / std::max<u64>(bound_n, 1) + 1);
+  // (whole 256-entry library tiles, at most half of the library; 0: no seed,
+  // libraries below 512 entries are collected whole)
+  p->seed_n = std::min<u64>(1ull << std::max(0, std::min(seed_log2, 40)), L->n / 2) / 256 * 256;
+  p->npass = 0;
+  u64 prev = p->seed_n;
+  for (size_t pos = 0; pos < levels.size() && p->npass < MMA_MAX_PASS - 1;) {
+    const size_t c = levels.find(',', pos);
+    const int lg = std::atoi(levels.substr(pos, c == std::string::npos ? std::string::npos : c - pos).c_str());
+    pos = c == std::string::npos ? levels.size() : c + 1;
+    if (lg <= 0 || lg > 40) continue;
+    const u64 m = 1ull << lg;
+    if (m > prev && L->n >= 2 * m) p->n_scan[p->npass++] = prev = m;
+  }
+  p->n_scan[p->npass++] = L->n;
+  for (int pass = 0; pass < p->npass; ++pass) {
+    const u64 bound_n = pass == 0 ? p->seed_n : p->n_scan[pass - 1];
+    const u64 expect = (u64)k * (p->n_scan[pass] / std::max<u64>(bound_n, 1) + 2);
     const u64 want = std::min<u64>(std::max<u64>(8 * expect, 16384), 1u << 22);
     const u64 fit = budget / ((u64)Q * 8);
     if (fit < 2 * expect || fit < 1024) return false;
@@ -1131,7 +1157,7 @@ int mma4x_launch_n(fps_lib* L, u32 ctas, cudaStream_t s, const fps::MmArgs& a) {
 // ordered by u = T - |q|, then the scan. mode 0 appends candidate keys to the
 // per-query lists L->cand (capacity cap); mode 1 appends range hits to out.
 int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64* out_cnt, u64 out_cap,
-            cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull) {
+            cudaStream_t s, bool prepare_only, u64 n_scan = ~0ull, u64 n_start = 0) {
   int rc;
   const MmaKind kind = mma_kind(L, Q, mode);
   const bool fp4 = kind != MMA_I8;
@@ -1140,9 +1166,10 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   if (const char* en = std::getenv("FPS_MMA_N"))  // experiments: accumulator width (fp4: 64/128/160/208/240)
     if (fp4) NN = (u32)std::atoi(en);
   const u32 nchunks = (Q + NN - 1) / NN;
-  n_scan = std::min<u64>(n_scan, L->n);  // entries [0, n_scan) (a prefix pass of the top-k path)
+  n_scan = std::min<u64>(n_scan, L->n);  // entries [n_start, n_scan) (a range pass of the top-k path)
   const u64 n_tiles = (n_scan + fps::MM_M - 1) / fps::MM_M;
-  const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles));
+  const u64 tile0 = std::min<u64>(n_start, n_scan) / 256 * 2;  // (whole 256-entry library tiles)
+  const u32 parts = (u32)std::max<u64>(1, std::min<u64>(std::max<u32>(1, L->sms / nchunks), n_tiles - tile0));
   if ((rc = L->mm_bop.ensure((size_t)nchunks * (fp4 ? fps::mm4_b_bytes((int)NN) : fps::mm_b_bytes((int)NN)))) ||
       (rc = L->mm_ucol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_qpop.ensure((size_t)nchunks * NN * 4)) ||
       (rc = L->mm_qcol.ensure((size_t)nchunks * NN * 4)) || (rc = L->mm_keys.ensure((size_t)Q * 8)) ||
@@ -1179,6 +1206,7 @@ int mma_run(fps_lib* L, const u64* d_q, u32 Q, u32 mode, u32 cap, u64* out, u64*
   a.n = n_scan;
   a.index_base = L->index_base;
   a.n_tiles = n_tiles;
+  a.tile0 = tile0;
   a.Q = Q;
   a.nchunks = nchunks;
   a.parts = parts;
@@ -1226,30 +1254,39 @@ int topk_mma(fps_lib* L, const u64* d_q, u32 Q, u32 k, u64* d_keys, u32* d_cnt, 
   int rc;
   if ((rc = L->mm_ovf.ensure(256))) return rc;
   u32* ovf = L->mm_ovf.as<u32>();
+  if ((rc = ensure_state(L, Q))) return rc;
   if (!prepare_only) CUDA_TRY(cudaMemsetAsync(ovf, 0, 4, s));
   // 1. seed bound: exact top-k of a short library prefix (POPC scan)
-  L->timing_suspend = true;
-  rc = topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, plan.seed_n);
-  L->timing_suspend = false;
-  if (rc) return rc;
-  // 2. on long libraries, a tensor-core pass over a longer prefix first: its
-  //    top-k bound is tighter, so the full pass collects ~16x fewer pairs
-  //    (every pair within a bound is collected: each pass is exact for its range)
+  if (plan.seed_n) {
+    L->timing_suspend = true;
+    rc = topk_fused<8, 2, true>(L, d_q, Q, k, d_keys, d_cnt, s, prepare_only, plan.seed_n);
+    L->timing_suspend = false;
+    if (rc) return rc;
+  } else if (!prepare_only) {
+    CUDA_TRY(cudaMemsetAsync(d_cnt, 0, (size_t)Q * 4, s));  // no seed: every pair is a candidate
+  }
+  // 2. tensor-core passes over growing ranges (mma_plan): each starts from the
+  //    exact top-k of everything before it, carried into its candidate lists,
+  //    and collects every pair within that bound -- so its select is the exact
+  //    top-k so far and the next bound; no entry is read twice
   int kp = 1;
   while (kp < (int)k) kp <<= 1;
-  for (int pass = plan.pre_n ? 0 : 1; pass < 2; ++pass) {
-    const u64 n_scan = pass == 0 ? plan.pre_n : L->n;
+  for (int pass = 0; pass < plan.npass; ++pass) {
+    const u64 n_start = pass == 0 ? plan.seed_n : plan.n_scan[pass - 1];
+    const u64 n_scan = plan.n_scan[pass];
     const u32 cap = plan.cap[pass];
     if ((rc = L->mm_tq.ensure((size_t)Q * 4)) || (rc = L->cand.ensure((size_t)Q * cap * 8))) return rc;
     if (!prepare_only) {
       fps::mm_seed_kernel<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->mm_tq.as<u32>());
       fps::bs_seed_tg<<<(Q + 127) / 128, 128, 0, s>>>(d_keys, d_cnt, Q, k, L->tg.as<u32>(), tg_replicas(Q),
                                                        ghist_stride(Q));
-      L->launches += 2;
+      fps::mm_carry_kernel<<<dim3((k + 127) / 128, Q), 128, 0, s>>>(d_keys, d_cnt, k, L->cand.as<u64>(),
+                                                                    L->cand_cnt.as<u32>(), cap);
+      L->launches += 3;
     }
-    if (pass == 0) L->timing_suspend = true;
-    rc = mma_run(L, d_q, Q, 0, cap, nullptr, nullptr, 0, s, prepare_only, n_scan);
-    L->timing_suspend = false;
+    L->timing_continue = pass > 0;  // the passes of a call are one timed scan
+    rc = mma_run(L, d_q, Q, 0, cap, nullptr, nullptr, 0, s, prepare_only, n_scan, n_start);
+    L->timing_continue = false;
     if (rc) return rc;
     if (prepare_only) continue;
     // distances of the collected pairs (the scan stores their indices)
@@ -2609,6 +2646,7 @@ int fps_timing(fps_lib* lib, int enable) {
   std::lock_guard<std::mutex> lk(lib->mu);
   lib->timing = enable != 0;
   lib->ev_used = 0;
+  lib->ev_groups = 0;
   return FPS_OK;
 }
 
@@ -2624,8 +2662,9 @@ int fps_timing_read(fps_lib* lib, double* total_ms, uint64_t* count) {
     t += ms;
   }
   if (total_ms) *total_ms = t;
-  if (count) *count = lib->ev_used;
+  if (count) *count = lib->ev_groups;
   lib->ev_used = 0;
+  lib->ev_groups = 0;
   return FPS_OK;
 }
 

@@ -149,10 +149,22 @@ __global__ void mm_fix_kernel(PlanesOut lib, u64 index_base, const u64* __restri
   }
 }
 
+// The exact top-k so far (keys, cnt: the previous pass's select) opens the
+// candidate lists of the next range pass: indices only, as the scan stores
+// them (mm_fix_kernel recomputes the distances of the whole list).
+__global__ void mm_carry_kernel(const u64* __restrict__ keys, const u32* __restrict__ cnt, u32 k,
+                                u64* __restrict__ cand, u32* __restrict__ cand_cnt, u32 cap) {
+  const u32 qi = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 n = min(cnt[qi], k);
+  if (i < n && i < cap) cand[(u64)qi * cap + i] = keys[(u64)qi * k + i] & IDX_MASK;
+  if (i == 0) cand_cnt[qi] = n;
+}
+
 struct MmArgs {
   PlanesOut lib;
   u64 n, index_base;
   u64 n_tiles;              // ceil(n / 128)
+  u64 tile0;                // first 128-entry tile of this pass (a multiple of the library tile): entries [128 tile0, n)
   u32 Q, nchunks, parts;    // CTA c: chunk c % nchunks, tile range part c / nchunks
   const unsigned char* bop; // [nchunks][48 KB] canonical B
   const int* tcol;          // [nchunks * 256] T of each column's query (d = T - D)
@@ -275,7 +287,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma_scan_kernel(const MmArgs a)
   const u32 SUB = a.lib.compact ? TILE_CMP / MM_M : TILE_FULL / MM_M;
   const u32 RAW_BYTES = (u32)tile_bytes(a.lib.compact);
   const u64 n_raw = (a.n + tile_entries(a.lib.compact) - 1) / tile_entries(a.lib.compact);
-  const u64 r0 = part * n_raw / a.parts, r1 = (part + 1) * n_raw / a.parts;
+  const u64 raw0 = a.tile0 / (tile_entries(a.lib.compact) / MM_M);
+  const u64 r0 = raw0 + part * (n_raw - raw0) / a.parts, r1 = raw0 + (part + 1) * (n_raw - raw0) / a.parts;
   const u64 nraw = r1 > r0 ? r1 - r0 : 0;
   const u64 t0 = r0 * SUB;
 

@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(MM_THREADS, 1) mma4_scan_kernel(const MmArgs a
   const u32 SUB = a.lib.compact ? TILE_CMP / MM_M : TILE_FULL / MM_M;
   const u32 RAW_BYTES = (u32)tile_bytes(a.lib.compact);
   const u64 n_raw = (a.n + tile_entries(a.lib.compact) - 1) / tile_entries(a.lib.compact);
-  const u64 r0 = part * n_raw / a.parts, r1 = (part + 1) * n_raw / a.parts;
+  const u64 raw0 = a.tile0 / (tile_entries(a.lib.compact) / MM_M);
+  const u64 r0 = raw0 + part * (n_raw - raw0) / a.parts, r1 = raw0 + (part + 1) * (n_raw - raw0) / a.parts;
   const u64 nraw = r1 > r0 ? r1 - r0 : 0;
   const u64 t0 = r0 * SUB;
 

@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(mm4x_threads(EPI), 1)
   const int tid = threadIdx.x, warp = mm_warp_uniform(tid >> 5), lane = tid & 31;
   const u32 chunk = blockIdx.x % a.nchunks;
   const u64 part = blockIdx.x / a.nchunks;
-  const u64 t0 = part * a.n_tiles / a.parts, t1 = (part + 1) * a.n_tiles / a.parts;
+  const u64 nt = a.n_tiles - a.tile0;  // tiles of this pass
+  const u64 t0 = a.tile0 + part * nt / a.parts, t1 = a.tile0 + (part + 1) * nt / a.parts;
   const u64 ntile = t1 > t0 ? t1 - t0 : 0;
 
   // ---- setup: B chunk, barriers, TMEM (+ scale factors)

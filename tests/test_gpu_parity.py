@@ -848,12 +848,13 @@ def test_bitslice_all_ties_buffer_capacity(Q, monkeypatch):
             assert res.hits(i) == [(j, 1) for j in range(k)], (Q, k, i)
 
 
-@pytest.mark.parametrize("prefix_log2", [12, 14])
+@pytest.mark.parametrize("prefix_log2", [12, 14, "11,13,15", "0", "12,12,9,16"])
 def test_mma_two_pass_prefix_bound(prefix_log2, monkeypatch):
-    """Tensor-core top-k with the prefix pass (a tensor-core top-k of a
-    library prefix tightens the bound of the full pass), forced on a small
-    library: every pair within each pass's bound is collected, so the result
-    is the exact top-k."""
+    """Tensor-core top-k in range passes (each pass scans the entries after
+    the previous one, starting from the exact top-k so far, carried into its
+    candidate lists), forced on a small library: every pair within each
+    pass's bound is collected and no entry is read twice, so the result is the
+    exact top-k -- with one prefix range, several, none, or a malformed list."""
     monkeypatch.setenv("FPS_MMA", "1")
     monkeypatch.setenv("FPS_MMA_PREFIX", str(prefix_log2))
     monkeypatch.setenv("FPS_MMA_SEED", "10")
