@@ -213,6 +213,13 @@ int fps_last_kernel(const fps_lib* lib);
  * fp4 expanded in the kernel (kind::mxf4), 3 block-scaled fp4 from the
  * library's fp4 operand copy (the default; FPS_MMA_KIND=i8|fp4|fp4x). */
 int fps_last_mma_kind(const fps_lib* lib);
+/* Optional hint for the stream-ordered single-query calls (fps_topk_async with
+ * Q = 1), whose query lives on the device: the host copy of the query the next
+ * calls will scan (3 words), so the plane scan can size its shared-memory ring
+ * and warp count to the query's plane list (queries with more than 40 set or
+ * clear keys otherwise run at half the warps). NULL forgets the hint. The
+ * host-query entry points (fps_topk: scan.py:239-287) need no hint. */
+int fps_query_hint(fps_lib* lib, const uint64_t* query);
 /* Diagnostic (synchronises the device): 1 if the last tensor-core top-k had a
  * candidate list overflow its capacity, so its exact POPC fallback pass ran
  * (expected only for adversarial ties; the answer is exact either way). */

@@ -74,6 +74,7 @@ SIGNATURES = {
     "fps_last_kernel": (C.c_int, [_vp]),
     "fps_last_mma_kind": (C.c_int, [_vp]),
     "fps_mma_overflowed": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "fps_query_hint": (C.c_int, [_vp, _vp]),
     "fps_timing": (C.c_int, [_vp, C.c_int]),
     "fps_timing_read": (C.c_int, [_vp, C.POINTER(C.c_double), _u64p]),
     "fps_memory": (C.c_int, [_vp, _u64p, _u64p, _u64p, C.POINTER(C.c_double)]),

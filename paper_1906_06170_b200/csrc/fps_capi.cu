@@ -178,9 +178,10 @@ struct fps_lib {
   // getenv is a linear scan of the environment, and this is the per-call path
   struct PqKnobs {
     bool init = false, sorted = false;
-    int bpl = 0, warps = 8, stages = 2, smem_kb = 210, copy = 1, refresh = 0, wave_pct = 50, wave_ns = 8000;
+    int bpl = 0, warps = 8, stages = 2, smem_kb = 210, copy = 1, refresh = 0, wave_pct = 50, wave_ns = 8000, shape = 1;
   } pqk;
   u32 done_seq = 0;  // completion sequence of the single-query host path
+  u32 pq_hint_np = 0;  // stage positions of the next device-resident single query (fps_query_hint; 0: unknown)
   // tensor-core multi-query path (fps_mma.cuh, FPS_MMA=1): |a| per entry and per-call operands
   DevBuf mm_bop, mm_ucol, mm_qpop, mm_tq, mm_qcol, mm_keys, mm_sorted, mm_tmp, mm_priv;
   DevBuf mm_ovf;  // candidate-list overflow flag of the tensor-core top-k (gates its fallback pass)
@@ -802,6 +803,12 @@ bool pq_wanted(fps_lib* L) {
     // wave_pct % of the warps have posted their first step's witnesses
     L->pqk.wave_pct = std::max(0, std::min(100, ev("FPS_PQ_WAVE_PCT", 50)));
     L->pqk.wave_ns = std::max(0, ev("FPS_PQ_WAVE_NS", 8000));
+    // shape policy: 1 (default) = 1,024-entry steps with as many warps (<= 16)
+    // as hold two stages of the query's plane list; 0 = the knobs above for
+    // every query (8 warps x 2,048-entry steps; lists wider than 48 positions
+    // fold to 4 warps); 2 = policy 0 for lists of <= 48 positions, 1 for wider
+    // ones. Explicit shape knobs imply 0.
+    L->pqk.shape = ev("FPS_PQ_SHAPE", (std::getenv("FPS_PQ_BPL") || std::getenv("FPS_PQ_WARPS")) ? 0 : 1);
     L->pqk.init = true;
   }
   if (pm_ensure(L, L->pqk.sorted) != FPS_OK) {
@@ -824,29 +831,44 @@ u32 pq_positions(const u64* q) {
 int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u32* d_cnt, cudaStream_t s,
             bool prepare_only, u32* done_flag = nullptr, u32 done_seq = 0) {
   int rc;
-  // Shape (tools/pq_sweep.py, profiles/r01_experiments.md): 8 warps x two
-  // 32-entry blocks per lane x 2 ring stages; long scans read the global
+  // Shape: sized to the query's plane list (below); long scans read the global
   // bound every 8th step (C3 109.5 -> 95.5 us), short ones every step (the
   // first steps set it: C2 29.1 vs 33.5 us).
   const bool long_scan = L->n >= (32u << 20);
-  const int bpl = L->pqk.bpl;  // 32-entry blocks per lane
+  const bool srt = L->pm_sorted;
+  // stage positions of the query's plane list: known when the query is on the
+  // host (or hinted, fps_query_hint); 48 = up to 40 listed planes otherwise
+  const u32 np = h_qin ? pq_positions(h_qin) : (L->pq_hint_np ? L->pq_hint_np : 48);
+  int bpl = L->pqk.bpl;  // 32-entry blocks per lane
+  int nwb = L->pqk.warps;
+  const int stages = L->pqk.stages;
+  u32 budget = (u32)L->pqk.smem_kb * 1024;
+  // (short libraries, fewer than two 1,024-entry steps per warp at 16 warps,
+  // keep the 8-warp shape unless the list is wide: C1 e2e 37 vs 40 us)
+  const bool many_steps = L->n / fps::PqStep<1>::ENTRIES >= 32ull * (u64)L->sms;
+  if (!srt && ((L->pqk.shape == 1 && (many_steps || np > 48)) || (L->pqk.shape == 2 && np > 48))) {
+    // 1,024-entry steps and as many warps as hold two stages of this list
+    // (16 up to 48 positions, 13 at 56, 8 at 96): two stages of 2,048-entry
+    // steps fit 8 warps only up to 48 positions, beyond which the kernel folds
+    // to 4 warps (C3: 98 -> 157 us from 48 to 49 planes; tools/dbg/pq_width.py:
+    // now 98 -> 98.7 us, and 16 warps are 3-8 % faster on narrow lists too:
+    // C3 |q| = 20 / 30 / 40: 76.1 / 88.1 / 98.2 -> 69.9 / 81.1 / 95.5 us).
+    bpl = 1;
+    budget = std::max<u32>(budget, 218u * 1024);
+    for (nwb = 16; nwb > 4; --nwb)
+      if (fps::pq_smem(nwb, (2 * np * fps::PqStep<1>::CHUNK + 255) / 256 * 256) <= budget) break;
+  }
   const u32 chunk = bpl == 1 ? fps::PqStep<1>::CHUNK : fps::PqStep<2>::CHUNK;
   const u64 step_entries = bpl == 1 ? fps::PqStep<1>::ENTRIES : fps::PqStep<2>::ENTRIES;
-  const int nwb = L->pqk.warps;
-  const int stages = L->pqk.stages;
-  // ring per warp: `stages` stages of a typical list (48 positions = up to
-  // 40 listed planes); wider lists fold warps in the kernel; with the query
-  // on the host the ring is sized to it exactly
-  const u32 np = h_qin ? pq_positions(h_qin) : 48;
+  // ring per warp: `stages` stages of the list; wider lists than the ring was
+  // sized for fold warps in the kernel
   // (capped by the shared memory of one CTA; at least two stages of the
   // widest list over the whole CTA)
-  const u32 budget = (u32)L->pqk.smem_kb * 1024;
   const u32 ring_cap = (u32)((budget - (u32)fps::pq_smem(nwb, 0)) / nwb) / 256 * 256;
-  u32 ring = std::min<u32>((u32)stages * np * chunk, ring_cap);
+  u32 ring = std::min<u32>(((u32)stages * np * chunk + 255) / 256 * 256, ring_cap);
   ring = std::max<u32>(ring, (u32)((2 * fps::PQ_NPMAX * chunk + nwb - 1) / nwb + 255) / 256 * 256);
   const u64 steps = (L->n + step_entries - 1) / step_entries;
   const u64 grid = std::max<u64>(1, std::min<u64>((u64)L->sms, steps));
-  const bool srt = L->pm_sorted;
   const u32 meta_cap = srt ? (u32)((steps + grid - 1) / grid + 1) : 0u;
   const size_t smem = fps::pq_smem(nwb, ring, meta_cap);
   if (smem > 226 * 1024) return fail(FPS_EINVAL, "plane scan: shared memory ring too large (FPS_PQ_WARPS/STAGES)");
@@ -854,8 +876,15 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   const u32 cap = (std::max<u32>(2 * k, k + (u32)step_entries) + 31) / 32 * 32;
   const u64 cand_cap = warps * (u64)k;
   if ((rc = ensure_state(L, 1))) return rc;
-  if ((rc = L->buf.ensure(warps * (size_t)cap * 8))) return rc;
-  if ((rc = L->cand.ensure(cand_cap * 8))) return rc;
+  {
+    // sized for every shape the policy may pick for later queries (a call must
+    // not reallocate inside a captured or pipelined stream)
+    const size_t c1 = (std::max<u32>(2 * k, k + (u32)fps::PqStep<1>::ENTRIES) + 31) / 32 * 32;
+    const size_t c2 = (std::max<u32>(2 * k, k + (u32)fps::PqStep<2>::ENTRIES) + 31) / 32 * 32;
+    const size_t per_cta = std::max<size_t>({(size_t)nwb * cap, 16 * c1, (size_t)L->pqk.warps * c2});
+    if ((rc = L->buf.ensure((size_t)L->sms * per_cta * 8))) return rc;
+    if ((rc = L->cand.ensure((size_t)L->sms * std::max<size_t>(16, nwb) * k * 8))) return rc;
+  }
   const int copy = L->pqk.copy;  // 1: cp.async 16 B per lane (default, measured faster), 0: bulk copies
   const int kv = srt ? 4 + (bpl == 2 ? 1 : 0) : (copy == 1 ? 1 : 0) * 2 + (bpl == 2 ? 1 : 0);
   void (*const kerns[6])(fps::PqArgs) = {fps::pq_scan_kernel<0, 1, false>, fps::pq_scan_kernel<0, 2, false>,
@@ -881,11 +910,12 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   a.meta_cap = meta_cap;
   a.pub_every = (u32)std::max<u64>(1, warps / 512);
   {
-    // warps whose first step is a full one post k witnesses each
-    const u64 tw = std::min<u64>(L->n / step_entries, warps);
-    const u64 need = tw * (u64)L->pqk.wave_pct / 100;
+    // warps whose first step is a full one post k witnesses each; the kernel
+    // sizes the wait from its active warps (wide plane lists fold warps).
     // (libraries with fewer than two steps per warp have no second step to speed up)
-    a.wave_target = (k <= step_entries && need > 0 && steps >= 2 * warps) ? (u32)std::min<u64>(need * k, 0x7fffffffu) : 0u;
+    const bool on = k <= step_entries && steps >= 2 * warps;
+    a.wave_pct = on ? (u32)L->pqk.wave_pct : 0u;
+    a.wave_steps = L->n / step_entries;
     a.wave_wait_ns = (u32)L->pqk.wave_ns;
   }
   a.flags = scan_flags();
@@ -2626,6 +2656,13 @@ uint64_t fps_launch_count(const fps_lib* lib) { return lib ? lib->launches.load(
 
 int fps_last_kernel(const fps_lib* lib) { return lib ? lib->last_kernel : 0; }
 int fps_last_mma_kind(const fps_lib* lib) { return lib ? lib->last_mma_kind : 0; }
+
+int fps_query_hint(fps_lib* lib, const uint64_t* query) {
+  if (int rc = check_lib(lib)) return rc;
+  std::lock_guard<std::mutex> lk(lib->mu);
+  lib->pq_hint_np = query ? pq_positions(reinterpret_cast<const u64*>(query)) : 0u;
+  return FPS_OK;
+}
 
 int fps_mma_overflowed(fps_lib* lib, int* flag) {
   if (int rc = check_lib(lib)) return rc;

@@ -184,6 +184,8 @@ int group_topk_dev(fps_group* G, int what, const u64* h_q, const u64* d_q, u32 Q
     if (!L->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&L->ev_done, cudaEventDisableTiming));
     if (h_q) {
       CUDA_TRY(cudaMemcpyAsync(L->queries.p, h_q, (size_t)Q * 24, cudaMemcpyHostToDevice, L->stream));
+      // (a single host query: the plane scan sizes its ring to the query's plane list)
+      L->pq_hint_np = (Q == 1 && what != GRP_MIN) ? pq_positions(h_q) : 0u;
     } else {
       CUDA_TRY(cudaStreamWaitEvent(L->stream, G->ev_in, 0));
       CUDA_TRY(cudaMemcpyPeerAsync(L->queries.p, L->device, d_q, G->root, (size_t)Q * 24, L->stream));

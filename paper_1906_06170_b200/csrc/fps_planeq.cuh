@@ -125,7 +125,9 @@ struct PqArgs {
   u32 pub_every;        // warps with g % pub_every == 0 publish witnesses
   u32 flags;            // FPS_SCAN_FLAGS: 1 = no publishing, 2 = no tg refresh
   u32 refresh;          // steps between reads of the global bound (1 = every step)
-  u32 wave_target;      // witnesses of the first wave a warp waits for before its second step (0: no wait)
+  u32 wave_pct;         // first wave: a warp's second step waits for the witnesses of this share of the
+                        // active warps with a full first step (0: no wave)
+  u64 wave_steps;       // full steps of the library (warps with one post k witnesses each)
   u32 wave_wait_ns;     // ... for at most this long
   u32* tg;
   u32* ghist;
@@ -256,14 +258,15 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
   const u32 np = s_np, nc = s_nc, pop = s_pop;
   const bool dense = s_dense != 0;
   const u32 stage_bytes = np * PQ_CHUNK;
-  // Fold warps until every active warp has >= 2 stages (wide lists on a ring
-  // sized for typical ones): warp wib < nact owns `fold` consecutive rings.
-  u32 fold = 1;
-  while (fold < (u32)nwb && (a.ring_bytes * fold) / stage_bytes < 2) fold <<= 1;
-  const u32 nact = (u32)nwb / fold;
+  // Lists wider than the ring was sized for (a device-resident query of
+  // unknown width): as many warps as the CTA's ring memory gives two stages
+  // stay active (16 -> 13 at 56 positions, 8 at 96), the others leave.
+  const u32 total_ring = a.ring_bytes * (u32)nwb;
+  u32 nact = total_ring / (2 * stage_bytes);
+  nact = nact > (u32)nwb ? (u32)nwb : (nact < 1 ? 1u : nact);
   if ((u32)wib >= nact) return;
-  const u32 rbytes = a.ring_bytes * fold;
-  const u32 S = min((u32)PQ_SMAX, rbytes / stage_bytes);
+  const u32 rbytes = (total_ring / nact) / 256 * 256;
+  const u32 S = min((u32)PQ_SMAX, max(1u, rbytes / stage_bytes));
 
   char* ring = reinterpret_cast<char*>(pqs) + (size_t)wib * rbytes;
   u64* bars = reinterpret_cast<u64*>(pqs + (size_t)nwb * a.ring_bytes) + wib * PQ_SMAX;
@@ -417,6 +420,8 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
     return (tt < T_OPEN ? tt : T_OPEN - 1) + 1;
   };
   bool first = true;  // the warp's first tile: the bound is read afresh
+  // (the active warps of this launch: wide plane lists fold warps)
+  const u32 wave_target = (u32)min((min((u64)gridDim.x * nact, a.wave_steps) * a.wave_pct / 100) * a.k, (u64)0x7fffffffu);
   bool wave = false;  // first-step witnesses posted: the second step waits for the first wave's
 
   // Compaction to the k best by (d, index): every entry with d < tt (the
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
 #pragma unroll
           for (int i = 0; i < 7; ++i) sum += hv[i];
           sum = __reduce_add_sync(FULL, sum);
-          if (sum >= a.wave_target || pq_now_ns() - t0 > a.wave_wait_ns) break;
+          if (sum >= wave_target || pq_now_ns() - t0 > a.wave_wait_ns) break;
         }
         lim = finish_tighten(true);
         if (lane == 0) *(volatile u32*)&s_wave_T = lim | 0x80000000u;
@@ -900,7 +905,7 @@ __global__ void __launch_bounds__(512, 1) pq_scan_kernel(const PqArgs a) {
       Tsv = 256;  // fewer than k entries: every one is a candidate
       if (nv >= a.k) {
         u32 town1 = 0;
-        const bool wv = a.wave_target != 0 && !(a.flags & 1);
+        const bool wv = wave_target != 0 && !(a.flags & 1);
         if (publisher || wv) {
           // witnesses: 1 at the smallest distance, 1 at the 2nd, 2 at the 4th,
           // k - 4 at the k-th (ranks capped at k). With many more warps than

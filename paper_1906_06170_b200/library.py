@@ -354,6 +354,15 @@ class Library:
         N.check(N.load().fps_topk_async(self._h, N.ptr(d_queries), Q, k, N.ptr(d_keys), N.ptr(d_cnt), stream),
                 "fps_topk_async")
 
+    def query_hint(self, query=None) -> None:
+        """Host copy of the single device-resident query the next ``topk_async``
+        calls scan (sizes the plane scan to its plane list); None forgets it."""
+        if query is None:
+            N.check(N.load().fps_query_hint(self._h, None), "fps_query_hint")
+            return
+        q = np.ascontiguousarray(as_query_words(query)[:1])
+        N.check(N.load().fps_query_hint(self._h, q.ctypes.data), "fps_query_hint")
+
     def range_async(self, d_queries, Q: int, d_radius, d_out, cap: int, d_count, stream: int) -> None:
         N.check(N.load().fps_range_async(self._h, N.ptr(d_queries), Q, N.ptr(d_radius), N.ptr(d_out), cap,
                                          N.ptr(d_count), stream), "fps_range_async")
