@@ -848,14 +848,19 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
   const bool many_steps = L->n / fps::PqStep<1>::ENTRIES >= 32ull * (u64)L->sms;
   if (!srt && ((L->pqk.shape == 1 && (many_steps || np > 48)) || (L->pqk.shape == 2 && np > 48))) {
     // 1,024-entry steps and as many warps as hold two stages of this list
-    // (16 up to 48 positions, 13 at 56, 8 at 96): two stages of 2,048-entry
+    // (16 below 48 positions, 14 at 48, 13 at 56, 8 at 96): two stages of 2,048-entry
     // steps fit 8 warps only up to 48 positions, beyond which the kernel folds
     // to 4 warps (C3: 98 -> 157 us from 48 to 49 planes; tools/dbg/pq_width.py:
     // now 98 -> 98.7 us, and 16 warps are 3-8 % faster on narrow lists too:
     // C3 |q| = 20 / 30 / 40: 76.1 / 88.1 / 98.2 -> 69.9 / 81.1 / 95.5 us).
     bpl = 1;
     budget = std::max<u32>(budget, 218u * 1024);
-    for (nwb = 16; nwb > 4; --nwb)
+    // At most 14 warps at 48 positions (C3: 95.7 / 94.4 / 94.9 / 95.9 us at 13 /
+    // 14 / 15 / 16 warps, 98.5 at 12), 16 on narrower lists (|q| = 20 / 30:
+    // 70 / 81 us at 16 warps, 76 / 85 at 14); FPS_PQ_MAXW overrides.
+    static const int maxw_env = std::getenv("FPS_PQ_MAXW") ? std::atoi(std::getenv("FPS_PQ_MAXW")) : 0;
+    const int maxw = maxw_env > 0 ? maxw_env : (np >= 48 ? 14 : 16);
+    for (nwb = std::max(5, std::min(16, maxw)); nwb > 4; --nwb)
       if (fps::pq_smem(nwb, (2 * np * fps::PqStep<1>::CHUNK + 255) / 256 * 256) <= budget) break;
   }
   const u32 chunk = bpl == 1 ? fps::PqStep<1>::CHUNK : fps::PqStep<2>::CHUNK;
