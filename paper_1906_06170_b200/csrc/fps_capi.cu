@@ -862,6 +862,11 @@ int topk_pq(fps_lib* L, const u64* d_q, const u64* h_qin, u32 k, u64* d_keys, u3
     const int maxw = maxw_env > 0 ? maxw_env : (np >= 48 ? 14 : 16);
     for (nwb = std::max(5, std::min(16, maxw)); nwb > 4; --nwb)
       if (fps::pq_smem(nwb, (2 * np * fps::PqStep<1>::CHUNK + 255) / 256 * 256) <= budget) break;
+  } else if (!srt && L->pqk.shape == 1) {
+    // short libraries: 6 warps x 2,048-entry steps (a smaller CTA launches
+    // faster; host-path call, tools/dbg/pq_small.py: 1 M entries 29.0 vs 30.8 us
+    // with 8 warps, 2 M 28.1 vs 32.8, 4 M 28.8 vs 29.7)
+    nwb = 6;
   }
   const u32 chunk = bpl == 1 ? fps::PqStep<1>::CHUNK : fps::PqStep<2>::CHUNK;
   const u64 step_entries = bpl == 1 ? fps::PqStep<1>::ENTRIES : fps::PqStep<2>::ENTRIES;
