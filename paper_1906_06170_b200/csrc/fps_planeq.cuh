@@ -14,9 +14,13 @@
 //
 // Layout (plane-major): plane p occupies pstride u32 words from pm + p *
 // pstride; word w is 32-entry block w. A warp step covers 1,024 x BPL entries
-// (BPL = 2 by default: a lane owns two consecutive blocks and reads both with
-// one 64-bit shared load, as in fps_bitslice.cuh), i.e. 128 x BPL bytes of
-// every listed plane.
+// (a lane owns BPL consecutive blocks; BPL = 2 reads both with one 64-bit
+// shared load, as in fps_bitslice.cuh), i.e. 128 x BPL bytes of every listed
+// plane. The host picks the shape per query (topk_pq in fps_capi.cu): BPL = 1
+// with as many warps (<= 16) as hold two stages of the query's plane list on
+// libraries with at least two steps per warp, 6 warps x BPL = 2 on shorter
+// ones; a list wider than the ring was sized for (a device-resident query of
+// unknown width) keeps as many warps active as the ring memory allows.
 //
 // Per warp, a ring of S stages in shared memory: position 0..7 = popcount
 // planes, 8.. = the query's list (zero-padded to a multiple of 8). COPY 1
@@ -34,7 +38,9 @@
 // has no bound yet: it computes the step's distances bit-sliced, finds the
 // k-th smallest by radix select (no per-entry work), publishes witnesses at a
 // few ranks, and holds its entries back one step so they are inserted under
-// the tighter global bound the first wave of witnesses produces.
+// the tighter global bound the first wave of witnesses produces: before its
+// second step's test a warp takes the bound of the whole first wave (one
+// warp per CTA polls the global histogram, the others read shared memory).
 #pragma once
 #include "fps_bitslice.cuh"
 
